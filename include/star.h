@@ -1,0 +1,212 @@
+/*
+ * star.h -- C ABI of the B200-native hot path of STAR (arxiv 2510.13668,
+ * "Adaptive Rescheduling in Prefill-Decode Disaggregated LLM Inference").
+ *
+ * Per decode iteration, on every decode instance (one instance or a block of instances per
+ * B200), the path is:
+ *   lenpred_forward        Eq. 2: remaining-length prediction from each
+ *                          running request's last-token, last-layer hidden state, quantized
+ *                          to integer tokens N_hat (readings A8-A10).
+ *   project_instance_load  worker-side local future-state simulation:
+ *                          current token load N_i(B_i) and projected loads
+ *                          N_hat_i(B_{i,t}), t = 1..H, w_i (Alg. 1 line 13).
+ *   (NCCL all-gather of the per-rank records -- done by the caller)
+ *   plan_reschedule        Alg. 1: InstanceClassification,
+ *                          CandidateEnumeration, OptimalSelection over Eq. 3-4's objective,
+ *                          exact integers, greedy rounds.
+ *
+ * Conventions (all entry points):
+ *  - Return star_status: 0 = OK, < 0 = error.  No exception crosses the ABI.  On error
+ *    star_last_error() returns a thread-local message valid until the next call on that
+ *    thread; nothing was enqueued unless the error is STAR_ECUDA from the launch itself.
+ *  - Array pointers are DEVICE pointers (cudaMalloc / torch CUDA memory) owned by the caller,
+ *    unless stated otherwise.  The library never frees caller memory.
+ *  - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default stream) and the call
+ *    returns immediately; results are valid after the stream is synchronised.
+ *  - Hot-path calls (lenpred_forward, project_instance_load, plan_reschedule*) do no
+ *    allocation and no host synchronisation, so they can be captured in a CUDA graph.
+ *  - Scalar arguments are validated on the host (STAR_EINVAL / STAR_ERANGE).  Per-element
+ *    problems found on the device (instance id out of range, N(r) outside [1, 2^17],
+ *    N_hat < 0, count overflow) set bits in *err_flag (device int32, nullable, never
+ *    cleared by the library) and the offending element is ignored.
+ *  - Only sm_100a (B200) is supported; every call fails with STAR_ENOTSUP elsewhere.  There
+ *    is no CPU fallback.
+ */
+#ifndef STAR_H_
+#define STAR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* star_stream_t;   /* ABI-identical to cudaStream_t */
+
+typedef enum {
+  STAR_OK = 0,
+  STAR_EINVAL = -1,   /* bad pointer / shape / flag combination */
+  STAR_ERANGE = -2,   /* a size exceeds the exactness bounds documented below */
+  STAR_ECUDA = -3,    /* CUDA runtime / driver error (message has the CUDA error string) */
+  STAR_ENOTSUP = -4,  /* device is not sm_100 or the shape is outside what the kernels tile */
+  STAR_ENOMEM = -5    /* allocation failed (create only) */
+} star_status;
+
+typedef enum { STAR_F32 = 0, STAR_BF16 = 1 } star_dtype;
+
+/* err_flag bits (device side) */
+#define STAR_ERRF_INST   1  /* instance id outside [inst_base, inst_base + n_inst) */
+#define STAR_ERRF_NTOK   2  /* N(r) outside [1, 2^17] */
+#define STAR_ERRF_NHAT   4  /* N_hat(r) < 0 */
+#define STAR_ERRF_COUNT  8  /* more than 2^16 requests on one instance */
+#define STAR_ERRF_PLAN   16 /* plan input inconsistent (segment count > capacity, etc.) */
+
+const char* star_last_error(void);
+/* Library version string, e.g. "star-b200 0.1 sm_100a". */
+const char* star_version(void);
+
+/* =====================================================================================
+ * Length predictor  (Eq. 2)
+ *     y_hat = w4 . phi(W3 phi(W2 phi(W1 h)))      phi = ReLU
+ * d = hidden size (any multiple of 8), m1 = 2048, m2 = 512, m3 = 64 for the paper's model
+ * (reading A2: the widths are fixed for every d).  Supported: m1, m2 multiples
+ * of 256 (bf16) / 128 (f32), m3 == 64.
+ * Precision: STAR_BF16 -> bf16 operands on tcgen05 kind::f16, fp32 accumulation in TMEM,
+ * Z1/Z2 rounded to bf16; STAR_F32 -> fp32 operands via 3xTF32 (hi/lo split,
+ * hi*hi + hi*lo + lo*hi, tcgen05 kind::tf32), fp32 accumulation.  Layer 4 and the biases are
+ * fp32 on the CUDA cores.
+ * ===================================================================================== */
+typedef struct star_predictor star_predictor;  /* opaque: TMA descriptors, scratch Z1/Z2 */
+
+/* Creates a predictor bound to caller-owned device weights (they must outlive the handle):
+ *   W1 [m1][d], W2 [m2][m1], W3 [m3][m2] row-major in `dt` (nn.Linear [out][in] layout =
+ *   K-major, the UMMA B operand as-is);  w4 [m3] fp32;  b1 [m1], b2 [m2], b3 [m3], b4 [1] fp32
+ *   or NULL (NULL reproduces Eq. 2 literally, reading A1).
+ * max_rows bounds R of later forward calls.  For STAR_F32 the weights are split into tf32
+ * hi/lo copies here (library-owned).  This is the only call that allocates device memory;
+ * it synchronises `stream` before returning. */
+star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, int m3, star_dtype dt,
+                                  const void* W1, const void* W2, const void* W3, const float* w4,
+                                  const float* b1, const float* b2, const float* b3, const float* b4,
+                                  int max_rows, star_stream_t stream);
+star_status star_predictor_destroy(star_predictor* p);
+
+/* Forward for R rows of h (row r at h + r*ld_h elements, dtype of the predictor, ld_h >= d,
+ * ld_h*elem_size a multiple of 16 bytes).  Outputs (each nullable):
+ *   y_hat [R] fp32      the regression output of Eq. 2
+ *   n_hat [R] int32     N_hat = (int) rint(fminf(fmaxf(y_hat, 0), cap_r)),
+ *                       cap_r = max(0, max_ctx_len - n_tok[r])   (n_tok NULL => cap = max_ctx_len)
+ *                       round-half-to-even, NaN -> 0 (readings A8-A10; PAPER.md:491 32K context)
+ * R = 0 is legal (nothing enqueued).  R <= max_rows.  Not thread-safe per handle. */
+star_status lenpred_forward(star_predictor* p, const void* h, int64_t ld_h, int R,
+                            const int32_t* n_tok, int32_t max_ctx_len,
+                            float* y_hat, int32_t* n_hat, star_stream_t stream);
+
+/* The quantizer alone, on a caller-given fp32 y_hat (the exact device function the forward
+ * epilogue uses).  Lets quantizer parity be tested on identical fp32 inputs. */
+star_status lenpred_quantize(const float* y_hat, const int32_t* n_tok, int R, int32_t max_ctx_len,
+                             int32_t* n_hat, star_stream_t stream);
+
+/* Optional per-handle timing hook: when both events are non-NULL, lenpred_forward records
+ * ev_start / ev_end (cudaEvent_t) around the layer-1 GEMM launch on `stream`.  NULL disables. */
+star_status star_predictor_set_layer1_events(star_predictor* p, void* ev_start, void* ev_end);
+
+/* =====================================================================================
+ * Projected per-instance load  (readings A4-A6)
+ * For instance i in [0, n_inst) (request r belongs to i = inst[r] - inst_base):
+ *   L[i][0] = sum_{r in B_i} N(r)                                 N(r) = n_tok[r] (prompt + generated)
+ *   L[i][t] = sum_{r in B_i, t < N_hat(r)} (N(r) + t),  t = 1..H    (a request stays resident while
+ *                                                                  t < N_hat, growing one token/step)
+ *   W[i]    = sum_{t=1}^{H} beta_q[t] * L[i][t]                    (w_i of Alg. 1 line 13, Q16 units)
+ *   peak[i] = max_{0<=t<=H} L[i][t]   growth[i] = sum min(N_hat, H)   count[i] = |B_i|
+ * Exact int64 integers: bounds N(r) <= 2^17, count <= 2^16, H <= 256, beta_q <= 2^16
+ * (then L <= 2^33, W <= 2^57).  Any output pointer except L may be NULL.
+ * workspace: device buffer of star_project_workspace_bytes(n_inst, H) bytes, ZERO-FILLED by
+ * the caller once at allocation; each call leaves it zeroed again.  May be NULL when
+ * R <= star_project_single_cta_max_rows(): then one CTA does the whole reduction.
+ * Implementation: vectorised coalesced int4 loads, warp-aggregated (match_any + redux) shared-
+ * memory histogram over (instance, min(N_hat, H+1)), suffix scan -> L, W, peak, growth.
+ * ===================================================================================== */
+size_t star_project_workspace_bytes(int n_inst, int H);
+int star_project_single_cta_max_rows(void);
+star_status project_instance_load(int R, int n_inst, int inst_base, int H,
+                                  const int32_t* inst, const int32_t* n_tok, const int32_t* n_hat,
+                                  const uint32_t* beta_q,
+                                  int64_t* L, int64_t* W, int64_t* peak, int64_t* growth, int32_t* count,
+                                  void* workspace, int32_t* err_flag, star_stream_t stream);
+
+/* =====================================================================================
+ * Reschedule plan  (Alg. 1; objective Eq. 3-4)
+ * Exact integer semantics (reading A11): with Q = 65536 and the Q16 schedule beta_q,
+ *   Phi*n^2 = sum_{t=0}^{H} beta_q[t] * (n * sum_i L[i][t]^2 - (sum_i L[i][t])^2)
+ * Per round (at most max_moves rounds, a request moves at most once per call):
+ *   Phase 1  W_i as above (STAR_CURRENT_ONLY: W_i = beta_q[0]*L[i][0]);
+ *            O = { i : n*den*W_i > (den+num)*sum_j W_j }                 (w_i > (1+theta) w_bar)
+ *            U = { i not in O : n*den*Q*L[i][0] < (den+num)*sum_j W_j }  (reading A13)
+ *            O empty -> stop.
+ *   Phase 2  candidates (r, s in O, t in U), r on s, not pinned, not yet moved, with
+ *            (a) N_hat(r) * (a + b*L[t][0]) > c0 + c1*N(r)    (N_hat > C_mig / T_exec, PAPER.md:435,
+ *                readings A15-A17; skipped in STAR_CURRENT_ONLY)
+ *            (b) L[t][0] + reserved[t] + N(r) + N_hat(r) <= c_mem[t]  (reading A18;
+ *                STAR_STRICT_MEM: L[t][0] + N_hat(r) <= c_mem[t]; CURRENT_ONLY drops N_hat;
+ *                c_mem NULL disables the filter)
+ *   Phase 3  gain = Phi*n^2(before) - Phi*n^2(r moved s->t) (reading A19), exact __int128;
+ *            keep gain > 0 (sigma2_max starts at 0); best = max gain, ties ->
+ *            lowest req_id, then lowest target (reading A20).  Apply, emit, next round.
+ * The whole plan runs in one CTA: per-request warp argmax over target instances of the
+ * closed-form score, then a block argmax over requests.
+ * ===================================================================================== */
+#define STAR_STRICT_MEM    1u
+#define STAR_CURRENT_ONLY  2u
+
+typedef struct {
+  int n_inst, H, max_moves;            /* n_inst >= 1, 0 <= H <= 256, 0 <= max_moves <= 1024 */
+  int32_t theta_num, theta_den;        /* theta = num/den >= 0, den >= 1 (default 1/10) */
+  const uint32_t* beta_q;              /* [H+1] device, Q16 (beta_q[0] weights sigma0^2) */
+  const int64_t* c_mem;                /* [n_inst] device tokens, NULL = no memory filter */
+  const int64_t* reserved;             /* [n_inst] device tokens in flight inbound, NULL = 0 */
+  int64_t t_exec_a_ps, t_exec_b_ps;    /* T_exec(t) = a + b*L[t][0] picoseconds (Fig. 6 linearity) */
+  int64_t mig_c0_ps, mig_c1_ps;        /* C_mig(r) = c0 + c1*N(r) picoseconds (KV bytes / bandwidth) */
+  uint32_t flags;                      /* STAR_STRICT_MEM | STAR_CURRENT_ONLY */
+} star_plan_params;
+
+typedef struct {
+  int32_t req_id, src, dst, round;
+  int64_t gain_hi;                     /* gain = Phi*n^2 decrease as signed __int128 (hi:lo) */
+  uint64_t gain_lo;
+} star_move;                           /* 32 bytes */
+
+/* Contiguous form: L [n_inst][H+1] and R_total requests (SoA, device).  inst[] holds global
+ * instance ids in [0, n_inst).  pinned nullable.  moves [max_moves] and n_moves (device int32)
+ * are outputs. */
+star_status plan_reschedule(const star_plan_params* p, const int64_t* L, int R_total,
+                            const int32_t* req_id, const int32_t* inst, const int32_t* n_tok,
+                            const int32_t* n_hat, const uint8_t* pinned,
+                            star_move* moves, int32_t* n_moves, int32_t* err_flag, star_stream_t stream);
+
+/* Segmented form, reading the gathered per-rank records in place (no unpack copy):
+ * segment k (k < world) owns instances [k*n_loc, (k+1)*n_loc) and for every pointer P below
+ * its data lives at (char*)P + k*seg_stride:  L [n_loc][H+1] int64, r_count (int32, number of
+ * valid requests in the segment, <= r_cap), req_id/inst/n_tok/n_hat [r_cap] int32,
+ * pinned [r_cap] uint8 (nullable).  world*n_loc must equal p->n_inst. */
+typedef struct {
+  int world, n_loc, r_cap;
+  int64_t seg_stride;                  /* bytes */
+  const int64_t* L;
+  const int32_t* r_count;
+  const int32_t* req_id;
+  const int32_t* inst;
+  const int32_t* n_tok;
+  const int32_t* n_hat;
+  const uint8_t* pinned;
+} star_plan_segments;
+
+star_status plan_reschedule_segmented(const star_plan_params* p, const star_plan_segments* seg,
+                                      star_move* moves, int32_t* n_moves, int32_t* err_flag,
+                                      star_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STAR_H_ */

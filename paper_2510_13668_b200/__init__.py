@@ -1,0 +1,17 @@
+"""paper_2510_13668_b200 -- B200-native hot path of STAR (arxiv 2510.13668).
+
+Public API (names follow the C ABI in include/star.h):
+    Predictor, lenpred_forward, lenpred_quantize       Eq. 2 predictor + quantizer
+    project_instance_load                              per-instance projected loads
+    PlanParams, plan_reschedule, plan_reschedule_segmented   Alg. 1 plan
+    step.Step                                          one decode-step pass over ranks (NCCL)
+Importing the package does not load the CUDA library; the first call does, and raises
+StarError if it is missing (there is no CPU fallback).
+"""
+from ._lib import (CURRENT_ONLY, L_CTX, STRICT_MEM, Predictor, PlanParams, ProjectOut, StarError,  # noqa: F401
+                   alloc_moves, decode_moves, lenpred_forward, lenpred_quantize, plan_reschedule,
+                   plan_reschedule_segmented, project_instance_load, project_workspace_bytes, version)
+
+__all__ = ["Predictor", "lenpred_forward", "lenpred_quantize", "project_instance_load", "PlanParams",
+           "plan_reschedule", "plan_reschedule_segmented", "decode_moves", "alloc_moves", "StarError",
+           "project_workspace_bytes", "version", "STRICT_MEM", "CURRENT_ONLY", "L_CTX", "ProjectOut"]

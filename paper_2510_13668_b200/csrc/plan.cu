@@ -1,0 +1,345 @@
+// plan.cu -- Alg. 1 on the GPU, exact integers, one CTA.
+//
+// Objective (Eq. 3-4; readings A11/A12), Q16 weights beta_q:
+//   Phi*n^2 = sum_{t=0}^{H} beta_q[t] * (n sum_i L_i[t]^2 - (sum_i L_i[t])^2)
+// Moving request r (N = N(r), contribution c_t = N + t for t <= T_r, T_r = min(H, max(0, N_hat-1)))
+// from s to u changes sum_i L_i[t]^2 by -2 c_t (L_s[t] - L_u[t] - c_t) and leaves sum_i L_i[t]
+// unchanged, so the exact objective decrease is
+//   gain = 2n * score,  score = sum_{t<=T_r} beta_t c_t (L_s[t] - L_u[t] - c_t)
+//        = N (P0_s[T] - P0_u[T]) + (P1_s[T] - P1_u[T]) - (N^2 B0[T] + 2N B1[T] + B2[T])
+// with per-instance prefix sums P0_i[T] = sum_{t<=T} beta_t L_i[t], P1_i[T] = sum_{t<=T} t beta_t L_i[t]
+// and B0/B1/B2[T] = sum_{t<=T} beta_t {1, t, t^2}.  (The CPU oracle instead rebuilds the loads and
+// recomputes Phi from scratch per candidate; parity between the two is a real check.)
+// For a fixed request only -(N P0_u[T] + P1_u[T]) depends on the target, so each thread scores
+// its requests against every target in U (filters (a)/(b) applied) and keeps the best; a
+// warp-shuffle + shared-memory argmax over requests then picks m* with the key
+// (gain desc, req_id asc, dst asc) (reading A20).  Greedy rounds (reading A21).
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "star_internal.h"
+
+namespace star {
+
+typedef __int128 i128;
+constexpr int kPlanThreads = 1024;
+
+struct PlanArgs {
+  int n, H, max_moves;
+  int32_t theta_num, theta_den;
+  const uint32_t* beta_q;
+  const int64_t* c_mem;
+  const int64_t* reserved;
+  int64_t a_ps, b_ps, c0_ps, c1_ps;
+  uint32_t flags;
+  int world, n_loc, r_cap;
+  int64_t seg_stride;
+  const int64_t* L;
+  const int32_t* r_count;   // nullptr -> every segment holds r_cap requests
+  const int32_t* req_id;
+  const int32_t* inst;
+  const int32_t* n_tok;
+  const int32_t* n_hat;
+  const uint8_t* pinned;
+  star_move* moves;
+  int32_t* n_moves;
+  int32_t* err;
+};
+
+template <typename T>
+__device__ __forceinline__ const T* seg_ptr(const T* base, int k, int64_t stride) {
+  return reinterpret_cast<const T*>(reinterpret_cast<const uint8_t*>(base) + (int64_t)k * stride);
+}
+
+struct Cand {
+  i128 score;
+  int32_t id, dst, g;   // g = flat request slot (k * r_cap + j), -1 = none
+};
+
+__device__ __forceinline__ bool cand_better(const Cand& x, const Cand& y) {  // x strictly better than y
+  if (x.g < 0) return false;
+  if (y.g < 0) return true;
+  if (x.score != y.score) return x.score > y.score;
+  if (x.id != y.id) return x.id < y.id;
+  return x.dst < y.dst;
+}
+
+__device__ __forceinline__ Cand shfl_cand(const Cand& c, int src_lane) {
+  Cand o;
+  const uint64_t lo = (uint64_t)c.score, hi = (uint64_t)(c.score >> 64);
+  const uint64_t lo2 = __shfl_sync(0xFFFFFFFFu, lo, src_lane);
+  const uint64_t hi2 = __shfl_sync(0xFFFFFFFFu, hi, src_lane);
+  o.score = (i128)(((unsigned __int128)hi2 << 64) | lo2);
+  o.id = __shfl_sync(0xFFFFFFFFu, c.id, src_lane);
+  o.dst = __shfl_sync(0xFFFFFFFFu, c.dst, src_lane);
+  o.g = __shfl_sync(0xFFFFFFFFu, c.g, src_lane);
+  return o;
+}
+
+__device__ __forceinline__ Cand warp_argmax(Cand c) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    Cand o = shfl_cand(c, lane ^ off);
+    if (cand_better(o, c)) c = o;
+  }
+  return c;
+}
+
+struct PlanSmem {
+  int64_t* Ls;     // [n][H+1]
+  i128* P0;        // [n][H+1]
+  i128* P1;        // [n][H+1]
+  i128* B;         // [3][H+1]
+  i128* Wv;        // [n]
+  uint8_t* inO;    // [n]
+  uint8_t* inU;    // [n]
+  int* ulist;      // [n]
+  uint32_t* moved; // bitmap [world*r_cap]
+  int* seg_count;  // [world]
+};
+
+__global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  const int n = a.n, H1 = a.H + 1;
+  const bool strict = (a.flags & 1u) != 0;
+  const bool cur_only = (a.flags & 2u) != 0;
+  const int nslots = a.world * a.r_cap;
+  PlanSmem s;
+  {
+    uint8_t* p = smraw;
+    s.P0 = reinterpret_cast<i128*>(p); p += sizeof(i128) * n * H1;
+    s.P1 = reinterpret_cast<i128*>(p); p += sizeof(i128) * n * H1;
+    s.B = reinterpret_cast<i128*>(p); p += sizeof(i128) * 3 * H1;
+    s.Wv = reinterpret_cast<i128*>(p); p += sizeof(i128) * n;
+    s.Ls = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * n * H1;
+    s.moved = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * ((nslots + 31) / 32);
+    s.seg_count = reinterpret_cast<int*>(p); p += sizeof(int) * a.world;
+    s.ulist = reinterpret_cast<int*>(p); p += sizeof(int) * n;
+    s.inO = p; p += n;
+    s.inU = p; p += n;
+  }
+  __shared__ Cand warp_best[kPlanThreads / 32];
+  __shared__ int s_stop, s_nU, s_nmoves;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // ---- load gathered loads (segment k holds instances [k*n_loc, (k+1)*n_loc)) ----
+  for (int e = tid; e < n * H1; e += blockDim.x) {
+    const int i = e / H1, t = e % H1;
+    const int k = i / a.n_loc, il = i % a.n_loc;
+    s.Ls[e] = seg_ptr(a.L, k, a.seg_stride)[(int64_t)il * H1 + t];
+  }
+  for (int w = tid; w < (nslots + 31) / 32; w += blockDim.x) s.moved[w] = 0u;
+  for (int k = tid; k < a.world; k += blockDim.x) {
+    int c = a.r_cap;
+    if (a.r_count) {
+      c = *seg_ptr(a.r_count, k, a.seg_stride);
+      if (c < 0 || c > a.r_cap) {
+        if (a.err) atomicOr(a.err, 16);
+        c = c < 0 ? 0 : a.r_cap;
+      }
+    }
+    s.seg_count[k] = c;
+  }
+  if (tid == 0) {   // B0/B1/B2[T] = sum_{t<=T} beta_t {1, t, t^2} (H+1 terms, serial)
+    i128 b0 = 0, b1 = 0, b2 = 0;
+    for (int u = 0; u < H1; ++u) {
+      const i128 bt = (i128)a.beta_q[u];
+      b0 += bt;
+      b1 += bt * u;
+      b2 += bt * u * u;
+      s.B[u] = b0;
+      s.B[H1 + u] = b1;
+      s.B[2 * H1 + u] = b2;
+    }
+  }
+  if (tid == 0) s_nmoves = 0;
+  __syncthreads();
+
+  for (int round = 0; round < a.max_moves; ++round) {
+    // ---- Phase 1: InstanceClassification ----
+    for (int i = tid; i < n; i += blockDim.x) {
+      i128 w = 0;
+      const int64_t* Li = s.Ls + (int64_t)i * H1;
+      if (cur_only) {
+        w = (i128)a.beta_q[0] * Li[0];
+      } else {
+        for (int t = 1; t < H1; ++t) w += (i128)a.beta_q[t] * Li[t];
+      }
+      s.Wv[i] = w;
+      // prefix sums for Phase 3: P0_i[T] = sum_{t<=T} beta_t L_i[t], P1_i[T] = sum_{t<=T} t beta_t L_i[t]
+      i128 p0 = 0, p1 = 0;
+      for (int t = 0; t < H1; ++t) {
+        const i128 bl = (i128)a.beta_q[t] * Li[t];
+        p0 += bl;
+        p1 += bl * t;
+        s.P0[(int64_t)i * H1 + t] = p0;
+        s.P1[(int64_t)i * H1 + t] = p1;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      i128 wsum = 0;
+      for (int i = 0; i < n; ++i) wsum += s.Wv[i];
+      const i128 rhs = (i128)(a.theta_den + a.theta_num) * wsum;
+      bool anyO = false;
+      for (int i = 0; i < n; ++i) {
+        s.inO[i] = ((i128)n * a.theta_den * s.Wv[i] > rhs) ? 1 : 0;
+        anyO |= s.inO[i] != 0;
+      }
+      int nU = 0;
+      for (int i = 0; i < n; ++i) {
+        const bool u = !s.inO[i] && ((i128)n * a.theta_den * (i128)65536 * s.Ls[(int64_t)i * H1] < rhs);
+        s.inU[i] = u ? 1 : 0;
+        if (u) s.ulist[nU++] = i;
+      }
+      s_nU = nU;
+      s_stop = anyO ? 0 : 1;
+    }
+    __syncthreads();
+    if (s_stop) break;
+
+    // ---- Phase 2 + 3: per-request best target, then block argmax ----
+    Cand best;
+    best.score = 0;
+    best.id = 0;
+    best.dst = 0;
+    best.g = -1;
+    const int nU = s_nU;
+    for (int g = tid; g < nslots; g += blockDim.x) {
+      const int k = g / a.r_cap, j = g % a.r_cap;
+      if (j >= s.seg_count[k]) continue;
+      if ((s.moved[g >> 5] >> (g & 31)) & 1u) continue;
+      const int32_t src = seg_ptr(a.inst, k, a.seg_stride)[j];
+      if (src < 0 || src >= n) {
+        if (a.err) atomicOr(a.err, 1);
+        continue;
+      }
+      if (!s.inO[src]) continue;
+      if (a.pinned && seg_ptr(a.pinned, k, a.seg_stride)[j]) continue;
+      const int64_t N = seg_ptr(a.n_tok, k, a.seg_stride)[j];
+      const int64_t nh = seg_ptr(a.n_hat, k, a.seg_stride)[j];
+      const int32_t rid = seg_ptr(a.req_id, k, a.seg_stride)[j];
+      int T = (int)(nh - 1 < 0 ? 0 : (nh - 1 > a.H ? a.H : nh - 1));
+      if (cur_only) T = 0;
+      const i128 self = (i128)N * N * s.B[T] + (i128)2 * N * s.B[H1 + T] + s.B[2 * H1 + T];
+      const i128 src_part = (i128)N * s.P0[(int64_t)src * H1 + T] + s.P1[(int64_t)src * H1 + T];
+      const i128 mig = (i128)a.c0_ps + (i128)a.c1_ps * N;
+      for (int q = 0; q < nU; ++q) {
+        const int u = s.ulist[q];
+        const int64_t Lu0 = s.Ls[(int64_t)u * H1];
+        if (!cur_only) {  // filter (a): N_hat * T_exec(u) > C_mig(r)
+          if (!((i128)nh * ((i128)a.a_ps + (i128)a.b_ps * Lu0) > mig)) continue;
+        }
+        if (a.c_mem) {    // filter (b): memory safety on the target
+          i128 need = Lu0;
+          if (strict) {
+            if (!cur_only) need += nh;
+          } else {
+            need += (a.reserved ? a.reserved[u] : 0) + N + (cur_only ? 0 : nh);
+          }
+          if (!(need <= (i128)a.c_mem[u])) continue;
+        }
+        const i128 score = src_part - ((i128)N * s.P0[(int64_t)u * H1 + T] + s.P1[(int64_t)u * H1 + T]) - self;
+        if (score <= 0) continue;
+        Cand c;
+        c.score = score;
+        c.id = rid;
+        c.dst = u;
+        c.g = g;
+        if (cand_better(c, best)) best = c;
+      }
+    }
+    best = warp_argmax(best);
+    if (lane == 0) warp_best[warp] = best;
+    __syncthreads();
+    if (warp == 0) {
+      Cand c;
+      if (lane < (int)(blockDim.x >> 5)) {
+        c = warp_best[lane];
+      } else {
+        c.score = 0; c.id = 0; c.dst = 0; c.g = -1;
+      }
+      c = warp_argmax(c);
+      if (lane == 0) {
+        if (c.g < 0) {
+          s_stop = 1;
+        } else {
+          // ExecuteMigration is out of the path: apply m* to the loads for the next round.
+          const int k = c.g / a.r_cap, j = c.g % a.r_cap;
+          const int src = seg_ptr(a.inst, k, a.seg_stride)[j];
+          const int64_t N = seg_ptr(a.n_tok, k, a.seg_stride)[j];
+          const int64_t nh = seg_ptr(a.n_hat, k, a.seg_stride)[j];
+          for (int t = 0; t < H1; ++t) {
+            const int64_t ct = (t == 0) ? N : (t < nh ? N + t : 0);
+            s.Ls[(int64_t)src * H1 + t] -= ct;
+            s.Ls[(int64_t)c.dst * H1 + t] += ct;
+          }
+          s.moved[c.g >> 5] |= 1u << (c.g & 31);
+          const i128 gain = (i128)2 * n * c.score;
+          star_move mv;
+          mv.req_id = c.id;
+          mv.src = src;
+          mv.dst = c.dst;
+          mv.round = round;
+          mv.gain_hi = (int64_t)(gain >> 64);
+          mv.gain_lo = (uint64_t)gain;
+          a.moves[s_nmoves] = mv;
+          s_nmoves = s_nmoves + 1;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;
+  }
+  if (tid == 0) *a.n_moves = s_nmoves;
+}
+
+size_t plan_smem_bytes(int n, int H, int world, int r_cap) {
+  const size_t H1 = (size_t)H + 1, nn = (size_t)n;
+  size_t b = 16 * nn * H1 * 2 + 16 * 3 * H1 + 16 * nn + 8 * nn * H1;
+  b += 4 * (((size_t)world * r_cap + 31) / 32) + 4 * (size_t)world + 4 * nn + 2 * nn;
+  return (b + 15) & ~size_t(15);
+}
+
+cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg, star_move* moves, int32_t* n_moves,
+                        int32_t* err_flag, cudaStream_t stream) {
+  PlanArgs a{};
+  a.n = p->n_inst;
+  a.H = p->H;
+  a.max_moves = p->max_moves;
+  a.theta_num = p->theta_num;
+  a.theta_den = p->theta_den;
+  a.beta_q = p->beta_q;
+  a.c_mem = p->c_mem;
+  a.reserved = p->reserved;
+  a.a_ps = p->t_exec_a_ps;
+  a.b_ps = p->t_exec_b_ps;
+  a.c0_ps = p->mig_c0_ps;
+  a.c1_ps = p->mig_c1_ps;
+  a.flags = p->flags;
+  a.world = sg->world;
+  a.n_loc = sg->n_loc;
+  a.r_cap = sg->r_cap;
+  a.seg_stride = sg->seg_stride;
+  a.L = sg->L;
+  a.r_count = sg->r_count;
+  a.req_id = sg->req_id;
+  a.inst = sg->inst;
+  a.n_tok = sg->n_tok;
+  a.n_hat = sg->n_hat;
+  a.pinned = sg->pinned;
+  a.moves = moves;
+  a.n_moves = n_moves;
+  a.err = err_flag;
+  const size_t smem = plan_smem_bytes(a.n, a.H, a.world, a.r_cap);
+  static int attr_bytes = 48 * 1024;
+  if ((int)smem > attr_bytes) {
+    cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_bytes = (int)smem;
+  }
+  plan_kernel<<<1, kPlanThreads, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace star

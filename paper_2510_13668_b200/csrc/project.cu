@@ -1,0 +1,264 @@
+// project.cu -- worker-side local future-state simulation:
+//   L_i[0] = sum_{r in B_i} N(r)                        current token load
+//   L_i[t] = sum_{r in B_i, t < N_hat_r} (N(r) + t)     predicted load N_hat_i(B_{i,t})
+//   W_i = sum_{t=1}^{H} beta_t L_i[t]  (w_i, Alg. 1 line 13), peak_i, growth_i, count_i
+//
+// Design (B200): the per-request work is a keyed histogram, not an O(R*H) loop.  A request
+// with b = min(N_hat, H+1) is resident exactly for t in [1, b) (and always at t = 0), so with
+// per-(instance, b) counts C and token sums S:
+//   L_i[t] = sum_{b > t} (S_i[b] + t * C_i[b])   (t >= 1),   L_i[0] = sum_b S_i[b]
+//   growth_i = sum_b C_i[b] * min(b, H)
+// Pass 1 streams (inst, N, N_hat) with coalesced 16-byte loads (4 requests / thread / load),
+// aggregates equal keys inside each warp (__match_any_sync + __reduce_add_sync; the hot bin
+// b = H+1 holds ~78% of a long-tailed CoT batch), and adds into a shared-memory histogram.
+// Multi-CTA grids merge through a global workspace; the last CTA to arrive finalises and
+// re-zeroes the workspace.  Pass 2 (one CTA) is a suffix scan per instance.
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "star_internal.h"
+
+namespace star {
+
+constexpr int kProjThreads = 512;
+constexpr int kProjMaxSmemBins = 12288;   // n_inst*(H+2) handled in shared memory
+
+struct ProjArgs {
+  int R, n_inst, inst_base, H;
+  const int32_t* inst;
+  const int32_t* n_tok;
+  const int32_t* n_hat;
+  const uint32_t* beta_q;
+  int64_t* L;
+  int64_t* W;
+  int64_t* peak;
+  int64_t* growth;
+  int32_t* count;
+  uint32_t* ws_cnt;                // [nb]
+  unsigned long long* ws_sum;      // [nb]
+  unsigned int* ws_arrive;         // [1]
+  int32_t* err;
+  int vec_ok;                      // all three arrays 16-byte aligned
+};
+
+__device__ __forceinline__ int4 ld_stream_int4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// One request per lane; all 32 lanes of the warp must call this (valid may be false).
+__device__ __forceinline__ void proj_accumulate(const ProjArgs& a, bool valid, int32_t inst, int32_t ntok,
+                                                int32_t nhat, uint32_t* scnt, unsigned long long* ssum,
+                                                uint32_t& errbits) {
+  const int i = inst - a.inst_base;
+  bool ok = valid;
+  if (valid) {
+    if (i < 0 || i >= a.n_inst) { errbits |= 1u; ok = false; }
+    if (ntok < 1 || ntok > (1 << 17)) { errbits |= 2u; ok = false; }
+    if (nhat < 0) { errbits |= 4u; ok = false; }
+  }
+  const int b = nhat > a.H + 1 ? a.H + 1 : nhat;
+  const uint32_t key = ok ? (uint32_t)(i * (a.H + 2) + b) : 0xFFFFFFFFu;
+  const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
+  const uint32_t s = __reduce_add_sync(peers, ok ? (uint32_t)ntok : 0u);   // 32 * 2^17 < 2^32
+  const int leader = __ffs(peers) - 1;
+  if (ok && (int)(threadIdx.x & 31) == leader) {
+    atomicAdd(scnt + key, (uint32_t)__popc(peers));
+    atomicAdd(ssum + key, (unsigned long long)s);
+  }
+}
+
+__device__ void proj_finalize(const ProjArgs& a, const uint32_t* cnt, const unsigned long long* sum) {
+  const int HB = a.H + 2;
+  for (int i = threadIdx.x; i < a.n_inst; i += blockDim.x) {
+    const uint32_t* c = cnt + i * HB;
+    const unsigned long long* s = sum + i * HB;
+    int64_t* Li = a.L + (int64_t)i * (a.H + 1);
+    int64_t L0 = 0, cnt_all = 0, grow = 0;
+    for (int b = 0; b < HB; ++b) {
+      L0 += (int64_t)s[b];
+      cnt_all += c[b];
+      grow += (int64_t)c[b] * (b < a.H ? b : a.H);
+    }
+    Li[0] = L0;
+    int64_t peak = L0, w = 0, cge = 0, sge = 0;
+    for (int t = a.H; t >= 1; --t) {
+      cge += c[t + 1];
+      sge += (int64_t)s[t + 1];
+      const int64_t lt = sge + (int64_t)t * cge;
+      Li[t] = lt;
+      w += (int64_t)a.beta_q[t] * lt;
+      peak = lt > peak ? lt : peak;
+    }
+    if (a.W) a.W[i] = w;
+    if (a.peak) a.peak[i] = peak;
+    if (a.growth) a.growth[i] = grow;
+    if (a.count) a.count[i] = (int32_t)cnt_all;
+    if (cnt_all > 65536 && a.err) atomicOr(a.err, 8);
+  }
+}
+
+// SMEM_BINS: histogram lives in shared memory (else directly in the global workspace).
+template <bool SMEM_BINS>
+__global__ void __launch_bounds__(kProjThreads) project_kernel(const ProjArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int nb = a.n_inst * (a.H + 2);
+  unsigned long long* ssum;
+  uint32_t* scnt;
+  if (SMEM_BINS) {
+    ssum = reinterpret_cast<unsigned long long*>(sm);
+    scnt = reinterpret_cast<uint32_t*>(ssum + nb);
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+      ssum[k] = 0;
+      scnt[k] = 0;
+    }
+    __syncthreads();
+  } else {
+    ssum = a.ws_sum;
+    scnt = a.ws_cnt;
+  }
+  __shared__ int s_last;
+  uint32_t errbits = 0;
+  const int lane = threadIdx.x & 31;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int64_t done = 0;
+  if (a.vec_ok) {
+    const int64_t nvec = a.R / 4;
+    const int4* vi = reinterpret_cast<const int4*>(a.inst);
+    const int4* vn = reinterpret_cast<const int4*>(a.n_tok);
+    const int4* vh = reinterpret_cast<const int4*>(a.n_hat);
+    for (int64_t base = (int64_t)warp_global * 32; base < nvec; base += (int64_t)nwarps * 32) {
+      const int64_t g = base + lane;
+      const bool valid = g < nvec;
+      int4 x = make_int4(0, 0, 0, 0), n = x, h = x;
+      if (valid) {
+        x = ld_stream_int4(vi + g);
+        n = ld_stream_int4(vn + g);
+        h = ld_stream_int4(vh + g);
+      }
+      proj_accumulate(a, valid, x.x, n.x, h.x, scnt, ssum, errbits);
+      proj_accumulate(a, valid, x.y, n.y, h.y, scnt, ssum, errbits);
+      proj_accumulate(a, valid, x.z, n.z, h.z, scnt, ssum, errbits);
+      proj_accumulate(a, valid, x.w, n.w, h.w, scnt, ssum, errbits);
+    }
+    done = nvec * 4;
+  }
+  for (int64_t base = done + (int64_t)warp_global * 32; base < a.R; base += (int64_t)nwarps * 32) {
+    const int64_t r = base + lane;
+    const bool valid = r < a.R;
+    proj_accumulate(a, valid, valid ? a.inst[r] : 0, valid ? a.n_tok[r] : 0, valid ? a.n_hat[r] : 0, scnt, ssum,
+                    errbits);
+  }
+  if (errbits && a.err) atomicOr(a.err, (int)errbits);
+  __syncthreads();
+
+  if (gridDim.x == 1) {
+    proj_finalize(a, scnt, ssum);
+    if (!SMEM_BINS) {  // leave the workspace zeroed
+      __syncthreads();
+      for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+        a.ws_sum[k] = 0;
+        a.ws_cnt[k] = 0;
+      }
+    }
+    return;
+  }
+  if (SMEM_BINS) {
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+      if (scnt[k]) {
+        atomicAdd(a.ws_cnt + k, scnt[k]);
+        atomicAdd(a.ws_sum + k, ssum[k]);
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(a.ws_arrive, 1u) == gridDim.x - 1) ? 1 : 0;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (SMEM_BINS) {
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+      scnt[k] = __ldcg(a.ws_cnt + k);
+      ssum[k] = __ldcg(a.ws_sum + k);
+      a.ws_cnt[k] = 0;
+      a.ws_sum[k] = 0;
+    }
+    __syncthreads();
+    proj_finalize(a, scnt, ssum);
+  } else {
+    proj_finalize(a, a.ws_cnt, a.ws_sum);
+    __syncthreads();
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+      a.ws_sum[k] = 0;
+      a.ws_cnt[k] = 0;
+    }
+  }
+  if (threadIdx.x == 0) *a.ws_arrive = 0;
+}
+
+size_t project_workspace_bytes(int n_inst, int H) {
+  const size_t nb = (size_t)n_inst * (size_t)(H + 2);
+  return nb * 8 + nb * 4 + 16;
+}
+
+int project_single_cta_max_rows() { return 1 << 15; }
+
+cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_t* inst, const int32_t* n_tok,
+                           const int32_t* n_hat, const uint32_t* beta_q, int64_t* L, int64_t* W, int64_t* peak,
+                           int64_t* growth, int32_t* count, void* workspace, int32_t* err_flag,
+                           cudaStream_t stream, int* grid_out) {
+  ProjArgs a{};
+  a.R = R;
+  a.n_inst = n_inst;
+  a.inst_base = inst_base;
+  a.H = H;
+  a.inst = inst;
+  a.n_tok = n_tok;
+  a.n_hat = n_hat;
+  a.beta_q = beta_q;
+  a.L = L;
+  a.W = W;
+  a.peak = peak;
+  a.growth = growth;
+  a.count = count;
+  a.err = err_flag;
+  const size_t nb = (size_t)n_inst * (size_t)(H + 2);
+  if (workspace) {
+    a.ws_sum = reinterpret_cast<unsigned long long*>(workspace);
+    a.ws_cnt = reinterpret_cast<uint32_t*>(a.ws_sum + nb);
+    a.ws_arrive = reinterpret_cast<unsigned int*>(reinterpret_cast<uint8_t*>(workspace) + nb * 12);
+  }
+  a.vec_ok = ((reinterpret_cast<uintptr_t>(inst) | reinterpret_cast<uintptr_t>(n_tok) |
+               reinterpret_cast<uintptr_t>(n_hat)) & 15u) == 0;
+  const bool smem_bins = nb <= (size_t)kProjMaxSmemBins;
+  int grid = 1;
+  if (workspace && R > project_single_cta_max_rows() / 8) {
+    const int64_t per_cta = (int64_t)kProjThreads * 16;   // 4 vec loads of 4 requests per thread
+    grid = (int)((R + per_cta - 1) / per_cta);
+    const int max_grid = g_num_sms * (smem_bins ? 2 : 4);
+    if (grid > max_grid) grid = max_grid;
+    if (grid < 1) grid = 1;
+  }
+  if (!smem_bins && !workspace) return cudaErrorInvalidValue;
+  if (grid_out) *grid_out = grid;
+  const size_t smem = smem_bins ? nb * 12 : 0;
+  if (smem_bins) {
+    static int attr_bytes = 48 * 1024;
+    if ((int)smem > attr_bytes) {
+      cudaError_t e = cudaFuncSetAttribute(project_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      attr_bytes = (int)smem;
+    }
+    project_kernel<true><<<grid, kProjThreads, smem, stream>>>(a);
+  } else {
+    project_kernel<false><<<grid, kProjThreads, 0, stream>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace star

@@ -1,0 +1,26 @@
+// star_internal.h -- declarations shared by the product's CUDA translation units.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/star.h"
+
+namespace star {
+
+constexpr int kMaxSmemBytes = 227 * 1024;
+extern int g_num_sms;   // set once by ensure_device()
+
+// project.cu
+size_t project_workspace_bytes(int n_inst, int H);
+int project_single_cta_max_rows();
+cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_t* inst, const int32_t* n_tok,
+                           const int32_t* n_hat, const uint32_t* beta_q, int64_t* L, int64_t* W, int64_t* peak,
+                           int64_t* growth, int32_t* count, void* workspace, int32_t* err_flag,
+                           cudaStream_t stream, int* grid_out);
+
+// plan.cu
+size_t plan_smem_bytes(int n, int H, int world, int r_cap);
+cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg, star_move* moves, int32_t* n_moves,
+                        int32_t* err_flag, cudaStream_t stream);
+
+}  // namespace star

@@ -1,0 +1,252 @@
+"""GPU parity tests (`-m gpu`, B200 only): the CUDA path, called through the C ABI, against
+the CPU oracle on the same seeded inputs.  Bars (BASELINE.json north_star):
+  * predictor: max_r |y_gpu - y_ref| / max(|y_ref|, 1) <= 1e-3 (fp32) / 2e-2 (bf16)  (reading A7)
+  * quantizer, projected loads, plans: bit-exact (plans on the oracle's N_hat)."""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": 1e-3, "bf16": 2e-2}
+
+
+@pytest.fixture(scope="module")
+def star():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_2510_13668_b200 as star
+    star.version()   # loads libstar.so; raises if missing
+    return star
+
+
+def _dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def _weights_dev(pw, biases=False):
+    tdt = torch.bfloat16 if pw.dtype == "bf16" else torch.float32
+    W = [_dev(pw.W1, tdt), _dev(pw.W2, tdt), _dev(pw.W3, tdt), _dev(pw.w4)]
+    b = [None] * 4
+    if biases:
+        b = [_dev(pw.b1), _dev(pw.b2), _dev(pw.b3), _dev(np.array([pw.b4], np.float32))]
+    return W, b
+
+
+def _rel_err(y, ref):
+    return float(np.max(np.abs(y.astype(np.float64) - ref) / np.maximum(np.abs(ref), 1.0)))
+
+
+# ============================================================================ quantizer
+def test_quantizer_bitexact(star, oracle_mod):
+    g = datagen.rng(1)
+    y = np.concatenate([g.normal(3000, 8000, 5000).astype(np.float32),
+                        np.array([2.5, 3.5, -0.4, np.nan, np.inf, -np.inf, 32767.5, 1e30, -0.0, 0.5],
+                                 np.float32)])
+    y[:200] = np.round(y[:200]) + 0.5   # exact halves
+    n_tok = g.integers(1, 40000, y.shape[0]).astype(np.int32)
+    for nt in (None, n_tok):
+        ref = oracle_mod.quantize(y, nt)
+        got = star.lenpred_quantize(_dev(y), None if nt is None else _dev(nt)).cpu().numpy()
+        assert np.array_equal(got, ref)
+
+
+# ============================================================================ projection
+@pytest.mark.parametrize("seed,n,R,H", [(0, 1, 0, 50), (1, 1, 1, 50), (2, 8, 2048, 50), (3, 8, 4096, 50),
+                                       (4, 3, 1001, 7), (5, 5, 333, 0), (6, 64, 12345, 50), (7, 2, 77, 256),
+                                       (8, 8, 300_000, 50), (9, 300, 50_000, 50)])
+def test_projection_bitexact(star, oracle_mod, seed, n, R, H):
+    snap = datagen.make_snapshot(seed, n, max(R // n, 1))
+    g = datagen.rng(seed)
+    if R != snap.R:
+        idx = g.integers(0, snap.R, R) if snap.R else np.zeros(0, np.int64)
+        inst, n_tok, n_hat = snap.inst[idx], snap.n_tok[idx], snap.true_rem[idx]
+    else:
+        inst, n_tok, n_hat = snap.inst, snap.n_tok, snap.true_rem
+    n_hat = np.where(g.random(R) < 0.2, g.integers(0, H + 3, R), n_hat).astype(np.int32)
+    beta = datagen.beta_schedule_q16(H)
+    ref = oracle_mod.project(inst, n_tok, n_hat, n, H, beta)
+    ws = torch.zeros(star.project_workspace_bytes(n, H), dtype=torch.uint8, device="cuda")
+    for use_ws in (False, True) if n * (H + 2) <= 12288 else (True,):
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        out = star.project_instance_load(_dev(inst.astype(np.int32)), _dev(n_tok), _dev(n_hat), n, H,
+                                         _dev(beta.astype(np.int32)), workspace=ws if use_ws else None,
+                                         err_flag=err)
+        torch.cuda.synchronize()
+        assert err.item() == 0
+        assert np.array_equal(out.L.cpu().numpy(), ref["L"])
+        for k in ("W", "peak", "growth", "count"):
+            assert np.array_equal(getattr(out, k).cpu().numpy(), ref[k]), k
+    assert int(ws.sum().item()) == 0   # workspace left zeroed
+
+
+def test_projection_inst_base_and_errors(star, oracle_mod):
+    inst = np.array([4, 5, 4, 9, 5], np.int32)
+    n_tok = np.array([3, 4, 5, 6, 0], np.int32)   # inst 9 out of range, N=0 invalid
+    n_hat = np.array([9, 9, 9, 9, 9], np.int32)
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    beta = datagen.beta_schedule_q16(2).astype(np.int32)
+    out = star.project_instance_load(_dev(inst), _dev(n_tok), _dev(n_hat), 2, 2, _dev(beta), inst_base=4,
+                                     err_flag=err)
+    torch.cuda.synchronize()
+    assert out.L.cpu().numpy().tolist() == [[8, 10, 12], [4, 5, 6]]   # invalid rows ignored
+    assert err.item() & 1 and err.item() & 2
+
+
+# ============================================================================ plan
+def _plan_gpu(star, params_h, L, snap, n_hat):
+    pp = star.PlanParams.from_host(params_h)
+    moves, nm = star.plan_reschedule(pp, _dev(L), _dev(snap.req_id), _dev(snap.inst), _dev(snap.n_tok),
+                                     _dev(n_hat.astype(np.int32)), _dev(snap.pinned))
+    torch.cuda.synchronize()
+    return star.decode_moves(moves, nm)
+
+
+@pytest.mark.parametrize("seed", range(240))
+def test_plan_bitexact_tiny(star, oracle_mod, seed):
+    g = datagen.rng(seed)
+    n, R, H = int(g.integers(1, 7)), int(g.integers(0, 30)), int(g.integers(0, 9))
+    snap, n_hat, params = datagen.tiny_fixture(3000 + seed, n, R, H)
+    if seed % 5 == 0 and R >= 2:
+        snap.n_tok[1], n_hat[1], snap.inst[1] = snap.n_tok[0], n_hat[0], snap.inst[0]
+        snap.pinned[:2] = 0
+    params.max_moves = int(g.integers(0, 6))
+    L = oracle_mod.project(snap.inst, snap.n_tok, n_hat, n, H, params.beta_q)["L"]
+    ref = oracle_mod.plan(params, L, snap.req_id, snap.inst, snap.n_tok, n_hat, snap.pinned)
+    assert _plan_gpu(star, params, L, snap, n_hat) == ref
+
+
+@pytest.mark.parametrize("cfg,seed,flags", [("C1", 0, 0), ("C2", 1, 0), ("C3", 2, 0), ("C4", 3, 0), ("TGT", 4, 0),
+                                            ("C2", 5, 1), ("C4", 6, 2), ("C4", 7, 3)])
+def test_plan_bitexact_full_configs(star, oracle_mod, cfg, seed, flags):
+    c = datagen.CONFIGS[cfg]
+    snap = datagen.make_snapshot(seed, c["n_inst"], c["r_per_inst"], skewed=c.get("skewed", False),
+                                 pinned_frac=0.05)
+    n_hat = snap.true_rem.copy()   # STAR-Oracle predictions (north-star parity rule)
+    params = datagen.make_plan_params(snap, mem_factor=c.get("mem_factor", 1.10), max_moves=max(c["max_moves"], 4),
+                                      flags=flags, reserved_seed=seed)
+    L = oracle_mod.project(snap.inst, snap.n_tok, n_hat, snap.n_inst, params.H, params.beta_q)["L"]
+    ref = oracle_mod.plan(params, L, snap.req_id, snap.inst, snap.n_tok, n_hat, snap.pinned)
+    assert _plan_gpu(star, params, L, snap, n_hat) == ref
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_plan_segmented_equals_contiguous(star, oracle_mod, world):
+    """c9: the plan over gathered per-rank records equals the plan on the concatenated state."""
+    n_loc, r_per = 8 // world, 96
+    snap = datagen.make_snapshot(11, 8, r_per)
+    n_hat = snap.true_rem.astype(np.int32)
+    params = datagen.make_plan_params(snap, max_moves=4)
+    H = params.H
+    order = np.argsort(snap.inst, kind="stable")   # group requests by owning rank
+    inst, n_tok, ids, pin, nh = (a[order] for a in (snap.inst, snap.n_tok, snap.req_id, snap.pinned, n_hat))
+    L = oracle_mod.project(inst, n_tok, nh, 8, H, params.beta_q)["L"]
+    ref = oracle_mod.plan(params, L, ids, inst, n_tok, nh, pin)
+    # build a [world][record] buffer: L block | count | req_id | inst | n_tok | n_hat | pinned
+    r_cap = r_per * n_loc + 5
+    rec_i64 = n_loc * (H + 1) + 1 + (4 * r_cap + (r_cap + 7) // 8 * 2 + 1) // 2 + 1
+    buf = np.zeros((world, rec_i64), np.int64)
+    offs = {}
+    for k in range(world):
+        sel = (inst >= k * n_loc) & (inst < (k + 1) * n_loc)
+        cnt = int(sel.sum())
+        rec = buf[k].view(np.uint8)
+        o = 0
+        rec[o:o + 8 * n_loc * (H + 1)] = L[k * n_loc:(k + 1) * n_loc].reshape(-1).view(np.uint8); offs["L"] = o
+        o += 8 * n_loc * (H + 1)
+        rec[o:o + 4] = np.array([cnt], np.int32).view(np.uint8); offs["cnt"] = o; o += 8
+        for name, arr in (("id", ids), ("inst", inst), ("ntok", n_tok), ("nhat", nh)):
+            v = np.zeros(r_cap, np.int32)
+            v[:cnt] = arr[sel]
+            rec[o:o + 4 * r_cap] = v.view(np.uint8); offs[name] = o; o += 4 * r_cap
+        v = np.zeros(r_cap, np.uint8)
+        v[:cnt] = pin[sel]
+        rec[o:o + r_cap] = v; offs["pin"] = o
+    d = _dev(buf)
+    base = d.data_ptr()
+    seg = star._lib.PlanSegmentsC(world, n_loc, r_cap, rec_i64 * 8, base + offs["L"], base + offs["cnt"],
+                                  base + offs["id"], base + offs["inst"], base + offs["ntok"], base + offs["nhat"],
+                                  base + offs["pin"])
+    pp = star.PlanParams.from_host(params)
+    moves, nm = star.plan_reschedule_segmented(pp, seg)
+    torch.cuda.synchronize()
+    assert star.decode_moves(moves, nm) == ref
+
+
+# ============================================================================ predictor
+def _predict(star, pw, h, biases=False, n_tok=None, max_rows=None):
+    W, b = _weights_dev(pw, biases)
+    pred = star.Predictor(*W, *b, max_rows=max_rows or max(h.shape[0], 1))
+    tdt = torch.bfloat16 if pw.dtype == "bf16" else torch.float32
+    y, nh = star.lenpred_forward(pred, _dev(h, tdt), None if n_tok is None else _dev(n_tok))
+    torch.cuda.synchronize()
+    return pred, y.cpu().numpy(), nh.cpu().numpy()
+
+
+@pytest.mark.parametrize("d,dtype,R,biases", [(896, "f32", 128, False), (896, "f32", 333, True),
+                                              (4096, "bf16", 300, False), (4096, "bf16", 129, True),
+                                              (5120, "bf16", 257, False), (1024, "bf16", 1, False),
+                                              (896, "bf16", 640, False)])
+def test_predictor_parity(star, oracle_mod, d, dtype, R, biases):
+    pw = datagen.make_predictor_weights(d, d, dtype, biases=biases)
+    h = datagen.make_hidden(d + 1, R, d, dtype)
+    n_tok = datagen.make_snapshot(d, 1, R).n_tok
+    _, y, nh = _predict(star, pw, h, biases, n_tok)
+    ref = oracle_mod.lenpred_weights(h, pw)
+    err = _rel_err(y, ref)
+    assert err <= TOL[dtype], f"max rel err {err:.3e}"
+    # the forward's quantizer equals the oracle quantizer on the GPU's own fp32 y_hat
+    assert np.array_equal(nh, oracle_mod.quantize(y, n_tok))
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "TGT"])
+def test_predictor_full_size_sampled(star, oracle_mod, cfg):
+    """Full BASELINE sizes in the bench's launch configuration, checked on sampled rows."""
+    c = datagen.CONFIGS[cfg]
+    R = c["n_inst"] * c["r_per_inst"]
+    pw = datagen.make_predictor_weights(0, c["d"], c["dtype"])
+    h = datagen.make_hidden(0, R, c["d"], c["dtype"])
+    _, y, _ = _predict(star, pw, h)
+    rows = np.unique(np.concatenate([datagen.rng(1).integers(0, R, 48), [0, R - 1]]))
+    ref = oracle_mod.lenpred_weights(h[rows], pw)
+    assert _rel_err(y[rows], ref) <= TOL[c["dtype"]]
+
+
+def test_predictor_homogeneity_bitexact(star):
+    """Pin (ii): bias-free Eq. 2 is positively homogeneous; scaling h by 2 scales every
+    product, partial sum and bf16 rounding by 2, so y(2h) == 2 y(h) bit for bit."""
+    pw = datagen.make_predictor_weights(3, 4096, "bf16")
+    h = datagen.make_hidden(3, 700, 4096, "bf16")
+    pred, y1, _ = _predict(star, pw, h, max_rows=700)
+    y2, _ = star.lenpred_forward(pred, _dev(h * 2, torch.bfloat16))
+    assert np.array_equal(y2.cpu().numpy(), 2 * y1)
+
+
+def test_predictor_deterministic_and_row_independent(star):
+    pw = datagen.make_predictor_weights(4, 4096, "bf16")
+    h = datagen.make_hidden(4, 512, 4096, "bf16")
+    pred, y1, _ = _predict(star, pw, h, max_rows=512)
+    y2, _ = star.lenpred_forward(pred, _dev(h, torch.bfloat16))
+    assert np.array_equal(y2.cpu().numpy(), y1)                      # run-to-run (fixed-order split-K)
+    perm = datagen.rng(0).permutation(512)
+    y3, _ = star.lenpred_forward(pred, _dev(h[perm], torch.bfloat16))
+    np.testing.assert_allclose(y3.cpu().numpy(), y1[perm], rtol=1e-5)  # rows independent
+
+
+def test_fused_step_projection_equals_oracle(star, oracle_mod):
+    """Fused = standalone: the projection of the GPU predictor's own N_hat equals the oracle
+    projection of that N_hat bit for bit (c3 pin)."""
+    c = datagen.CONFIGS["C2"]
+    snap = datagen.make_snapshot(5, c["n_inst"], c["r_per_inst"])
+    pw = datagen.make_predictor_weights(5, c["d"], "bf16")
+    h = datagen.make_hidden(5, snap.R, c["d"], "bf16")
+    _, _, nh = _predict(star, pw, h, n_tok=snap.n_tok)
+    beta = datagen.beta_schedule_q16(50)
+    out = star.project_instance_load(_dev(snap.inst), _dev(snap.n_tok), _dev(nh), c["n_inst"], 50,
+                                     _dev(beta.astype(np.int32)))
+    ref = oracle_mod.project(snap.inst, snap.n_tok, nh, c["n_inst"], 50, beta)
+    assert np.array_equal(out.L.cpu().numpy(), ref["L"])
