@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""bench.py -- requests predicted+planned per second for the STAR hot path on B200.
+
+One "step" = one pass of the whole hot path over one batch of synthetic
+input: Eq. 2 predictor on every running request's hidden state -> integer projection of the
+per-instance loads -> (NCCL all-gather of the per-rank records when N > 1) -> Alg. 1 plan.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config C2] [--impl star|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+Defaults: N=1, workload BASELINE.json configs[1] ("C2": 8 instances x 256 requests, hidden 4096,
+bf16, long-tailed CoT lengths).  Sharding: the 8 instances are split in contiguous blocks over
+the N ranks (strong scaling: total work fixed).  The step is captured in one CUDA graph; L2 is
+flushed (256 MB write) before every timed step, outside the timed span; each step is timed with
+CUDA events on its stream; the reported time is the max over ranks.  Prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "requests predicted+planned/sec and µs per decode step at 1/2/4/8 B200"
+UNIT = "requests/s"
+CONFIG_ORDER = ["C1", "C2", "C3", "C4", "TGT"]
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["star", "reference"], default="star")
+    ap.add_argument("--config", default="C2", choices=CONFIG_ORDER)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU budget of the cpu_baseline sample")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu: no clocks/e2e/cpu legs")
+    ap.add_argument("--json-out", default=None)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return dict(hbm_gbs=d["hbm_gbs"], bf16_tflops=d["bf16_tflops"],
+                    bf16_tflops_sustained=d.get("bf16_tflops_sustained"), source="MEASURED_PEAKS.json")
+    return dict(hbm_gbs=6650.0, bf16_tflops=1590.0, bf16_tflops_sustained=1400.0,
+                source="fallback (B200_PROFILING.md)")
+
+
+# ------------------------------------------------------------------------------ workload
+def make_workload(cfg_name, world, rank, seed):
+    import datagen
+    from paper_2510_13668_b200.step import split_snapshot_by_rank
+    c = datagen.CONFIGS[cfg_name]
+    n_inst, r_per = c["n_inst"], c["r_per_inst"]
+    if n_inst % world:
+        raise SystemExit(f"config {cfg_name} has {n_inst} instances; --gpus {world} must divide it")
+    snap = datagen.make_snapshot(seed, n_inst, r_per, skewed=c.get("skewed", False))
+    params = datagen.make_plan_params(snap, H=50, mem_factor=c.get("mem_factor", 1.10), max_moves=c["max_moves"])
+    idx = split_snapshot_by_rank(snap.inst, n_inst, world, rank)
+    pw = datagen.make_predictor_weights(seed, c["d"], c["dtype"])
+    h = datagen.make_hidden(seed * 1000 + rank, len(idx), c["d"], c["dtype"])
+    return c, snap, params, idx, pw, h
+
+
+def config_block(cfg_name, c, world, graph, flush):
+    return {"workload": f"{cfg_name}: {c['desc']}", "n_inst": c["n_inst"], "requests_per_instance": c["r_per_inst"],
+            "total_requests": c["n_inst"] * c["r_per_inst"], "hidden": c["d"], "m1_m2_m3": [2048, 512, 64],
+            "H": 50, "max_moves": c["max_moves"], "instances_per_gpu": c["n_inst"] // world,
+            "parallelism": f"instance-sharded x{world} (one NCCL all-gather of per-rank records)",
+            "l2": "flushed before every timed step (256 MB write, outside the timed span)" if flush else "warm",
+            "cuda_graph": graph, "n_hat_source": "GPU predictor (hidden rows scaled so predictions are long-tailed)"}
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, dev_index):
+        self.samples, self.reasons, self.stop_ev = [], 0, threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+
+    def stop(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self.stop_ev.set()
+        self.t.join()
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": float(self.max_mhz), "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------ oracle timing
+def oracle_step_sample(snap, params, idx_all, pw, h_rows, nthreads):
+    """Times the oracle (as it stands) on: predictor over the given hidden rows, projection and
+    plan over the whole snapshot.  Returns (t_pred, n_rows, t_proj, t_plan)."""
+    import oracle
+    t0 = time.perf_counter()
+    oracle.lenpred_weights(h_rows, pw, nthreads=nthreads)
+    t1 = time.perf_counter()
+    n_hat = snap.true_rem
+    P = oracle.project(snap.inst, snap.n_tok, n_hat, snap.n_inst, params.H, params.beta_q)
+    t2 = time.perf_counter()
+    oracle.plan(params, P["L"], snap.req_id, snap.inst, snap.n_tok, n_hat, snap.pinned)
+    t3 = time.perf_counter()
+    return t1 - t0, h_rows.shape[0], t2 - t1, t3 - t2
+
+
+def cpu_baseline(cfg_name, seed, budget_s):
+    import datagen
+    c, snap, params, idx, pw, _ = make_workload(cfg_name, 1, 0, seed)
+    R_total = snap.R
+    cores = os.cpu_count() or 1
+    h1 = datagen.make_hidden(seed + 99, 1, c["d"], c["dtype"])
+    tp, _, _, _ = oracle_step_sample(snap, params, idx, pw, h1, cores)   # calibration
+    rows = int(max(cores, min(R_total, budget_s / max(tp, 1e-4) * 0.8)))
+    rows = max(1, min(rows, R_total))
+    h = datagen.make_hidden(seed + 98, rows, c["d"], c["dtype"])
+    t_pred, n_rows, t_proj, t_plan = oracle_step_sample(snap, params, idx, pw, h, cores)
+    t_step = t_pred * (R_total / n_rows) + t_proj + t_plan
+    return {"value": R_total / t_step, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": (f"oracle predictor (fp64 loops, OpenMP {cores} threads) on {n_rows} of {R_total} hidden rows "
+                       f"({t_pred:.2f} s, extrapolated linearly); projection ({t_proj * 1e3:.1f} ms) and plan "
+                       f"({t_plan * 1e3:.1f} ms) single-threaded on the full snapshot"),
+            "s_per_step_extrapolated": t_step}
+
+
+# ------------------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    import datagen
+    import oracle
+    oracle.build()
+    c, snap, params, idx, pw, _ = make_workload(args.config, 1, 0, args.seed)
+    R_total = snap.R
+    cores = os.cpu_count() or 1
+    per_step_budget = max(0.05, min(2.0, 150.0 / max(args.steps + args.warmup, 1)))
+    h1 = datagen.make_hidden(args.seed + 99, 1, c["d"], c["dtype"])
+    tp, _, tproj, tplan = oracle_step_sample(snap, params, idx, pw, h1, cores)
+    rows = int(max(1, min(R_total, (per_step_budget - tproj - tplan) / max(tp, 1e-4))))
+    h = datagen.make_hidden(args.seed + 98, rows, c["d"], c["dtype"])
+    for _ in range(args.warmup):
+        oracle_step_sample(snap, params, idx, pw, h, cores)
+    est = []
+    t_wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        t_pred, n_rows, t_proj, t_plan = oracle_step_sample(snap, params, idx, pw, h, cores)
+        est.append(t_pred * (R_total / n_rows) + t_proj + t_plan)
+    wall = time.perf_counter() - t_wall0
+    t_step = float(np.mean(est))
+    value = R_total / t_step
+    sample = (f"each step: oracle predictor on {rows} of {R_total} rows (OpenMP {cores} threads, extrapolated "
+              f"linearly to all rows) + projection and plan on the full snapshot")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args.config, c, 1, False, False),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s_timed": wall,
+            "note": "The paper ships no code; the reference arm is the plain CPU oracle written from the paper."}
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------------------ product arm
+def run_star(args):
+    import torch
+    rank, local_rank, world = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    import paper_2510_13668_b200 as star
+    from paper_2510_13668_b200.step import Step
+
+    c, snap, params_h, idx, pw, h_np = make_workload(args.config, world, rank, args.seed)
+    tdt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
+    R = len(idx)
+    W = [torch.from_numpy(x).to(tdt).to(dev) for x in (pw.W1, pw.W2, pw.W3)]
+    w4 = torch.from_numpy(pw.w4).to(dev)
+    pred = star.Predictor(*W, w4, max_rows=max(R, 1))
+    params = star.PlanParams.from_host(params_h, device=dev)
+
+    # long-tailed self-predictions: scale h rows so the GPU's y_hat tracks the snapshot's true
+    # remaining lengths (positive homogeneity of the bias-free Eq. 2)
+    h0 = torch.from_numpy(h_np).to(tdt).to(dev)
+    y0, _ = star.lenpred_forward(pred, h0)
+    med = float(torch.median(y0.float()).item())
+    target = np.maximum(snap.true_rem[idx], 1).astype(np.float32)
+    scale = target / max(med, 1e-3)
+    h_np = (h_np * scale[:, None]).astype(np.float32)
+    h_dev = torch.from_numpy(h_np).to(tdt).to(dev)
+    h_pin = h_dev.cpu().pin_memory()
+
+    step = Step(pred, params, c["n_inst"], r_cap=max(R, 1), rank=rank, world=world, group=group, device=dev)
+    req_np = [snap.req_id[idx], snap.inst[idx], snap.n_tok[idx], snap.pinned[idx]]
+    step.load_requests(*(torch.from_numpy(np.ascontiguousarray(a)) for a in req_np[:3]),
+                       pinned=torch.from_numpy(np.ascontiguousarray(req_np[3])))
+    req_pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in req_np]
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    pred.layer1_timing(True)
+    use_graph = not args.no_graph
+    if use_graph:
+        step.capture(h_dev)
+    run = step.replay if use_graph else (lambda: step.run(h_dev))
+    flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def one(timed_list, l1_list):
+        if flush is not None:
+            flush.fill_(1.0)
+        s, e = ev(), ev()
+        s.record(stream)
+        run()
+        e.record(stream)
+        e.synchronize()
+        if timed_list is not None:
+            timed_list.append(s.elapsed_time(e))
+            l1_list.append(pred.layer1_ms())
+
+    for _ in range(args.warmup):
+        one(None, None)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local_rank) if not args.profile else None
+    if clk:
+        clk.start()
+    t0 = time.perf_counter()
+    step_ms, l1_ms = [], []
+    for _ in range(args.steps):
+        one(step_ms, l1_ms)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    wall = time.perf_counter() - t0
+    clocks = clk.stop() if clk else None
+
+    tot = torch.tensor([sum(step_ms), sum(l1_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
+    ms_per_step = float(tot[0].item()) / args.steps
+    l1_avg_ms = float(tot[1].item()) / args.steps
+    R_total = c["n_inst"] * c["r_per_inst"]
+    value = R_total / (ms_per_step / 1e3)
+
+    # ---- per-stage breakdown (eager, events between stages; outside the timed region) ----
+    stage = {}
+    if not args.profile:
+        acc = {"predictor": 0.0, "projection": 0.0, "allgather": 0.0, "plan": 0.0}
+        nrep = 30
+        v = step.v
+        for _ in range(nrep):
+            if flush is not None:
+                flush.fill_(1.0)
+            es = [ev() for _ in range(5)]
+            es[0].record(stream)
+            star.lenpred_forward(pred, h_dev[:R], n_tok=v["n_tok"][:R], n_hat=v["n_hat"][:R], want_y=False)
+            es[1].record(stream)
+            star.project_instance_load(v["inst"], v["n_tok"], v["n_hat"], step.n_loc, step.H, params.beta_q,
+                                       inst_base=rank * step.n_loc, out=step.proj_out, workspace=step.ws, R=R)
+            es[2].record(stream)
+            if world > 1:
+                from paper_2510_13668_b200.step import exchange
+                exchange(step.send, step.recv, group)
+            es[3].record(stream)
+            star.plan_reschedule_segmented(params, step.seg, step.moves, step.n_moves)
+            es[4].record(stream)
+            es[4].synchronize()
+            for k, name in enumerate(acc):
+                acc[name] += es[k].elapsed_time(es[k + 1]) * 1e3 / nrep
+        stage = {k: round(x, 2) for k, x in acc.items()}
+
+    # ---- e2e: pinned host inputs -> device, step, moves -> host, every step ----
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        moves_h = torch.empty_like(step.moves, device="cpu").pin_memory()
+        nm_h = torch.empty(1, dtype=torch.int32).pin_memory()
+        v = step.v
+        e2e_ms = []
+        for i in range(args.warmup + args.steps):
+            if flush is not None:
+                flush.fill_(1.0)
+            s, e = ev(), ev()
+            s.record(stream)
+            h_dev.copy_(h_pin, non_blocking=True)
+            v["req_id"][:R].copy_(req_pin[0], non_blocking=True)
+            v["inst"][:R].copy_(req_pin[1], non_blocking=True)
+            v["n_tok"][:R].copy_(req_pin[2], non_blocking=True)
+            v["pinned"][:R].copy_(req_pin[3], non_blocking=True)
+            run()
+            moves_h.copy_(step.moves, non_blocking=True)
+            nm_h.copy_(step.n_moves, non_blocking=True)
+            e.record(stream)
+            e.synchronize()
+            if i >= args.warmup:
+                e2e_ms.append(s.elapsed_time(e))
+        te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms_step = float(te.item()) / args.steps
+        h2d = h_pin.numel() * h_pin.element_size() + sum(t.numel() * t.element_size() for t in req_pin)
+        d2h = moves_h.numel() + 4
+        e2e = {"value": R_total / (e2e_ms_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms_step,
+               "path": "Step public API: pinned-host h + request arrays -> device, graph replay of the C-ABI "
+                       "kernels, moves -> pinned host, every step"}
+
+    # ---- roofline: the layer-1 tcgen05 GEMM (dominant kernel) ----
+    peaks = load_peaks()
+    flops_l1 = 2.0 * R * c["d"] * 2048
+    achieved = flops_l1 / (l1_avg_ms / 1e3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"{args.config}/w{world}/layer1")
+    roofline = {"kernel": "umma_gemm_kernel<256,bf16> (predictor layer 1, tcgen05 + TMA)", "bound": "tensor",
+                "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
+                "algorithmic_flop_per_launch": flops_l1, "avg_launch_us": l1_avg_ms * 1e3,
+                "share_of_step": l1_avg_ms / ms_per_step,
+                "peak_source": peaks["source"] + " bf16_tflops (burst: kernel timed in a ~30 us step)"}
+
+    launches_per_step = 5   # layer-1 GEMM, layer-2 GEMM, layer-3+head GEMM, projection, plan
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "us_per_step": ms_per_step * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": c["dtype"],
+            "data": "synthetic (seeded datagen: N(0,1) hidden states, He-normal weights, long-tailed CoT lengths)",
+            "config": config_block(args.config, c, world, use_graph, flush is not None),
+            "roofline": roofline, "stage_us": stage, "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks, "e2e": e2e, "wall_s_timed": wall,
+            "step_us_p50": float(np.median(step_ms)) * 1e3, "step_us_p99": float(np.percentile(step_ms, 99)) * 1e3}
+    if world == 1 and not args.no_cpu_baseline and not args.profile and rank == 0:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args.config, args.seed, args.cpu_seconds)
+        except Exception as ex:  # keep the bench line even if the oracle cannot be built
+            line["cpu_baseline"] = {"value": None, "error": str(ex)}
+    if rank == 0:
+        print(json.dumps(line))
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                json.dump(line, f, indent=1)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    pred.close()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_star(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

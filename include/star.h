@@ -108,9 +108,12 @@ star_status lenpred_forward(star_predictor* p, const void* h, int64_t ld_h, int 
 star_status lenpred_quantize(const float* y_hat, const int32_t* n_tok, int R, int32_t max_ctx_len,
                              int32_t* n_hat, star_stream_t stream);
 
-/* Optional per-handle timing hook: when both events are non-NULL, lenpred_forward records
- * ev_start / ev_end (cudaEvent_t) around the layer-1 GEMM launch on `stream`.  NULL disables. */
-star_status star_predictor_set_layer1_events(star_predictor* p, void* ev_start, void* ev_end);
+/* Optional per-handle timing of the dominant kernel: with enable != 0 the handle creates two
+ * CUDA events and every later lenpred_forward records them around the layer-1 GEMM launch on
+ * its stream (also inside a captured CUDA graph).  star_predictor_layer1_ms() returns the
+ * elapsed milliseconds of the most recent completed forward (it synchronises on the end event). */
+star_status star_predictor_layer1_timing(star_predictor* p, int enable);
+star_status star_predictor_layer1_ms(star_predictor* p, float* ms);
 
 /* =====================================================================================
  * Projected per-instance load  (readings A4-A6)

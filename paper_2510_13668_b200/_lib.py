@@ -57,7 +57,8 @@ def lib() -> C.CDLL:
         "star_version": ([], C.c_char_p),
         "star_predictor_create": ([C.POINTER(P), I, I, I, I, I, P, P, P, P, P, P, P, P, I, P], I),
         "star_predictor_destroy": ([P], I),
-        "star_predictor_set_layer1_events": ([P, P, P], I),
+        "star_predictor_layer1_timing": ([P, I], I),
+        "star_predictor_layer1_ms": ([P, C.POINTER(C.c_float)], I),
         "lenpred_forward": ([P, P, I64, I, P, I32, P, P, P], I),
         "lenpred_quantize": ([P, P, I, I32, P, P], I),
         "star_project_workspace_bytes": ([I, I], C.c_size_t),
@@ -145,10 +146,14 @@ class Predictor:
         except Exception:
             pass
 
-    def set_layer1_events(self, ev0: Optional[torch.cuda.Event], ev1: Optional[torch.cuda.Event]):
-        p0 = C.c_void_p(ev0.cuda_event) if ev0 is not None else None
-        p1 = C.c_void_p(ev1.cuda_event) if ev1 is not None else None
-        _check(lib().star_predictor_set_layer1_events(self.handle, p0, p1), "set_layer1_events")
+    def layer1_timing(self, enable: bool = True):
+        """Library-owned CUDA events around every layer-1 GEMM launch (see star.h)."""
+        _check(lib().star_predictor_layer1_timing(self.handle, int(enable)), "layer1_timing")
+
+    def layer1_ms(self) -> float:
+        ms = C.c_float()
+        _check(lib().star_predictor_layer1_ms(self.handle, C.byref(ms)), "layer1_ms")
+        return float(ms.value)
 
 
 def lenpred_forward(pred: Predictor, h: torch.Tensor, n_tok: Optional[torch.Tensor] = None,

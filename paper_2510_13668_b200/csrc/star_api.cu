@@ -128,6 +128,18 @@ static cudaError_t launch_gemm(int BN, bool tf32, const CUtensorMap& a, const CU
   return launch_gemm_t<64, false>(a, b, p, m_tiles, st);
 }
 
+// Timing events must be real event-record nodes inside a captured graph (External flag);
+// outside capture a plain record.  Errors are cleared so they cannot leak into a launch check.
+static void record_timing_event(cudaEvent_t ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(ev, st);
+  cudaGetLastError();
+}
+
 static int pick_bn(int N) {
   if (N % 256 == 0) return 256;
   if (N % 128 == 0) return 128;
@@ -181,6 +193,8 @@ const char* star_version(void) { return "star-b200 0.1 sm_100a"; }
 
 static void free_pred(star_predictor* p) {
   if (!p) return;
+  if (p->ev0) cudaEventDestroy(p->ev0);
+  if (p->ev1) cudaEventDestroy(p->ev1);
   cudaFree(p->W1s);
   cudaFree(p->W2s);
   cudaFree(p->W3s);
@@ -281,10 +295,24 @@ star_status star_predictor_destroy(star_predictor* p) {
   return STAR_OK;
 }
 
-star_status star_predictor_set_layer1_events(star_predictor* p, void* ev_start, void* ev_end) {
+star_status star_predictor_layer1_timing(star_predictor* p, int enable) {
   if (!p) return fail(STAR_EINVAL, "predictor is NULL");
-  p->ev0 = reinterpret_cast<cudaEvent_t>(ev_start);
-  p->ev1 = reinterpret_cast<cudaEvent_t>(ev_end);
+  if (enable && !p->ev0) {
+    STAR_CUDA(cudaEventCreate(&p->ev0));
+    STAR_CUDA(cudaEventCreate(&p->ev1));
+  } else if (!enable && p->ev0) {
+    cudaEventDestroy(p->ev0);
+    cudaEventDestroy(p->ev1);
+    p->ev0 = p->ev1 = nullptr;
+  }
+  return STAR_OK;
+}
+
+star_status star_predictor_layer1_ms(star_predictor* p, float* ms) {
+  if (!p || !ms) return fail(STAR_EINVAL, "predictor / ms is NULL");
+  if (!p->ev0) return fail(STAR_EINVAL, "layer-1 timing is not enabled");
+  STAR_CUDA(cudaEventSynchronize(p->ev1));
+  STAR_CUDA(cudaEventElapsedTime(ms, p->ev0, p->ev1));
   return STAR_OK;
 }
 
@@ -330,10 +358,10 @@ star_status lenpred_forward(star_predictor* p, const void* h, int64_t ld_h, int 
     g.out = p->Z1;
     g.ld_out = (int64_t)p->m1 * kx;
     g.bias = p->b1;
-    if (p->ev0) cudaEventRecord(p->ev0, st);
+    if (p->ev0) record_timing_event(p->ev0, st);
     cudaError_t e = launch_gemm(p->bn1, f32, p->tmA1, p->tmB1, g, m_tiles, st);
     if (e != cudaSuccess) return cuda_fail(e, "layer-1 GEMM launch");
-    if (p->ev1) cudaEventRecord(p->ev1, st);
+    if (p->ev1) record_timing_event(p->ev1, st);
   }
   // ---- layer 2: Z2 = relu(W2 Z1 + b2) ----
   {

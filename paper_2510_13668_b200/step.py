@@ -1,0 +1,187 @@
+"""One decode-step pass of the STAR hot path on one rank (one process per GPU).
+
+    lenpred_forward -> project_instance_load -> all-gather(records) -> plan_reschedule_segmented
+
+Sharding follows the paper's deployment unit (one decode instance per GPU, PAPER.md:488;
+SURVEY.md §8(e)): the n decode instances are split into contiguous blocks of n_loc = n/W per
+rank; each rank predicts and projects only its own requests ("workers ... perform local future
+state simulation and proactively report").  The rank's whole state lives in one
+fixed-size byte record that is also the exchange buffer (zero-copy packing):
+
+    [count i32 | pad] [L n_loc*(H+1) i64] [W | peak | growth n_loc i64] [count n_loc i32]
+    [req_id | inst | n_tok | n_hat  r_cap i32 each] [pinned r_cap u8]      (16-byte aligned sections)
+
+The predictor writes N_hat straight into the record, the projection writes L/W/peak/growth
+into it, one NCCL all-gather (torch.distributed, NVLink) concatenates the W records, and every
+rank runs the identical integer plan directly on the gathered buffer (plan_reschedule_segmented
+reads the W segments in place).  Plans agree across ranks by construction (same bytes in, same
+bytes out).  PyTorch is used for device memory, streams, CUDA graphs and the process group only.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def _align(x: int, a: int = 16) -> int:
+    return (x + a - 1) // a * a
+
+
+@dataclasses.dataclass
+class RecordLayout:
+    n_loc: int
+    H: int
+    r_cap: int
+
+    def __post_init__(self):
+        o = 0
+        self.off_count = o; o += 16
+        self.off_L = o; o = _align(o + 8 * self.n_loc * (self.H + 1))
+        self.off_W = o; o = _align(o + 8 * self.n_loc)
+        self.off_peak = o; o = _align(o + 8 * self.n_loc)
+        self.off_growth = o; o = _align(o + 8 * self.n_loc)
+        self.off_icount = o; o = _align(o + 4 * self.n_loc)
+        self.off_req_id = o; o = _align(o + 4 * self.r_cap)
+        self.off_inst = o; o = _align(o + 4 * self.r_cap)
+        self.off_n_tok = o; o = _align(o + 4 * self.r_cap)
+        self.off_n_hat = o; o = _align(o + 4 * self.r_cap)
+        self.off_pinned = o; o = _align(o + self.r_cap)
+        self.nbytes = o
+
+    def views(self, buf: torch.Tensor) -> dict:
+        """Typed views into one record (a uint8 tensor of nbytes; works on CPU or CUDA)."""
+        assert buf.dtype == torch.uint8 and buf.numel() == self.nbytes
+
+        def v(off, n, dt, shape=None):
+            t = buf[off:off + n * torch.empty((), dtype=dt).element_size()].view(dt)
+            return t.view(shape) if shape is not None else t
+
+        return dict(
+            count=v(self.off_count, 1, torch.int32),
+            L=v(self.off_L, self.n_loc * (self.H + 1), torch.int64, (self.n_loc, self.H + 1)),
+            W=v(self.off_W, self.n_loc, torch.int64),
+            peak=v(self.off_peak, self.n_loc, torch.int64),
+            growth=v(self.off_growth, self.n_loc, torch.int64),
+            icount=v(self.off_icount, self.n_loc, torch.int32),
+            req_id=v(self.off_req_id, self.r_cap, torch.int32),
+            inst=v(self.off_inst, self.r_cap, torch.int32),
+            n_tok=v(self.off_n_tok, self.r_cap, torch.int32),
+            n_hat=v(self.off_n_hat, self.r_cap, torch.int32),
+            pinned=v(self.off_pinned, self.r_cap, torch.uint8),
+        )
+
+    def segments(self, base_ptr: int, world: int) -> "_lib.PlanSegmentsC":
+        return _lib.PlanSegmentsC(world, self.n_loc, self.r_cap, self.nbytes, base_ptr + self.off_L,
+                                  base_ptr + self.off_count, base_ptr + self.off_req_id, base_ptr + self.off_inst,
+                                  base_ptr + self.off_n_tok, base_ptr + self.off_n_hat, base_ptr + self.off_pinned)
+
+
+def exchange(send: torch.Tensor, recv: torch.Tensor, group=None):
+    """All-gather of the fixed-size records: recv[k*nbytes:(k+1)*nbytes] = rank k's record.
+    One NCCL collective over NVLink on GPU; the same call runs over gloo on CPU (tests)."""
+    import torch.distributed as dist
+    if send.is_cuda:
+        dist.all_gather_into_tensor(recv, send, group=group)
+    else:   # gloo: list form
+        world = recv.numel() // send.numel()
+        outs = list(recv.view(world, send.numel()).unbind(0))
+        dist.all_gather(outs, send, group=group)
+
+
+class Step:
+    """Per-rank decode-step pass.  `rank`/`world` describe the instance sharding; `group` is
+    the torch.distributed process group (None when world == 1)."""
+
+    def __init__(self, predictor: _lib.Predictor, params: _lib.PlanParams, n_inst: int, r_cap: int,
+                 rank: int = 0, world: int = 1, group=None, device: Optional[torch.device] = None,
+                 max_ctx_len: int = _lib.L_CTX):
+        if n_inst % world:
+            raise ValueError(f"n_inst={n_inst} must be divisible by world={world}")
+        self.pred, self.params = predictor, params
+        self.n_inst, self.world, self.rank, self.group = n_inst, world, rank, group
+        self.n_loc = n_inst // world
+        self.H = params.H
+        self.r_cap = r_cap
+        self.max_ctx_len = max_ctx_len
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.layout = RecordLayout(self.n_loc, self.H, r_cap)
+        self.send = torch.zeros(self.layout.nbytes, dtype=torch.uint8, device=self.device)
+        self.recv = (torch.zeros(world * self.layout.nbytes, dtype=torch.uint8, device=self.device)
+                     if world > 1 else self.send)
+        self.v = self.layout.views(self.send)
+        self.seg = self.layout.segments(self.recv.data_ptr(), world)
+        self.ws = torch.zeros(_lib.project_workspace_bytes(self.n_loc, self.H), dtype=torch.uint8, device=self.device)
+        self.moves, self.n_moves = _lib.alloc_moves(params.max_moves, self.device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.proj_out = _lib.ProjectOut(self.n_loc, self.H, self.device, L=self.v["L"])
+        self.proj_out.W, self.proj_out.peak, self.proj_out.growth = self.v["W"], self.v["peak"], self.v["growth"]
+        self.proj_out.count = self.v["icount"]
+        self.R = 0
+        self.graph = None
+
+    # ---------------------------------------------------------------- state
+    def load_requests(self, req_id, inst, n_tok, pinned=None, non_blocking=False):
+        """Installs this rank's running requests (global instance ids in this rank's block)."""
+        R = int(req_id.shape[0])
+        if R > self.r_cap:
+            raise ValueError(f"{R} requests exceed r_cap={self.r_cap}")
+        v = self.v
+        for name, src in (("req_id", req_id), ("inst", inst), ("n_tok", n_tok)):
+            v[name][:R].copy_(torch.as_tensor(src), non_blocking=non_blocking)
+        if pinned is not None:
+            v["pinned"][:R].copy_(torch.as_tensor(pinned), non_blocking=non_blocking)
+        else:
+            v["pinned"][:R].zero_()
+        v["count"].fill_(R)
+        self.R = R
+
+    # ---------------------------------------------------------------- the pass
+    def run(self, h: torch.Tensor, stream=None):
+        """h: [R, d] hidden states of this rank's running requests (row r <-> request slot r)."""
+        v, R = self.v, self.R
+        _lib.lenpred_forward(self.pred, h[:R], n_tok=v["n_tok"][:R], max_ctx_len=self.max_ctx_len,
+                             n_hat=v["n_hat"][:R], want_y=False, stream=stream)
+        _lib.project_instance_load(v["inst"], v["n_tok"], v["n_hat"], self.n_loc, self.H, self.params.beta_q,
+                                   inst_base=self.rank * self.n_loc, out=self.proj_out, workspace=self.ws,
+                                   err_flag=self.err, R=R, stream=stream)
+        if self.world > 1:
+            exchange(self.send, self.recv, self.group)
+        _lib.plan_reschedule_segmented(self.params, self.seg, self.moves, self.n_moves, self.err, stream=stream)
+        return self.moves, self.n_moves
+
+    def capture(self, h: torch.Tensor):
+        """Captures run(h) into a CUDA graph (one launch per step)."""
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.run(h)   # warm-up (sets function attributes, TMA maps)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run(h)
+        self.graph = g
+        return g
+
+    def replay(self):
+        self.graph.replay()
+        return self.moves, self.n_moves
+
+    def result(self):
+        return _lib.decode_moves(self.moves, self.n_moves)
+
+    def gathered_views(self):
+        """Typed views of every rank's record in the gathered buffer (for reporting/tests)."""
+        nb = self.layout.nbytes
+        return [self.layout.views(self.recv[k * nb:(k + 1) * nb]) for k in range(self.world)]
+
+
+def split_snapshot_by_rank(inst: np.ndarray, n_inst: int, world: int, rank: int) -> np.ndarray:
+    """Indices of the requests owned by `rank` (instances [rank*n_loc, (rank+1)*n_loc))."""
+    n_loc = n_inst // world
+    return np.nonzero((inst >= rank * n_loc) & (inst < (rank + 1) * n_loc))[0]
