@@ -103,6 +103,23 @@ star_status lenpred_forward(star_predictor* p, const void* h, int64_t ld_h, int 
                             const int32_t* n_tok, int32_t max_ctx_len,
                             float* y_hat, int32_t* n_hat, star_stream_t stream);
 
+/* Forward fused with the projection of its own N_hat (the worker-side "predict, then simulate
+ * the local future state" of PAPER.md:384): exactly lenpred_forward followed by
+ * project_instance_load(R, n_inst, inst_base, H, inst, n_tok, n_hat, beta_q, ...), with the same
+ * outputs bit for bit, but for bf16 predictors with m2 a multiple of 256 and m3 == 64 it runs as
+ * TWO launches: the layer-1 GEMM and one fused tail kernel (layer 2 -> layer 3 -> w4 dot ->
+ * quantizer -> keyed projection histogram -> last-CTA finalize), so Z2, Z3 and N_hat never
+ * make a round trip through HBM before the projection.  Other predictors run the unfused
+ * kernels.  n_hat (the N_hat output) must be non-NULL; n_tok and inst are required when R > 0;
+ * workspace (star_project_workspace_bytes(n_inst, H) bytes, zero-filled once by the caller) is
+ * required and is left zeroed.  R = 0 writes zero loads.  Argument meaning, layouts and
+ * err_flag bits are those of lenpred_forward and project_instance_load below. */
+star_status lenpred_forward_project(star_predictor* p, const void* h, int64_t ld_h, int R,
+                                    const int32_t* n_tok, int32_t max_ctx_len, float* y_hat, int32_t* n_hat,
+                                    int n_inst, int inst_base, int H, const int32_t* inst, const uint32_t* beta_q,
+                                    int64_t* L, int64_t* W, int64_t* peak, int64_t* growth, int32_t* count,
+                                    void* workspace, int32_t* err_flag, star_stream_t stream);
+
 /* The quantizer alone, on a caller-given fp32 y_hat (the exact device function the forward
  * epilogue uses).  Lets quantizer parity be tested on identical fp32 inputs. */
 star_status lenpred_quantize(const float* y_hat, const int32_t* n_tok, int R, int32_t max_ctx_len,
@@ -113,6 +130,12 @@ star_status lenpred_quantize(const float* y_hat, const int32_t* n_tok, int R, in
  * its stream (also inside a captured CUDA graph).  star_predictor_layer1_ms() returns the
  * elapsed milliseconds of the most recent completed forward (it synchronises on the end event). */
 star_status star_predictor_layer1_timing(star_predictor* p, int enable);
+/* Diagnostics: with enable != 0 every later fused-tail launch (see lenpred_forward_project)
+ * records per-CTA %globaltimer stamps (ns) of its phases into a library-owned device buffer
+ * [CTAs][16] (slot 15 = SM id).  With host_out != NULL the call synchronises the device and
+ * copies the stamps of the most recent launch (at most max_ctas CTAs) to host_out, writing the
+ * CTA count to *n_ctas.  enable == 0 frees the buffer.  Not for the hot path. */
+star_status star_predictor_timeline(star_predictor* p, int enable, uint64_t* host_out, int max_ctas, int* n_ctas);
 star_status star_predictor_layer1_ms(star_predictor* p, float* ms);
 
 /* =====================================================================================

@@ -9,9 +9,9 @@ Importing the package does not load the CUDA library; the first call does, and r
 StarError if it is missing (there is no CPU fallback).
 """
 from ._lib import (CURRENT_ONLY, L_CTX, STRICT_MEM, Predictor, PlanParams, ProjectOut, StarError,  # noqa: F401
-                   alloc_moves, decode_moves, lenpred_forward, lenpred_quantize, plan_reschedule,
+                   alloc_moves, decode_moves, lenpred_forward, lenpred_forward_project, lenpred_quantize, plan_reschedule,
                    plan_reschedule_segmented, project_instance_load, project_workspace_bytes, version)
 
-__all__ = ["Predictor", "lenpred_forward", "lenpred_quantize", "project_instance_load", "PlanParams",
+__all__ = ["Predictor", "lenpred_forward", "lenpred_forward_project", "lenpred_quantize", "project_instance_load", "PlanParams",
            "plan_reschedule", "plan_reschedule_segmented", "decode_moves", "alloc_moves", "StarError",
            "project_workspace_bytes", "version", "STRICT_MEM", "CURRENT_ONLY", "L_CTX", "ProjectOut"]

@@ -59,8 +59,10 @@ def lib() -> C.CDLL:
         "star_predictor_destroy": ([P], I),
         "star_predictor_layer1_timing": ([P, I], I),
         "star_predictor_layer1_ms": ([P, C.POINTER(C.c_float)], I),
+        "star_predictor_timeline": ([P, I, P, I, C.POINTER(I)], I),
         "lenpred_forward": ([P, P, I64, I, P, I32, P, P, P], I),
         "lenpred_quantize": ([P, P, I, I32, P, P], I),
+        "lenpred_forward_project": ([P, P, I64, I, P, I32, P, P, I, I, I, P, P, P, P, P, P, P, P, P, P], I),
         "star_project_workspace_bytes": ([I, I], C.c_size_t),
         "star_project_single_cta_max_rows": ([], I),
         "project_instance_load": ([I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P], I),
@@ -150,6 +152,17 @@ class Predictor:
         """Library-owned CUDA events around every layer-1 GEMM launch (see star.h)."""
         _check(lib().star_predictor_layer1_timing(self.handle, int(enable)), "layer1_timing")
 
+    def timeline(self, enable: bool = True, fetch: bool = False):
+        """Diagnostics: per-CTA phase stamps of the fused tail (star_predictor_timeline)."""
+        if not fetch:
+            _check(lib().star_predictor_timeline(self.handle, int(enable), None, 0, None), "timeline")
+            return None
+        buf = np.zeros((4 * 148, 16), dtype=np.uint64)
+        n = I()
+        _check(lib().star_predictor_timeline(self.handle, 1, buf.ctypes.data_as(P), buf.shape[0], C.byref(n)),
+               "timeline")
+        return buf[: n.value]
+
     def layer1_ms(self) -> float:
         ms = C.c_float()
         _check(lib().star_predictor_layer1_ms(self.handle, C.byref(ms)), "layer1_ms")
@@ -177,6 +190,35 @@ def lenpred_forward(pred: Predictor, h: torch.Tensor, n_tok: Optional[torch.Tens
     _check(lib().lenpred_forward(pred.handle, _ptr(h), h.stride(0), R, _ptr(n_tok), max_ctx_len,
                                  _ptr(y_hat), _ptr(n_hat), _stream(stream)), "lenpred_forward")
     return y_hat, n_hat
+
+
+def lenpred_forward_project(pred: Predictor, h: torch.Tensor, n_tok: torch.Tensor, inst: torch.Tensor, n_inst: int,
+                            H: int, beta_q: torch.Tensor, workspace: torch.Tensor, inst_base: int = 0,
+                            max_ctx_len: int = L_CTX, y_hat: Optional[torch.Tensor] = None,
+                            n_hat: Optional[torch.Tensor] = None, out: Optional["ProjectOut"] = None,
+                            err_flag: Optional[torch.Tensor] = None, want_y: bool = True, stream=None):
+    """Eq. 2 forward fused with the projection of its N_hat (star.h lenpred_forward_project)."""
+    R = h.shape[0]
+    if h.dim() != 2 or h.stride(1) != 1:
+        raise StarError("h must be 2-D with unit column stride")
+    exp = torch.bfloat16 if pred.dt == STAR_BF16 else torch.float32
+    if h.dtype != exp or not h.is_cuda:
+        raise StarError(f"h must be a CUDA {exp} tensor")
+    for n_, t in (("n_tok", n_tok), ("inst", inst), ("beta_q", beta_q)):
+        _req(t, torch.int32, n_)
+    dev = h.device
+    if y_hat is None and want_y:
+        y_hat = torch.empty(R, dtype=torch.float32, device=dev)
+    if n_hat is None:
+        n_hat = torch.empty(max(R, 1), dtype=torch.int32, device=dev)
+    if out is None:
+        out = ProjectOut(n_inst, H, dev)
+    _check(lib().lenpred_forward_project(pred.handle, _ptr(h), h.stride(0), R, _ptr(n_tok), max_ctx_len,
+                                         _ptr(y_hat), _ptr(n_hat), n_inst, inst_base, H, _ptr(inst), _ptr(beta_q),
+                                         _ptr(out.L), _ptr(out.W), _ptr(out.peak), _ptr(out.growth),
+                                         _ptr(out.count), _ptr(workspace), _ptr(err_flag), _stream(stream)),
+           "lenpred_forward_project")
+    return y_hat, n_hat, out
 
 
 def lenpred_quantize(y_hat: torch.Tensor, n_tok: Optional[torch.Tensor] = None, max_ctx_len: int = L_CTX,

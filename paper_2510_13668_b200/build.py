@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(HERE, "libstar.so")
 SOURCES = ["star_api.cu", "project.cu", "plan.cu"]
-HEADERS = ["ptx.cuh", "lenpred_kernels.cuh", "star_internal.h"]
+HEADERS = ["ptx.cuh", "lenpred_kernels.cuh", "lenpred_tail.cuh", "project_core.cuh", "star_internal.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -64,7 +64,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
         tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
+        vmap = os.path.join(BUILD, "star.map")   # export the C ABI only (include/star.h)
+        with open(vmap, "w") as f:
+            f.write("{\n  global:\n    star_*;\n    lenpred_*;\n    project_instance_load;\n"
+                    "    plan_reschedule*;\n  local: *;\n};\n")
+        cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
+               "-Xlinker", "--version-script=" + vmap]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

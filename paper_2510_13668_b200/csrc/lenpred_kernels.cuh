@@ -9,13 +9,20 @@
 //   warp 1      MMA issuer     (one elected lane, tcgen05.mma cta_group::1, M=128, N=BN,
 //                               accumulator in TMEM; tcgen05.commit frees smem slots)
 //   warps 2..5  epilogue       (tcgen05.ld 32x32b -> registers -> fused epilogue -> HBM)
-// Epilogues:  EPI_RELU_BF16   z = relu(acc + b) stored bf16 (next layer's A operand)
+// Epilogues:  EPI_RELU_BF16   z = relu(acc + b) -> bf16, staged in 128B-swizzled smem and
+//                             written with TMA stores (next layer's A operand)
 //             EPI_RELU_TF32X3 z = relu(acc + b) stored as [hi | hi | lo] tf32 split
 //                             (3xTF32: next layer computes hi*hi + hi*lo + lo*hi)
 //             EPI_HEAD        z3 = relu(acc + b3); y = w4 . z3 + b4; N_hat = quantize(y)
-// Split-K (grid.z) when the tile count cannot fill the 148 SMs: each split writes its fp32
-// partial tile, the last-arriving CTA of a tile sums the partials in fixed split order
-// (deterministic, run-to-run bit-identical) and runs the epilogue.
+// Split-K (grid.z = S splits, launched as a thread-block cluster of S CTAs along z) when
+// the tile count cannot fill the 148 SMs.  Every split owns BN/S of the tile's columns.
+// Phase 1: each CTA publishes its fp32 partial of the columns the OTHER splits own, in a
+// lane-contiguous layout ([col/4][row][4]: a warp's 32 rows are 512 contiguous bytes);
+// cluster barrier; phase 2: each CTA sums the S partials of its own columns in fixed split
+// order 0..S-1 (deterministic, run-to-run bit-identical) and runs the epilogue on them.
+// The reduction is spread over all S CTAs of the cluster instead of one "last" CTA.
+// EPI_HEAD adds a second cluster step: per-owner partial dots w4 . z3 are summed by split 0
+// in fixed order.
 #pragma once
 #include "ptx.cuh"
 #include <cuda_bf16.h>
@@ -28,8 +35,9 @@ struct GemmArgs {
   int M, N;              // output rows (requests) / columns
   int num_kb;            // number of 128-byte K blocks
   int kb_per_split;      // K blocks per split (grid.z splits)
-  int splits;
+  int splits;            // power of two <= 8, BN/splits multiple of 16
   int epi;
+  int tma_store;         // EPI_RELU_BF16: stage in smem + TMA store (owned width % 64 == 0)
   void* out;             // EPI_RELU_*: output matrix
   int64_t ld_out;        // elements between output rows
   const float* bias;     // [N] or nullptr
@@ -41,8 +49,8 @@ struct GemmArgs {
   float* y_hat;          // [M] or nullptr
   int32_t* n_hat;        // [M] or nullptr
   // split-K
-  float* ws;             // [splits][M][N] fp32 partials
-  int* counters;         // [tiles] arrival counters (zero between launches)
+  float* ws;             // [tiles][splits (producer)][splits (owner)][OW/4][128][4] fp32 partials
+  float* head_ws;        // [tiles][splits][128] per-owner partial dots (EPI_HEAD)
 };
 
 // Quantizer (readings A8-A10): cap = max(0, L_ctx - N(r)) (no n_tok -> L_ctx);
@@ -70,59 +78,70 @@ struct GemmSmem {
   static constexpr int STAGES = (int)((196u * 1024u) / STAGE_BYTES) > 8 ? 8 : (int)((196u * 1024u) / STAGE_BYTES);
   static constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
   static constexpr uint32_t BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+  static_assert(STAGES * STAGE_BYTES >= 4u * (BN / 64 > 0 ? BN / 64 : 1) * 4096u, "epilogue staging fits");
 };
 
-// Epilogue warps: apply the fused epilogue to 32 consecutive columns [c0, c0+32) of one row.
-template <int BN, bool TF32>
-__device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int col0, float (&f)[32],
-                                               float& head_acc) {
+// Fused epilogue on 16 consecutive columns [col0, col0+16) of one row.
+//   stage: this warp's 32x128B swizzled staging box (TMA-store path) or nullptr
+//   cb   : 16B-chunk index of col0 inside the 64-column box (0, 2, 4, 6)
+template <bool TF32>
+__device__ __forceinline__ void epilogue16(const GemmArgs& p, int row, int col0, float (&f)[16], float& head_acc,
+                                           uint8_t* stage, int cb) {
   if (p.bias) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) f[j] += __ldg(p.bias + col0 + j);
+    for (int j = 0; j < 16; ++j) f[j] += __ldg(p.bias + col0 + j);
   }
 #pragma unroll
-  for (int j = 0; j < 32; ++j) f[j] = fmaxf(f[j], 0.0f);
+  for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.0f);
   if (p.epi == EPI_HEAD) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) head_acc = fmaf(__ldg(p.w4 + col0 + j), f[j], head_acc);
+    for (int j = 0; j < 16; ++j) head_acc = fmaf(__ldg(p.w4 + col0 + j), f[j], head_acc);
     return;
   }
-  if (row >= p.M) return;
   if (p.epi == EPI_RELU_BF16) {
-    uint32_t w[16];
+    uint32_t w[8];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < 8; ++j) {
       __nv_bfloat162 b2 = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
       w[j] = *reinterpret_cast<uint32_t*>(&b2);
     }
-    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)row * p.ld_out + col0);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
-  } else {  // EPI_RELU_TF32X3: row = [hi (N) | hi (N) | lo (N)]
-    float* base = reinterpret_cast<float*>(p.out) + (int64_t)row * p.ld_out + col0;
-    float hi[32], lo[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      hi[j] = tf32_rna(f[j]);
-      lo[j] = f[j] - hi[j];
+    if (stage) {   // 128B swizzle: 16B chunk c of row r lives at chunk (c ^ (r & 7))
+      const int r = threadIdx.x & 31;
+      uint4* rowp = reinterpret_cast<uint4*>(stage + r * 128);
+      rowp[(cb) ^ (r & 7)] = make_uint4(w[0], w[1], w[2], w[3]);
+      rowp[(cb + 1) ^ (r & 7)] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else if (row < p.M) {
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)row * p.ld_out + col0);
+      dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
     }
-    float4* d0 = reinterpret_cast<float4*>(base);
-    float4* d1 = reinterpret_cast<float4*>(base + p.N);
-    float4* d2 = reinterpret_cast<float4*>(base + 2 * p.N);
+    return;
+  }
+  // EPI_RELU_TF32X3: row = [hi (N) | hi (N) | lo (N)]
+  if (row >= p.M) return;
+  float* base = reinterpret_cast<float*>(p.out) + (int64_t)row * p.ld_out + col0;
+  float hi[16], lo[16];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float4 h4 = make_float4(hi[4 * j], hi[4 * j + 1], hi[4 * j + 2], hi[4 * j + 3]);
-      d0[j] = h4;
-      d1[j] = h4;
-      d2[j] = make_float4(lo[4 * j], lo[4 * j + 1], lo[4 * j + 2], lo[4 * j + 3]);
-    }
+  for (int j = 0; j < 16; ++j) {
+    hi[j] = tf32_rna(f[j]);
+    lo[j] = f[j] - hi[j];
+  }
+  float4* d0 = reinterpret_cast<float4*>(base);
+  float4* d1 = reinterpret_cast<float4*>(base + p.N);
+  float4* d2 = reinterpret_cast<float4*>(base + 2 * p.N);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float4 h4 = make_float4(hi[4 * j], hi[4 * j + 1], hi[4 * j + 2], hi[4 * j + 3]);
+    d0[j] = h4;
+    d1[j] = h4;
+    d2[j] = make_float4(lo[4 * j], lo[4 * j + 1], lo[4 * j + 2], lo[4 * j + 3]);
   }
 }
 
 template <int BN, bool TF32>
 __global__ void __launch_bounds__(192, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const GemmArgs p) {
+                     const __grid_constant__ CUtensorMap tmC, const GemmArgs p) {
   using S = GemmSmem<BN>;
   constexpr int BM = 128;
   constexpr int ELEM = TF32 ? 4 : 2;
@@ -139,18 +158,19 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* empty = full + S::STAGES;
   uint64_t* accum = empty + S::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
-  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
+  const int splits = p.splits;
   const int kb0 = split * p.kb_per_split;
   const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-  const int nkb = kb1 - kb0;
+  const int nkb = kb1 - kb0;   // >= 1 (host guarantees)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (p.tma_store) tma_prefetch_desc(&tmC);
     for (int s = 0; s < S::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -163,6 +183,20 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: the prologue above overlapped the previous kernel's tail; from here on we read
+  // (and overwrite) memory it may own.
+  pdl_wait();
+  pdl_launch_dependents();
+
+  const int OW = BN / splits;                 // columns owned by each split
+  const int own0 = split * OW;                // first owned column (tile-relative)
+  const int q = warp & 3;                     // TMEM lane quarter accessible to this warp
+  const int row_in_tile = q * 32 + lane;
+  const int row = m_tile * BM + row_in_tile;
+  const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+  const int n0 = n_tile * BN;
+  const int tile_id = blockIdx.y * gridDim.x + blockIdx.x;
+  float* wsb = p.ws + (int64_t)tile_id * splits * BN * BM;   // this tile's partial blocks
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -179,6 +213,7 @@ __global__ void __launch_bounds__(192, 1)
         tma_load_2d(sB + s * S::B_BYTES, &tmB, &full[s], kc, n_tile * BN, pol_b);
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (elect_one()) {
@@ -200,86 +235,254 @@ __global__ void __launch_bounds__(192, 1)
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue (warps 2..5) ----------------
-    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
-    const int row = m_tile * BM + q * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    const int n0 = n_tile * BN;
+    // ---------------- epilogue phase 1: wait for the accumulator, publish partials --------
     mbar_wait(accum, 0);
     tc_fence_after();
-    float head_acc = 0.0f;
-    if (p.splits == 1) {
+    if (splits > 1) {
+      for (int o = 0; o < splits; ++o) {
+        if (o == split) continue;
+        float4* dst = reinterpret_cast<float4*>(wsb + (int64_t)(split * splits + o) * OW * BM) + row_in_tile;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(trow + c * 32, v);
-        tmem_ld_wait();
-        float f[32];
+        for (int c = 0; c < OW; c += 16) {
+          uint32_t v[16];
+          tmem_ld_32x32b_x16(trow + (uint32_t)(o * OW + c), v);
+          tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-        epilogue_chunk<BN, TF32>(p, row, n0 + c * 32, f, head_acc);
-      }
-    } else {
-      // 1) publish this split's fp32 partial tile
-      float* mine = p.ws + ((int64_t)split * p.M + row) * p.N + n0;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(trow + c * 32, v);
-        tmem_ld_wait();
-        if (row < p.M) {
-          float4* d = reinterpret_cast<float4*>(mine + c * 32);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            d[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                               __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          for (int j = 0; j < 4; ++j)
+            dst[(c / 4 + j) * BM] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
         }
       }
-      __threadfence();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      const int tile_id = blockIdx.y * gridDim.x + blockIdx.x;
-      if (warp == 2 && lane == 0) {
-        const int prev = atomicAdd(p.counters + tile_id, 1);
-        *last_flag = (prev == p.splits - 1) ? 1 : 0;
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (*last_flag) {
-        __threadfence();
-        // 2) last arriving split: fixed-order reduction of all partials + epilogue
+    }
+  }
+  if (splits > 1) cluster_sync_all();   // partials of every split of this tile are visible
+
+  float head_acc = 0.0f;
+  if (warp >= 2) {
+    // ---------------- epilogue phase 2: reduce owned columns (fixed split order) + epilogue ----
+    uint8_t* stage_base = p.tma_store ? smem + (q * (OW / 64)) * 4096 : nullptr;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          float f[32];
+    for (int c = 0; c < OW; c += 16) {
+      float f[16];
+      if (splits == 1) {
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(trow + (uint32_t)c, v);
+        tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) f[j] = 0.0f;
-          if (row < p.M) {
-            for (int s = 0; s < p.splits; ++s) {
-              const float4* src = reinterpret_cast<const float4*>(p.ws + ((int64_t)s * p.M + row) * p.N + n0 + c * 32);
+        for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
+      } else {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float4 x = __ldcg(src + j);
-                f[4 * j] += x.x;
-                f[4 * j + 1] += x.y;
-                f[4 * j + 2] += x.z;
-                f[4 * j + 3] += x.w;
-              }
+        for (int j = 0; j < 16; ++j) f[j] = 0.0f;
+        for (int s = 0; s < splits; ++s) {
+          if (s == split) {
+            uint32_t v[16];
+            tmem_ld_32x32b_x16(trow + (uint32_t)(own0 + c), v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) f[j] += __uint_as_float(v[j]);
+          } else {
+            const float4* src =
+                reinterpret_cast<const float4*>(wsb + (int64_t)(s * splits + split) * OW * BM) + row_in_tile;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 x = __ldcg(src + (c / 4 + j) * BM);
+              f[4 * j] += x.x;
+              f[4 * j + 1] += x.y;
+              f[4 * j + 2] += x.z;
+              f[4 * j + 3] += x.w;
             }
           }
-          epilogue_chunk<BN, TF32>(p, row, n0 + c * 32, f, head_acc);
         }
-        if (warp == 2 && lane == 0) p.counters[tile_id] = 0;  // re-arm for the next launch
+      }
+      uint8_t* stage = stage_base ? stage_base + (c / 64) * 4096 : nullptr;
+      epilogue16<TF32>(p, row, n0 + own0 + c, f, head_acc, stage, (c % 64) / 8);
+      if (stage && (c % 64) == 48) {   // a 32-row x 64-column box is complete: TMA store it
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmC, stage, n0 + own0 + (c / 64) * 64, m_tile * BM + q * 32);
+          bulk_commit();
+        }
       }
     }
-    if (p.epi == EPI_HEAD && (p.splits == 1 || *last_flag) && row < p.M) {
-      const float y = head_acc + (p.b4 ? __ldg(p.b4) : 0.0f);
-      if (p.y_hat) p.y_hat[row] = y;
-      if (p.n_hat) p.n_hat[row] = quantize_nhat(y, p.n_tok, row, p.max_ctx);
+    if (stage_base && lane == 0) bulk_wait_all();
+    if (p.epi == EPI_HEAD && splits > 1) p.head_ws[((int64_t)tile_id * splits + split) * BM + row_in_tile] = head_acc;
+  }
+  if (p.epi == EPI_HEAD && splits > 1) cluster_sync_all();   // per-owner partial dots visible
+  if (warp >= 2 && p.epi == EPI_HEAD && (splits == 1 || split == 0) && row < p.M) {
+    float y = head_acc;
+    if (splits > 1) {
+      y = 0.0f;
+      for (int s = 0; s < splits; ++s) y += __ldcg(p.head_ws + ((int64_t)tile_id * splits + s) * BM + row_in_tile);
     }
+    y += p.b4 ? __ldg(p.b4) : 0.0f;
+    if (p.y_hat) p.y_hat[row] = y;
+    if (p.n_hat) p.n_hat[row] = quantize_nhat(y, p.n_tok, row, p.max_ctx);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<S::TMEM_COLS>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// CTA-pair variant (tcgen05 cta_group::2) for the large bf16 layer-1 GEMM: a cluster of two
+// CTAs on neighbouring SMs computes one 256 x BN tile.  Each CTA stages its own 128 rows of A
+// and HALF of the BN rows of B (so every SM ingests 32 KB per 64-wide K block instead of 48 KB
+// for a 128 x 256 single-CTA tile: the per-SM TMA ingest, ~75 B/clk measured, is what bounds
+// the single-CTA kernel); the leader CTA issues the 256 x BN MMAs, which read the A and B
+// halves from both CTAs' shared memory, and each CTA's TMEM receives its 128 x BN accumulator.
+//   full[s]  lives in the leader: both CTAs' TMA loads complete their bytes on it
+//   empty[s] / accum live in both CTAs: the leader's commits multicast to the pair
+// Epilogue (both CTAs): relu(acc + b) -> bf16 -> 128B-swizzled smem -> TMA store.
+constexpr int kPrefetchKB = 8;   // L2 prefetch distance (K blocks) of the GEMM producers
+
+template <int BN>
+struct PairSmem {
+  static constexpr uint32_t A_BYTES = 128u * 128u;
+  static constexpr uint32_t B_BYTES = (uint32_t)(BN / 2) * 128u;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (int)((196u * 1024u) / STAGE_BYTES) > 8 ? 8 : (int)((196u * 1024u) / STAGE_BYTES);
+  static constexpr uint32_t BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+  static_assert(STAGES * STAGE_BYTES >= 4u * (BN / 64) * 4096u, "epilogue staging fits");
+};
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    umma_pair_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmC, const GemmArgs p) {
+  using S = PairSmem<BN>;
+  constexpr int BK = 64;
+  constexpr uint32_t IDESC = umma_idesc(false, 256, BN);
+  static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S::STAGES * S::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S::STAGES * S::B_BYTES);
+  uint64_t* empty = full + S::STAGES;
+  uint64_t* accum = empty + S::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();       // 0 = leader (issues the MMAs), 1 = peer
+  const int m_row0 = blockIdx.x * 128;           // this CTA's 128 rows (pair covers 256)
+  const int n_tile = blockIdx.y;
+  const int nkb = p.num_kb;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmC);
+    for (int s = 0; s < S::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<BN>(tmem_slot);
+  tc_fence_before();
+  cluster_sync_all();   // barriers of both CTAs initialised before any cross-CTA signal
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    if (elect_one()) {
+      const uint64_t pol_a = policy_evict_first();
+      const uint64_t pol_b = policy_evict_last();
+      const uint32_t full0 = mapa_shared(smem_u32(&full[0]), 0);   // leader's full[0]
+      const int b_row = n_tile * BN + (int)rank * (BN / 2);
+      // the weights do not depend on the previous kernel: their first stages go out before
+      // griddepcontrol.wait (PDL overlap)
+      const int pre = nkb < S::STAGES ? nkb : S::STAGES;
+      for (int i = 0; i < pre; ++i) {
+        if (rank == 0) mbar_arrive_expect_tx(&full[i], 2 * S::STAGE_BYTES);
+        tma_load_2d_pair(sB + i * S::B_BYTES, &tmB, full0 + (uint32_t)(i * 8), i * BK, b_row, pol_b);
+      }
+      pdl_wait();
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % S::STAGES;
+        const uint32_t ph = (uint32_t)(i / S::STAGES) & 1u;
+        if (i >= pre) {
+          mbar_wait(&empty[s], ph ^ 1u);
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * S::STAGE_BYTES);
+          tma_load_2d_pair(sB + s * S::B_BYTES, &tmB, full0 + (uint32_t)(s * 8), i * BK, b_row, pol_b);
+        }
+        tma_load_2d_pair(sA + s * S::A_BYTES, &tmA, full0 + (uint32_t)(s * 8), i * BK, m_row0, pol_a);
+        if (i + kPrefetchKB < nkb) {   // pull a later K block into L2 so its TMA load is an L2 hit
+          tma_prefetch_2d(&tmA, (i + kPrefetchKB) * BK, m_row0);
+          tma_prefetch_2d(&tmB, (i + kPrefetchKB) * BK, b_row);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader only) ----------------
+    if (rank == 0 && elect_one()) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % S::STAGES;
+        const uint32_t ph = (uint32_t)(i / S::STAGES) & 1u;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * S::A_BYTES));
+        const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * S::B_BYTES));
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          umma_pair(tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC, (i | k) != 0 ? 1u : 0u);
+        umma_commit_pair(&empty[s], (uint16_t)3);
+      }
+      umma_commit_pair(accum, (uint16_t)3);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue (both CTAs): own 128 lanes x BN columns ----------------
+    const int q = warp & 3;
+    const int row = m_row0 + q * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    const int n0 = n_tile * BN;
+    pdl_wait();   // Z1 may still be read by the previous kernel
+    mbar_wait(accum, 0);
+    tc_fence_after();
+    uint8_t* stage_base = smem + (q * (BN / 64)) * 4096;
+    float head_acc = 0.0f;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t v[16], u[16];
+      tmem_ld_32x32b_x16(trow + (uint32_t)c, v);
+      tmem_ld_32x32b_x16(trow + (uint32_t)(c + 16), u);
+      tmem_ld_wait();
+      float f[16], g[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        f[j] = __uint_as_float(v[j]);
+        g[j] = __uint_as_float(u[j]);
+      }
+      uint8_t* stage = stage_base + (c / 64) * 4096;
+      epilogue16<false>(p, row, n0 + c, f, head_acc, stage, (c % 64) / 8);
+      epilogue16<false>(p, row, n0 + c + 16, g, head_acc, stage, (c % 64) / 8 + 2);
+      if ((c % 64) == 32) {   // a 32-row x 64-column box is complete: TMA store it
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmC, stage, n0 + (c / 64) * 64, m_row0 + q * 32);
+          bulk_commit();
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  cluster_sync_all();   // the pair's MMAs and TMEM reads are done before the pair frees TMEM
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<BN>(tmem);
   }
 }
 

@@ -16,12 +16,13 @@
 // (gain desc, req_id asc, dst asc) (reading A20).  Greedy rounds (reading A21).
 #include <cstdint>
 #include <cuda_runtime.h>
+#include "ptx.cuh"
 #include "star_internal.h"
 
 namespace star {
 
 typedef __int128 i128;
-constexpr int kPlanThreads = 1024;
+constexpr int kPlanThreads = 512;
 
 struct PlanArgs {
   int n, H, max_moves;
@@ -85,25 +86,49 @@ __device__ __forceinline__ Cand warp_argmax(Cand c) {
   return c;
 }
 
+__device__ __forceinline__ i128 shfl_up_i128(i128 v, int off) {
+  const unsigned long long lo = __shfl_up_sync(0xFFFFFFFFu, (unsigned long long)v, off);
+  const long long hi = __shfl_up_sync(0xFFFFFFFFu, (long long)(v >> 64), off);
+  return (i128)(((unsigned __int128)(unsigned long long)hi << 64) | lo);
+}
+__device__ __forceinline__ i128 shfl_idx_i128(i128 v, int src) {
+  const unsigned long long lo = __shfl_sync(0xFFFFFFFFu, (unsigned long long)v, src);
+  const long long hi = __shfl_sync(0xFFFFFFFFu, (long long)(v >> 64), src);
+  return (i128)(((unsigned __int128)(unsigned long long)hi << 64) | lo);
+}
+__device__ __forceinline__ i128 shfl_xor_i128(i128 v, int m) {
+  const unsigned long long lo = __shfl_xor_sync(0xFFFFFFFFu, (unsigned long long)v, m);
+  const long long hi = __shfl_xor_sync(0xFFFFFFFFu, (long long)(v >> 64), m);
+  return (i128)(((unsigned __int128)(unsigned long long)hi << 64) | lo);
+}
+
+// Shared-memory state of the plan (dynamic part; see plan_smem_bytes for the layout).
 struct PlanSmem {
-  int64_t* Ls;     // [n][H+1]
   i128* P0;        // [n][H+1]
   i128* P1;        // [n][H+1]
   i128* B;         // [3][H+1]
   i128* Wv;        // [n]
+  int64_t* Ls;     // [n][H+1]
+  uint32_t* beta;  // [H+1]
+  int32_t* rid;    // [slots] staged request table (only when `staged`)
+  int32_t* rinst;
+  int32_t* rntok;
+  int32_t* rnhat;
+  uint8_t* rpin;
+  uint32_t* moved; // bitmap [slots]
+  int* seg_count;  // [world]
+  int* ulist;      // [n]
   uint8_t* inO;    // [n]
   uint8_t* inU;    // [n]
-  int* ulist;      // [n]
-  uint32_t* moved; // bitmap [world*r_cap]
-  int* seg_count;  // [world]
 };
 
-__global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a) {
+__global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a, const int staged) {
   extern __shared__ __align__(16) uint8_t smraw[];
   const int n = a.n, H1 = a.H + 1;
   const bool strict = (a.flags & 1u) != 0;
   const bool cur_only = (a.flags & 2u) != 0;
   const int nslots = a.world * a.r_cap;
+  const int nstage = staged ? nslots : 0;
   PlanSmem s;
   {
     uint8_t* p = smraw;
@@ -112,22 +137,30 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a)
     s.B = reinterpret_cast<i128*>(p); p += sizeof(i128) * 3 * H1;
     s.Wv = reinterpret_cast<i128*>(p); p += sizeof(i128) * n;
     s.Ls = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * n * H1;
+    s.rid = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * nstage;
+    s.rinst = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * nstage;
+    s.rntok = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * nstage;
+    s.rnhat = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * nstage;
+    s.beta = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * H1;
     s.moved = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * ((nslots + 31) / 32);
     s.seg_count = reinterpret_cast<int*>(p); p += sizeof(int) * a.world;
     s.ulist = reinterpret_cast<int*>(p); p += sizeof(int) * n;
+    s.rpin = p; p += nstage;
     s.inO = p; p += n;
     s.inU = p; p += n;
   }
   __shared__ Cand warp_best[kPlanThreads / 32];
   __shared__ int s_stop, s_nU, s_nmoves;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
 
-  // ---- load gathered loads (segment k holds instances [k*n_loc, (k+1)*n_loc)) ----
-  for (int e = tid; e < n * H1; e += blockDim.x) {
+  pdl_wait();   // inputs come from the projection / all-gather (PDL launch)
+  // ---- stage inputs in shared memory (all loads issued in parallel) ----
+  for (int e = tid; e < n * H1; e += blockDim.x) {   // segment k holds instances [k*n_loc, (k+1)*n_loc)
     const int i = e / H1, t = e % H1;
     const int k = i / a.n_loc, il = i % a.n_loc;
     s.Ls[e] = seg_ptr(a.L, k, a.seg_stride)[(int64_t)il * H1 + t];
   }
+  for (int t = tid; t < H1; t += blockDim.x) s.beta[t] = a.beta_q[t];
   for (int w = tid; w < (nslots + 31) / 32; w += blockDim.x) s.moved[w] = 0u;
   for (int k = tid; k < a.world; k += blockDim.x) {
     int c = a.r_cap;
@@ -140,10 +173,20 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a)
     }
     s.seg_count[k] = c;
   }
-  if (tid == 0) {   // B0/B1/B2[T] = sum_{t<=T} beta_t {1, t, t^2} (H+1 terms, serial)
+  for (int g = tid; g < nstage; g += blockDim.x) {
+    const int k = g / a.r_cap, j = g % a.r_cap;
+    s.rid[g] = seg_ptr(a.req_id, k, a.seg_stride)[j];
+    s.rinst[g] = seg_ptr(a.inst, k, a.seg_stride)[j];
+    s.rntok[g] = seg_ptr(a.n_tok, k, a.seg_stride)[j];
+    s.rnhat[g] = seg_ptr(a.n_hat, k, a.seg_stride)[j];
+    s.rpin[g] = a.pinned ? seg_ptr(a.pinned, k, a.seg_stride)[j] : (uint8_t)0;
+  }
+  if (tid == 0) s_nmoves = 0;
+  __syncthreads();
+  if (tid == 0) {   // B0/B1/B2[T] = sum_{t<=T} beta_t {1, t, t^2}
     i128 b0 = 0, b1 = 0, b2 = 0;
     for (int u = 0; u < H1; ++u) {
-      const i128 bt = (i128)a.beta_q[u];
+      const i128 bt = (i128)s.beta[u];
       b0 += bt;
       b1 += bt * u;
       b2 += bt * u * u;
@@ -152,29 +195,39 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a)
       s.B[2 * H1 + u] = b2;
     }
   }
-  if (tid == 0) s_nmoves = 0;
-  __syncthreads();
 
   for (int round = 0; round < a.max_moves; ++round) {
     // ---- Phase 1: InstanceClassification ----
-    for (int i = tid; i < n; i += blockDim.x) {
-      i128 w = 0;
+    // one warp per instance: W_i (warp reduction) and the Phase-3 prefix sums
+    //   P0_i[T] = sum_{t<=T} beta_t L_i[t],  P1_i[T] = sum_{t<=T} t beta_t L_i[t]  (warp scan)
+    for (int i = warp; i < n; i += nwarps) {
       const int64_t* Li = s.Ls + (int64_t)i * H1;
-      if (cur_only) {
-        w = (i128)a.beta_q[0] * Li[0];
-      } else {
-        for (int t = 1; t < H1; ++t) w += (i128)a.beta_q[t] * Li[t];
+      i128 wpart = 0, c0 = 0, c1 = 0;
+      for (int base = 0; base < H1; base += 32) {
+        const int t = base + lane;
+        const i128 x = t < H1 ? (i128)s.beta[t] * Li[t] : (i128)0;
+        if (t >= 1) wpart += x;
+        i128 x0 = x, x1 = x * t;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off);
+          if (lane >= off) {
+            x0 += y0;
+            x1 += y1;
+          }
+        }
+        x0 += c0;
+        x1 += c1;
+        if (t < H1) {
+          s.P0[(int64_t)i * H1 + t] = x0;
+          s.P1[(int64_t)i * H1 + t] = x1;
+        }
+        c0 = shfl_idx_i128(x0, 31);
+        c1 = shfl_idx_i128(x1, 31);
       }
-      s.Wv[i] = w;
-      // prefix sums for Phase 3: P0_i[T] = sum_{t<=T} beta_t L_i[t], P1_i[T] = sum_{t<=T} t beta_t L_i[t]
-      i128 p0 = 0, p1 = 0;
-      for (int t = 0; t < H1; ++t) {
-        const i128 bl = (i128)a.beta_q[t] * Li[t];
-        p0 += bl;
-        p1 += bl * t;
-        s.P0[(int64_t)i * H1 + t] = p0;
-        s.P1[(int64_t)i * H1 + t] = p1;
-      }
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) wpart += shfl_xor_i128(wpart, m);
+      if (lane == 0) s.Wv[i] = cur_only ? (i128)s.beta[0] * Li[0] : wpart;
     }
     __syncthreads();
     if (tid == 0) {
@@ -209,16 +262,16 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a)
       const int k = g / a.r_cap, j = g % a.r_cap;
       if (j >= s.seg_count[k]) continue;
       if ((s.moved[g >> 5] >> (g & 31)) & 1u) continue;
-      const int32_t src = seg_ptr(a.inst, k, a.seg_stride)[j];
+      const int32_t src = staged ? s.rinst[g] : seg_ptr(a.inst, k, a.seg_stride)[j];
       if (src < 0 || src >= n) {
         if (a.err) atomicOr(a.err, 1);
         continue;
       }
       if (!s.inO[src]) continue;
-      if (a.pinned && seg_ptr(a.pinned, k, a.seg_stride)[j]) continue;
-      const int64_t N = seg_ptr(a.n_tok, k, a.seg_stride)[j];
-      const int64_t nh = seg_ptr(a.n_hat, k, a.seg_stride)[j];
-      const int32_t rid = seg_ptr(a.req_id, k, a.seg_stride)[j];
+      if (staged ? s.rpin[g] : (a.pinned && seg_ptr(a.pinned, k, a.seg_stride)[j])) continue;
+      const int64_t N = staged ? s.rntok[g] : seg_ptr(a.n_tok, k, a.seg_stride)[j];
+      const int64_t nh = staged ? s.rnhat[g] : seg_ptr(a.n_hat, k, a.seg_stride)[j];
+      const int32_t rid = staged ? s.rid[g] : seg_ptr(a.req_id, k, a.seg_stride)[j];
       int T = (int)(nh - 1 < 0 ? 0 : (nh - 1 > a.H ? a.H : nh - 1));
       if (cur_only) T = 0;
       const i128 self = (i128)N * N * s.B[T] + (i128)2 * N * s.B[H1 + T] + s.B[2 * H1 + T];
@@ -254,26 +307,26 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a)
     __syncthreads();
     if (warp == 0) {
       Cand c;
-      if (lane < (int)(blockDim.x >> 5)) {
+      if (lane < nwarps) {
         c = warp_best[lane];
       } else {
         c.score = 0; c.id = 0; c.dst = 0; c.g = -1;
       }
-      c = warp_argmax(c);
-      if (lane == 0) {
-        if (c.g < 0) {
-          s_stop = 1;
-        } else {
-          // ExecuteMigration is out of the path: apply m* to the loads for the next round.
-          const int k = c.g / a.r_cap, j = c.g % a.r_cap;
-          const int src = seg_ptr(a.inst, k, a.seg_stride)[j];
-          const int64_t N = seg_ptr(a.n_tok, k, a.seg_stride)[j];
-          const int64_t nh = seg_ptr(a.n_hat, k, a.seg_stride)[j];
-          for (int t = 0; t < H1; ++t) {
-            const int64_t ct = (t == 0) ? N : (t < nh ? N + t : 0);
-            s.Ls[(int64_t)src * H1 + t] -= ct;
-            s.Ls[(int64_t)c.dst * H1 + t] += ct;
-          }
+      c = warp_argmax(c);   // butterfly: every lane holds the winner
+      if (c.g < 0) {
+        if (lane == 0) s_stop = 1;
+      } else {
+        // ExecuteMigration is out of the path: apply m* to the loads for the next round.
+        const int k = c.g / a.r_cap, j = c.g % a.r_cap;
+        const int src = staged ? s.rinst[c.g] : seg_ptr(a.inst, k, a.seg_stride)[j];
+        const int64_t N = staged ? s.rntok[c.g] : seg_ptr(a.n_tok, k, a.seg_stride)[j];
+        const int64_t nh = staged ? s.rnhat[c.g] : seg_ptr(a.n_hat, k, a.seg_stride)[j];
+        for (int t = lane; t < H1; t += 32) {
+          const int64_t ct = (t == 0) ? N : (t < nh ? N + t : 0);
+          s.Ls[(int64_t)src * H1 + t] -= ct;
+          s.Ls[(int64_t)c.dst * H1 + t] += ct;
+        }
+        if (lane == 0) {
           s.moved[c.g >> 5] |= 1u << (c.g & 31);
           const i128 gain = (i128)2 * n * c.score;
           star_move mv;
@@ -294,12 +347,17 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a)
   if (tid == 0) *a.n_moves = s_nmoves;
 }
 
-size_t plan_smem_bytes(int n, int H, int world, int r_cap) {
-  const size_t H1 = (size_t)H + 1, nn = (size_t)n;
+// Dynamic shared memory of plan_kernel (staged = request table copied into shared memory).
+static size_t plan_smem_layout(int n, int H, int world, int r_cap, bool staged) {
+  const size_t H1 = (size_t)H + 1, nn = (size_t)n, slots = (size_t)world * r_cap;
   size_t b = 16 * nn * H1 * 2 + 16 * 3 * H1 + 16 * nn + 8 * nn * H1;
-  b += 4 * (((size_t)world * r_cap + 31) / 32) + 4 * (size_t)world + 4 * nn + 2 * nn;
+  if (staged) b += 16 * slots + slots;
+  b += 4 * H1 + 4 * ((slots + 31) / 32) + 4 * (size_t)world + 4 * nn + 2 * nn;
   return (b + 15) & ~size_t(15);
 }
+
+// Minimum dynamic shared memory (request table read from global memory).
+size_t plan_smem_bytes(int n, int H, int world, int r_cap) { return plan_smem_layout(n, H, world, r_cap, false); }
 
 cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg, star_move* moves, int32_t* n_moves,
                         int32_t* err_flag, cudaStream_t stream) {
@@ -331,15 +389,27 @@ cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg,
   a.moves = moves;
   a.n_moves = n_moves;
   a.err = err_flag;
-  const size_t smem = plan_smem_bytes(a.n, a.H, a.world, a.r_cap);
+  // Stage the request table in shared memory when it fits (it is re-read every round).
+  const size_t lim = (size_t)kMaxSmemBytes - 4096;   // static shared memory + slack
+  const bool staged = plan_smem_layout(a.n, a.H, a.world, a.r_cap, true) <= lim;
+  const size_t smem = plan_smem_layout(a.n, a.H, a.world, a.r_cap, staged);
   static int attr_bytes = 48 * 1024;
   if ((int)smem > attr_bytes) {
     cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_bytes = (int)smem;
   }
-  plan_kernel<<<1, kPlanThreads, smem, stream>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1, 1, 1);
+  cfg.blockDim = dim3(kPlanThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, plan_kernel, a, staged ? 1 : 0);
 }
 
 }  // namespace star

@@ -15,90 +15,14 @@
 // re-zeroes the workspace.  Pass 2 (one CTA) is a suffix scan per instance.
 #include <cstdint>
 #include <cuda_runtime.h>
+#include "project_core.cuh"
+#include "ptx.cuh"
 #include "star_internal.h"
 
 namespace star {
 
 constexpr int kProjThreads = 512;
 constexpr int kProjMaxSmemBins = 12288;   // n_inst*(H+2) handled in shared memory
-
-struct ProjArgs {
-  int R, n_inst, inst_base, H;
-  const int32_t* inst;
-  const int32_t* n_tok;
-  const int32_t* n_hat;
-  const uint32_t* beta_q;
-  int64_t* L;
-  int64_t* W;
-  int64_t* peak;
-  int64_t* growth;
-  int32_t* count;
-  uint32_t* ws_cnt;                // [nb]
-  unsigned long long* ws_sum;      // [nb]
-  unsigned int* ws_arrive;         // [1]
-  int32_t* err;
-  int vec_ok;                      // all three arrays 16-byte aligned
-};
-
-__device__ __forceinline__ int4 ld_stream_int4(const int4* p) {
-  int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-// One request per lane; all 32 lanes of the warp must call this (valid may be false).
-__device__ __forceinline__ void proj_accumulate(const ProjArgs& a, bool valid, int32_t inst, int32_t ntok,
-                                                int32_t nhat, uint32_t* scnt, unsigned long long* ssum,
-                                                uint32_t& errbits) {
-  const int i = inst - a.inst_base;
-  bool ok = valid;
-  if (valid) {
-    if (i < 0 || i >= a.n_inst) { errbits |= 1u; ok = false; }
-    if (ntok < 1 || ntok > (1 << 17)) { errbits |= 2u; ok = false; }
-    if (nhat < 0) { errbits |= 4u; ok = false; }
-  }
-  const int b = nhat > a.H + 1 ? a.H + 1 : nhat;
-  const uint32_t key = ok ? (uint32_t)(i * (a.H + 2) + b) : 0xFFFFFFFFu;
-  const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
-  const uint32_t s = __reduce_add_sync(peers, ok ? (uint32_t)ntok : 0u);   // 32 * 2^17 < 2^32
-  const int leader = __ffs(peers) - 1;
-  if (ok && (int)(threadIdx.x & 31) == leader) {
-    atomicAdd(scnt + key, (uint32_t)__popc(peers));
-    atomicAdd(ssum + key, (unsigned long long)s);
-  }
-}
-
-__device__ void proj_finalize(const ProjArgs& a, const uint32_t* cnt, const unsigned long long* sum) {
-  const int HB = a.H + 2;
-  for (int i = threadIdx.x; i < a.n_inst; i += blockDim.x) {
-    const uint32_t* c = cnt + i * HB;
-    const unsigned long long* s = sum + i * HB;
-    int64_t* Li = a.L + (int64_t)i * (a.H + 1);
-    int64_t L0 = 0, cnt_all = 0, grow = 0;
-    for (int b = 0; b < HB; ++b) {
-      L0 += (int64_t)s[b];
-      cnt_all += c[b];
-      grow += (int64_t)c[b] * (b < a.H ? b : a.H);
-    }
-    Li[0] = L0;
-    int64_t peak = L0, w = 0, cge = 0, sge = 0;
-    for (int t = a.H; t >= 1; --t) {
-      cge += c[t + 1];
-      sge += (int64_t)s[t + 1];
-      const int64_t lt = sge + (int64_t)t * cge;
-      Li[t] = lt;
-      w += (int64_t)a.beta_q[t] * lt;
-      peak = lt > peak ? lt : peak;
-    }
-    if (a.W) a.W[i] = w;
-    if (a.peak) a.peak[i] = peak;
-    if (a.growth) a.growth[i] = grow;
-    if (a.count) a.count[i] = (int32_t)cnt_all;
-    if (cnt_all > 65536 && a.err) atomicOr(a.err, 8);
-  }
-}
 
 // SMEM_BINS: histogram lives in shared memory (else directly in the global workspace).
 template <bool SMEM_BINS>
@@ -114,12 +38,15 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const ProjArgs a)
       ssum[k] = 0;
       scnt[k] = 0;
     }
-    __syncthreads();
   } else {
     ssum = a.ws_sum;
     scnt = a.ws_cnt;
   }
   __shared__ int s_last;
+  __shared__ uint32_t sbeta[257];
+  pdl_wait();   // inputs may come from the previous kernel (PDL launch)
+  for (int t = threadIdx.x; t <= a.H; t += blockDim.x) sbeta[t] = a.beta_q[t];
+  __syncthreads();   // zeroed bins and beta visible
   uint32_t errbits = 0;
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -156,7 +83,7 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const ProjArgs a)
   __syncthreads();
 
   if (gridDim.x == 1) {
-    proj_finalize(a, scnt, ssum);
+    proj_finalize(a, scnt, ssum, sbeta, threadIdx.x >> 5, blockDim.x >> 5);
     if (!SMEM_BINS) {  // leave the workspace zeroed
       __syncthreads();
       for (int k = threadIdx.x; k < nb; k += blockDim.x) {
@@ -188,9 +115,9 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const ProjArgs a)
       a.ws_sum[k] = 0;
     }
     __syncthreads();
-    proj_finalize(a, scnt, ssum);
+    proj_finalize(a, scnt, ssum, sbeta, threadIdx.x >> 5, blockDim.x >> 5);
   } else {
-    proj_finalize(a, a.ws_cnt, a.ws_sum);
+    proj_finalize(a, a.ws_cnt, a.ws_sum, sbeta, threadIdx.x >> 5, blockDim.x >> 5);
     __syncthreads();
     for (int k = threadIdx.x; k < nb; k += blockDim.x) {
       a.ws_sum[k] = 0;
@@ -207,10 +134,9 @@ size_t project_workspace_bytes(int n_inst, int H) {
 
 int project_single_cta_max_rows() { return 1 << 15; }
 
-cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_t* inst, const int32_t* n_tok,
-                           const int32_t* n_hat, const uint32_t* beta_q, int64_t* L, int64_t* W, int64_t* peak,
-                           int64_t* growth, int32_t* count, void* workspace, int32_t* err_flag,
-                           cudaStream_t stream, int* grid_out) {
+ProjArgs make_proj_args(int R, int n_inst, int inst_base, int H, const int32_t* inst, const int32_t* n_tok,
+                        const int32_t* n_hat, const uint32_t* beta_q, int64_t* L, int64_t* W, int64_t* peak,
+                        int64_t* growth, int32_t* count, void* workspace, int32_t* err_flag) {
   ProjArgs a{};
   a.R = R;
   a.n_inst = n_inst;
@@ -234,6 +160,16 @@ cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_
   }
   a.vec_ok = ((reinterpret_cast<uintptr_t>(inst) | reinterpret_cast<uintptr_t>(n_tok) |
                reinterpret_cast<uintptr_t>(n_hat)) & 15u) == 0;
+  return a;
+}
+
+cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_t* inst, const int32_t* n_tok,
+                           const int32_t* n_hat, const uint32_t* beta_q, int64_t* L, int64_t* W, int64_t* peak,
+                           int64_t* growth, int32_t* count, void* workspace, int32_t* err_flag,
+                           cudaStream_t stream, int* grid_out) {
+  ProjArgs a = make_proj_args(R, n_inst, inst_base, H, inst, n_tok, n_hat, beta_q, L, W, peak, growth, count,
+                              workspace, err_flag);
+  const size_t nb = (size_t)n_inst * (size_t)(H + 2);
   const bool smem_bins = nb <= (size_t)kProjMaxSmemBins;
   int grid = 1;
   if (workspace && R > project_single_cta_max_rows() / 8) {
@@ -246,6 +182,18 @@ cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_
   if (!smem_bins && !workspace) return cudaErrorInvalidValue;
   if (grid_out) *grid_out = grid;
   const size_t smem = smem_bins ? nb * 12 : 0;
+  // Programmatic dependent launch: the kernel zeroes its shared histogram before
+  // griddepcontrol.wait, overlapping the previous kernel's tail.
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kProjThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
   if (smem_bins) {
     static int attr_bytes = 48 * 1024;
     if ((int)smem > attr_bytes) {
@@ -254,11 +202,9 @@ cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_
       if (e != cudaSuccess) return e;
       attr_bytes = (int)smem;
     }
-    project_kernel<true><<<grid, kProjThreads, smem, stream>>>(a);
-  } else {
-    project_kernel<false><<<grid, kProjThreads, 0, stream>>>(a);
+    return cudaLaunchKernelEx(&cfg, project_kernel<true>, a);
   }
-  return cudaGetLastError();
+  return cudaLaunchKernelEx(&cfg, project_kernel<false>, a);
 }
 
 }  // namespace star

@@ -5,11 +5,13 @@
 #include <cuda_runtime.h>
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
 
 #include "lenpred_kernels.cuh"
+#include "lenpred_tail.cuh"
 #include "star_internal.h"
 
 namespace star {
@@ -102,8 +104,8 @@ static star_status make_tmap(CUtensorMap* m, const void* base, bool f32, uint64_
 }
 
 template <int BN, bool TF32>
-static cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int m_tiles,
-                                 cudaStream_t st) {
+static cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmArgs& p,
+                                 int m_tiles, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(umma_gemm_kernel<BN, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -111,21 +113,64 @@ static cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, con
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid(m_tiles, p.N / BN, p.splits);
-  umma_gemm_kernel<BN, TF32><<<grid, 192, GemmSmem<BN>::BYTES, st>>>(a, b, p);
-  return cudaGetLastError();
+  // grid (m tiles, n tiles, K splits); the splits of one output tile form a cluster along z
+  // (co-scheduled, so they can exchange partials behind a cluster barrier).  Programmatic
+  // dependent launch lets the prologue overlap the previous kernel; the kernel calls
+  // griddepcontrol.wait before touching memory.
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(m_tiles, p.N / BN, p.splits);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = GemmSmem<BN>::BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = (unsigned)p.splits;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, umma_gemm_kernel<BN, TF32>, a, b, c, p);
 }
 
-static cudaError_t launch_gemm(int BN, bool tf32, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p,
-                               int m_tiles, cudaStream_t st) {
+static cudaError_t launch_gemm(int BN, bool tf32, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                               const GemmArgs& p, int m_tiles, cudaStream_t st) {
   if (tf32) {
-    if (BN == 256) return launch_gemm_t<256, true>(a, b, p, m_tiles, st);
-    if (BN == 128) return launch_gemm_t<128, true>(a, b, p, m_tiles, st);
-    return launch_gemm_t<64, true>(a, b, p, m_tiles, st);
+    if (BN == 256) return launch_gemm_t<256, true>(a, b, c, p, m_tiles, st);
+    if (BN == 128) return launch_gemm_t<128, true>(a, b, c, p, m_tiles, st);
+    return launch_gemm_t<64, true>(a, b, c, p, m_tiles, st);
   }
-  if (BN == 256) return launch_gemm_t<256, false>(a, b, p, m_tiles, st);
-  if (BN == 128) return launch_gemm_t<128, false>(a, b, p, m_tiles, st);
-  return launch_gemm_t<64, false>(a, b, p, m_tiles, st);
+  if (BN == 256) return launch_gemm_t<256, false>(a, b, c, p, m_tiles, st);
+  if (BN == 128) return launch_gemm_t<128, false>(a, b, c, p, m_tiles, st);
+  return launch_gemm_t<64, false>(a, b, c, p, m_tiles, st);
+}
+
+// CTA-pair layer-1 GEMM: grid (m tiles rounded up to even, n tiles), clusters of 2 along M, PDL.
+static cudaError_t launch_pair_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmArgs& p,
+                                   int m_tiles, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(umma_pair_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)PairSmem<256>::BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((m_tiles + 1) & ~1, p.N / 256, 1);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = PairSmem<256>::BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, umma_pair_gemm_kernel<256>, a, b, c, p);
 }
 
 // Timing events must be real event-record nodes inside a captured graph (External flag);
@@ -146,20 +191,74 @@ static int pick_bn(int N) {
   return 64;
 }
 
-// Split-K so that tiles * splits fills (but does not exceed) the SMs; every split gets >= 2 K blocks.
-static void plan_splits(int m_tiles, int n_tiles, int num_kb, int* splits, int* kb_per_split) {
-  const int tiles = m_tiles * n_tiles;
-  int s = 1;
-  if (tiles < g_num_sms) {
-    s = g_num_sms / tiles;
-    const int max_s = num_kb / 2 > 0 ? num_kb / 2 : 1;
-    if (s > max_s) s = max_s;
-    if (s < 1) s = 1;
+// Split-K choice.  splits is a power of two <= 8 (one portable cluster) with tiles*splits <=
+// SMs, owned width BN/splits >= 16 columns and >= 2 K blocks per split.  Among those, pick the
+// split count with the lowest modelled time (cycles), from B200 measurements
+// (tools/tma_bench.cu, tools/timeline.py):
+//   operand delivery  per-CTA bytes / 60 B/clk (per-SM TMA ingest with a 4-stage ring)
+//   MMA               128 * BN * K_split / 4096 MAC/clk   (bf16; x2 for the 3xTF32 layout)
+//   reduction         (splits > 1) 2 * (S-1)/S * 128*BN*4 B / 25 B/clk + 1500 (cluster barrier)
+// (delivery dominates large tiles; the exchange and barrier dominate small ones, e.g. the
+// 64-column head, which is fastest unsplit).
+static void plan_splits(int tiles, int num_kb, int bn, bool tf32, int* splits, int* kb_per_split) {
+  int best_s = 1, best_k = num_kb;
+  double best_t = 1e30;
+  for (int s = 1; s <= 8; s *= 2) {
+    if (s > 1 && (tiles * s > g_num_sms || bn / s < 16 || num_kb / s < 2)) break;
+    const int k = (num_kb + s - 1) / s;
+    if (s > 1 && (s - 1) * k >= num_kb) break;
+    const double cta_bytes = (128.0 + bn) * 128.0 * k;
+    const double load = cta_bytes / 60.0;
+    const double mma = 128.0 * bn * (k * (tf32 ? 32.0 : 64.0)) / 4096.0 * (tf32 ? 2.0 : 1.0);
+    const double red = s > 1 ? 2.0 * (s - 1) / s * 128.0 * bn * 4.0 / 25.0 + 1500.0 : 0.0;
+    const double t = std::max(load, mma) + red;
+    if (t < best_t * 0.97) {   // prefer fewer splits unless clearly faster
+      best_t = t;
+      best_s = s;
+      best_k = k;
+    }
   }
-  int kps = (num_kb + s - 1) / s;
-  s = (num_kb + kps - 1) / kps;
-  *splits = s;
-  *kb_per_split = kps;
+  *splits = best_s;
+  *kb_per_split = best_k;
+}
+
+
+// Fused tail (layer 2 -> layer 3 -> head -> quantizer [-> projection]) launch: grid
+// (m_tiles, n2, S), one cluster per layer-2 tile (its S split-K CTAs), PDL.
+static cudaError_t launch_tail(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& w3, const TailArgs& t,
+                               int m_tiles, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TailSmem::BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(m_tiles, t.n2_tiles, t.splits);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = TailSmem::BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = (unsigned)t.splits;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, tail_kernel, a, b, w3, t);
+}
+
+// Split count of the fused tail: S = 4 when m_tiles * n2 * 4 CTAs fit one wave, else 2
+// (n2 * S <= 8 keeps the workspace bounds).  Returns 0 when the shape cannot use the tail.
+static int tail_splits(int m_tiles, int n2, int num_kb) {
+  for (int s = 4; s >= 2; s /= 2) {
+    if (n2 * s > 8 || num_kb / s < 2) continue;
+    if (s == 4 && m_tiles * n2 * s > g_num_sms) continue;
+    return s;
+  }
+  return 0;
 }
 
 }  // namespace star
@@ -176,10 +275,16 @@ struct star_predictor {
   float *W1s = nullptr, *W2s = nullptr, *W3s = nullptr;   // 3xTF32 [hi|lo|hi] weights (f32 mode)
   void* hs = nullptr;                                      // 3xTF32 [hi|hi|lo] h (f32 mode)
   void *Z1 = nullptr, *Z2 = nullptr;
-  float* ws = nullptr;
-  int* counters = nullptr;
+  float* ws = nullptr;        // split-K partials
+  float* head_ws = nullptr;   // split-K head partial dots
+  float* ws3 = nullptr;       // fused tail: layer-3 partials [m_tiles][16][64][128]
+  int* tail_cnt = nullptr;    // fused tail: per (m-tile, split) arrival counters
+  uint64_t* tl = nullptr;     // diagnostics: fused-tail phase timeline [ctas][16]
+  int tl_ctas = 0;            // CTAs of the most recent timed tail launch
   size_t ws_floats = 0;
   CUtensorMap tmA1, tmB1, tmA2, tmB2, tmA3, tmB3;
+  CUtensorMap tmC1, tmC2;     // TMA-store maps of Z1 / Z2 (bf16, 64 x 32 boxes)
+  CUtensorMap tmB1p;          // W1 with 128-row boxes (CTA-pair kernel: each CTA loads half of B)
   const void* last_h = nullptr;
   int64_t last_ld = 0;
   int last_R = -1;
@@ -202,7 +307,10 @@ static void free_pred(star_predictor* p) {
   cudaFree(p->Z1);
   cudaFree(p->Z2);
   cudaFree(p->ws);
-  cudaFree(p->counters);
+  cudaFree(p->head_ws);
+  cudaFree(p->ws3);
+  cudaFree(p->tail_cnt);
+  cudaFree(p->tl);
   delete p;
 }
 
@@ -246,7 +354,9 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
   ok &= alloc(&p->Z2, (size_t)max_rows * m2 * esz * kx);
   p->ws_floats = (size_t)g_num_sms * 128 * 256;
   ok &= alloc(reinterpret_cast<void**>(&p->ws), p->ws_floats * 4);
-  ok &= alloc(reinterpret_cast<void**>(&p->counters), 4096 * sizeof(int));
+  ok &= alloc(reinterpret_cast<void**>(&p->head_ws), (size_t)g_num_sms * 128 * 4);
+  ok &= alloc(reinterpret_cast<void**>(&p->ws3), (size_t)((max_rows + 127) / 128) * 16 * 64 * 128 * 4);
+  ok &= alloc(reinterpret_cast<void**>(&p->tail_cnt), (size_t)((max_rows + 127) / 128) * 8 * sizeof(int));
   if (f32) {
     ok &= alloc(&p->hs, (size_t)max_rows * d * 4 * 3);
     ok &= alloc(reinterpret_cast<void**>(&p->W1s), (size_t)m1 * d * 4 * 3);
@@ -258,7 +368,7 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
     free_pred(p);
     return fail(STAR_ENOMEM, "device allocation failed");
   }
-  cudaError_t e = cudaMemsetAsync(p->counters, 0, 4096 * sizeof(int), stream);
+  cudaError_t e = cudaMemsetAsync(p->tail_cnt, 0, (size_t)((max_rows + 127) / 128) * 8 * sizeof(int), stream);
   if (e == cudaSuccess && f32) {
     tf32x3_split_kernel<<<1024, 256, 0, stream>>>(static_cast<const float*>(W1), d, m1, d, p->W1s, 1);
     tf32x3_split_kernel<<<256, 256, 0, stream>>>(static_cast<const float*>(W2), m1, m2, m1, p->W2s, 1);
@@ -279,7 +389,10 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
       (st = make_tmap(&p->tmB3, B3, f32, K3, m3, K3 * esz, 64)) != STAR_OK ||
       (st = make_tmap(&p->tmA2, p->Z1, f32, K2, max_rows, K2 * esz, 128)) != STAR_OK ||
       (st = make_tmap(&p->tmA3, p->Z2, f32, K3, max_rows, K3 * esz, 128)) != STAR_OK ||
-      (f32 && (st = make_tmap(&p->tmA1, p->hs, true, K1, max_rows, K1 * 4, 128)) != STAR_OK)) {
+      (f32 && (st = make_tmap(&p->tmA1, p->hs, true, K1, max_rows, K1 * 4, 128)) != STAR_OK) ||
+      (!f32 && (st = make_tmap(&p->tmC1, p->Z1, false, m1, max_rows, (uint64_t)m1 * 2, 32)) != STAR_OK) ||
+      (!f32 && (st = make_tmap(&p->tmB1p, B1, false, K1, m1, K1 * esz, 128)) != STAR_OK) ||
+      (!f32 && (st = make_tmap(&p->tmC2, p->Z2, false, m2, max_rows, (uint64_t)m2 * 2, 32)) != STAR_OK)) {
     free_pred(p);
     return st;
   }
@@ -308,6 +421,25 @@ star_status star_predictor_layer1_timing(star_predictor* p, int enable) {
   return STAR_OK;
 }
 
+star_status star_predictor_timeline(star_predictor* p, int enable, uint64_t* host_out, int max_ctas, int* n_ctas) {
+  if (!p) return fail(STAR_EINVAL, "predictor is NULL");
+  if (enable && !p->tl) {
+    const size_t bytes = (size_t)g_num_sms * 4 * 16 * sizeof(uint64_t);
+    STAR_CUDA(cudaMalloc(&p->tl, bytes));
+    STAR_CUDA(cudaMemset(p->tl, 0, bytes));
+  } else if (!enable && p->tl) {
+    cudaFree(p->tl);
+    p->tl = nullptr;
+  }
+  if (host_out && p->tl) {
+    STAR_CUDA(cudaDeviceSynchronize());
+    const int n = p->tl_ctas < max_ctas ? p->tl_ctas : max_ctas;
+    STAR_CUDA(cudaMemcpy(host_out, p->tl, (size_t)n * 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    if (n_ctas) *n_ctas = n;
+  }
+  return STAR_OK;
+}
+
 star_status star_predictor_layer1_ms(star_predictor* p, float* ms) {
   if (!p || !ms) return fail(STAR_EINVAL, "predictor / ms is NULL");
   if (!p->ev0) return fail(STAR_EINVAL, "layer-1 timing is not enabled");
@@ -316,15 +448,14 @@ star_status star_predictor_layer1_ms(star_predictor* p, float* ms) {
   return STAR_OK;
 }
 
-star_status lenpred_forward(star_predictor* p, const void* h, int64_t ld_h, int R, const int32_t* n_tok,
-                            int32_t max_ctx_len, float* y_hat, int32_t* n_hat, star_stream_t stream_) {
+// Forward of Eq. 2 (+ optionally the projection of its N_hat, `proj`).  bf16 predictors run
+// 2 launches (layer-1 GEMM, fused tail); fp32 predictors run the 3 GEMM launches (+ the
+// standalone projection kernel when `proj` is set).
+static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, int R, const int32_t* n_tok,
+                                int32_t max_ctx_len, float* y_hat, int32_t* n_hat, const ProjArgs* proj,
+                                void* proj_ws, cudaStream_t st) {
   if (!p) return fail(STAR_EINVAL, "predictor is NULL");
   if (R < 0 || R > p->max_rows) return fail(STAR_ERANGE, "R=%d outside [0, max_rows=%d]", R, p->max_rows);
-  if (R == 0) return STAR_OK;
-  if (!h) return fail(STAR_EINVAL, "h is NULL");
-  if (ld_h < p->d) return fail(STAR_EINVAL, "ld_h=%lld < d=%d", (long long)ld_h, p->d);
-  if (max_ctx_len < 0) return fail(STAR_EINVAL, "max_ctx_len < 0");
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
   star_status s;
   const bool f32 = p->f32;
   const int kx = f32 ? 3 : 1;
@@ -347,33 +478,76 @@ star_status lenpred_forward(star_predictor* p, const void* h, int64_t ld_h, int 
   g.M = R;
   g.max_ctx = max_ctx_len;
   g.ws = p->ws;
-  g.counters = p->counters;
+  g.head_ws = p->head_ws;
+  const CUtensorMap& tmC1 = f32 ? p->tmA1 : p->tmC1;   // unused in fp32 mode (direct stores)
+  const CUtensorMap& tmC2 = f32 ? p->tmA1 : p->tmC2;
   // ---- layer 1: Z1 = relu(W1 h + b1) ----
   {
     const int num_kb = (p->d * kx * (f32 ? 4 : 2) + 127) / 128;
     g.N = p->m1;
     g.num_kb = num_kb;
-    plan_splits(m_tiles, p->m1 / p->bn1, num_kb, &g.splits, &g.kb_per_split);
+    plan_splits(m_tiles * (p->m1 / p->bn1), num_kb, p->bn1, f32, &g.splits, &g.kb_per_split);
     g.epi = f32 ? EPI_RELU_TF32X3 : EPI_RELU_BF16;
+    g.tma_store = (!f32 && (p->bn1 / g.splits) % 64 == 0) ? 1 : 0;
     g.out = p->Z1;
     g.ld_out = (int64_t)p->m1 * kx;
     g.bias = p->b1;
+    // CTA pairs when the unsplit pair grid already fills most of the SMs
+    const bool pair = !f32 && p->bn1 == 256 && ((m_tiles + 1) & ~1) * (p->m1 / 256) >= (g_num_sms * 5) / 8;
+    if (pair) {
+      g.splits = 1;
+      g.kb_per_split = num_kb;
+      g.tma_store = 1;
+    }
     if (p->ev0) record_timing_event(p->ev0, st);
-    cudaError_t e = launch_gemm(p->bn1, f32, p->tmA1, p->tmB1, g, m_tiles, st);
+    cudaError_t e = pair ? launch_pair_gemm(p->tmA1, p->tmB1p, tmC1, g, m_tiles, st)
+                         : launch_gemm(p->bn1, f32, p->tmA1, p->tmB1, tmC1, g, m_tiles, st);
     if (e != cudaSuccess) return cuda_fail(e, "layer-1 GEMM launch");
     if (p->ev1) record_timing_event(p->ev1, st);
+  }
+  // ---- fused tail: layer 2 -> layer 3 -> head -> quantizer [-> projection] ----
+  const int n2 = p->m2 / 256;
+  const int num_kb2 = p->m1 * 2 / 128;
+  const int ts = (!f32 && p->bn2 == 256 && p->m3 == 64) ? tail_splits(m_tiles, n2, num_kb2) : 0;
+  if (ts) {
+    TailArgs t{};
+    t.M = R;
+    t.num_kb = num_kb2;
+    t.splits = ts;
+    t.kb_per_split = (num_kb2 + ts - 1) / ts;
+    t.n2_tiles = n2;
+    t.b2 = p->b2;
+    t.b3 = p->b3;
+    t.w4 = p->w4;
+    t.b4 = p->b4;
+    t.n_tok = n_tok;
+    t.max_ctx = max_ctx_len;
+    t.y_hat = y_hat;
+    t.n_hat = n_hat;
+    t.ws2 = p->ws;
+    t.ws3a = p->ws3;
+    t.ws3b = p->ws3 + (size_t)m_tiles * n2 * ts * 64 * 128;
+    t.cnt = p->tail_cnt;
+    t.tl = p->tl;
+    p->tl_ctas = m_tiles * n2 * ts;
+    t.project = proj ? 1 : 0;
+    if (proj) t.pa = *proj;
+    cudaError_t e = launch_tail(p->tmA2, p->tmB2, p->tmB3, t, m_tiles, st);
+    if (e != cudaSuccess) return cuda_fail(e, "fused tail launch");
+    return STAR_OK;
   }
   // ---- layer 2: Z2 = relu(W2 Z1 + b2) ----
   {
     const int num_kb = (p->m1 * kx * (f32 ? 4 : 2)) / 128;
     g.N = p->m2;
     g.num_kb = num_kb;
-    plan_splits(m_tiles, p->m2 / p->bn2, num_kb, &g.splits, &g.kb_per_split);
+    plan_splits(m_tiles * (p->m2 / p->bn2), num_kb, p->bn2, f32, &g.splits, &g.kb_per_split);
     g.epi = f32 ? EPI_RELU_TF32X3 : EPI_RELU_BF16;
+    g.tma_store = (!f32 && (p->bn2 / g.splits) % 64 == 0) ? 1 : 0;
     g.out = p->Z2;
     g.ld_out = (int64_t)p->m2 * kx;
     g.bias = p->b2;
-    cudaError_t e = launch_gemm(p->bn2, f32, p->tmA2, p->tmB2, g, m_tiles, st);
+    cudaError_t e = launch_gemm(p->bn2, f32, p->tmA2, p->tmB2, tmC2, g, m_tiles, st);
     if (e != cudaSuccess) return cuda_fail(e, "layer-2 GEMM launch");
   }
   // ---- layer 3 + head: z3 = relu(W3 Z2 + b3); y = w4 . z3 + b4; N_hat = quantize(y) ----
@@ -381,8 +555,9 @@ star_status lenpred_forward(star_predictor* p, const void* h, int64_t ld_h, int 
     const int num_kb = (p->m2 * kx * (f32 ? 4 : 2)) / 128;
     g.N = p->m3;
     g.num_kb = num_kb;
-    plan_splits(m_tiles, 1, num_kb, &g.splits, &g.kb_per_split);
+    plan_splits(m_tiles, num_kb, 64, f32, &g.splits, &g.kb_per_split);
     g.epi = EPI_HEAD;
+    g.tma_store = 0;
     g.out = nullptr;
     g.ld_out = 0;
     g.bias = p->b3;
@@ -391,10 +566,53 @@ star_status lenpred_forward(star_predictor* p, const void* h, int64_t ld_h, int 
     g.n_tok = n_tok;
     g.y_hat = y_hat;
     g.n_hat = n_hat;
-    cudaError_t e = launch_gemm(64, f32, p->tmA3, p->tmB3, g, m_tiles, st);
+    cudaError_t e = launch_gemm(64, f32, p->tmA3, p->tmB3, p->tmA3, g, m_tiles, st);
     if (e != cudaSuccess) return cuda_fail(e, "layer-3/head GEMM launch");
   }
+  if (proj) {   // unfused shapes: the standalone projection kernel on the forward's N_hat
+    cudaError_t e = launch_project(R, proj->n_inst, proj->inst_base, proj->H, proj->inst, n_tok, n_hat, proj->beta_q,
+                                   proj->L, proj->W, proj->peak, proj->growth, proj->count, proj_ws, proj->err, st,
+                                   nullptr);
+    if (e != cudaSuccess) return cuda_fail(e, "project_kernel launch");
+  }
   return STAR_OK;
+}
+
+star_status lenpred_forward(star_predictor* p, const void* h, int64_t ld_h, int R, const int32_t* n_tok,
+                            int32_t max_ctx_len, float* y_hat, int32_t* n_hat, star_stream_t stream_) {
+  if (!p) return fail(STAR_EINVAL, "predictor is NULL");
+  if (R < 0 || R > p->max_rows) return fail(STAR_ERANGE, "R=%d outside [0, max_rows=%d]", R, p->max_rows);
+  if (R == 0) return STAR_OK;
+  if (!h) return fail(STAR_EINVAL, "h is NULL");
+  if (ld_h < p->d) return fail(STAR_EINVAL, "ld_h=%lld < d=%d", (long long)ld_h, p->d);
+  if (max_ctx_len < 0) return fail(STAR_EINVAL, "max_ctx_len < 0");
+  return forward_impl(p, h, ld_h, R, n_tok, max_ctx_len, y_hat, n_hat, nullptr, nullptr,
+                      reinterpret_cast<cudaStream_t>(stream_));
+}
+
+star_status lenpred_forward_project(star_predictor* p, const void* h, int64_t ld_h, int R, const int32_t* n_tok,
+                                    int32_t max_ctx_len, float* y_hat, int32_t* n_hat, int n_inst, int inst_base,
+                                    int H, const int32_t* inst, const uint32_t* beta_q, int64_t* L, int64_t* W,
+                                    int64_t* peak, int64_t* growth, int32_t* count, void* workspace,
+                                    int32_t* err_flag, star_stream_t stream_) {
+  if (!p) return fail(STAR_EINVAL, "predictor is NULL");
+  if (R < 0 || R > p->max_rows) return fail(STAR_ERANGE, "R=%d outside [0, max_rows=%d]", R, p->max_rows);
+  if (n_inst < 1 || n_inst > (1 << 16)) return fail(STAR_ERANGE, "n_inst=%d outside [1, 65536]", n_inst);
+  if (H < 0 || H > 256) return fail(STAR_ERANGE, "H=%d outside [0, 256]", H);
+  if (!L || !beta_q || !workspace || !n_hat) return fail(STAR_EINVAL, "L, beta_q, workspace and n_hat must be non-NULL");
+  if (max_ctx_len < 0) return fail(STAR_EINVAL, "max_ctx_len < 0");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+  if (R == 0) {   // empty batch: zero loads from the standalone kernel
+    cudaError_t e = launch_project(0, n_inst, inst_base, H, inst, n_tok, n_hat, beta_q, L, W, peak, growth, count,
+                                   workspace, err_flag, st, nullptr);
+    if (e != cudaSuccess) return cuda_fail(e, "project_kernel launch");
+    return STAR_OK;
+  }
+  if (!h || !inst || !n_tok) return fail(STAR_EINVAL, "h, inst and n_tok must be non-NULL");
+  if (ld_h < p->d) return fail(STAR_EINVAL, "ld_h=%lld < d=%d", (long long)ld_h, p->d);
+  ProjArgs pa = make_proj_args(R, n_inst, inst_base, H, inst, n_tok, n_hat, beta_q, L, W, peak, growth, count,
+                               workspace, err_flag);
+  return forward_impl(p, h, ld_h, R, n_tok, max_ctx_len, y_hat, n_hat, &pa, workspace, st);
 }
 
 star_status lenpred_quantize(const float* y_hat, const int32_t* n_tok, int R, int32_t max_ctx_len, int32_t* n_hat,

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "../../include/star.h"
+#include "project_core.cuh"
 
 namespace star {
 
@@ -17,6 +18,10 @@ cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_
                            const int32_t* n_hat, const uint32_t* beta_q, int64_t* L, int64_t* W, int64_t* peak,
                            int64_t* growth, int32_t* count, void* workspace, int32_t* err_flag,
                            cudaStream_t stream, int* grid_out);
+
+ProjArgs make_proj_args(int R, int n_inst, int inst_base, int H, const int32_t* inst, const int32_t* n_tok,
+                        const int32_t* n_hat, const uint32_t* beta_q, int64_t* L, int64_t* W, int64_t* peak,
+                        int64_t* growth, int32_t* count, void* workspace, int32_t* err_flag);
 
 // plan.cu
 size_t plan_smem_bytes(int n, int H, int world, int r_cap);

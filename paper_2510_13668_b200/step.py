@@ -1,6 +1,7 @@
 """One decode-step pass of the STAR hot path on one rank (one process per GPU).
 
-    lenpred_forward -> project_instance_load -> all-gather(records) -> plan_reschedule_segmented
+    lenpred_forward_project (predictor fused with project_instance_load) -> all-gather(records)
+    -> plan_reschedule_segmented
 
 Sharding follows the paper's deployment unit (one decode instance per GPU, PAPER.md:488;
 SURVEY.md §8(e)): the n decode instances are split into contiguous blocks of n_loc = n/W per
@@ -144,11 +145,11 @@ class Step:
     def run(self, h: torch.Tensor, stream=None):
         """h: [R, d] hidden states of this rank's running requests (row r <-> request slot r)."""
         v, R = self.v, self.R
-        _lib.lenpred_forward(self.pred, h[:R], n_tok=v["n_tok"][:R], max_ctx_len=self.max_ctx_len,
-                             n_hat=v["n_hat"][:R], want_y=False, stream=stream)
-        _lib.project_instance_load(v["inst"], v["n_tok"], v["n_hat"], self.n_loc, self.H, self.params.beta_q,
-                                   inst_base=self.rank * self.n_loc, out=self.proj_out, workspace=self.ws,
-                                   err_flag=self.err, R=R, stream=stream)
+        # predictor fused with the projection of its own N_hat (2 launches for bf16 predictors)
+        _lib.lenpred_forward_project(self.pred, h[:R], v["n_tok"][:R], v["inst"][:R], self.n_loc, self.H,
+                                     self.params.beta_q, self.ws, inst_base=self.rank * self.n_loc,
+                                     max_ctx_len=self.max_ctx_len, n_hat=v["n_hat"][:max(R, 1)],
+                                     out=self.proj_out, err_flag=self.err, want_y=False, stream=stream)
         if self.world > 1:
             exchange(self.send, self.recv, self.group)
         _lib.plan_reschedule_segmented(self.params, self.seg, self.moves, self.n_moves, self.err, stream=stream)

@@ -250,3 +250,51 @@ def test_fused_step_projection_equals_oracle(star, oracle_mod):
                                      _dev(beta.astype(np.int32)))
     ref = oracle_mod.project(snap.inst, snap.n_tok, nh, c["n_inst"], 50, beta)
     assert np.array_equal(out.L.cpu().numpy(), ref["L"])
+
+
+# ============================================================================ fused forward+projection
+@pytest.mark.parametrize("cfg,R,seed", [("C2", 2048, 0), ("C2", 2047, 1), ("C2", 1, 2), ("C2", 100, 3),
+                                        ("C3", 4096, 4), ("TGT", 512, 5), ("C2", 256, 6), ("C1", 128, 7),
+                                        ("C4", 4096, 8), ("C2", 3000, 9)])
+def test_fused_forward_project_equals_standalone(star, oracle_mod, cfg, R, seed):
+    """lenpred_forward_project == lenpred_forward + project_instance_load, bit for bit (y_hat,
+    N_hat, L, W, peak, growth, count), and its projection equals the oracle projection of the
+    GPU's own N_hat (c3 "fused = standalone" pin).  Ragged R (not a multiple of 128) included."""
+    c = datagen.CONFIGS[cfg]
+    n = c["n_inst"]
+    snap = datagen.make_snapshot(seed, n, (R + n - 1) // n)
+    inst, n_tok = snap.inst[:R].copy(), snap.n_tok[:R].copy()
+    pw = datagen.make_predictor_weights(seed, c["d"], c["dtype"], biases=(seed % 2 == 1))
+    scale = np.exp(datagen.rng(seed).normal(0.0, 1.5, R)).astype(np.float32)   # long-tailed N_hat
+    h = datagen.make_hidden(seed, R, c["d"], c["dtype"], scale=scale)
+    tdt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
+    W, b = _weights_dev(pw, biases=(seed % 2 == 1))
+    pred = star.Predictor(*W, *b, max_rows=R)
+    H = 50
+    beta = datagen.beta_schedule_q16(H)
+    bq = _dev(beta.astype(np.int32))
+    hd, ntd, ind = _dev(h, tdt), _dev(n_tok), _dev(inst)
+    ws = torch.zeros(star.project_workspace_bytes(n, H), dtype=torch.uint8, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    y1, nh1, out1 = star.lenpred_forward_project(pred, hd, ntd, ind, n, H, bq, ws, err_flag=err)
+    y2, nh2 = star.lenpred_forward(pred, hd, ntd)
+    out2 = star.project_instance_load(ind, ntd, nh2, n, H, bq)
+    torch.cuda.synchronize()
+    assert err.item() == 0
+    assert np.array_equal(y1.cpu().numpy(), y2.cpu().numpy())
+    assert np.array_equal(nh1.cpu().numpy(), nh2.cpu().numpy())
+    for k in ("L", "W", "peak", "growth", "count"):
+        assert np.array_equal(getattr(out1, k).cpu().numpy(), getattr(out2, k).cpu().numpy()), k
+    ref = oracle_mod.project(inst, n_tok, nh1.cpu().numpy(), n, H, beta)
+    for k in ("L", "W", "peak", "growth", "count"):
+        assert np.array_equal(getattr(out1, k).cpu().numpy(), ref[k]), k
+    assert int(ws.sum().item()) == 0
+    # predictor parity on sampled rows (full-size case) against the fp64 oracle
+    rows = np.unique(np.concatenate([datagen.rng(seed + 1).integers(0, R, 24), [0, R - 1]]))
+    y_ref = oracle_mod.lenpred_weights(h[rows], pw)
+    assert _rel_err(y1.cpu().numpy()[rows], y_ref) <= TOL[c["dtype"]]
+    # repeated calls: workspace re-armed, results identical
+    y3, nh3, out3 = star.lenpred_forward_project(pred, hd, ntd, ind, n, H, bq, ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(out3.L.cpu().numpy(), out1.L.cpu().numpy())
+    pred.close()

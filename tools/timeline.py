@@ -1,0 +1,34 @@
+"""Fused-tail phase timeline (diagnostics): per-phase median/max offsets across CTAs."""
+import os
+import sys
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import datagen  # noqa: E402
+import paper_2510_13668_b200 as star  # noqa: E402
+
+R = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
+d = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
+pw = datagen.make_predictor_weights(0, d, "bf16")
+W = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in (pw.W1, pw.W2, pw.W3)]
+pred = star.Predictor(*W, torch.from_numpy(pw.w4).cuda(), max_rows=R)
+h = torch.from_numpy(datagen.make_hidden(0, R, d, "bf16")).to(torch.bfloat16).cuda()
+snap = datagen.make_snapshot(0, 8, R // 8)
+nt, ins = torch.from_numpy(snap.n_tok).cuda(), torch.from_numpy(snap.inst).cuda()
+beta = torch.from_numpy(datagen.beta_schedule_q16(50).astype(np.int32)).cuda()
+ws = torch.zeros(star.project_workspace_bytes(8, 50), dtype=torch.uint8, device="cuda")
+pred.timeline(True)
+for _ in range(5):
+    star.lenpred_forward_project(pred, h, nt, ins, 8, 50, beta, ws)
+torch.cuda.synchronize()
+tl = pred.timeline(fetch=True).astype(np.int64)
+names = ["entry", "prologue", "prod pdl_wait", "prod issued", "mma done", "epi consts", "accum ready",
+         "publish L2", "csync1", "A3 done", "l3 ready", "publish Z3", "csync2", "stageA+ctr", "end"]
+t0 = tl[:, 0].min()
+print(f"R={R} ctas={tl.shape[0]} SMs used={len(set(tl[:, 15]))}")
+for k, nm in enumerate(names):
+    v = tl[:, k]
+    v = v[v > 0] - t0
+    if len(v):
+        print(f"{k:2d} {nm:14s} min {v.min()/1e3:7.2f}  med {np.median(v)/1e3:7.2f}  max {v.max()/1e3:7.2f} us")
