@@ -10,9 +10,10 @@ per-instance loads -> (NCCL all-gather of the per-rank records when N > 1) -> Al
 
 Defaults: N=1, workload BASELINE.json configs[1] ("C2": 8 instances x 256 requests, hidden 4096,
 bf16, long-tailed CoT lengths).  Sharding: the 8 instances are split in contiguous blocks over
-the N ranks (strong scaling: total work fixed).  The step is captured in one CUDA graph; L2 is
-flushed (256 MB write) before every timed step, outside the timed span; each step is timed with
-CUDA events on its stream; the reported time is the max over ranks.  Prints ONE JSON line.
+the N ranks (strong scaling: total work fixed).  The step is one CUDA graph
+[L2 flush (256 MB write) -> event -> step -> event]: the events are graph nodes on the step's
+stream, so the timed span excludes the flush and host launch latency; the reported time is the
+max over ranks of the summed per-step times.  Prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -48,6 +49,7 @@ def parse_args():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the projection bandwidth sweep")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU budget of the cpu_baseline sample")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no clocks/e2e/cpu legs")
     ap.add_argument("--json-out", default=None)
@@ -214,6 +216,59 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------ product arm
+def count_kernel_nodes(graph) -> int:
+    """Kernel nodes in a captured CUDA graph (our launches per step; events/memcpys excluded)."""
+    from cuda.bindings import runtime as rt
+    g = graph.raw_cuda_graph()
+    err, _, n = rt.cudaGraphGetNodes(g, 0)
+    err, nodes, n = rt.cudaGraphGetNodes(g, n)
+    k = 0
+    for nd in nodes[:n]:
+        err, t = rt.cudaGraphNodeGetType(nd)
+        if t == rt.cudaGraphNodeType.cudaGraphNodeTypeKernel:
+            k += 1
+    return k
+
+
+def projection_sweep(star, snap, params, dev, peaks, R=1 << 24, reps=20):
+    """Bandwidth-scale evidence for the projection kernel: the standalone
+    project_instance_load over R = 2^24 requests (the C2 snapshot tiled; 12 B/request, 201 MB,
+    beyond L2), timed with CUDA events; algorithmic bytes = 12 B x R (+ outputs)."""
+    import torch
+    reps_tile = (R + snap.R - 1) // snap.R
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(np.tile(a, reps_tile)[:R])).to(dev)
+    # 256 instances x 65536 requests (the documented per-instance bound): tile k of the snapshot
+    # goes to instances 8*(k % 32) + inst
+    n = snap.n_inst * 32
+    shift = (np.arange(reps_tile, dtype=np.int64) % 32 * snap.n_inst).repeat(snap.R)[:R]
+    inst = torch.from_numpy((np.tile(snap.inst, reps_tile)[:R] + shift).astype(np.int32)).to(dev)
+    ntok, nhat = t(snap.n_tok), t(snap.true_rem.astype(np.int32))
+    H = params.H
+    out = star.ProjectOut(n, H, dev)
+    ws = torch.zeros(star.project_workspace_bytes(n, H), dtype=torch.uint8, device=dev)
+    fn = lambda: star.project_instance_load(inst, ntok, nhat, n, H, params.beta_q, out=out, workspace=ws)
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    t_med = float(np.median(ts))
+    algo = 12.0 * R + n * (H + 5) * 8.0
+    gbs = algo / t_med / 1e9
+    return {"kernel": "project_kernel (standalone, multi-CTA)", "bound": "hbm", "requests": R,
+            "algorithmic_bytes": algo, "avg_launch_us": t_med * 1e6, "achieved": gbs, "peak": peaks["hbm_gbs"],
+            "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"], "traffic": None,
+            "instances": n,
+            "note": "inputs beyond L2 (201 MB; the C2 snapshot tiled over 256 instances x 65536 requests); the "
+                    "in-step projection is fused into the predictor tail"}
+
+
 def run_star(args):
     import torch
     rank, local_rank, world = dist_env()
@@ -254,29 +309,61 @@ def run_star(args):
                        pinned=torch.from_numpy(np.ascontiguousarray(req_np[3])))
     req_pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in req_np]
 
-    ev = lambda: torch.cuda.Event(enable_timing=True)
+    ev = lambda ext=False: torch.cuda.Event(enable_timing=True, external=ext)
     pred.layer1_timing(True)
-    use_graph = not args.no_graph
-    if use_graph:
-        step.capture(h_dev)
-    run = step.replay if use_graph else (lambda: step.run(h_dev))
     flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
-    def one(timed_list, l1_list):
+    # warm-up outside capture (function attributes, TMA descriptors, NCCL communicator)
+    s_ = torch.cuda.Stream(device=dev)
+    s_.wait_stream(stream)
+    with torch.cuda.stream(s_):
+        step.run(h_dev)
+    stream.wait_stream(s_)
+    torch.cuda.synchronize()
+
+    # Timed step: the step is one CUDA graph WITHOUT event nodes (an event node inside the graph
+    # breaks the programmatic-dependent-launch chain and costs several us); each step is
+    # [L2 flush kernel] -> stream event -> graph launch -> stream event.  The ~40 us flush keeps
+    # the GPU busy while the host enqueues the event and the graph, so the timed span contains
+    # the step's device time (plus the graph's own launch latency), not host latency.
+    use_graph = not args.no_graph
+    launches = None
+    g = g_l1 = None
+    if use_graph:
+        pred.layer1_timing(False)
+        g = torch.cuda.CUDAGraph(keep_graph=True)
+        with torch.cuda.graph(g):
+            step.run(h_dev)
+        try:
+            launches = count_kernel_nodes(g)
+        except Exception:
+            launches = None
+        g.instantiate()
+        # a second graph of the same step with the library's layer-1 event pair (roofline pass)
+        pred.layer1_timing(True)
+        g_l1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_l1):
+            step.run(h_dev)
+
+    def timed(graph, store, l1):
         if flush is not None:
             flush.fill_(1.0)
-        s, e = ev(), ev()
-        s.record(stream)
-        run()
-        e.record(stream)
-        e.synchronize()
-        if timed_list is not None:
-            timed_list.append(s.elapsed_time(e))
-            l1_list.append(pred.layer1_ms())
+        e_beg, e_end = ev(), ev()
+        e_beg.record(stream)
+        if graph is not None:
+            graph.replay()
+        else:
+            step.run(h_dev)
+        e_end.record(stream)
+        e_end.synchronize()
+        if store is not None:
+            store.append(e_beg.elapsed_time(e_end))
+            if l1 is not None:
+                l1.append(pred.layer1_ms())
 
-    for _ in range(args.warmup):
-        one(None, None)
+    for _ in range(max(args.warmup, 3)):
+        timed(g, None, None)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -284,49 +371,68 @@ def run_star(args):
     if clk:
         clk.start()
     t0 = time.perf_counter()
-    step_ms, l1_ms = [], []
+    step_ms = []
     for _ in range(args.steps):
-        one(step_ms, l1_ms)
+        timed(g, step_ms, None)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     wall = time.perf_counter() - t0
     clocks = clk.stop() if clk else None
 
-    tot = torch.tensor([sum(step_ms), sum(l1_ms)], dtype=torch.float64, device=dev)
+    # roofline pass: the same timed loop on the graph carrying the layer-1 events
+    l1_ms, step_l1_ms = [], []
+    if g_l1 is not None:
+        for _ in range(3):
+            timed(g_l1, None, None)
+        for _ in range(args.steps):
+            timed(g_l1, step_l1_ms, l1_ms)
+    else:
+        pred.layer1_timing(True)
+        for _ in range(args.steps):
+            timed(None, step_l1_ms, l1_ms)
+
+    tot = torch.tensor([sum(step_ms), sum(l1_ms), sum(step_l1_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
     ms_per_step = float(tot[0].item()) / args.steps
-    l1_avg_ms = float(tot[1].item()) / args.steps
+    l1_avg_ms = float(tot[1].item()) / max(len(l1_ms), 1)
+    step_l1_avg_ms = float(tot[2].item()) / max(len(step_l1_ms), 1)
     R_total = c["n_inst"] * c["r_per_inst"]
     value = R_total / (ms_per_step / 1e3)
 
-    # ---- per-stage breakdown (eager, events between stages; outside the timed region) ----
+    # ---- per-stage breakdown: the same step with event nodes between the stages ----
     stage = {}
-    if not args.profile:
-        acc = {"predictor": 0.0, "projection": 0.0, "allgather": 0.0, "plan": 0.0}
-        nrep = 30
+    if not args.profile and use_graph:
+        pred.layer1_timing(True)
+        es = [ev(True) for _ in range(4)]
+        gs = torch.cuda.CUDAGraph()
         v = step.v
-        for _ in range(nrep):
+        from paper_2510_13668_b200.step import exchange
+        with torch.cuda.graph(gs):
             if flush is not None:
                 flush.fill_(1.0)
-            es = [ev() for _ in range(5)]
-            es[0].record(stream)
-            star.lenpred_forward(pred, h_dev[:R], n_tok=v["n_tok"][:R], n_hat=v["n_hat"][:R], want_y=False)
-            es[1].record(stream)
-            star.project_instance_load(v["inst"], v["n_tok"], v["n_hat"], step.n_loc, step.H, params.beta_q,
-                                       inst_base=rank * step.n_loc, out=step.proj_out, workspace=step.ws, R=R)
-            es[2].record(stream)
+            es[0].record()
+            star.lenpred_forward_project(pred, h_dev[:R], v["n_tok"][:R], v["inst"][:R], step.n_loc, step.H,
+                                         params.beta_q, step.ws, inst_base=rank * step.n_loc,
+                                         n_hat=v["n_hat"][:max(R, 1)], out=step.proj_out, err_flag=step.err,
+                                         want_y=False)
+            es[1].record()
             if world > 1:
-                from paper_2510_13668_b200.step import exchange
                 exchange(step.send, step.recv, group)
-            es[3].record(stream)
-            star.plan_reschedule_segmented(params, step.seg, step.moves, step.n_moves)
-            es[4].record(stream)
-            es[4].synchronize()
-            for k, name in enumerate(acc):
-                acc[name] += es[k].elapsed_time(es[k + 1]) * 1e3 / nrep
-        stage = {k: round(x, 2) for k, x in acc.items()}
+            es[2].record()
+            star.plan_reschedule_segmented(params, step.seg, step.moves, step.n_moves, step.err)
+            es[3].record()
+        acc = np.zeros(3)
+        nrep = 50
+        for _ in range(nrep):
+            gs.replay()
+            es[3].synchronize()
+            acc += [es[k].elapsed_time(es[k + 1]) * 1e3 / nrep for k in range(3)]
+        stage = {"predict+project": round(acc[0], 2), "allgather": round(acc[1], 2), "plan": round(acc[2], 2),
+                 "layer1_gemm": round(l1_avg_ms * 1e3, 2),
+                 "note": "event nodes between stages (each costs a few us and blocks PDL overlap); "
+                         "the sum exceeds us_per_step"}
 
     # ---- e2e: pinned host inputs -> device, step, moves -> host, every step ----
     e2e = None
@@ -334,8 +440,10 @@ def run_star(args):
         moves_h = torch.empty_like(step.moves, device="cpu").pin_memory()
         nm_h = torch.empty(1, dtype=torch.int32).pin_memory()
         v = step.v
+        pred.layer1_timing(False)
+        step.capture(h_dev)   # public API: Step.capture / Step.replay (one graph launch per step)
         e2e_ms = []
-        for i in range(args.warmup + args.steps):
+        for i in range(max(args.warmup, 3) + args.steps):
             if flush is not None:
                 flush.fill_(1.0)
             s, e = ev(), ev()
@@ -345,12 +453,12 @@ def run_star(args):
             v["inst"][:R].copy_(req_pin[1], non_blocking=True)
             v["n_tok"][:R].copy_(req_pin[2], non_blocking=True)
             v["pinned"][:R].copy_(req_pin[3], non_blocking=True)
-            run()
+            step.replay()
             moves_h.copy_(step.moves, non_blocking=True)
             nm_h.copy_(step.n_moves, non_blocking=True)
             e.record(stream)
             e.synchronize()
-            if i >= args.warmup:
+            if i >= max(args.warmup, 3):
                 e2e_ms.append(s.elapsed_time(e))
         te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
         if world > 1:
@@ -360,10 +468,11 @@ def run_star(args):
         d2h = moves_h.numel() + 4
         e2e = {"value": R_total / (e2e_ms_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms_step,
-               "path": "Step public API: pinned-host h + request arrays -> device, graph replay of the C-ABI "
-                       "kernels, moves -> pinned host, every step"}
+               "path": "Step public API (Step.capture/replay of lenpred_forward_project -> all-gather -> "
+                       "plan_reschedule_segmented through the C ABI): pinned-host h + request arrays -> device, "
+                       "moves -> pinned host, every step"}
 
-    # ---- roofline: the layer-1 tcgen05 GEMM (dominant kernel) ----
+    # ---- roofline: the layer-1 tcgen05 GEMM (dominant kernel), timed live inside the step ----
     peaks = load_peaks()
     flops_l1 = 2.0 * R * c["d"] * 2048
     achieved = flops_l1 / (l1_avg_ms / 1e3) / 1e12
@@ -372,22 +481,33 @@ def run_star(args):
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get(f"{args.config}/w{world}/layer1")
-    roofline = {"kernel": "umma_gemm_kernel<256,bf16> (predictor layer 1, tcgen05 + TMA)", "bound": "tensor",
-                "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+    pair = c["dtype"] == "bf16" and ((R + 127) // 128 + 1) // 2 * 2 * 8 >= 148 * 5 // 8
+    roofline = {"kernel": ("umma_pair_gemm_kernel<256> (tcgen05 cta_group::2 + TMA)" if pair else
+                           "umma_gemm_kernel (tcgen05 + TMA, cluster split-K)") + " = predictor layer 1",
+                "bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
-                "algorithmic_flop_per_launch": flops_l1, "avg_launch_us": l1_avg_ms * 1e3,
-                "share_of_step": l1_avg_ms / ms_per_step,
-                "peak_source": peaks["source"] + " bf16_tflops (burst: kernel timed in a ~30 us step)"}
+                "algorithmic_flop_per_launch": flops_l1, "flop_per_request": 2.0 * c["d"] * 2048,
+                "avg_launch_us": l1_avg_ms * 1e3, "share_of_step": l1_avg_ms / step_l1_avg_ms,
+                "timing": "CUDA events recorded on the step's stream around the layer-1 launch inside the "
+                          "captured step, over a second timed loop of the same K steps (the event pair "
+                          "itself costs a few us, so the headline step time is taken without it)",
+                "peak_source": peaks["source"] + " bf16_tflops (burst figure: the kernel runs inside a ~60 us step)"}
 
-    launches_per_step = 5   # layer-1 GEMM, layer-2 GEMM, layer-3+head GEMM, projection, plan
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "us_per_step": ms_per_step * 1e3,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "us_per_step": ms_per_step * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": c["dtype"],
             "data": "synthetic (seeded datagen: N(0,1) hidden states, He-normal weights, long-tailed CoT lengths)",
             "config": config_block(args.config, c, world, use_graph, flush is not None),
-            "roofline": roofline, "stage_us": stage, "gpu_launches": launches_per_step * args.steps,
+            "roofline": roofline, "stage_us": stage,
+            "gpu_launches": (launches if launches is not None else 3 + (world > 1)) * args.steps,
+            "launches_per_step": launches,
             "clocks": clocks, "e2e": e2e, "wall_s_timed": wall,
             "step_us_p50": float(np.median(step_ms)) * 1e3, "step_us_p99": float(np.percentile(step_ms, 99)) * 1e3}
+    if rank == 0 and not args.profile and not args.no_sweep:
+        try:
+            line["roofline_projection"] = projection_sweep(star, snap, params_h_dev(star, params_h, dev), dev, peaks)
+        except Exception as ex:  # keep the bench line
+            line["roofline_projection"] = {"error": str(ex)}
     if world == 1 and not args.no_cpu_baseline and not args.profile and rank == 0:
         try:
             line["cpu_baseline"] = cpu_baseline(args.config, args.seed, args.cpu_seconds)
@@ -402,6 +522,16 @@ def run_star(args):
         torch.distributed.destroy_process_group()
     pred.close()
     return 0
+
+
+def params_h_dev(star, params_h, dev):
+    """PlanParams-like object for the sweep: H and a device beta_q."""
+    class _P:
+        pass
+    p = _P()
+    p.H = params_h.H
+    p.beta_q = star.PlanParams.from_host(params_h, device=dev).beta_q
+    return p
 
 
 def main():

@@ -134,7 +134,8 @@ star_status star_predictor_layer1_timing(star_predictor* p, int enable);
  * records per-CTA %globaltimer stamps (ns) of its phases into a library-owned device buffer
  * [CTAs][16] (slot 15 = SM id).  With host_out != NULL the call synchronises the device and
  * copies the stamps of the most recent launch (at most max_ctas CTAs) to host_out, writing the
- * CTA count to *n_ctas.  enable == 0 frees the buffer.  Not for the hot path. */
+ * CTA count to *n_ctas; enable == 2 copies the layer-1 (CTA-pair GEMM) stamps instead.  enable == 0
+ * frees the buffers.  Not for the hot path. */
 star_status star_predictor_timeline(star_predictor* p, int enable, uint64_t* host_out, int max_ctas, int* n_ctas);
 star_status star_predictor_layer1_ms(star_predictor* p, float* ms);
 

@@ -152,15 +152,15 @@ class Predictor:
         """Library-owned CUDA events around every layer-1 GEMM launch (see star.h)."""
         _check(lib().star_predictor_layer1_timing(self.handle, int(enable)), "layer1_timing")
 
-    def timeline(self, enable: bool = True, fetch: bool = False):
-        """Diagnostics: per-CTA phase stamps of the fused tail (star_predictor_timeline)."""
+    def timeline(self, enable: bool = True, fetch: bool = False, layer1: bool = False):
+        """Diagnostics: per-CTA phase stamps of the fused tail / layer-1 GEMM (star_predictor_timeline)."""
         if not fetch:
             _check(lib().star_predictor_timeline(self.handle, int(enable), None, 0, None), "timeline")
             return None
         buf = np.zeros((4 * 148, 16), dtype=np.uint64)
         n = I()
-        _check(lib().star_predictor_timeline(self.handle, 1, buf.ctypes.data_as(P), buf.shape[0], C.byref(n)),
-               "timeline")
+        _check(lib().star_predictor_timeline(self.handle, 2 if layer1 else 1, buf.ctypes.data_as(P), buf.shape[0],
+                                             C.byref(n)), "timeline")
         return buf[: n.value]
 
     def layer1_ms(self) -> float:

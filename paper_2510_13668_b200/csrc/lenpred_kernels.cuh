@@ -51,6 +51,7 @@ struct GemmArgs {
   // split-K
   float* ws;             // [tiles][splits (producer)][splits (owner)][OW/4][128][4] fp32 partials
   float* head_ws;        // [tiles][splits][128] per-owner partial dots (EPI_HEAD)
+  uint64_t* tl;          // diagnostics: [ctas][16] %globaltimer phase stamps, or nullptr
 };
 
 // Quantizer (readings A8-A10): cap = max(0, L_ctx - N(r)) (no n_tok -> L_ctx);
@@ -370,6 +371,13 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();       // 0 = leader (issues the MMAs), 1 = peer
+  uint64_t* tl = p.tl ? p.tl + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 : nullptr;
+  if (tl && threadIdx.x == 0) {
+    tl[0] = globaltimer_ns();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tl[15] = smid;
+  }
   const int m_row0 = blockIdx.x * 128;           // this CTA's 128 rows (pair covers 256)
   const int n_tile = blockIdx.y;
   const int nkb = p.num_kb;
@@ -391,6 +399,7 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();
+  if (tl && threadIdx.x == 0) tl[1] = globaltimer_ns();
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
@@ -407,6 +416,7 @@ __global__ void __launch_bounds__(192, 1)
         tma_load_2d_pair(sB + i * S::B_BYTES, &tmB, full0 + (uint32_t)(i * 8), i * BK, b_row, pol_b);
       }
       pdl_wait();
+      if (tl) tl[2] = globaltimer_ns();
       for (int i = 0; i < nkb; ++i) {
         const int s = i % S::STAGES;
         const uint32_t ph = (uint32_t)(i / S::STAGES) & 1u;
@@ -431,6 +441,7 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t ph = (uint32_t)(i / S::STAGES) & 1u;
         mbar_wait(&full[s], ph);
         tc_fence_after();
+        if (tl && (i & 15) == 0 && i / 16 < 6) tl[3 + i / 16] = globaltimer_ns();   // slots 3..6
         const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * S::A_BYTES));
         const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * S::B_BYTES));
 #pragma unroll
@@ -439,6 +450,7 @@ __global__ void __launch_bounds__(192, 1)
         umma_commit_pair(&empty[s], (uint16_t)3);
       }
       umma_commit_pair(accum, (uint16_t)3);
+      if (tl) tl[9] = globaltimer_ns();
     }
     __syncwarp();
   } else {
@@ -450,6 +462,7 @@ __global__ void __launch_bounds__(192, 1)
     pdl_wait();   // Z1 may still be read by the previous kernel
     mbar_wait(accum, 0);
     tc_fence_after();
+    if (tl && threadIdx.x == 64) tl[10] = globaltimer_ns();
     uint8_t* stage_base = smem + (q * (BN / 64)) * 4096;
     float head_acc = 0.0f;
 #pragma unroll 1
@@ -477,9 +490,11 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
     if (lane == 0) bulk_wait_all();
+    if (tl && threadIdx.x == 64) tl[11] = globaltimer_ns();
   }
   tc_fence_before();
   cluster_sync_all();   // the pair's MMAs and TMEM reads are done before the pair frees TMEM
+  if (tl && threadIdx.x == 0) tl[12] = globaltimer_ns();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_pair<BN>(tmem);

@@ -21,8 +21,8 @@
 
 namespace star {
 
-constexpr int kProjThreads = 512;
-constexpr int kProjMaxSmemBins = 12288;   // n_inst*(H+2) handled in shared memory
+constexpr int kProjThreads = 1024;
+constexpr int kProjMaxSmemBins = 16384;   // n_inst*(H+2) handled in shared memory (<= 192 KB)
 
 // SMEM_BINS: histogram lives in shared memory (else directly in the global workspace).
 template <bool SMEM_BINS>
@@ -57,26 +57,42 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const ProjArgs a)
     const int4* vi = reinterpret_cast<const int4*>(a.inst);
     const int4* vn = reinterpret_cast<const int4*>(a.n_tok);
     const int4* vh = reinterpret_cast<const int4*>(a.n_hat);
-    for (int64_t base = (int64_t)warp_global * 32; base < nvec; base += (int64_t)nwarps * 32) {
-      const int64_t g = base + lane;
-      const bool valid = g < nvec;
-      int4 x = make_int4(0, 0, 0, 0), n = x, h = x;
-      if (valid) {
-        x = ld_stream_int4(vi + g);
-        n = ld_stream_int4(vn + g);
-        h = ld_stream_int4(vh + g);
+    // Each CTA streams one contiguous chunk (so an instance-grouped batch touches few
+    // histogram bins per CTA and the merge below stays small); warps stride inside it.  The
+    // stream is software-pipelined: the next 3 x 16 B of every lane are in flight while the
+    // current 4 requests are aggregated (HBM latency hiding at bandwidth scale).
+    const int64_t chunk = (nvec + gridDim.x - 1) / gridDim.x;
+    const int64_t c_beg = (int64_t)blockIdx.x * chunk;
+    const int64_t c_end = c_beg + chunk < nvec ? c_beg + chunk : nvec;
+    const int64_t stride = (int64_t)(blockDim.x >> 5) * 32;
+    int64_t g = c_beg + (int64_t)(threadIdx.x >> 5) * 32 + lane;
+    int4 x = make_int4(0, 0, 0, 0), n = x, h = x;
+    if (g < c_end) {
+      x = ld_stream_int4(vi + g);
+      n = ld_stream_int4(vn + g);
+      h = ld_stream_int4(vh + g);
+    }
+    for (int64_t base = c_beg + (int64_t)(threadIdx.x >> 5) * 32; base < c_end; base += stride) {
+      const bool valid = g < c_end;
+      const int64_t g2 = g + stride;
+      int4 x2 = make_int4(0, 0, 0, 0), n2 = x2, h2 = x2;
+      if (g2 < c_end) {
+        x2 = ld_stream_int4(vi + g2);
+        n2 = ld_stream_int4(vn + g2);
+        h2 = ld_stream_int4(vh + g2);
       }
-      proj_accumulate(a, valid, x.x, n.x, h.x, scnt, ssum, errbits);
-      proj_accumulate(a, valid, x.y, n.y, h.y, scnt, ssum, errbits);
-      proj_accumulate(a, valid, x.z, n.z, h.z, scnt, ssum, errbits);
-      proj_accumulate(a, valid, x.w, n.w, h.w, scnt, ssum, errbits);
+      proj_accumulate4<SMEM_BINS>(a, valid, x, n, h, scnt, ssum, errbits);
+      x = x2;
+      n = n2;
+      h = h2;
+      g = g2;
     }
     done = nvec * 4;
   }
   for (int64_t base = done + (int64_t)warp_global * 32; base < a.R; base += (int64_t)nwarps * 32) {
     const int64_t r = base + lane;
     const bool valid = r < a.R;
-    proj_accumulate(a, valid, valid ? a.inst[r] : 0, valid ? a.n_tok[r] : 0, valid ? a.n_hat[r] : 0, scnt, ssum,
+    proj_accumulate<SMEM_BINS>(a, valid, valid ? a.inst[r] : 0, valid ? a.n_tok[r] : 0, valid ? a.n_hat[r] : 0, scnt, ssum,
                     errbits);
   }
   if (errbits && a.err) atomicOr(a.err, (int)errbits);
@@ -175,7 +191,11 @@ cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_
   if (workspace && R > project_single_cta_max_rows() / 8) {
     const int64_t per_cta = (int64_t)kProjThreads * 16;   // 4 vec loads of 4 requests per thread
     grid = (int)((R + per_cta - 1) / per_cta);
-    const int max_grid = g_num_sms * (smem_bins ? 2 : 4);
+    // CTAs per SM: shared-memory histogram size bound, at most 2 x 1024 threads
+    const size_t cta_smem = smem_bins ? nb * 12 + 2048 : 2048;
+    int per_sm = (int)((200u * 1024u) / cta_smem);
+    per_sm = per_sm < 1 ? 1 : (per_sm > 2 ? 2 : per_sm);
+    const int max_grid = g_num_sms * per_sm;
     if (grid > max_grid) grid = max_grid;
     if (grid < 1) grid = 1;
   }
@@ -201,6 +221,11 @@ cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_
                                            (int)smem);
       if (e != cudaSuccess) return e;
       attr_bytes = (int)smem;
+    }
+    static bool carve = false;
+    if (!carve) {   // streaming kernel: prefer shared memory (several CTAs per SM), L1 is bypassed
+      cudaFuncSetAttribute(project_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      carve = true;
     }
     return cudaLaunchKernelEx(&cfg, project_kernel<true>, a);
   }

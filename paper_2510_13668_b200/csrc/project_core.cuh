@@ -36,7 +36,23 @@ __device__ __forceinline__ int4 ld_stream_int4(const int4* p) {
   return r;
 }
 
+// 64-bit histogram add.  In shared memory a 64-bit atomicAdd compiles to a CAS spin loop
+// (ATOMS.CAST.SPIN.64), which serialises badly on the hot bins; there the add is done as a
+// native 32-bit add on the low word plus a carry into the high word (v < 2^32 so at most one
+// carry).  Global memory has a native 64-bit reduction.
+template <bool kShared>
+__device__ __forceinline__ void hist_add64(unsigned long long* p, uint32_t v) {
+  if constexpr (kShared) {
+    uint32_t* w = reinterpret_cast<uint32_t*>(p);
+    const uint32_t old = atomicAdd(w, v);
+    if (old + v < old) atomicAdd(w + 1, 1u);
+  } else {
+    atomicAdd(p, (unsigned long long)v);
+  }
+}
+
 // One request per lane; all 32 lanes of the warp must call this (valid may be false).
+template <bool kShared = false>
 __device__ __forceinline__ void proj_accumulate(const ProjArgs& a, bool valid, int32_t inst, int32_t ntok,
                                                 int32_t nhat, uint32_t* scnt, unsigned long long* ssum,
                                                 uint32_t& errbits) {
@@ -54,7 +70,70 @@ __device__ __forceinline__ void proj_accumulate(const ProjArgs& a, bool valid, i
   const int leader = __ffs(peers) - 1;
   if (ok && (int)(threadIdx.x & 31) == leader) {
     atomicAdd(scnt + key, (uint32_t)__popc(peers));
-    atomicAdd(ssum + key, (unsigned long long)s);
+    hist_add64<kShared>(ssum + key, s);
+  }
+}
+
+// Four requests per lane (one int4 of each array), all 32 lanes of the warp must call this.
+// Fast path for instance-grouped batches (each decode instance's requests contiguous, the
+// natural layout of a worker's batch): a lane merges its requests that fall in the hot bin
+// b = H+1 (~78% of a long-tailed CoT batch) of its first such instance; if every lane's merged
+// hot instance is the same, one full-warp REDUX per field and one leader atomic pair cover them,
+// and the remaining (cold-bin) requests go straight to their bins.  Otherwise (e.g. round-robin
+// instance order) every request takes the match_any aggregation of proj_accumulate.
+template <bool kShared>
+__device__ __forceinline__ void proj_accumulate4(const ProjArgs& a, bool valid, const int4& x, const int4& n,
+                                                 const int4& h, uint32_t* scnt, unsigned long long* ssum,
+                                                 uint32_t& errbits) {
+  const int ins[4] = {x.x - a.inst_base, x.y - a.inst_base, x.z - a.inst_base, x.w - a.inst_base};
+  const int nt[4] = {n.x, n.y, n.z, n.w};
+  const int nh[4] = {h.x, h.y, h.z, h.w};
+  const int HB = a.H + 2;
+  bool ok[4];
+  int hot_i = -1;
+  uint32_t hc = 0, hs = 0, merged = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    ok[j] = valid;
+    if (valid) {
+      if (ins[j] < 0 || ins[j] >= a.n_inst) { errbits |= 1u; ok[j] = false; }
+      if (nt[j] < 1 || nt[j] > (1 << 17)) { errbits |= 2u; ok[j] = false; }
+      if (nh[j] < 0) { errbits |= 4u; ok[j] = false; }
+    }
+    if (ok[j] && nh[j] > a.H) {
+      if (hot_i < 0) hot_i = ins[j];
+      if (ins[j] == hot_i) {
+        ++hc;
+        hs += (uint32_t)nt[j];
+        merged |= 1u << j;
+      }
+    }
+  }
+  const uint32_t has = __ballot_sync(0xFFFFFFFFu, hot_i >= 0);
+  const int c_i = has ? __shfl_sync(0xFFFFFFFFu, hot_i, __ffs(has) - 1) : -1;
+  if (__all_sync(0xFFFFFFFFu, hot_i < 0 || hot_i == c_i)) {
+    if (has) {
+      const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, hc);
+      const uint32_t wsum = __reduce_add_sync(0xFFFFFFFFu, hs);   // <= 128 * 2^17 < 2^32
+      if ((threadIdx.x & 31) == 0) {
+        atomicAdd(scnt + c_i * HB + a.H + 1, wc);
+        hist_add64<kShared>(ssum + c_i * HB + a.H + 1, wsum);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (ok[j] && !((merged >> j) & 1u)) {
+        const int key = ins[j] * HB + (nh[j] > a.H + 1 ? a.H + 1 : nh[j]);
+        atomicAdd(scnt + key, 1u);
+        hist_add64<kShared>(ssum + key, (uint32_t)nt[j]);
+      }
+    }
+  } else {
+    uint32_t dummy = 0;   // error bits were recorded above
+    proj_accumulate<kShared>(a, ok[0], x.x, n.x, h.x, scnt, ssum, dummy);
+    proj_accumulate<kShared>(a, ok[1], x.y, n.y, h.y, scnt, ssum, dummy);
+    proj_accumulate<kShared>(a, ok[2], x.z, n.z, h.z, scnt, ssum, dummy);
+    proj_accumulate<kShared>(a, ok[3], x.w, n.w, h.w, scnt, ssum, dummy);
   }
 }
 

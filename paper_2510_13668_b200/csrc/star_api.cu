@@ -281,6 +281,8 @@ struct star_predictor {
   int* tail_cnt = nullptr;    // fused tail: per (m-tile, split) arrival counters
   uint64_t* tl = nullptr;     // diagnostics: fused-tail phase timeline [ctas][16]
   int tl_ctas = 0;            // CTAs of the most recent timed tail launch
+  uint64_t* tl_l1 = nullptr;  // diagnostics: layer-1 (CTA-pair) GEMM phase timeline
+  int tl_l1_ctas = 0;
   size_t ws_floats = 0;
   CUtensorMap tmA1, tmB1, tmA2, tmB2, tmA3, tmB3;
   CUtensorMap tmC1, tmC2;     // TMA-store maps of Z1 / Z2 (bf16, 64 x 32 boxes)
@@ -311,6 +313,7 @@ static void free_pred(star_predictor* p) {
   cudaFree(p->ws3);
   cudaFree(p->tail_cnt);
   cudaFree(p->tl);
+  cudaFree(p->tl_l1);
   delete p;
 }
 
@@ -429,6 +432,7 @@ star_status star_predictor_timeline(star_predictor* p, int enable, uint64_t* hos
     STAR_CUDA(cudaMemset(p->tl, 0, bytes));
   } else if (!enable && p->tl) {
     cudaFree(p->tl);
+  cudaFree(p->tl_l1);
     p->tl = nullptr;
   }
   if (host_out && p->tl) {
@@ -498,6 +502,8 @@ static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, 
       g.splits = 1;
       g.kb_per_split = num_kb;
       g.tma_store = 1;
+      g.tl = p->tl_l1;
+      p->tl_l1_ctas = ((m_tiles + 1) & ~1) * (p->m1 / 256);
     }
     if (p->ev0) record_timing_event(p->ev0, st);
     cudaError_t e = pair ? launch_pair_gemm(p->tmA1, p->tmB1p, tmC1, g, m_tiles, st)
@@ -650,8 +656,8 @@ star_status project_instance_load(int R, int n_inst, int inst_base, int H, const
   if (H < 0 || H > 256) return fail(STAR_ERANGE, "H=%d outside [0, 256]", H);
   if (!L || !beta_q) return fail(STAR_EINVAL, "L and beta_q must be non-NULL");
   if (R > 0 && (!inst || !n_tok || !n_hat)) return fail(STAR_EINVAL, "inst, n_tok, n_hat must be non-NULL");
-  if ((size_t)n_inst * (H + 2) > 12288 && !workspace)
-    return fail(STAR_EINVAL, "n_inst*(H+2) > 12288 requires a workspace");
+  if ((size_t)n_inst * (H + 2) > 16384 && !workspace)
+    return fail(STAR_EINVAL, "n_inst*(H+2) > 16384 requires a workspace");
   cudaError_t e = launch_project(R, n_inst, inst_base, H, inst, n_tok, n_hat, beta_q, L, W, peak, growth, count,
                                  workspace, err_flag, reinterpret_cast<cudaStream_t>(stream_), nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "project_kernel launch");

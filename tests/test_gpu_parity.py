@@ -71,7 +71,7 @@ def test_projection_bitexact(star, oracle_mod, seed, n, R, H):
     beta = datagen.beta_schedule_q16(H)
     ref = oracle_mod.project(inst, n_tok, n_hat, n, H, beta)
     ws = torch.zeros(star.project_workspace_bytes(n, H), dtype=torch.uint8, device="cuda")
-    for use_ws in (False, True) if n * (H + 2) <= 12288 else (True,):
+    for use_ws in (False, True) if n * (H + 2) <= 16384 else (True,):
         err = torch.zeros(1, dtype=torch.int32, device="cuda")
         out = star.project_instance_load(_dev(inst.astype(np.int32)), _dev(n_tok), _dev(n_hat), n, H,
                                          _dev(beta.astype(np.int32)), workspace=ws if use_ws else None,

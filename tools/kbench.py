@@ -114,6 +114,40 @@ def main():
             if it >= 5:
                 ts.append(e0.elapsed_time(e1) * 1e3 / K)
         res[f"{name}_marginal_us"] = round(statistics.median(ts), 2)
+    # cost of the layer-1 timing events inside the graph: marginal step time without them
+    pred.layer1_timing(False)
+    e0 = torch.cuda.Event(enable_timing=True, external=True)
+    e1 = torch.cuda.Event(enable_timing=True, external=True)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        e0.record()
+        for _ in range(10):
+            step()
+        e1.record()
+    ts = []
+    for it in range(30):
+        g.replay()
+        e1.synchronize()
+        if it >= 5:
+            ts.append(e0.elapsed_time(e1) * 1e3 / 10)
+    res["step_marginal_no_l1_events_us"] = round(statistics.median(ts), 2)
+    # (B) step graph without event nodes; stream events around its launch, flush kernel before
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2):
+        step()
+    for mode in ("cold", "warm"):
+        ts = []
+        for it in range(110):
+            if mode == "cold":
+                flush.fill_(1.0)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            g2.replay()
+            a1.record()
+            a1.synchronize()
+            if it >= 10:
+                ts.append(a0.elapsed_time(a1) * 1e3)
+        res[f"step_streamevents_{mode}_us"] = round(statistics.median(ts), 2)
     print(json.dumps(res))
 
 

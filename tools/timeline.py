@@ -32,3 +32,20 @@ for k, nm in enumerate(names):
     v = v[v > 0] - t0
     if len(v):
         print(f"{k:2d} {nm:14s} min {v.min()/1e3:7.2f}  med {np.median(v)/1e3:7.2f}  max {v.max()/1e3:7.2f} us")
+
+tl1 = pred.timeline(fetch=True, layer1=True).astype(np.int64)
+names1 = ["entry", "prologue", "prod pdl_wait", "mma kb0", "mma kb16", "mma kb32", "mma kb48", "", "", "mma done",
+          "accum ready", "epilogue end", "exit sync"]
+t0 = tl1[:, 0].min()
+print(f"layer 1: ctas={tl1.shape[0]}")
+for k, nm in enumerate(names1):
+    if not nm:
+        continue
+    v = tl1[:, k]
+    v = v[v > 0] - t0
+    if len(v):
+        print(f"{k:2d} {nm:14s} min {v.min()/1e3:7.2f}  med {np.median(v)/1e3:7.2f}  max {v.max()/1e3:7.2f} us")
+print("per-CTA (us from own prologue), leader CTAs 0,2,64:")
+for cta in (0, 2, 64):
+    r = tl1[cta].astype(np.int64)
+    print(cta, [round((r[k] - r[1]) / 1e3, 2) if r[k] else None for k in (2, 3, 4, 5, 6, 9, 10, 11, 12)])
