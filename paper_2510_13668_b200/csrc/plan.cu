@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
 
   pdl_wait();   // inputs come from the projection / all-gather (PDL launch)
+  pdl_launch_dependents();
   // ---- stage inputs in shared memory (all loads issued in parallel) ----
   for (int e = tid; e < n * H1; e += blockDim.x) {   // segment k holds instances [k*n_loc, (k+1)*n_loc)
     const int i = e / H1, t = e % H1;
@@ -183,24 +184,41 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a,
   }
   if (tid == 0) s_nmoves = 0;
   __syncthreads();
-  if (tid == 0) {   // B0/B1/B2[T] = sum_{t<=T} beta_t {1, t, t^2}
-    i128 b0 = 0, b1 = 0, b2 = 0;
-    for (int u = 0; u < H1; ++u) {
-      const i128 bt = (i128)s.beta[u];
-      b0 += bt;
-      b1 += bt * u;
-      b2 += bt * u * u;
-      s.B[u] = b0;
-      s.B[H1 + u] = b1;
-      s.B[2 * H1 + u] = b2;
+  if (warp == nwarps - 1) {   // B0/B1/B2[T] = sum_{t<=T} beta_t {1, t, t^2}: warp scan (last warp)
+    i128 c0 = 0, c1 = 0, c2 = 0;
+    for (int base = 0; base < H1; base += 32) {
+      const int u = base + lane;
+      const i128 bt = u < H1 ? (i128)s.beta[u] : (i128)0;
+      i128 x0 = bt, x1 = bt * u, x2 = bt * u * u;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off), y2 = shfl_up_i128(x2, off);
+        if (lane >= off) {
+          x0 += y0;
+          x1 += y1;
+          x2 += y2;
+        }
+      }
+      x0 += c0;
+      x1 += c1;
+      x2 += c2;
+      if (u < H1) {
+        s.B[u] = x0;
+        s.B[H1 + u] = x1;
+        s.B[2 * H1 + u] = x2;
+      }
+      c0 = shfl_idx_i128(x0, 31);
+      c1 = shfl_idx_i128(x1, 31);
+      c2 = shfl_idx_i128(x2, 31);
     }
   }
+  const int p1_warps = nwarps - 1;   // Phase-1 warps (the last one built B above)
 
   for (int round = 0; round < a.max_moves; ++round) {
     // ---- Phase 1: InstanceClassification ----
     // one warp per instance: W_i (warp reduction) and the Phase-3 prefix sums
     //   P0_i[T] = sum_{t<=T} beta_t L_i[t],  P1_i[T] = sum_{t<=T} t beta_t L_i[t]  (warp scan)
-    for (int i = warp; i < n; i += nwarps) {
+    for (int i = warp; i < n && warp < p1_warps; i += p1_warps) {
       const int64_t* Li = s.Ls + (int64_t)i * H1;
       i128 wpart = 0, c0 = 0, c1 = 0;
       for (int base = 0; base < H1; base += 32) {
@@ -230,23 +248,32 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a,
       if (lane == 0) s.Wv[i] = cur_only ? (i128)s.beta[0] * Li[0] : wpart;
     }
     __syncthreads();
-    if (tid == 0) {
+    if (warp == 0) {   // classification: lanes over instances, ballots build the ordered U list
       i128 wsum = 0;
-      for (int i = 0; i < n; ++i) wsum += s.Wv[i];
+      for (int i = lane; i < n; i += 32) wsum += s.Wv[i];
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) wsum += shfl_xor_i128(wsum, m);
       const i128 rhs = (i128)(a.theta_den + a.theta_num) * wsum;
       bool anyO = false;
-      for (int i = 0; i < n; ++i) {
-        s.inO[i] = ((i128)n * a.theta_den * s.Wv[i] > rhs) ? 1 : 0;
-        anyO |= s.inO[i] != 0;
-      }
       int nU = 0;
-      for (int i = 0; i < n; ++i) {
-        const bool u = !s.inO[i] && ((i128)n * a.theta_den * (i128)65536 * s.Ls[(int64_t)i * H1] < rhs);
-        s.inU[i] = u ? 1 : 0;
-        if (u) s.ulist[nU++] = i;
+      for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        bool o = false, u = false;
+        if (i < n) {
+          o = (i128)n * a.theta_den * s.Wv[i] > rhs;
+          u = !o && ((i128)n * a.theta_den * (i128)65536 * s.Ls[(int64_t)i * H1] < rhs);
+          s.inO[i] = o ? 1 : 0;
+          s.inU[i] = u ? 1 : 0;
+        }
+        anyO |= __any_sync(0xFFFFFFFFu, o) != 0;
+        const uint32_t um = __ballot_sync(0xFFFFFFFFu, u);
+        if (u) s.ulist[nU + __popc(um & ((1u << lane) - 1u))] = i;
+        nU += __popc(um);
       }
-      s_nU = nU;
-      s_stop = anyO ? 0 : 1;
+      if (lane == 0) {
+        s_nU = nU;
+        s_stop = anyO ? 0 : 1;
+      }
     }
     __syncthreads();
     if (s_stop) break;
@@ -398,6 +425,11 @@ cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg,
     cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_bytes = (int)smem;
+  }
+  static bool carve = false;
+  if (!carve) {   // same L1/shared split as the GEMM kernels before it: no SM reconfiguration between launches
+    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    carve = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(1, 1, 1);

@@ -131,6 +131,22 @@ def main():
         if it >= 5:
             ts.append(e0.elapsed_time(e1) * 1e3 / 10)
     res["step_marginal_no_l1_events_us"] = round(statistics.median(ts), 2)
+    for name, fn in (("forward", fwd), ("plan", plan), ("proj", proj)):
+        e0 = torch.cuda.Event(enable_timing=True, external=True)
+        e1 = torch.cuda.Event(enable_timing=True, external=True)
+        gg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gg):
+            e0.record()
+            for _ in range(10):
+                fn()
+            e1.record()
+        ts = []
+        for it in range(30):
+            gg.replay()
+            e1.synchronize()
+            if it >= 5:
+                ts.append(e0.elapsed_time(e1) * 1e3 / 10)
+        res[f"{name}_marginal_no_l1_events_us"] = round(statistics.median(ts), 2)
     # (B) step graph without event nodes; stream events around its launch, flush kernel before
     g2 = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g2):
