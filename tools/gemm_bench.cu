@@ -110,6 +110,36 @@ int main(int argc, char** argv) {
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, umma_gemm_kernel<256, false>, tA, tB256, tC, g);
   };
+  // ---- 1-CTA kernel with cluster split-K ----
+  std::vector<float> ws_buf;
+  float* ws;
+  cudaMalloc(&ws, (size_t)148 * 128 * 256 * 4);
+  for (int S : {2, 4, 8}) {
+    GemmArgs gs = g;
+    gs.splits = S;
+    gs.kb_per_split = (K / 64 + S - 1) / S;
+    gs.ws = ws;
+    gs.tma_store = (256 / S) % 64 == 0;
+    if (m_tiles * (N / 256) * S > 148) continue;
+    auto split = [&]() {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(m_tiles, N / 256, S);
+      cfg.blockDim = dim3(192, 1, 1);
+      cfg.dynamicSmemBytes = GemmSmem<256>::BYTES;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 1;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = S;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      cudaLaunchKernelEx(&cfg, umma_gemm_kernel<256, false>, tA, tB256, tC, gs);
+    };
+    const float w = time_batch(split, nrep, flush, 0), c = time_batch(split, 1, flush, fb);
+    printf("M=%d K=%d N=%d  1-CTA split %d: %.2f us warm (%.0f TF/s), %.2f us cold\n", M, K, N, S, w, flop / w / 1e6, c);
+  }
   float tp_w = time_batch(pair, nrep, flush, 0), tp_c = time_batch(pair, 1, flush, fb);
   float ts_w = time_batch(single, nrep, flush, 0), ts_c = time_batch(single, 1, flush, fb);
   printf("M=%d K=%d N=%d  pair: %.2f us warm (%.0f TF/s), %.2f us cold   1-CTA: %.2f us warm (%.0f TF/s), %.2f us cold\n",
