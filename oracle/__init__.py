@@ -11,6 +11,7 @@ Function map (each cites the passage it follows in oracle.cpp):
   project(...)    PAPER.md:366, 375, 384, 425 (literal O(R*H) loop)
   objective(...)  Eq. 3-4, PAPER.md:368-380 (exact integer Phi*n^2)
   plan(...)       Alg. 1, PAPER.md:405-453 (from-scratch objective per candidate)
+  dispatch(...)   P -> D placement (reading A28), objective from scratch
 """
 from __future__ import annotations
 
@@ -56,6 +57,8 @@ def lib():
                                      C.c_int64, C.c_int64, C.c_uint32, P, I, P, P, P, P, P,
                                      P, P, P, P, P, P]
         _lib.oracle_plan.restype = I
+        _lib.oracle_dispatch.argtypes = [I, I, I, P, P, P, P, I, P, P, C.c_int32, P]
+        _lib.oracle_dispatch.restype = I
     return _lib
 
 
@@ -149,3 +152,18 @@ def plan(params, L, req_id, inst, n_tok, n_hat, pinned=None):
         g = (int(ghi[k]) << 64) | int(glo[k])
         out.append((int(mv[0][k]), int(mv[1][k]), int(mv[2][k]), int(mv[3][k]), g))
     return out
+
+
+DISPATCH_RR, DISPATCH_CURRENT_LOAD, DISPATCH_PROJECTED = 0, 1, 2
+
+
+def dispatch(policy, L, beta_q, n_tok, n_hat, c_mem=None, reserved=None, counter=0):
+    """Places arrivals in order; returns (assign [A] int32 (-1 = not placed), updated L)."""
+    L = np.array(L, dtype=np.int64, copy=True)
+    n, H1 = L.shape
+    A = int(np.asarray(n_tok).shape[0])
+    out = np.zeros(max(A, 1), dtype=np.int32)
+    lib().oracle_dispatch(int(policy), n, H1 - 1, _p(_c(beta_q, np.uint32)), _p(L), _p(_c(c_mem, np.int64)),
+                          _p(_c(reserved, np.int64)), A, _p(_c(n_tok, np.int32)), _p(_c(n_hat, np.int32)),
+                          int(counter), _p(out))
+    return out[:A], L

@@ -134,3 +134,36 @@ def optimal_assignment_phi(n, H, n_tok, n_hat, beta_q, current_only=False):
         if best is None or v < best:
             best = v
     return best
+
+
+def dispatch(policy, L, beta_q, n_tok, n_hat, c_mem=None, reserved=None, counter=0):
+    """P -> D placement in arrival order (reading A28), real-valued
+    objective with exact rationals: for the projected policy every feasible placement is tried
+    and the textbook weighted variance (phi) of the resulting loads is compared."""
+    L = [list(map(int, row)) for row in L]
+    n, H = len(L), len(L[0]) - 1
+    out = []
+    for a, (N, nh) in enumerate(zip(n_tok, n_hat)):
+        N, nh = int(N), int(nh)
+        if policy == 0:
+            best = (counter + a) % n
+        elif policy == 1:
+            best = min(range(n), key=lambda i: (L[i][0], i))
+        else:
+            best, best_phi = -1, None
+            for i in range(n):
+                if c_mem is not None:
+                    res = 0 if reserved is None else int(reserved[i])
+                    if L[i][0] + res + N + nh > int(c_mem[i]):
+                        continue
+                L2 = [row[:] for row in L]
+                for t in range(H + 1):
+                    L2[i][t] += request_load(N, nh, t)
+                ph = phi(L2, beta_q)
+                if best < 0 or ph < best_phi:
+                    best, best_phi = i, ph
+        out.append(best)
+        if best >= 0:
+            for t in range(H + 1):
+                L[best][t] += request_load(N, nh, t)
+    return out, L

@@ -273,4 +273,53 @@ int oracle_plan(int n, int H, int max_moves, int32_t theta_num, int32_t theta_de
   return nm;
 }
 
+// ---------------------------------------------------------------------------------
+// P -> D dispatch of newly prefilled requests (NEXT-2; "forwarded to a decode
+// instance according to its input length, predicted output length, and the current load";
+// baselines PAPER.md:98-99).  Arrivals a = 0..A-1 are placed in order.
+//   policy 0 (round robin):   i = (counter + a) mod n
+//   policy 1 (current load):  i = argmin_i L_i[0]                 (ties -> lowest id)
+//   policy 2 (projected, STAR, reading A28): among instances passing the memory filter
+//     L_i[0] + reserved_i + N + N_hat <= C_mem_i (reading A18; c_mem NULL -> all), the one whose
+//     objective Phi (Eq. 3-4, exact integer Phi*n^2) AFTER placing the request is smallest
+//     (ties -> lowest id); none feasible -> -1 (not placed).  The objective is recomputed from
+//     scratch for every candidate placement.
+// The chosen instance's loads are updated with the request's contribution c_r[t] (reading A5)
+// before the next arrival.  Returns the number placed.
+// ---------------------------------------------------------------------------------
+int oracle_dispatch(int policy, int n, int H, const uint32_t* beta_q, int64_t* L, const int64_t* c_mem,
+                    const int64_t* reserved, int A, const int32_t* n_tok, const int32_t* n_hat, int32_t counter,
+                    int32_t* assign) {
+  std::vector<int64_t> Lv(L, L + (long)n * (H + 1));
+  int placed = 0;
+  for (int a = 0; a < A; ++a) {
+    int best = -1;
+    if (policy == 0) {
+      best = (int)(((int64_t)counter + a) % n);
+    } else if (policy == 1) {
+      for (int i = 0; i < n; ++i)
+        if (best < 0 || Lv[(long)i * (H + 1)] < Lv[(long)best * (H + 1)]) best = i;
+    } else {
+      i128 best_phi = 0;
+      for (int i = 0; i < n; ++i) {
+        if (c_mem) {
+          i128 need = (i128)Lv[(long)i * (H + 1)] + (reserved ? reserved[i] : 0) + n_tok[a] + n_hat[a];
+          if (!(need <= (i128)c_mem[i])) continue;
+        }
+        std::vector<int64_t> L2 = Lv;
+        for (int t = 0; t <= H; ++t) L2[(long)i * (H + 1) + t] += contrib(n_tok[a], n_hat[a], t);
+        i128 ph = phi_n2(n, H, L2, beta_q, false);
+        if (best < 0 || ph < best_phi) { best = i; best_phi = ph; }
+      }
+    }
+    assign[a] = best;
+    if (best >= 0) {
+      for (int t = 0; t <= H; ++t) Lv[(long)best * (H + 1) + t] += contrib(n_tok[a], n_hat[a], t);
+      ++placed;
+    }
+  }
+  for (long k = 0; k < (long)n * (H + 1); ++k) L[k] = Lv[k];
+  return placed;
+}
+
 }  // extern "C"

@@ -392,3 +392,72 @@ def test_plan_current_only_max_to_min(oracle_mod):
     p0 = datagen.PlanParams(n_inst=3, H=0, beta_q=beta[:1], max_moves=1)
     P0 = oracle_mod.project(inst, n_tok, n_hat, 3, 0, beta[:1])
     assert oracle_mod.plan(p0, P0["L"], np.arange(5, dtype=np.int32), inst, n_tok, n_hat) == []
+
+
+# =============================================================================== P -> D dispatch (NEXT-2)
+def test_dispatch_round_robin_spec_examples(oracle_mod):
+    """counter 0, n 3 -> 0; counter 7, n 3 -> 1; 300 assignments -> 100 each."""
+    L = np.zeros((3, 3), np.int64)
+    beta = datagen.beta_schedule_q16(2)
+    a, _ = oracle_mod.dispatch(0, L, beta, [5], [5], counter=0)
+    assert a.tolist() == [0]
+    a, _ = oracle_mod.dispatch(0, L, beta, [5], [5], counter=7)
+    assert a.tolist() == [1]
+    a, _ = oracle_mod.dispatch(0, L, beta, [5] * 300, [5] * 300, counter=0)
+    assert np.bincount(a, minlength=3).tolist() == [100, 100, 100]
+
+
+def test_dispatch_current_load_spec_examples(oracle_mod):
+    """loads [500,200,900] -> 1; [200,200,900] -> 0 (lowest id); after assigning a
+    request of N tokens the re-query sees the increased load (two-step fixture)."""
+    beta = datagen.beta_schedule_q16(0)
+    a, _ = oracle_mod.dispatch(1, np.array([[500], [200], [900]]), beta, [10], [1])
+    assert a.tolist() == [1]
+    a, _ = oracle_mod.dispatch(1, np.array([[200], [200], [900]]), beta, [10], [1])
+    assert a.tolist() == [0]
+    a, L = oracle_mod.dispatch(1, np.array([[200], [150], [900]]), beta, [100, 10], [1, 1])
+    assert a.tolist() == [1, 0] and L[:, 0].tolist() == [210, 250, 900]
+
+
+def test_dispatch_projected_closed_forms(oracle_mod):
+    """Projected policy (reading A28): (i) with N_hat <= 1 only t = 0 carries the request, so the
+    choice is the current-load argmin; (ii) identical instances -> lowest id; (iii) a long request
+    avoids the instance whose FUTURE load is high even though its current load is lower
+    (the paper's point: current load alone misleads)."""
+    beta = datagen.beta_schedule_q16(4)
+    L = np.array([[300, 0, 0, 0, 0], [100, 100, 100, 100, 100], [200, 10, 10, 10, 10]], np.int64)
+    a, _ = oracle_mod.dispatch(2, L, beta, [50], [1])
+    assert a.tolist() == [1]                                    # (i) argmin L[0]
+    a, _ = oracle_mod.dispatch(2, np.zeros((3, 5), np.int64), beta, [50], [9])
+    assert a.tolist() == [0]                                    # (ii)
+    a, _ = oracle_mod.dispatch(2, L, beta, [50], [100])
+    assert a.tolist() == [2]                                    # (iii) hand-checked below
+    # hand check of (iii): score_i = sum_t beta_t (50+t) L_i[t] over t = 0..4
+    sc = [sum(int(beta[t]) * (50 + t) * int(L[i][t]) for t in range(5)) for i in range(3)]
+    assert int(np.argmin(sc)) == 2
+    # memory filter (reading A18): 200 + 50 + 100 = 350 > 349 excludes instance 2 -> next best (0)
+    a, _ = oracle_mod.dispatch(2, L, beta, [50], [100], c_mem=np.array([10**9, 10**9, 349]))
+    assert a.tolist() == [0]
+    a, _ = oracle_mod.dispatch(2, L, beta, [50], [100], c_mem=np.array([10**9, 10**9, 350]))
+    assert a.tolist() == [2]                                    # boundary: exactly C_mem is admitted
+    a, L2 = oracle_mod.dispatch(2, L, beta, [50], [100], c_mem=np.array([1, 1, 1]))
+    assert a.tolist() == [-1] and np.array_equal(L2, L)       # nowhere feasible: not placed
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_dispatch_matches_brute_force(oracle_mod, seed):
+    """Exact-integer oracle == exact-rational brute force (real beta, textbook variance) on tiny
+    random batches, all three policies, with and without the memory filter."""
+    g = datagen.rng(7000 + seed)
+    n, H, A = int(g.integers(1, 5)), int(g.integers(0, 6)), int(g.integers(0, 8))
+    L = g.integers(0, 200, (n, H + 1)).astype(np.int64)
+    beta = np.concatenate([[65536], g.integers(1, 65537, H)]).astype(np.uint32)
+    n_tok = g.integers(1, 60, A).astype(np.int32)
+    n_hat = g.integers(0, H + 3, A).astype(np.int32)
+    c_mem = g.integers(100, 600, n).astype(np.int64) if seed % 2 else None
+    reserved = g.integers(0, 50, n).astype(np.int64) if seed % 3 == 0 else None
+    for policy in (0, 1, 2):
+        a, L_o = oracle_mod.dispatch(policy, L, beta, n_tok, n_hat, c_mem, reserved, counter=seed)
+        b, L_b = brute.dispatch(policy, L, beta, n_tok, n_hat, c_mem, reserved, counter=seed)
+        assert a.tolist() == b
+        assert L_o.tolist() == L_b
