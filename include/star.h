@@ -233,6 +233,34 @@ star_status plan_reschedule_segmented(const star_plan_params* p, const star_plan
                                       star_move* moves, int32_t* n_moves, int32_t* err_flag,
                                       star_stream_t stream);
 
+/* =====================================================================================
+ * P -> D dispatch of newly prefilled requests  (NEXT-2; a request "will be
+ * forwarded to a decode instance according to its input length, predicted output length, and
+ * the current load of each decode instance"; baselines PAPER.md:98-99)
+ * Arrivals a = 0..A-1 (n_tok[a] = N, n_hat[a] = predicted remaining length) are placed in
+ * order; the chosen instance's loads L [n_inst][H+1] (device, in/out: the projected loads of
+ * project_instance_load) get the request's contribution (c_0 = N, c_t = (N+t)[t < N_hat]) before
+ * the next arrival is placed.  assign[a] = instance, or -1 when no instance is feasible.
+ *   STAR_DISPATCH_ROUND_ROBIN   (counter + a) mod n_inst
+ *   STAR_DISPATCH_CURRENT_LOAD  argmin L[i][0], ties -> lowest id
+ *   STAR_DISPATCH_PROJECTED     (reading A28) among instances with
+ *                               L[i][0] + reserved[i] + N + N_hat <= c_mem[i] (c_mem NULL -> all),
+ *                               the one minimising the Eq. 3-4 objective after the placement
+ *                               (exact integers: argmin sum_{t<=T} beta_q[t] (N+t) L[i][t]),
+ *                               ties -> lowest id.  Needs `workspace`
+ *                               (star_dispatch_workspace_bytes(n_inst, H) bytes, no init).
+ * One CTA; sequential over arrivals by definition.  A = 0 enqueues nothing.
+ * ===================================================================================== */
+#define STAR_DISPATCH_ROUND_ROBIN  0
+#define STAR_DISPATCH_CURRENT_LOAD 1
+#define STAR_DISPATCH_PROJECTED    2
+
+size_t star_dispatch_workspace_bytes(int n_inst, int H);
+star_status dispatch_requests(int policy, int n_inst, int H, const uint32_t* beta_q, int64_t* L,
+                              const int64_t* c_mem, const int64_t* reserved, int A, const int32_t* n_tok,
+                              const int32_t* n_hat, int32_t counter, int32_t* assign, void* workspace,
+                              star_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,10 +8,11 @@ Public API (names follow the C ABI in include/star.h):
 Importing the package does not load the CUDA library; the first call does, and raises
 StarError if it is missing (there is no CPU fallback).
 """
-from ._lib import (CURRENT_ONLY, L_CTX, STRICT_MEM, Predictor, PlanParams, ProjectOut, StarError,  # noqa: F401
+from ._lib import (DISPATCH_CURRENT_LOAD, DISPATCH_PROJECTED, DISPATCH_ROUND_ROBIN, dispatch_requests,  # noqa: F401
+                   CURRENT_ONLY, L_CTX, STRICT_MEM, Predictor, PlanParams, ProjectOut, StarError,  # noqa: F401
                    alloc_moves, decode_moves, lenpred_forward, lenpred_forward_project, lenpred_quantize, plan_reschedule,
                    plan_reschedule_segmented, project_instance_load, project_workspace_bytes, version)
 
 __all__ = ["Predictor", "lenpred_forward", "lenpred_forward_project", "lenpred_quantize", "project_instance_load", "PlanParams",
            "plan_reschedule", "plan_reschedule_segmented", "decode_moves", "alloc_moves", "StarError",
-           "project_workspace_bytes", "version", "STRICT_MEM", "CURRENT_ONLY", "L_CTX", "ProjectOut"]
+           "project_workspace_bytes", "version", "dispatch_requests", "STRICT_MEM", "CURRENT_ONLY", "L_CTX", "ProjectOut"]

@@ -68,6 +68,8 @@ def lib() -> C.CDLL:
         "project_instance_load": ([I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P], I),
         "plan_reschedule": ([C.POINTER(PlanParamsC), P, I, P, P, P, P, P, P, P, P, P], I),
         "plan_reschedule_segmented": ([C.POINTER(PlanParamsC), C.POINTER(PlanSegmentsC), P, P, P, P], I),
+        "star_dispatch_workspace_bytes": ([I, I], C.c_size_t),
+        "dispatch_requests": ([I, I, I, P, P, P, P, I, P, P, I32, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -323,3 +325,28 @@ def plan_reschedule_segmented(params: PlanParams, seg: PlanSegmentsC, moves=None
     _check(lib().plan_reschedule_segmented(C.byref(params.c), C.byref(seg), _ptr(moves), _ptr(n_moves),
                                            _ptr(err_flag), _stream(stream)), "plan_reschedule_segmented")
     return moves, n_moves
+
+
+# ================================================================ P -> D dispatch (NEXT-2)
+DISPATCH_ROUND_ROBIN, DISPATCH_CURRENT_LOAD, DISPATCH_PROJECTED = 0, 1, 2
+
+
+def dispatch_requests(policy: int, L: torch.Tensor, beta_q: torch.Tensor, n_tok: torch.Tensor, n_hat: torch.Tensor,
+                      c_mem: Optional[torch.Tensor] = None, reserved: Optional[torch.Tensor] = None,
+                      counter: int = 0, assign: Optional[torch.Tensor] = None,
+                      workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Places the arrivals in order (star.h dispatch_requests); L is updated in place."""
+    _req(L, torch.int64, "L")
+    for n_, t in (("beta_q", beta_q), ("n_tok", n_tok), ("n_hat", n_hat)):
+        _req(t, torch.int32, n_)
+    n_inst, H1 = L.shape
+    A = int(n_tok.shape[0])
+    if assign is None:
+        assign = torch.empty(max(A, 1), dtype=torch.int32, device=L.device)
+    if workspace is None and policy == DISPATCH_PROJECTED:
+        workspace = torch.empty(int(lib().star_dispatch_workspace_bytes(n_inst, H1 - 1)), dtype=torch.uint8,
+                                device=L.device)
+    _check(lib().dispatch_requests(int(policy), n_inst, H1 - 1, _ptr(beta_q), _ptr(L), _ptr(c_mem), _ptr(reserved),
+                                   A, _ptr(n_tok), _ptr(n_hat), int(counter), _ptr(assign), _ptr(workspace),
+                                   _stream(stream)), "dispatch_requests")
+    return assign[:A]

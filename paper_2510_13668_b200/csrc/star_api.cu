@@ -664,6 +664,32 @@ star_status project_instance_load(int R, int n_inst, int inst_base, int H, const
   return STAR_OK;
 }
 
+size_t star_dispatch_workspace_bytes(int n_inst, int H) {
+  if (n_inst < 1 || H < 0) return 0;
+  return dispatch_workspace_bytes(n_inst, H);
+}
+
+star_status dispatch_requests(int policy, int n_inst, int H, const uint32_t* beta_q, int64_t* L, const int64_t* c_mem,
+                              const int64_t* reserved, int A, const int32_t* n_tok, const int32_t* n_hat,
+                              int32_t counter, int32_t* assign, void* workspace, star_stream_t stream_) {
+  star_status s = ensure_device();
+  if (s != STAR_OK) return s;
+  if (policy < STAR_DISPATCH_ROUND_ROBIN || policy > STAR_DISPATCH_PROJECTED)
+    return fail(STAR_EINVAL, "unknown dispatch policy %d", policy);
+  if (n_inst < 1 || n_inst > (1 << 16)) return fail(STAR_ERANGE, "n_inst=%d outside [1, 65536]", n_inst);
+  if (H < 0 || H > 256) return fail(STAR_ERANGE, "H=%d outside [0, 256]", H);
+  if (A < 0) return fail(STAR_EINVAL, "A < 0");
+  if (counter < 0) return fail(STAR_EINVAL, "counter < 0");
+  if (A == 0) return STAR_OK;
+  if (!L || !beta_q || !n_tok || !n_hat || !assign) return fail(STAR_EINVAL, "L, beta_q, n_tok, n_hat, assign must be non-NULL");
+  if (policy == STAR_DISPATCH_PROJECTED && !workspace)
+    return fail(STAR_EINVAL, "the projected policy needs a workspace of star_dispatch_workspace_bytes()");
+  cudaError_t e = launch_dispatch(policy, n_inst, H, beta_q, L, c_mem, reserved, A, n_tok, n_hat, counter, assign,
+                                  workspace, reinterpret_cast<cudaStream_t>(stream_));
+  if (e != cudaSuccess) return cuda_fail(e, "dispatch_kernel launch");
+  return STAR_OK;
+}
+
 static star_status check_plan_params(const star_plan_params* p) {
   if (!p) return fail(STAR_EINVAL, "params is NULL");
   if (p->n_inst < 1) return fail(STAR_EINVAL, "n_inst < 1");

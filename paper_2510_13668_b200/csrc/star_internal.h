@@ -28,4 +28,10 @@ size_t plan_smem_bytes(int n, int H, int world, int r_cap);
 cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg, star_move* moves, int32_t* n_moves,
                         int32_t* err_flag, cudaStream_t stream);
 
+// dispatch.cu
+size_t dispatch_workspace_bytes(int n, int H);
+cudaError_t launch_dispatch(int policy, int n, int H, const uint32_t* beta_q, int64_t* L, const int64_t* c_mem,
+                            const int64_t* reserved, int A, const int32_t* n_tok, const int32_t* n_hat,
+                            int32_t counter, int32_t* assign, void* workspace, cudaStream_t stream);
+
 }  // namespace star

@@ -298,3 +298,44 @@ def test_fused_forward_project_equals_standalone(star, oracle_mod, cfg, R, seed)
     torch.cuda.synchronize()
     assert np.array_equal(out3.L.cpu().numpy(), out1.L.cpu().numpy())
     pred.close()
+
+
+# ============================================================================ P -> D dispatch (NEXT-2)
+@pytest.mark.parametrize("seed", range(40))
+def test_dispatch_bitexact_tiny(star, oracle_mod, seed):
+    g = datagen.rng(9000 + seed)
+    n, H, A = int(g.integers(1, 9)), int(g.integers(0, 12)), int(g.integers(0, 20))
+    L = g.integers(0, 5000, (n, H + 1)).astype(np.int64)
+    beta = np.concatenate([[65536], g.integers(1, 65537, H)]).astype(np.uint32)
+    n_tok = g.integers(1, 3000, A).astype(np.int32)
+    n_hat = g.integers(0, H + 5, A).astype(np.int32)
+    c_mem = g.integers(2000, 12000, n).astype(np.int64) if seed % 2 else None
+    reserved = g.integers(0, 500, n).astype(np.int64) if seed % 3 == 0 else None
+    for policy in (0, 1, 2):
+        ref_a, ref_L = oracle_mod.dispatch(policy, L, beta, n_tok, n_hat, c_mem, reserved, counter=seed)
+        Ld = _dev(L)
+        got = star.dispatch_requests(policy, Ld, _dev(beta.astype(np.int32)), _dev(n_tok), _dev(n_hat),
+                                     None if c_mem is None else _dev(c_mem),
+                                     None if reserved is None else _dev(reserved), counter=seed)
+        torch.cuda.synchronize()
+        assert got.cpu().numpy().tolist() == ref_a.tolist(), policy
+        assert np.array_equal(Ld.cpu().numpy(), ref_L), policy
+
+
+@pytest.mark.parametrize("n,A", [(8, 64), (64, 256), (256, 64)])
+def test_dispatch_bitexact_cluster_scale(star, oracle_mod, n, A):
+    """Projected loads of a real snapshot (8 .. 256 instances, H = 50) + a burst of arrivals with
+    long-tailed predicted lengths; all policies bit-exact vs the from-scratch oracle."""
+    snap = datagen.make_snapshot(n, n, 32)
+    beta = datagen.beta_schedule_q16(50)
+    L = oracle_mod.project(snap.inst, snap.n_tok, snap.true_rem, n, 50, beta)["L"]
+    arr = datagen.make_snapshot(n + 1, 1, A)
+    c_mem = np.full(n, int(L[:, 0].mean() * 1.05), np.int64)
+    for policy in (0, 1, 2):
+        ref_a, ref_L = oracle_mod.dispatch(policy, L, beta, arr.n_tok, arr.true_rem, c_mem, None, counter=3)
+        Ld = _dev(L)
+        got = star.dispatch_requests(policy, Ld, _dev(beta.astype(np.int32)), _dev(arr.n_tok),
+                                     _dev(arr.true_rem.astype(np.int32)), _dev(c_mem), counter=3)
+        torch.cuda.synchronize()
+        assert got.cpu().numpy().tolist() == ref_a.tolist(), policy
+        assert np.array_equal(Ld.cpu().numpy(), ref_L), policy
