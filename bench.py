@@ -508,6 +508,11 @@ def run_star(args):
             line["roofline_projection"] = projection_sweep(star, snap, params_h_dev(star, params_h, dev), dev, peaks)
         except Exception as ex:  # keep the bench line
             line["roofline_projection"] = {"error": str(ex)}
+    if rank == 0 and not args.profile and not args.no_sweep:
+        try:
+            line["next_rows"] = next_rows_timing(star, dev)
+        except Exception as ex:
+            line["next_rows"] = {"error": str(ex)}
     if world == 1 and not args.no_cpu_baseline and not args.profile and rank == 0:
         try:
             line["cpu_baseline"] = cpu_baseline(args.config, args.seed, args.cpu_seconds)
@@ -522,6 +527,59 @@ def run_star(args):
         torch.distributed.destroy_process_group()
     pred.close()
     return 0
+
+
+def next_rows_timing(star, dev, seed=0):
+    """NEXT rows at the paper's cluster scale, timed with CUDA events (warm, median of 20):
+    the multi-CTA plan over 256 instances x 64 requests (H = 50; the paper budgets <= 300 ms at
+    256 instances) and the projected P->D dispatch of 64 arrivals onto them."""
+    import torch
+    import datagen
+    n, r_per = 256, 64
+    snap = datagen.make_snapshot(seed + 77, n, r_per)
+    out = {}
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    beta = datagen.beta_schedule_q16(50)
+    proj = star.project_instance_load(d(snap.inst), d(snap.n_tok), d(snap.true_rem.astype(np.int32)), n, 50,
+                                      d(beta.astype(np.int32)),
+                                      workspace=torch.zeros(star.project_workspace_bytes(n, 50), dtype=torch.uint8,
+                                                            device=dev))
+    for mm in (1, 4):
+        ph = datagen.make_plan_params(snap, max_moves=mm)
+        pp = star.PlanParams.from_host(ph, device=dev)
+        ws = torch.empty(star.plan_workspace_bytes(n, 50, snap.R), dtype=torch.uint8, device=dev)
+        moves, nm = star.alloc_moves(mm, dev)
+        args = (pp, proj.L, d(snap.req_id), d(snap.inst), d(snap.n_tok), d(snap.true_rem.astype(np.int32)))
+        fn = lambda: star.plan_reschedule_large(*args, moves=moves, n_moves=nm, workspace=ws)
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(20):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3)
+        out[f"plan_256x64_max_moves_{mm}_us"] = round(float(np.median(ts)), 2)
+        out[f"plan_256x64_max_moves_{mm}_moves"] = int(nm.item())
+    arr = datagen.make_snapshot(seed + 78, 1, 64)
+    L0 = proj.L.clone()
+    ts = []
+    for _ in range(20):
+        L1 = L0.clone()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        star.dispatch_requests(star.DISPATCH_PROJECTED, L1, d(beta.astype(np.int32)), d(arr.n_tok),
+                               d(arr.true_rem.astype(np.int32)))
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    out["dispatch_projected_64_arrivals_onto_256_us"] = round(float(np.median(ts)), 2)
+    out["note"] = ("paper: scheduler <= 300 ms at 256 instances (PAPER.md:460); NEXT rows of SURVEY 8(f), "
+                   "bit-exact vs the oracle in tests/test_gpu_parity.py")
+    return out
 
 
 def params_h_dev(star, params_h, dev):

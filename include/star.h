@@ -233,6 +233,18 @@ star_status plan_reschedule_segmented(const star_plan_params* p, const star_plan
                                       star_move* moves, int32_t* n_moves, int32_t* err_flag,
                                       star_stream_t stream);
 
+/* Cluster-scale form (NEXT-3: hundreds of instances, up to 2^20 request slots; the paper's
+ * budget is <= 300 ms at 256 instances): identical semantics and outputs, but the
+ * state lives in `workspace` (star_plan_workspace_bytes(n_inst, H, world*r_cap) bytes, no
+ * initialisation needed) and each round runs as two multi-CTA launches (per-instance prefix
+ * sums; candidate scan over all SMs + last-CTA selection), so n_inst is limited only by
+ * 16384 and by memory, not by one SM's shared memory.  workspace == NULL falls back to
+ * plan_reschedule_segmented (single CTA). */
+size_t star_plan_workspace_bytes(int n_inst, int H, int64_t request_slots);
+star_status plan_reschedule_segmented_ws(const star_plan_params* p, const star_plan_segments* seg,
+                                         star_move* moves, int32_t* n_moves, int32_t* err_flag, void* workspace,
+                                         star_stream_t stream);
+
 /* =====================================================================================
  * P -> D dispatch of newly prefilled requests  (NEXT-2; a request "will be
  * forwarded to a decode instance according to its input length, predicted output length, and

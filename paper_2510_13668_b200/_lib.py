@@ -69,6 +69,8 @@ def lib() -> C.CDLL:
         "plan_reschedule": ([C.POINTER(PlanParamsC), P, I, P, P, P, P, P, P, P, P, P], I),
         "plan_reschedule_segmented": ([C.POINTER(PlanParamsC), C.POINTER(PlanSegmentsC), P, P, P, P], I),
         "star_dispatch_workspace_bytes": ([I, I], C.c_size_t),
+        "star_plan_workspace_bytes": ([I, I, I64], C.c_size_t),
+        "plan_reschedule_segmented_ws": ([C.POINTER(PlanParamsC), C.POINTER(PlanSegmentsC), P, P, P, P, P], I),
         "dispatch_requests": ([I, I, I, P, P, P, P, I, P, P, I32, P, P, P], I),
     }
     for name, (args, res) in sig.items():
@@ -315,6 +317,42 @@ def plan_reschedule(params: PlanParams, L: torch.Tensor, req_id, inst, n_tok, n_
     _check(lib().plan_reschedule(C.byref(params.c), _ptr(L), R, _ptr(req_id), _ptr(inst), _ptr(n_tok), _ptr(n_hat),
                                  _ptr(pinned), _ptr(moves), _ptr(n_moves), _ptr(err_flag), _stream(stream)),
            "plan_reschedule")
+    return moves, n_moves
+
+
+def plan_workspace_bytes(n_inst: int, H: int, request_slots: int) -> int:
+    return int(lib().star_plan_workspace_bytes(n_inst, H, request_slots))
+
+
+def plan_reschedule_large(params: PlanParams, L: torch.Tensor, req_id, inst, n_tok, n_hat, pinned=None,
+                          moves=None, n_moves=None, err_flag=None, workspace=None, R_total: Optional[int] = None,
+                          stream=None):
+    """Cluster-scale multi-CTA plan (star.h plan_reschedule_segmented_ws) on a contiguous state."""
+    _req(L, torch.int64, "L")
+    for n_, t in (("req_id", req_id), ("inst", inst), ("n_tok", n_tok), ("n_hat", n_hat)):
+        _req(t, torch.int32, n_)
+    if pinned is not None:
+        _req(pinned, torch.uint8, "pinned")
+    if moves is None:
+        moves, n_moves = alloc_moves(params.max_moves, L.device)
+    R = req_id.shape[0] if R_total is None else R_total
+    if workspace is None:
+        workspace = torch.empty(plan_workspace_bytes(params.n_inst, params.H, R), dtype=torch.uint8, device=L.device)
+    seg = PlanSegmentsC(1, params.n_inst, R, 0, _ptr(L), None, _ptr(req_id), _ptr(inst), _ptr(n_tok), _ptr(n_hat),
+                        _ptr(pinned))
+    _check(lib().plan_reschedule_segmented_ws(C.byref(params.c), C.byref(seg), _ptr(moves), _ptr(n_moves),
+                                              _ptr(err_flag), _ptr(workspace), _stream(stream)),
+           "plan_reschedule_segmented_ws")
+    return moves, n_moves
+
+
+def plan_reschedule_segmented_ws(params: PlanParams, seg: PlanSegmentsC, workspace: torch.Tensor, moves=None,
+                                 n_moves=None, err_flag=None, stream=None):
+    if moves is None:
+        moves, n_moves = alloc_moves(params.max_moves, "cuda")
+    _check(lib().plan_reschedule_segmented_ws(C.byref(params.c), C.byref(seg), _ptr(moves), _ptr(n_moves),
+                                              _ptr(err_flag), _ptr(workspace), _stream(stream)),
+           "plan_reschedule_segmented_ws")
     return moves, n_moves
 
 

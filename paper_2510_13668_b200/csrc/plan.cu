@@ -16,91 +16,13 @@
 // (gain desc, req_id asc, dst asc) (reading A20).  Greedy rounds (reading A21).
 #include <cstdint>
 #include <cuda_runtime.h>
+#include "plan_core.cuh"
 #include "ptx.cuh"
 #include "star_internal.h"
 
 namespace star {
 
-typedef __int128 i128;
 constexpr int kPlanThreads = 512;
-
-struct PlanArgs {
-  int n, H, max_moves;
-  int32_t theta_num, theta_den;
-  const uint32_t* beta_q;
-  const int64_t* c_mem;
-  const int64_t* reserved;
-  int64_t a_ps, b_ps, c0_ps, c1_ps;
-  uint32_t flags;
-  int world, n_loc, r_cap;
-  int64_t seg_stride;
-  const int64_t* L;
-  const int32_t* r_count;   // nullptr -> every segment holds r_cap requests
-  const int32_t* req_id;
-  const int32_t* inst;
-  const int32_t* n_tok;
-  const int32_t* n_hat;
-  const uint8_t* pinned;
-  star_move* moves;
-  int32_t* n_moves;
-  int32_t* err;
-};
-
-template <typename T>
-__device__ __forceinline__ const T* seg_ptr(const T* base, int k, int64_t stride) {
-  return reinterpret_cast<const T*>(reinterpret_cast<const uint8_t*>(base) + (int64_t)k * stride);
-}
-
-struct Cand {
-  i128 score;
-  int32_t id, dst, g;   // g = flat request slot (k * r_cap + j), -1 = none
-};
-
-__device__ __forceinline__ bool cand_better(const Cand& x, const Cand& y) {  // x strictly better than y
-  if (x.g < 0) return false;
-  if (y.g < 0) return true;
-  if (x.score != y.score) return x.score > y.score;
-  if (x.id != y.id) return x.id < y.id;
-  return x.dst < y.dst;
-}
-
-__device__ __forceinline__ Cand shfl_cand(const Cand& c, int src_lane) {
-  Cand o;
-  const uint64_t lo = (uint64_t)c.score, hi = (uint64_t)(c.score >> 64);
-  const uint64_t lo2 = __shfl_sync(0xFFFFFFFFu, lo, src_lane);
-  const uint64_t hi2 = __shfl_sync(0xFFFFFFFFu, hi, src_lane);
-  o.score = (i128)(((unsigned __int128)hi2 << 64) | lo2);
-  o.id = __shfl_sync(0xFFFFFFFFu, c.id, src_lane);
-  o.dst = __shfl_sync(0xFFFFFFFFu, c.dst, src_lane);
-  o.g = __shfl_sync(0xFFFFFFFFu, c.g, src_lane);
-  return o;
-}
-
-__device__ __forceinline__ Cand warp_argmax(Cand c) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    Cand o = shfl_cand(c, lane ^ off);
-    if (cand_better(o, c)) c = o;
-  }
-  return c;
-}
-
-__device__ __forceinline__ i128 shfl_up_i128(i128 v, int off) {
-  const unsigned long long lo = __shfl_up_sync(0xFFFFFFFFu, (unsigned long long)v, off);
-  const long long hi = __shfl_up_sync(0xFFFFFFFFu, (long long)(v >> 64), off);
-  return (i128)(((unsigned __int128)(unsigned long long)hi << 64) | lo);
-}
-__device__ __forceinline__ i128 shfl_idx_i128(i128 v, int src) {
-  const unsigned long long lo = __shfl_sync(0xFFFFFFFFu, (unsigned long long)v, src);
-  const long long hi = __shfl_sync(0xFFFFFFFFu, (long long)(v >> 64), src);
-  return (i128)(((unsigned __int128)(unsigned long long)hi << 64) | lo);
-}
-__device__ __forceinline__ i128 shfl_xor_i128(i128 v, int m) {
-  const unsigned long long lo = __shfl_xor_sync(0xFFFFFFFFu, (unsigned long long)v, m);
-  const long long hi = __shfl_xor_sync(0xFFFFFFFFu, (long long)(v >> 64), m);
-  return (i128)(((unsigned __int128)(unsigned long long)hi << 64) | lo);
-}
 
 // Shared-memory state of the plan (dynamic part; see plan_smem_bytes for the layout).
 struct PlanSmem {
@@ -299,35 +221,8 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a,
       const int64_t N = staged ? s.rntok[g] : seg_ptr(a.n_tok, k, a.seg_stride)[j];
       const int64_t nh = staged ? s.rnhat[g] : seg_ptr(a.n_hat, k, a.seg_stride)[j];
       const int32_t rid = staged ? s.rid[g] : seg_ptr(a.req_id, k, a.seg_stride)[j];
-      int T = (int)(nh - 1 < 0 ? 0 : (nh - 1 > a.H ? a.H : nh - 1));
-      if (cur_only) T = 0;
-      const i128 self = (i128)N * N * s.B[T] + (i128)2 * N * s.B[H1 + T] + s.B[2 * H1 + T];
-      const i128 src_part = (i128)N * s.P0[(int64_t)src * H1 + T] + s.P1[(int64_t)src * H1 + T];
-      const i128 mig = (i128)a.c0_ps + (i128)a.c1_ps * N;
-      for (int q = 0; q < nU; ++q) {
-        const int u = s.ulist[q];
-        const int64_t Lu0 = s.Ls[(int64_t)u * H1];
-        if (!cur_only) {  // filter (a): N_hat * T_exec(u) > C_mig(r)
-          if (!((i128)nh * ((i128)a.a_ps + (i128)a.b_ps * Lu0) > mig)) continue;
-        }
-        if (a.c_mem) {    // filter (b): memory safety on the target
-          i128 need = Lu0;
-          if (strict) {
-            if (!cur_only) need += nh;
-          } else {
-            need += (a.reserved ? a.reserved[u] : 0) + N + (cur_only ? 0 : nh);
-          }
-          if (!(need <= (i128)a.c_mem[u])) continue;
-        }
-        const i128 score = src_part - ((i128)N * s.P0[(int64_t)u * H1 + T] + s.P1[(int64_t)u * H1 + T]) - self;
-        if (score <= 0) continue;
-        Cand c;
-        c.score = score;
-        c.id = rid;
-        c.dst = u;
-        c.g = g;
-        if (cand_better(c, best)) best = c;
-      }
+      const Cand c = best_target(a, strict, cur_only, g, src, N, nh, rid, s.ulist, nU, s.Ls, s.P0, s.P1, s.B, H1);
+      if (cand_better(c, best)) best = c;
     }
     best = warp_argmax(best);
     if (lane == 0) warp_best[warp] = best;
@@ -386,8 +281,8 @@ static size_t plan_smem_layout(int n, int H, int world, int r_cap, bool staged) 
 // Minimum dynamic shared memory (request table read from global memory).
 size_t plan_smem_bytes(int n, int H, int world, int r_cap) { return plan_smem_layout(n, H, world, r_cap, false); }
 
-cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg, star_move* moves, int32_t* n_moves,
-                        int32_t* err_flag, cudaStream_t stream) {
+PlanArgs make_plan_args(const star_plan_params* p, const star_plan_segments* sg, star_move* moves, int32_t* n_moves,
+                        int32_t* err_flag) {
   PlanArgs a{};
   a.n = p->n_inst;
   a.H = p->H;
@@ -416,6 +311,12 @@ cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg,
   a.moves = moves;
   a.n_moves = n_moves;
   a.err = err_flag;
+  return a;
+}
+
+cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg, star_move* moves, int32_t* n_moves,
+                        int32_t* err_flag, cudaStream_t stream) {
+  const PlanArgs a = make_plan_args(p, sg, moves, n_moves, err_flag);
   // Stage the request table in shared memory when it fits (it is re-read every round).
   const size_t lim = (size_t)kMaxSmemBytes - 4096;   // static shared memory + slack
   const bool staged = plan_smem_layout(a.n, a.H, a.world, a.r_cap, true) <= lim;

@@ -12,6 +12,7 @@
 
 #include "lenpred_kernels.cuh"
 #include "lenpred_tail.cuh"
+#include "plan_core.cuh"
 #include "star_internal.h"
 
 namespace star {
@@ -720,6 +721,34 @@ star_status plan_reschedule_segmented(const star_plan_params* p, const star_plan
     return fail(STAR_ENOTSUP, "plan state (%zu B) exceeds shared memory: n_inst*(H+1) too large", smem);
   cudaError_t e = launch_plan(p, sg, moves, n_moves, err_flag, reinterpret_cast<cudaStream_t>(stream_));
   if (e != cudaSuccess) return cuda_fail(e, "plan_kernel launch");
+  return STAR_OK;
+}
+
+size_t star_plan_workspace_bytes(int n_inst, int H, int64_t request_slots) {
+  if (n_inst < 1 || H < 0 || request_slots < 0) return 0;
+  return plan_large_workspace_bytes(n_inst, H, request_slots);
+}
+
+star_status plan_reschedule_segmented_ws(const star_plan_params* p, const star_plan_segments* sg, star_move* moves,
+                                         int32_t* n_moves, int32_t* err_flag, void* workspace,
+                                         star_stream_t stream_) {
+  if (!workspace) return plan_reschedule_segmented(p, sg, moves, n_moves, err_flag, stream_);
+  star_status s = ensure_device();
+  if (s != STAR_OK) return s;
+  if ((s = check_plan_params(p)) != STAR_OK) return s;
+  if (!sg || !sg->L) return fail(STAR_EINVAL, "segments / L is NULL");
+  if (!n_moves || (p->max_moves > 0 && !moves)) return fail(STAR_EINVAL, "moves / n_moves is NULL");
+  if (sg->world < 1 || sg->n_loc < 1 || (int64_t)sg->world * sg->n_loc != p->n_inst)
+    return fail(STAR_EINVAL, "world*n_loc must equal n_inst");
+  if (sg->r_cap < 0) return fail(STAR_EINVAL, "r_cap < 0");
+  if (sg->r_cap > 0 && (!sg->req_id || !sg->inst || !sg->n_tok || !sg->n_hat))
+    return fail(STAR_EINVAL, "request arrays must be non-NULL");
+  if ((int64_t)sg->world * sg->r_cap > (1 << 20)) return fail(STAR_ERANGE, "more than 2^20 request slots");
+  if (sg->world > 1 && sg->seg_stride <= 0) return fail(STAR_EINVAL, "seg_stride must be > 0 when world > 1");
+  if (!plan_large_supported(p->n_inst)) return fail(STAR_ENOTSUP, "n_inst=%d above the multi-CTA plan limit", p->n_inst);
+  const PlanArgs a = make_plan_args(p, sg, moves, n_moves, err_flag);
+  cudaError_t e = launch_plan_large(a, workspace, reinterpret_cast<cudaStream_t>(stream_));
+  if (e != cudaSuccess) return cuda_fail(e, "plan_large launch");
   return STAR_OK;
 }
 

@@ -28,6 +28,14 @@ size_t plan_smem_bytes(int n, int H, int world, int r_cap);
 cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg, star_move* moves, int32_t* n_moves,
                         int32_t* err_flag, cudaStream_t stream);
 
+// plan_large.cu (multi-CTA plan over a global workspace)
+struct PlanArgs;
+PlanArgs make_plan_args(const star_plan_params* p, const star_plan_segments* sg, star_move* moves, int32_t* n_moves,
+                        int32_t* err_flag);
+size_t plan_large_workspace_bytes(int n, int H, int64_t slots);
+bool plan_large_supported(int n);
+cudaError_t launch_plan_large(const PlanArgs& a, void* workspace, cudaStream_t stream);
+
 // dispatch.cu
 size_t dispatch_workspace_bytes(int n, int H);
 cudaError_t launch_dispatch(int policy, int n, int H, const uint32_t* beta_q, int64_t* L, const int64_t* c_mem,

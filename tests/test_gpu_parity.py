@@ -339,3 +339,39 @@ def test_dispatch_bitexact_cluster_scale(star, oracle_mod, n, A):
         torch.cuda.synchronize()
         assert got.cpu().numpy().tolist() == ref_a.tolist(), policy
         assert np.array_equal(Ld.cpu().numpy(), ref_L), policy
+
+
+# ============================================================================ cluster-scale plan (NEXT-3)
+def _plan_gpu_large(star, params_h, L, snap, n_hat):
+    pp = star.PlanParams.from_host(params_h)
+    moves, nm = star.plan_reschedule_large(pp, _dev(L), _dev(snap.req_id), _dev(snap.inst), _dev(snap.n_tok),
+                                           _dev(n_hat.astype(np.int32)), _dev(snap.pinned))
+    torch.cuda.synchronize()
+    return star.decode_moves(moves, nm)
+
+
+@pytest.mark.parametrize("seed", range(0, 240, 3))
+def test_plan_large_bitexact_tiny(star, oracle_mod, seed):
+    """The multi-CTA plan (workspace path) on the same tiny fixtures as the single-CTA plan."""
+    g = datagen.rng(seed)
+    n, R, H = int(g.integers(1, 7)), int(g.integers(0, 30)), int(g.integers(0, 9))
+    snap, n_hat, params = datagen.tiny_fixture(3000 + seed, n, R, H)
+    params.max_moves = int(g.integers(0, 6))
+    L = oracle_mod.project(snap.inst, snap.n_tok, n_hat, n, H, params.beta_q)["L"]
+    ref = oracle_mod.plan(params, L, snap.req_id, snap.inst, snap.n_tok, n_hat, snap.pinned)
+    assert _plan_gpu_large(star, params, L, snap, n_hat) == ref
+
+
+@pytest.mark.parametrize("n,r_per,moves,flags", [(256, 8, 3, 0), (64, 64, 4, 0), (128, 16, 2, 1), (96, 24, 3, 2),
+                                                  (8, 256, 4, 0)])
+def test_plan_large_bitexact_cluster_scale(star, oracle_mod, n, r_per, moves, flags):
+    """Cluster-scale shapes (up to 256 instances) vs the from-scratch oracle."""
+    snap = datagen.make_snapshot(n + r_per, n, r_per, pinned_frac=0.03)
+    n_hat = snap.true_rem.copy()
+    params = datagen.make_plan_params(snap, mem_factor=1.10, max_moves=moves, flags=flags, reserved_seed=n)
+    L = oracle_mod.project(snap.inst, snap.n_tok, n_hat, n, params.H, params.beta_q)["L"]
+    ref = oracle_mod.plan(params, L, snap.req_id, snap.inst, snap.n_tok, n_hat, snap.pinned)
+    got = _plan_gpu_large(star, params, L, snap, n_hat)
+    assert got == ref
+    if n <= 64:   # the single-CTA kernel agrees where its state fits one SM
+        assert _plan_gpu(star, params, L, snap, n_hat) == ref
