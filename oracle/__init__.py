@@ -167,3 +167,30 @@ def dispatch(policy, L, beta_q, n_tok, n_hat, c_mem=None, reserved=None, counter
                           _p(_c(reserved, np.int64)), A, _p(_c(n_tok, np.int32)), _p(_c(n_hat, np.int32)),
                           int(counter), _p(out))
     return out[:A], L
+
+
+def should_refresh(gen, g_last, k):
+    """true iff no prediction yet (g_last < 0) or gen - g_last >= k."""
+    return (np.asarray(g_last) < 0) | (np.asarray(gen, np.int64) - np.asarray(g_last) >= k)
+
+
+def refresh_step(h, pw, n_tok, gen, g_last, nhat_last, k, l_ctx=32768):
+    """One step of the prediction cadence (NEXT-1, reading A27), plain loops:
+    rows due for a refresh get N_hat = quantize(Eq. 2(h_r)) (fp64 oracle value rounded to fp32
+    before the quantizer) and g_last = gen, nhat_last = N_hat; the others age by the tokens
+    generated since their last prediction.  Returns (n_hat, g_last', nhat_last', refreshed mask)."""
+    gen = np.asarray(gen, np.int64)
+    g_last = np.array(g_last, np.int32, copy=True)
+    nhat_last = np.array(nhat_last, np.int32, copy=True)
+    due = should_refresh(gen, g_last, k)
+    n_hat = np.zeros(gen.shape[0], np.int32)
+    rows = np.nonzero(due)[0]
+    if rows.size:
+        y = lenpred_weights(h[rows], pw)
+        q = quantize(y.astype(np.float32), np.asarray(n_tok)[rows], l_ctx)
+        n_hat[rows] = q
+        g_last[rows] = gen[rows]
+        nhat_last[rows] = q
+    for r in np.nonzero(~due)[0]:
+        n_hat[r] = max(0, int(nhat_last[r]) - int(gen[r] - g_last[r]))
+    return n_hat, g_last, nhat_last, due

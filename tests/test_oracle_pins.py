@@ -461,3 +461,38 @@ def test_dispatch_matches_brute_force(oracle_mod, seed):
         b, L_b = brute.dispatch(policy, L, beta, n_tok, n_hat, c_mem, reserved, counter=seed)
         assert a.tolist() == b
         assert L_o.tolist() == L_b
+
+
+# =============================================================================== prediction cadence (NEXT-1)
+def test_should_refresh_spec_examples(oracle_mod):
+    """(last 100, gen 120, k 20) -> true; (100, 119, 20) -> false; fresh -> true."""
+    assert oracle_mod.should_refresh([120], [100], 20).tolist() == [True]
+    assert oracle_mod.should_refresh([119], [100], 20).tolist() == [False]
+    assert oracle_mod.should_refresh([0], [-1], 20).tolist() == [True]
+
+
+def test_prediction_overhead_formula():
+    """PAPER.md:466-469 / SPEC.md:180-183: overhead = 1.40 / (18.23 k): 7.68% at k=1, 0.38% at k=20."""
+    ov = lambda k: 1.40 / (18.23 * k)
+    assert round(100 * ov(1), 2) == 7.68
+    assert round(100 * ov(20), 2) == 0.38
+    assert abs(ov(10) - 2 * ov(20)) < 1e-15
+
+
+def test_refresh_schedule_and_aging(oracle_mod):
+    """over a request's lifetime the refresh fires ceil(L/k) times (the initial
+    prediction included); between refreshes the prediction ages one token per generated token
+    and never goes negative."""
+    pw = datagen.make_predictor_weights(0, 16, "f32", m1=32, m2=16, m3=8)
+    k, L_out = 20, 93
+    h = datagen.make_hidden(0, 1, 16, "f32")
+    g_last, nhat_last = np.array([-1], np.int32), np.array([0], np.int32)
+    fires, prev = 0, None
+    for g in range(L_out):
+        nh, g_last, nhat_last, due = oracle_mod.refresh_step(h, pw, [10 + g], [g], g_last, nhat_last, k)
+        fires += int(due[0])
+        if not due[0]:
+            assert nh[0] == max(0, prev - 1)
+        assert nh[0] >= 0
+        prev = int(nh[0])
+    assert fires == -(-L_out // k)
