@@ -508,6 +508,11 @@ def run_star(args):
             line["roofline_projection"] = projection_sweep(star, snap, params_h_dev(star, params_h, dev), dev, peaks)
         except Exception as ex:  # keep the bench line
             line["roofline_projection"] = {"error": str(ex)}
+    if world == 1 and not args.profile and not args.no_sweep and c["dtype"] == "bf16":
+        try:
+            line["refresh_k20"] = refresh_step_timing(star, Step, pred, params, c, snap, idx, h_dev, dev, flush)
+        except Exception as ex:
+            line["refresh_k20"] = {"error": str(ex)}
     if rank == 0 and not args.profile and not args.no_sweep:
         try:
             line["next_rows"] = next_rows_timing(star, dev)
@@ -580,6 +585,49 @@ def next_rows_timing(star, dev, seed=0):
     out["note"] = ("paper: scheduler <= 300 ms at 256 instances (PAPER.md:460); NEXT rows of SURVEY 8(f), "
                    "bit-exact vs the oracle in tests/test_gpu_parity.py")
     return out
+
+
+def refresh_step_timing(star, Step, pred, params, c, snap, idx, h_dev, dev, flush, k=20, reps=50):
+    """Steady-state step in the paper's deployment mode (prediction cadence k = 20):
+    1/k of the requests are due each step (slot r last predicted r mod k tokens ago), the rest
+    age.  One CUDA graph per step, L2 flushed before each, CUDA events around the graph launch."""
+    import torch
+    R = len(idx)
+    st = Step(pred, params, c["n_inst"], r_cap=max(R, 1), device=dev, refresh_k=k)
+    req = [snap.req_id[idx], snap.inst[idx], snap.n_tok[idx]]
+    st.load_requests(*(torch.from_numpy(np.ascontiguousarray(a)) for a in req))
+    gen = (snap.n_tok[idx] - np.minimum(snap.n_tok[idx] - 1, 36)).astype(np.int32) + 100
+    g_last = (gen - (np.arange(R) % k) - 1).astype(np.int32)   # slot r due when (r + 1) % k == 0 ...
+    nhat_last = np.maximum(snap.true_rem[idx], 1).astype(np.int32)
+    st.set_generation(torch.from_numpy(gen), torch.from_numpy(g_last), torch.from_numpy(nhat_last))
+    s_ = torch.cuda.Stream(device=dev)
+    s_.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s_):
+        st.run(h_dev)
+    torch.cuda.current_stream().wait_stream(s_)
+    torch.cuda.synchronize()
+    st.set_generation(torch.from_numpy(gen), torch.from_numpy(g_last), torch.from_numpy(nhat_last))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        st.run(h_dev)
+    ts, nref = [], []
+    for i in range(reps + 5):
+        st.set_generation(torch.from_numpy(gen + i))   # one token per step; the cadence state evolves
+        if flush is not None:
+            flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        e1.synchronize()
+        if i >= 5:
+            ts.append(e0.elapsed_time(e1) * 1e3)
+            nref.append(int(st.n_refreshed.item()))
+    t = float(np.median(ts))
+    return {"k": k, "us_per_step": round(t, 2), "requests_per_s": R / (t * 1e-6),
+            "rows_repredicted_per_step": float(np.mean(nref)), "launches_per_step": 7,
+            "note": "paper's deployment mode (k = 20, PAPER.md:463-469): due rows re-predicted, the rest "
+                    "aged; projection + plan over all requests every step"}
 
 
 def params_h_dev(star, params_h, dev):

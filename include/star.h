@@ -120,6 +120,24 @@ star_status lenpred_forward_project(star_predictor* p, const void* h, int64_t ld
                                     int64_t* L, int64_t* W, int64_t* peak, int64_t* growth, int32_t* count,
                                     void* workspace, int32_t* err_flag, star_stream_t stream);
 
+/* Prediction cadence k (NEXT-1): the paper predicts "at regular intervals" and
+ * sets the interval to k = 20 decode iterations.  Per request slot r:
+ *   gen[r]        tokens generated so far (device, in)
+ *   g_last[r]     gen at the request's last prediction, -1 = never predicted (device, in/out)
+ *   nhat_last[r]  that prediction (device, in/out)
+ * Rows with g_last < 0 or gen - g_last >= k (SPEC.md:164-172 should_refresh) are re-predicted from
+ * their hidden state exactly as lenpred_forward (Eq. 2 + quantizer with cap max_ctx_len - n_tok[r])
+ * and get g_last = gen, nhat_last = N_hat; every other row ages (reading A27):
+ *   N_hat = max(0, nhat_last - (gen - g_last)).
+ * n_hat [R] (out) = this step's N_hat for every row; n_refreshed (device int32, nullable) = number of
+ * rows re-predicted.  The selection, the gather of the selected rows and the predictor run on the
+ * device (the row count never visits the host), so the call stays graph-capturable.  bf16
+ * predictors with m2 % 256 == 0 and m3 == 64 only (STAR_ENOTSUP otherwise). */
+star_status lenpred_forward_refresh(star_predictor* p, const void* h, int64_t ld_h, int R,
+                                    const int32_t* n_tok, int32_t max_ctx_len, const int32_t* gen,
+                                    int32_t* g_last, int32_t* nhat_last, int32_t k, int32_t* n_hat,
+                                    int32_t* n_refreshed, star_stream_t stream);
+
 /* The quantizer alone, on a caller-given fp32 y_hat (the exact device function the forward
  * epilogue uses).  Lets quantizer parity be tested on identical fp32 inputs. */
 star_status lenpred_quantize(const float* y_hat, const int32_t* n_tok, int R, int32_t max_ctx_len,

@@ -10,7 +10,8 @@ StarError if it is missing (there is no CPU fallback).
 """
 from ._lib import (DISPATCH_CURRENT_LOAD, DISPATCH_PROJECTED, DISPATCH_ROUND_ROBIN, dispatch_requests,  # noqa: F401
                    CURRENT_ONLY, L_CTX, STRICT_MEM, Predictor, PlanParams, ProjectOut, StarError,  # noqa: F401
-                   alloc_moves, decode_moves, lenpred_forward, lenpred_forward_project, lenpred_quantize, plan_reschedule,
+                   alloc_moves, decode_moves, lenpred_forward, lenpred_forward_project, lenpred_forward_refresh,
+                   lenpred_quantize, plan_reschedule,
                    plan_reschedule_segmented, project_instance_load, plan_reschedule_large,
                    plan_reschedule_segmented_ws, plan_workspace_bytes, project_workspace_bytes, version)
 

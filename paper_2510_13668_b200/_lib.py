@@ -63,6 +63,7 @@ def lib() -> C.CDLL:
         "lenpred_forward": ([P, P, I64, I, P, I32, P, P, P], I),
         "lenpred_quantize": ([P, P, I, I32, P, P], I),
         "lenpred_forward_project": ([P, P, I64, I, P, I32, P, P, I, I, I, P, P, P, P, P, P, P, P, P, P], I),
+        "lenpred_forward_refresh": ([P, P, I64, I, P, I32, P, P, P, I32, P, P, P], I),
         "star_project_workspace_bytes": ([I, I], C.c_size_t),
         "star_project_single_cta_max_rows": ([], I),
         "project_instance_load": ([I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P], I),
@@ -223,6 +224,24 @@ def lenpred_forward_project(pred: Predictor, h: torch.Tensor, n_tok: torch.Tenso
                                          _ptr(out.count), _ptr(workspace), _ptr(err_flag), _stream(stream)),
            "lenpred_forward_project")
     return y_hat, n_hat, out
+
+
+def lenpred_forward_refresh(pred: Predictor, h: torch.Tensor, n_tok: torch.Tensor, gen: torch.Tensor,
+                            g_last: torch.Tensor, nhat_last: torch.Tensor, k: int, max_ctx_len: int = L_CTX,
+                            n_hat: Optional[torch.Tensor] = None, n_refreshed: Optional[torch.Tensor] = None,
+                            stream=None):
+    """Prediction cadence k (star.h lenpred_forward_refresh); g_last / nhat_last are updated in place."""
+    R = h.shape[0]
+    if h.dim() != 2 or h.stride(1) != 1 or h.dtype != torch.bfloat16 or not h.is_cuda:
+        raise StarError("h must be a 2-D CUDA bf16 tensor with unit column stride")
+    for n_, t in (("n_tok", n_tok), ("gen", gen), ("g_last", g_last), ("nhat_last", nhat_last)):
+        _req(t, torch.int32, n_)
+    if n_hat is None:
+        n_hat = torch.empty(max(R, 1), dtype=torch.int32, device=h.device)
+    _check(lib().lenpred_forward_refresh(pred.handle, _ptr(h), h.stride(0), R, _ptr(n_tok), max_ctx_len, _ptr(gen),
+                                         _ptr(g_last), _ptr(nhat_last), int(k), _ptr(n_hat), _ptr(n_refreshed),
+                                         _stream(stream)), "lenpred_forward_refresh")
+    return n_hat[:R]
 
 
 def lenpred_quantize(y_hat: torch.Tensor, n_tok: Optional[torch.Tensor] = None, max_ctx_len: int = L_CTX,

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(HERE, "libstar.so")
-SOURCES = ["star_api.cu", "project.cu", "plan.cu", "plan_large.cu", "dispatch.cu"]
+SOURCES = ["star_api.cu", "project.cu", "plan.cu", "plan_large.cu", "dispatch.cu", "refresh.cu"]
 HEADERS = ["ptx.cuh", "lenpred_kernels.cuh", "lenpred_tail.cuh", "project_core.cuh", "plan_core.cuh", "star_internal.h"]
 
 NVCC_FLAGS = [

@@ -52,6 +52,7 @@ struct GemmArgs {
   float* ws;             // [tiles][splits (producer)][splits (owner)][OW/4][128][4] fp32 partials
   float* head_ws;        // [tiles][splits][128] per-owner partial dots (EPI_HEAD)
   uint64_t* tl;          // diagnostics: [ctas][16] %globaltimer phase stamps, or nullptr
+  const int32_t* M_dev;  // device-side row count (refresh mode: rows selected on the device), or nullptr
 };
 
 // Quantizer (readings A8-A10): cap = max(0, L_ctx - N(r)) (no n_tok -> L_ctx);
@@ -168,6 +169,10 @@ __global__ void __launch_bounds__(192, 1)
   const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
   const int nkb = kb1 - kb0;   // >= 1 (host guarantees)
 
+  if (p.M_dev) {   // refresh mode: tiles beyond the device-side row count leave before any setup
+    pdl_wait();
+    if (m_tile * BM >= __ldcg(p.M_dev)) return;   // the whole cluster (same m-tile) leaves
+  }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);

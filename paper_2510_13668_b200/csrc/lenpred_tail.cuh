@@ -53,6 +53,7 @@ struct TailArgs {
   int project;         // fuse the projection (pa valid)
   ProjArgs pa;         // R / inst / n_tok / beta_q / outputs / workspace (ws_cnt, ws_sum, ws_arrive)
   uint64_t* tl;        // diagnostics: [ctas][16] %globaltimer phase stamps, or nullptr
+  const int32_t* M_dev;  // device-side row count (refresh mode), or nullptr (then M)
 };
 
 // Phase timestamp (diagnostics only; one designated thread per phase).
@@ -126,6 +127,12 @@ __global__ void __launch_bounds__(192, 1)
   const int kb0 = split * p.kb_per_split;
   const int nkb = min(p.num_kb, kb0 + p.kb_per_split) - kb0;
 
+  int Mrows = p.M;
+  if (p.M_dev) {   // refresh mode: the row count was produced on the device by the previous kernels
+    pdl_wait();
+    Mrows = __ldcg(p.M_dev);
+    if (m_tile * BM >= Mrows) return;   // every CTA of this m-tile (and its cluster) leaves before setup
+  }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -223,7 +230,7 @@ __global__ void __launch_bounds__(192, 1)
     pdl_wait();
     if (p.project)
       for (int t = te; t <= p.pa.H; t += 128) sbeta[t] = p.pa.beta_q[t];
-    if (red_g == 0 && grow < p.M) {
+    if (red_g == 0 && grow < Mrows) {
       if (p.n_tok) my_ntok = p.n_tok[grow];
       if (p.project) my_inst = p.pa.inst[grow];
     }
@@ -447,7 +454,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int j = 0; j < 16; ++j) dot = fmaf(sw4[c0 + cc + j], fmaxf(z[j] + sb3[c0 + cc + j], 0.0f), dot);
       }
       for (int off = 1; off < tpr; off <<= 1) dot += __shfl_xor_sync(0xFFFFFFFFu, dot, off);
-      const bool owner = red_g == 0 && grow < p.M;
+      const bool owner = red_g == 0 && grow < Mrows;
       int32_t nh = 0;
       if (owner) {
         const float y = dot + (p.b4 ? __ldg(p.b4) : 0.0f);

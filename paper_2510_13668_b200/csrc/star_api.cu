@@ -282,6 +282,11 @@ struct star_predictor {
   int* tail_cnt = nullptr;    // fused tail: per (m-tile, split) arrival counters
   uint64_t* tl = nullptr;     // diagnostics: fused-tail phase timeline [ctas][16]
   int tl_ctas = 0;            // CTAs of the most recent timed tail launch
+  // refresh cadence (NEXT-1) scratch: compacted rows and their hidden states
+  int32_t *r_idx = nullptr, *r_pos = nullptr, *r_ntok = nullptr, *r_nhat = nullptr, *r_M = nullptr;
+  void* r_h = nullptr;
+  float* r_ws = nullptr;      // layer-1 split-K partials for the refresh grid (all m-tiles x 4 splits)
+  CUtensorMap tmA_r;          // compacted hidden states [max_rows][d]
   uint64_t* tl_l1 = nullptr;  // diagnostics: layer-1 (CTA-pair) GEMM phase timeline
   int tl_l1_ctas = 0;
   size_t ws_floats = 0;
@@ -315,6 +320,13 @@ static void free_pred(star_predictor* p) {
   cudaFree(p->tail_cnt);
   cudaFree(p->tl);
   cudaFree(p->tl_l1);
+  cudaFree(p->r_idx);
+  cudaFree(p->r_pos);
+  cudaFree(p->r_ntok);
+  cudaFree(p->r_nhat);
+  cudaFree(p->r_M);
+  cudaFree(p->r_h);
+  cudaFree(p->r_ws);
   delete p;
 }
 
@@ -361,6 +373,16 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
   ok &= alloc(reinterpret_cast<void**>(&p->head_ws), (size_t)g_num_sms * 128 * 4);
   ok &= alloc(reinterpret_cast<void**>(&p->ws3), (size_t)((max_rows + 127) / 128) * 16 * 64 * 128 * 4);
   ok &= alloc(reinterpret_cast<void**>(&p->tail_cnt), (size_t)((max_rows + 127) / 128) * 8 * sizeof(int));
+  if (!f32) {
+    ok &= alloc(reinterpret_cast<void**>(&p->r_idx), (size_t)max_rows * 4);
+    ok &= alloc(reinterpret_cast<void**>(&p->r_pos), (size_t)max_rows * 4);
+    ok &= alloc(reinterpret_cast<void**>(&p->r_ntok), (size_t)max_rows * 4);
+    ok &= alloc(reinterpret_cast<void**>(&p->r_nhat), (size_t)max_rows * 4);
+    ok &= alloc(reinterpret_cast<void**>(&p->r_M), 16);
+    ok &= alloc(&p->r_h, (size_t)max_rows * d * 2);
+    ok &= alloc(reinterpret_cast<void**>(&p->r_ws),
+                (size_t)((max_rows + 127) / 128) * (m1 / 256 > 0 ? m1 / 256 : 1) * 4 * 256 * 128 * 4);
+  }
   if (f32) {
     ok &= alloc(&p->hs, (size_t)max_rows * d * 4 * 3);
     ok &= alloc(reinterpret_cast<void**>(&p->W1s), (size_t)m1 * d * 4 * 3);
@@ -396,6 +418,7 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
       (f32 && (st = make_tmap(&p->tmA1, p->hs, true, K1, max_rows, K1 * 4, 128)) != STAR_OK) ||
       (!f32 && (st = make_tmap(&p->tmC1, p->Z1, false, m1, max_rows, (uint64_t)m1 * 2, 32)) != STAR_OK) ||
       (!f32 && (st = make_tmap(&p->tmB1p, B1, false, K1, m1, K1 * esz, 128)) != STAR_OK) ||
+      (!f32 && (st = make_tmap(&p->tmA_r, p->r_h, false, (uint64_t)d, max_rows, (uint64_t)d * 2, 128)) != STAR_OK) ||
       (!f32 && (st = make_tmap(&p->tmC2, p->Z2, false, m2, max_rows, (uint64_t)m2 * 2, 32)) != STAR_OK)) {
     free_pred(p);
     return st;
@@ -434,6 +457,13 @@ star_status star_predictor_timeline(star_predictor* p, int enable, uint64_t* hos
   } else if (!enable && p->tl) {
     cudaFree(p->tl);
   cudaFree(p->tl_l1);
+  cudaFree(p->r_idx);
+  cudaFree(p->r_pos);
+  cudaFree(p->r_ntok);
+  cudaFree(p->r_nhat);
+  cudaFree(p->r_M);
+  cudaFree(p->r_h);
+  cudaFree(p->r_ws);
     p->tl = nullptr;
   }
   if (host_out && p->tl) {
@@ -620,6 +650,86 @@ star_status lenpred_forward_project(star_predictor* p, const void* h, int64_t ld
   ProjArgs pa = make_proj_args(R, n_inst, inst_base, H, inst, n_tok, n_hat, beta_q, L, W, peak, growth, count,
                                workspace, err_flag);
   return forward_impl(p, h, ld_h, R, n_tok, max_ctx_len, y_hat, n_hat, &pa, workspace, st);
+}
+
+star_status lenpred_forward_refresh(star_predictor* p, const void* h, int64_t ld_h, int R, const int32_t* n_tok,
+                                    int32_t max_ctx_len, const int32_t* gen, int32_t* g_last, int32_t* nhat_last,
+                                    int32_t k, int32_t* n_hat, int32_t* n_refreshed, star_stream_t stream_) {
+  if (!p) return fail(STAR_EINVAL, "predictor is NULL");
+  if (p->f32 || p->bn2 != 256 || p->m3 != 64)
+    return fail(STAR_ENOTSUP, "refresh mode needs a bf16 predictor (m2 %% 256 == 0, m3 == 64)");
+  if (R < 0 || R > p->max_rows) return fail(STAR_ERANGE, "R=%d outside [0, max_rows=%d]", R, p->max_rows);
+  if (k < 1) return fail(STAR_EINVAL, "k=%d must be >= 1", k);
+  if (max_ctx_len < 0) return fail(STAR_EINVAL, "max_ctx_len < 0");
+  if (R == 0) return STAR_OK;
+  if (!h || !gen || !g_last || !nhat_last || !n_hat)
+    return fail(STAR_EINVAL, "h, gen, g_last, nhat_last, n_hat must be non-NULL");
+  if (ld_h < p->d) return fail(STAR_EINVAL, "ld_h=%lld < d=%d", (long long)ld_h, p->d);
+  if ((reinterpret_cast<uintptr_t>(h) | (uintptr_t)(ld_h * 2)) & 15u)
+    return fail(STAR_EINVAL, "h rows must be 16-byte aligned");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+  cudaError_t e;
+  if ((e = launch_refresh_select(R, gen, g_last, k, n_tok, p->r_idx, p->r_ntok, p->r_pos, p->r_M, st)) != cudaSuccess)
+    return cuda_fail(e, "refresh_select launch");
+  if ((e = launch_refresh_gather(R, h, ld_h * 2, p->d * 2, p->r_idx, p->r_M, p->r_h, st)) != cudaSuccess)
+    return cuda_fail(e, "refresh_gather launch");
+  // layer 1 on the compacted rows: 1-CTA tiles + cluster split-K sized for the expected row count
+  // ~R/k (the grid covers R rows; tiles beyond the device-side count leave before any setup)
+  const int m_tiles = (R + 127) / 128;
+  const int m_est = ((R + k - 1) / k + 127) / 128;
+  GemmArgs g{};
+  g.M = R;
+  g.M_dev = p->r_M;
+  g.max_ctx = max_ctx_len;
+  g.head_ws = p->head_ws;
+  g.N = p->m1;
+  g.num_kb = (p->d * 2 + 127) / 128;
+  plan_splits((m_est < 1 ? 1 : m_est) * (p->m1 / p->bn1), g.num_kb, p->bn1, false, &g.splits, &g.kb_per_split);
+  if (g.splits > 4) {   // the refresh partial workspace holds 4 splits of every m-tile
+    g.splits = 4;
+    g.kb_per_split = (g.num_kb + 3) / 4;
+  }
+  g.ws = p->r_ws;
+  g.epi = EPI_RELU_BF16;
+  g.tma_store = (p->bn1 / g.splits) % 64 == 0 ? 1 : 0;
+  g.out = p->Z1;
+  g.ld_out = p->m1;
+  g.bias = p->b1;
+  if ((e = launch_gemm(p->bn1, false, p->tmA_r, p->tmB1, p->tmC1, g, m_tiles, st)) != cudaSuccess)
+    return cuda_fail(e, "refresh layer-1 launch");
+  const int n2 = p->m2 / 256;
+  const int num_kb2 = p->m1 * 2 / 128;
+  const int ts = tail_splits(m_est < 1 ? 1 : m_est, n2, num_kb2);
+  if (!ts) return fail(STAR_ENOTSUP, "shape not supported by the fused tail");
+  TailArgs t{};
+  t.M = R;
+  t.M_dev = p->r_M;
+  t.num_kb = num_kb2;
+  t.splits = ts;
+  t.kb_per_split = (num_kb2 + ts - 1) / ts;
+  t.n2_tiles = n2;
+  t.b2 = p->b2;
+  t.b3 = p->b3;
+  t.w4 = p->w4;
+  t.b4 = p->b4;
+  t.n_tok = n_tok ? p->r_ntok : nullptr;
+  t.max_ctx = max_ctx_len;
+  t.y_hat = nullptr;
+  t.n_hat = p->r_nhat;
+  t.ws2 = p->ws;
+  t.ws3a = p->ws3;
+  t.ws3b = p->ws3 + (size_t)m_tiles * n2 * ts * 64 * 128;
+  t.cnt = p->tail_cnt;
+  t.project = 0;
+  if ((e = launch_tail(p->tmA2, p->tmB2, p->tmB3, t, m_tiles, st)) != cudaSuccess)
+    return cuda_fail(e, "refresh tail launch");
+  if ((e = launch_refresh_scatter(R, p->r_pos, p->r_nhat, gen, g_last, nhat_last, n_hat, st)) != cudaSuccess)
+    return cuda_fail(e, "refresh_scatter launch");
+  if (n_refreshed) {
+    if ((e = cudaMemcpyAsync(n_refreshed, p->r_M, sizeof(int32_t), cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+      return cuda_fail(e, "n_refreshed copy");
+  }
+  return STAR_OK;
 }
 
 star_status lenpred_quantize(const float* y_hat, const int32_t* n_tok, int R, int32_t max_ctx_len, int32_t* n_hat,

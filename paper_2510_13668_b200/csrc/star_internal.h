@@ -36,6 +36,14 @@ size_t plan_large_workspace_bytes(int n, int H, int64_t slots);
 bool plan_large_supported(int n);
 cudaError_t launch_plan_large(const PlanArgs& a, void* workspace, cudaStream_t stream);
 
+// refresh.cu (prediction cadence k)
+cudaError_t launch_refresh_select(int R, const int32_t* gen, const int32_t* g_last, int32_t k, const int32_t* n_tok,
+                                  int32_t* idx, int32_t* ntok_c, int32_t* pos, int32_t* M_out, cudaStream_t st);
+cudaError_t launch_refresh_gather(int R, const void* h, int64_t ld_bytes, int row_bytes, const int32_t* idx,
+                                  const int32_t* M_dev, void* hc, cudaStream_t st);
+cudaError_t launch_refresh_scatter(int R, const int32_t* pos, const int32_t* nhat_c, const int32_t* gen,
+                                   int32_t* g_last, int32_t* nhat_last, int32_t* n_hat, cudaStream_t st);
+
 // dispatch.cu
 size_t dispatch_workspace_bytes(int n, int H);
 cudaError_t launch_dispatch(int policy, int n, int H, const uint32_t* beta_q, int64_t* L, const int64_t* c_mem,

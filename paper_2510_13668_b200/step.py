@@ -100,7 +100,7 @@ class Step:
 
     def __init__(self, predictor: _lib.Predictor, params: _lib.PlanParams, n_inst: int, r_cap: int,
                  rank: int = 0, world: int = 1, group=None, device: Optional[torch.device] = None,
-                 max_ctx_len: int = _lib.L_CTX):
+                 max_ctx_len: int = _lib.L_CTX, refresh_k: Optional[int] = None):
         if n_inst % world:
             raise ValueError(f"n_inst={n_inst} must be divisible by world={world}")
         self.pred, self.params = predictor, params
@@ -124,6 +124,14 @@ class Step:
         self.proj_out.count = self.v["icount"]
         self.R = 0
         self.graph = None
+        # prediction cadence (NEXT-1): re-predict a request every refresh_k generated tokens, age
+        # its prediction in between; None = predict every request every step
+        self.refresh_k = refresh_k
+        if refresh_k is not None:
+            self.gen = torch.zeros(r_cap, dtype=torch.int32, device=self.device)
+            self.g_last = torch.full((r_cap,), -1, dtype=torch.int32, device=self.device)
+            self.nhat_last = torch.zeros(r_cap, dtype=torch.int32, device=self.device)
+            self.n_refreshed = torch.zeros(1, dtype=torch.int32, device=self.device)
 
     # ---------------------------------------------------------------- state
     def load_requests(self, req_id, inst, n_tok, pinned=None, non_blocking=False):
@@ -141,10 +149,32 @@ class Step:
         v["count"].fill_(R)
         self.R = R
 
+    def set_generation(self, gen, g_last=None, nhat_last=None, non_blocking=False):
+        """Refresh mode: tokens generated so far per slot (and optionally the cadence state)."""
+        R = int(torch.as_tensor(gen).shape[0])
+        self.gen[:R].copy_(torch.as_tensor(gen), non_blocking=non_blocking)
+        if g_last is not None:
+            self.g_last[:R].copy_(torch.as_tensor(g_last), non_blocking=non_blocking)
+        if nhat_last is not None:
+            self.nhat_last[:R].copy_(torch.as_tensor(nhat_last), non_blocking=non_blocking)
+
     # ---------------------------------------------------------------- the pass
     def run(self, h: torch.Tensor, stream=None):
         """h: [R, d] hidden states of this rank's running requests (row r <-> request slot r)."""
         v, R = self.v, self.R
+        if self.refresh_k is not None:
+            # cadence k: re-predict only the due rows, age the rest, then project all of them
+            _lib.lenpred_forward_refresh(self.pred, h[:R], v["n_tok"][:R], self.gen[:R], self.g_last[:R],
+                                         self.nhat_last[:R], self.refresh_k, max_ctx_len=self.max_ctx_len,
+                                         n_hat=v["n_hat"][:max(R, 1)], n_refreshed=self.n_refreshed,
+                                         stream=stream)
+            _lib.project_instance_load(v["inst"], v["n_tok"], v["n_hat"], self.n_loc, self.H, self.params.beta_q,
+                                       inst_base=self.rank * self.n_loc, out=self.proj_out, workspace=self.ws,
+                                       err_flag=self.err, R=R, stream=stream)
+            if self.world > 1:
+                exchange(self.send, self.recv, self.group)
+            _lib.plan_reschedule_segmented(self.params, self.seg, self.moves, self.n_moves, self.err, stream=stream)
+            return self.moves, self.n_moves
         # predictor fused with the projection of its own N_hat (2 launches for bf16 predictors)
         _lib.lenpred_forward_project(self.pred, h[:R], v["n_tok"][:R], v["inst"][:R], self.n_loc, self.H,
                                      self.params.beta_q, self.ws, inst_base=self.rank * self.n_loc,

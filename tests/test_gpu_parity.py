@@ -375,3 +375,78 @@ def test_plan_large_bitexact_cluster_scale(star, oracle_mod, n, r_per, moves, fl
     assert got == ref
     if n <= 64:   # the single-CTA kernel agrees where its state fits one SM
         assert _plan_gpu(star, params, L, snap, n_hat) == ref
+
+
+# ============================================================================ prediction cadence (NEXT-1)
+def _nhat_close(got, ref_y, n_tok, tol):
+    """Refreshed rows: the GPU's N_hat within the bf16 tolerance of the quantized fp64 oracle."""
+    ref = np.clip(np.rint(ref_y), 0, np.maximum(0, 32768 - n_tok))
+    return np.all(np.abs(got.astype(np.float64) - ref) <= np.maximum(1.0, tol * np.abs(ref)) + 1.0)
+
+
+@pytest.mark.parametrize("R,k,seed", [(2048, 20, 0), (2047, 20, 1), (300, 7, 2), (4096, 20, 3), (64, 1, 4)])
+def test_refresh_step_parity(star, oracle_mod, R, k, seed):
+    c = datagen.CONFIGS["C2"]
+    g = datagen.rng(seed)
+    snap = datagen.make_snapshot(seed, 8, (R + 7) // 8)
+    n_tok = snap.n_tok[:R].copy()
+    pw = datagen.make_predictor_weights(seed, c["d"], "bf16")
+    scale = np.exp(g.normal(0.0, 1.5, R)).astype(np.float32)
+    h = datagen.make_hidden(seed, R, c["d"], "bf16", scale=scale)
+    gen = g.integers(0, 5000, R).astype(np.int32)
+    g_last = np.where(g.random(R) < 0.1, -1, gen - g.integers(0, 2 * k + 1, R)).astype(np.int32)
+    nhat_last = g.integers(0, 30000, R).astype(np.int32)
+    W, _ = _weights_dev(pw)
+    pred = star.Predictor(*W, max_rows=R)
+    gl_d, nl_d = _dev(g_last), _dev(nhat_last)
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nh = star.lenpred_forward_refresh(pred, _dev(h, torch.bfloat16), _dev(n_tok), _dev(gen), gl_d, nl_d, k,
+                                      n_refreshed=cnt)
+    torch.cuda.synchronize()
+    due = oracle_mod.should_refresh(gen, g_last, k)
+    assert cnt.item() == int(due.sum())
+    nh, gl2, nl2 = nh.cpu().numpy(), gl_d.cpu().numpy(), nl_d.cpu().numpy()
+    aged = ~due   # aged rows: exact integers (reading A27)
+    exp_aged = np.maximum(0, nhat_last[aged].astype(np.int64) - (gen[aged].astype(np.int64) - g_last[aged]))
+    assert np.array_equal(nh[aged], exp_aged)
+    assert np.array_equal(gl2[aged], g_last[aged]) and np.array_equal(nl2[aged], nhat_last[aged])
+    assert np.array_equal(gl2[due], gen[due]) and np.array_equal(nl2[due], nh[due])
+    rows = np.nonzero(due)[0]
+    if rows.size:
+        sample = rows[np.unique(datagen.rng(seed).integers(0, rows.size, 32))]
+        y_ref = oracle_mod.lenpred_weights(h[sample], pw)
+        assert _nhat_close(nh[sample], y_ref, n_tok[sample], 2e-2)
+    pred.close()
+
+
+def test_refresh_schedule_on_device(star, oracle_mod):
+    """45 decode steps (gen += 1 per step), k = 20: every row refreshes at its first step and then
+    every 20 generated tokens; in between the device ages it exactly like the oracle."""
+    R, k, d = 512, 20, 4096
+    pw = datagen.make_predictor_weights(9, d, "bf16")
+    h = datagen.make_hidden(9, R, d, "bf16", scale=np.exp(datagen.rng(9).normal(0, 1.5, R)).astype(np.float32))
+    W, _ = _weights_dev(pw)
+    pred = star.Predictor(*W, max_rows=R)
+    hd = _dev(h, torch.bfloat16)
+    start = datagen.rng(10).integers(0, 30, R).astype(np.int32)
+    n_tok0 = datagen.make_snapshot(9, 1, R).n_tok
+    gl_d = _dev(np.full(R, -1, np.int32))
+    nl_d = _dev(np.zeros(R, np.int32))
+    g_last = np.full(R, -1, np.int32)
+    nhat_last = np.zeros(R, np.int32)
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for step in range(45):
+        gen = (start + step).astype(np.int32)
+        n_tok = (n_tok0 + step).astype(np.int32)
+        nh = star.lenpred_forward_refresh(pred, hd, _dev(n_tok), _dev(gen), gl_d, nl_d, k, n_refreshed=cnt)
+        torch.cuda.synchronize()
+        due = oracle_mod.should_refresh(gen, g_last, k)
+        assert cnt.item() == int(due.sum()), step
+        assert step != 0 or due.all()
+        nh = nh.cpu().numpy()
+        gl2, nl2 = gl_d.cpu().numpy(), nl_d.cpu().numpy()
+        aged = ~due
+        assert np.array_equal(nh[aged], np.maximum(0, nhat_last[aged] - (gen[aged] - g_last[aged])))
+        assert np.array_equal(gl2[due], gen[due])
+        g_last, nhat_last = gl2, nl2
+    pred.close()
