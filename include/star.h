@@ -251,6 +251,11 @@ star_status plan_reschedule_segmented(const star_plan_params* p, const star_plan
                                       star_move* moves, int32_t* n_moves, int32_t* err_flag,
                                       star_stream_t stream);
 
+/* Diagnostics: %globaltimer stamps (ns) of the most recent single-CTA plan launch: [0] entry,
+ * [1] after griddepcontrol.wait, [2] inputs staged, [3] prefix sums, [4] classification,
+ * [5] candidate argmax, [6] move applied (first round), [7] end.  Synchronises the device. */
+star_status star_plan_timeline(uint64_t* host16);
+
 /* Cluster-scale form (NEXT-3: hundreds of instances, up to 2^20 request slots; the paper's
  * budget is <= 300 ms at 256 instances): identical semantics and outputs, but the
  * state lives in `workspace` (star_plan_workspace_bytes(n_inst, H, world*r_cap) bytes, no

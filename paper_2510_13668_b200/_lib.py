@@ -71,6 +71,7 @@ def lib() -> C.CDLL:
         "plan_reschedule_segmented": ([C.POINTER(PlanParamsC), C.POINTER(PlanSegmentsC), P, P, P, P], I),
         "star_dispatch_workspace_bytes": ([I, I], C.c_size_t),
         "star_plan_workspace_bytes": ([I, I, I64], C.c_size_t),
+        "star_plan_timeline": ([P], I),
         "plan_reschedule_segmented_ws": ([C.POINTER(PlanParamsC), C.POINTER(PlanSegmentsC), P, P, P, P, P], I),
         "dispatch_requests": ([I, I, I, P, P, P, P, I, P, P, I32, P, P, P], I),
     }
@@ -407,3 +408,10 @@ def dispatch_requests(policy: int, L: torch.Tensor, beta_q: torch.Tensor, n_tok:
                                    A, _ptr(n_tok), _ptr(n_hat), int(counter), _ptr(assign), _ptr(workspace),
                                    _stream(stream)), "dispatch_requests")
     return assign[:A]
+
+
+def plan_timeline():
+    """Diagnostics: phase stamps (ns) of the most recent single-CTA plan (star_plan_timeline)."""
+    buf = np.zeros(64, dtype=np.uint64)
+    _check(lib().star_plan_timeline(buf.ctypes.data_as(P)), "star_plan_timeline")
+    return buf

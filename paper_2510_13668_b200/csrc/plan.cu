@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "plan_core.cuh"
+#include "plan_fast.cuh"
 #include "ptx.cuh"
 #include "star_internal.h"
 
@@ -24,14 +25,30 @@ namespace star {
 
 constexpr int kPlanThreads = 512;
 
+// diagnostics: %globaltimer stamps of the most recent single-CTA plan (star_plan_timeline)
+__device__ uint64_t g_plan_tl[64];
 
-__global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a, const int staged) {
+cudaError_t plan_timeline(uint64_t* host16) {
+  return cudaMemcpyFromSymbol(host16, g_plan_tl, sizeof(uint64_t) * 64);
+}
+
+
+template <bool kStaged>
+__global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a) {
   extern __shared__ __align__(16) uint8_t smraw[];
   __shared__ Cand warp_best[kPlanThreads / 32];
   __shared__ int shv[4];
+  if (threadIdx.x == 0) g_plan_tl[0] = globaltimer_ns();
   pdl_wait();   // inputs come from the projection / all-gather (PDL launch)
   pdl_launch_dependents();
-  plan_cta(a, staged, smraw, (int)threadIdx.x, (int)blockDim.x, CtaSync{}, warp_best, shv);
+  if (threadIdx.x == 0) {
+    g_plan_tl[1] = globaltimer_ns();
+    g_plan_tl[33] = clock64();
+  }
+  if constexpr (kStaged)
+    plan_cta_fast(a, smraw, (int)threadIdx.x, (int)blockDim.x, warp_best, shv, g_plan_tl);
+  else
+    plan_cta<CtaSync, false>(a, smraw, (int)threadIdx.x, (int)blockDim.x, CtaSync{}, warp_best, shv, g_plan_tl);
 }
 
 // Minimum dynamic shared memory (request table read from global memory).
@@ -67,6 +84,9 @@ PlanArgs make_plan_args(const star_plan_params* p, const star_plan_segments* sg,
   a.moves = moves;
   a.n_moves = n_moves;
   a.err = err_flag;
+  auto al = [&](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  a.bulk = al(a.req_id) && al(a.inst) && al(a.n_tok) && al(a.n_hat) && (!a.pinned || al(a.pinned)) &&
+           (a.world == 1 || (a.seg_stride & 15) == 0);
   return a;
 }
 
@@ -75,18 +95,20 @@ cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg,
   const PlanArgs a = make_plan_args(p, sg, moves, n_moves, err_flag);
   // Stage the request table in shared memory when it fits (it is re-read every round).
   const size_t lim = (size_t)kMaxSmemBytes - 4096;   // static shared memory + slack
-  const bool staged = plan_smem_layout(a.n, a.H, a.world, a.r_cap, true) <= lim;
-  const size_t smem = plan_smem_layout(a.n, a.H, a.world, a.r_cap, staged);
-  static int attr_bytes = 48 * 1024;
-  if ((int)smem > attr_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const bool staged = plan_fast_smem_layout(a.n, a.H, a.world, a.r_cap) <= lim;
+  const size_t smem = staged ? plan_fast_smem_layout(a.n, a.H, a.world, a.r_cap)
+                             : plan_smem_layout(a.n, a.H, a.world, a.r_cap, false);
+  auto kern = staged ? plan_kernel<true> : plan_kernel<false>;
+  static int attr_bytes[2] = {48 * 1024, 48 * 1024};
+  if ((int)smem > attr_bytes[staged]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_bytes = (int)smem;
+    attr_bytes[staged] = (int)smem;
   }
-  static bool carve = false;
-  if (!carve) {   // same L1/shared split as the GEMM kernels before it: no SM reconfiguration between launches
-    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    carve = true;
+  static bool carve[2] = {false, false};
+  if (!carve[staged]) {   // same L1/shared split as the GEMM kernels before it: no SM reconfiguration
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    carve[staged] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(1, 1, 1);
@@ -98,7 +120,7 @@ cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg,
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, plan_kernel, a, staged ? 1 : 0);
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 }  // namespace star

@@ -31,6 +31,7 @@ struct PlanArgs {
   star_move* moves;
   int32_t* n_moves;
   int32_t* err;
+  int bulk;                 // every segment array 16-byte aligned: the table may be bulk-copied
 };
 
 template <typename T>
@@ -210,9 +211,18 @@ struct PlanSmem {
 // The whole plan executed by `nthreads` threads of one CTA (thread index tid; `sync` is the
 // barrier over exactly those threads): the body of plan_kernel, also called by the fused
 // predictor tail's finishing CTA (lenpred_forward_project_plan) so no extra launch is needed.
-template <class Sync>
-__device__ __forceinline__ void plan_cta(const PlanArgs& a, const int staged, uint8_t* smraw, const int tid,
-                                         const int nthreads, Sync sync, Cand* warp_best, int* shv) {
+template <class Sync, bool staged>
+__device__ __forceinline__ void plan_cta(const PlanArgs& a, uint8_t* smraw, const int tid,
+                                         const int nthreads, Sync sync, Cand* warp_best, int* shv,
+                                         uint64_t* tl = nullptr) {
+#define PLAN_TS(k)                                       \
+  do {                                                   \
+    if (tl && tid == 0) {                                \
+      uint64_t t_;                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); \
+      tl[k] = t_;                                        \
+    }                                                    \
+  } while (0)
   const int n = a.n, H1 = a.H + 1;
   const bool strict = (a.flags & 1u) != 0;
   const bool cur_only = (a.flags & 2u) != 0;
@@ -270,7 +280,7 @@ __device__ __forceinline__ void plan_cta(const PlanArgs& a, const int staged, ui
     s.rpin[g] = a.pinned ? seg_ptr(a.pinned, k, a.seg_stride)[j] : (uint8_t)0;
   }
   if (tid == 0) s_nmoves = 0;
-  sync();
+  sync(); PLAN_TS(2);
   if (warp == nwarps - 1) {   // B0/B1/B2[T] = sum_{t<=T} beta_t {1, t, t^2}: warp scan (last warp)
     i128 c0 = 0, c1 = 0, c2 = 0;
     for (int base = 0; base < H1; base += 32) {
@@ -334,7 +344,7 @@ __device__ __forceinline__ void plan_cta(const PlanArgs& a, const int staged, ui
       for (int m = 16; m >= 1; m >>= 1) wpart += shfl_xor_i128(wpart, m);
       if (lane == 0) s.Wv[i] = cur_only ? (i128)s.beta[0] * Li[0] : wpart;
     }
-    sync();
+    sync(); PLAN_TS(3);
     if (warp == 0) {   // classification: lanes over instances, ballots build the ordered U list
       i128 wsum = 0;
       for (int i = lane; i < n; i += 32) wsum += s.Wv[i];
@@ -362,7 +372,7 @@ __device__ __forceinline__ void plan_cta(const PlanArgs& a, const int staged, ui
         s_stop = anyO ? 0 : 1;
       }
     }
-    sync();
+    sync(); PLAN_TS(4);
     if (s_stop) break;
 
     // ---- Phase 2 + 3: per-request best target, then block argmax ----
@@ -372,6 +382,7 @@ __device__ __forceinline__ void plan_cta(const PlanArgs& a, const int staged, ui
     best.dst = 0;
     best.g = -1;
     const int nU = s_nU;
+    PLAN_TS(11);
     for (int g = tid; g < nslots; g += nthreads) {
       const int k = g / a.r_cap, j = g % a.r_cap;
       if (j >= s.seg_count[k]) continue;
@@ -389,9 +400,11 @@ __device__ __forceinline__ void plan_cta(const PlanArgs& a, const int staged, ui
       const Cand c = best_target(a, strict, cur_only, g, src, N, nh, rid, s.ulist, nU, s.Ls, s.P0, s.P1, s.B, H1);
       if (cand_better(c, best)) best = c;
     }
+    PLAN_TS(12);
     best = warp_argmax(best);
+    PLAN_TS(13);
     if (lane == 0) warp_best[warp] = best;
-    sync();
+    sync(); PLAN_TS(5);
     if (warp == 0) {
       Cand c;
       if (lane < nwarps) {
@@ -400,6 +413,7 @@ __device__ __forceinline__ void plan_cta(const PlanArgs& a, const int staged, ui
         c.score = 0; c.id = 0; c.dst = 0; c.g = -1;
       }
       c = warp_argmax(c);   // butterfly: every lane holds the winner
+      PLAN_TS(8);
       if (c.g < 0) {
         if (lane == 0) s_stop = 1;
       } else {
@@ -413,6 +427,7 @@ __device__ __forceinline__ void plan_cta(const PlanArgs& a, const int staged, ui
           s.Ls[(int64_t)src * H1 + t] -= ct;
           s.Ls[(int64_t)c.dst * H1 + t] += ct;
         }
+        PLAN_TS(9);
         if (lane == 0) {
           s.moved[c.g >> 5] |= 1u << (c.g & 31);
           const i128 gain = (i128)2 * n * c.score;
@@ -426,12 +441,15 @@ __device__ __forceinline__ void plan_cta(const PlanArgs& a, const int staged, ui
           a.moves[s_nmoves] = mv;
           s_nmoves = s_nmoves + 1;
         }
+        PLAN_TS(10);
       }
     }
-    sync();
+    sync(); PLAN_TS(6);
     if (s_stop) break;
   }
+  PLAN_TS(7);
   if (tid == 0) *a.n_moves = s_nmoves;
+#undef PLAN_TS
 }
 
 

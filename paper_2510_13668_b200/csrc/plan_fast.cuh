@@ -1,0 +1,527 @@
+// plan_fast.cuh -- the single-CTA Alg. 1 with the request table in shared
+// memory.  Same arithmetic, filters and candidate order as plan_cta (plan_core.cuh: closed-form
+// score, readings A15-A21); what changes is how the work of a round is laid out:
+//   * staging: the loads (needed by Phase 1) are read synchronously; the request table (needed
+//     only once an instance is overloaded) streams in with cp.async behind Phase 1 and the
+//     classification, so a round that finds no overloaded instance barely waits for it
+//   * Phase 1 recomputes the prefix sums P0/P1, W_i and T_exec(i) only for the instances the
+//     previous move changed (all of them in round 0)
+//   * Phases 2-3 first compact the requests of overloaded instances (warp ballots + one shared
+//     counter), so every lane scores a real candidate; the all-slots scan left most lanes of a
+//     warp idle while one lane evaluated a candidate (~4.6k cycles per warp iteration on B200)
+//   * warp collectives follow an explicit __syncwarp: a warp does not reconverge at a CTA
+//     barrier, and shuffles of a diverged warp take the slow path (measured 9k cycles for one
+//     5-step argmax)
+// The candidate order is extended by the slot index (cand_better_g), a total order, so the
+// compaction order does not matter.
+#pragma once
+#include "plan_core.cuh"
+#include "ptx.cuh"
+
+namespace star {
+
+struct FastSmem {
+  i128* P0;        // [n][H+1]
+  i128* P1;        // [n][H+1]
+  i128* B;         // [3][H+1]
+  i128* Wv;        // [n]
+  i128* texec;     // [n]  T_exec(i) = a + b * L_i[0]   (filter (a))
+  int64_t* Ls;     // [n][H+1]
+  int64_t* cmem;   // [n]  C_mem(i) - reserved(i) (non-strict) or C_mem(i) (strict); nullptr if no memory filter
+  uint32_t* beta;  // [H+1]
+  int32_t* rid;    // [slots] request table (slot order), cp.async
+  int32_t* rinst;  // [slots] source instance; after round 0's compaction -1 marks "never a candidate"
+  int32_t* rntok;
+  int32_t* rnhat;
+  int32_t* cidx;   // [slots] this round's candidates (slot indices)
+  uint32_t* moved; // bitmap [slots]
+  uint8_t* rpin;   // [slots]
+  int* seg_count;  // [world]
+  int* ulist;      // [n]
+  uint8_t* inO;    // [n]
+  uint8_t* dirty;  // [n]
+  uint64_t* bar;   // request-table bulk copies
+};
+
+// Shared-memory slot pitch per segment: a multiple of 16 so every segment's table block starts on
+// 16 bytes (bulk copies); slots with j >= r_cap are never valid.
+__host__ __device__ inline int plan_fast_pitch(int r_cap) { return (r_cap + 15) & ~15; }
+
+inline size_t plan_fast_smem_layout(int n, int H, int world, int r_cap) {
+  const size_t H1 = (size_t)H + 1, nn = (size_t)n, slots = (size_t)world * plan_fast_pitch(r_cap);
+  size_t b = 16 * (2 * nn * H1 + 3 * H1 + 2 * nn) + 8 * (nn * H1 + nn) + 4 * H1;
+  b += 4 * 5 * slots + 4 * ((slots + 31) / 32) + slots;
+  b += 4 * (size_t)world + 4 * nn + 2 * nn;
+  return b + 16 * 21;   // mbarrier + alignment slack (each of the 19 arrays starts on 16 bytes)
+}
+
+// Cand order extended by the slot index, so the winner does not depend on enumeration order.
+__device__ __forceinline__ bool cand_better_g(const Cand& x, const Cand& y) {
+  if (x.g < 0) return false;
+  if (y.g < 0) return true;
+  if (x.score != y.score) return x.score > y.score;
+  if (x.id != y.id) return x.id < y.id;
+  if (x.dst != y.dst) return x.dst < y.dst;
+  return x.g < y.g;
+}
+
+__device__ __forceinline__ Cand warp_argmax_g(Cand c) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    Cand o;
+    const uint64_t lo = __shfl_xor_sync(0xFFFFFFFFu, (uint64_t)c.score, off);
+    const uint64_t hi = __shfl_xor_sync(0xFFFFFFFFu, (uint64_t)(c.score >> 64), off);
+    o.score = (i128)(((unsigned __int128)hi << 64) | lo);
+    o.id = __shfl_xor_sync(0xFFFFFFFFu, c.id, off);
+    o.dst = __shfl_xor_sync(0xFFFFFFFFu, c.dst, off);
+    o.g = __shfl_xor_sync(0xFFFFFFFFu, c.g, off);
+    if (cand_better_g(o, c)) c = o;
+  }
+  return c;
+}
+
+// a * b (mod 2^128) for a 32-bit unsigned b: four 32x32->64 multiply-adds over the limbs of a
+// (the generic __int128 product costs ~4x as many IMADs and dominated the candidate scoring).
+__device__ __forceinline__ i128 mul_u32(i128 a, uint32_t b) {
+  const unsigned __int128 ua = (unsigned __int128)a;
+  const uint64_t lo = (uint64_t)ua, hi = (uint64_t)(ua >> 64);
+  const uint64_t p0 = (uint64_t)(uint32_t)lo * b;
+  const uint64_t p1 = (lo >> 32) * b + (p0 >> 32);
+  const uint64_t p2 = (uint64_t)(uint32_t)hi * b + (p1 >> 32);
+  const uint64_t p3 = (hi >> 32) * b + (p2 >> 32);
+  const uint64_t rlo = (p0 & 0xFFFFFFFFull) | (p1 << 32);
+  const uint64_t rhi = (p2 & 0xFFFFFFFFull) | (p3 << 32);
+  return (i128)(((unsigned __int128)rhi << 64) | rlo);
+}
+// a * b (mod 2^128) for a 32-bit signed b
+__device__ __forceinline__ i128 mul_i32(i128 a, int32_t b) {
+  const uint32_t m = b < 0 ? (uint32_t)(-(int64_t)b) : (uint32_t)b;
+  const i128 r = mul_u32(a, m);
+  return b < 0 ? -r : r;
+}
+
+template <class T>
+__device__ __forceinline__ T* carve(uint8_t*& p, size_t count) {
+  p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+  T* r = reinterpret_cast<T*>(p);
+  p += sizeof(T) * count;
+  return r;
+}
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Whole plan by one CTA of `nthreads` threads (multiple of 32).  tl: optional %globaltimer stamps.
+__device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw, const int tid, const int nthreads,
+                                              Cand* warp_best, int* shv, uint64_t* tl) {
+#define PLAN_TS(k)                                           \
+  do {                                                       \
+    if (tl && tid == 0) {                                    \
+      uint64_t t_;                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); \
+      tl[k] = t_;                                            \
+      tl[32 + (k)] = clock64();                              \
+    }                                                        \
+  } while (0)
+  const int n = a.n, H1 = a.H + 1;
+  const bool strict = (a.flags & 1u) != 0;
+  const bool cur_only = (a.flags & 2u) != 0;
+  const int rp = plan_fast_pitch(a.r_cap);   // slot g = k * rp + j
+  const int nslots = a.world * rp;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nthreads >> 5;
+  FastSmem s;
+  {
+    uint8_t* p = smraw;
+    s.P0 = carve<i128>(p, (size_t)n * H1);
+    s.P1 = carve<i128>(p, (size_t)n * H1);
+    s.B = carve<i128>(p, 3 * (size_t)H1);
+    s.Wv = carve<i128>(p, n);
+    s.texec = carve<i128>(p, n);
+    s.Ls = carve<int64_t>(p, (size_t)n * H1);
+    s.cmem = a.c_mem ? carve<int64_t>(p, n) : nullptr;
+    s.beta = carve<uint32_t>(p, H1);
+    s.rid = carve<int32_t>(p, nslots);
+    s.rinst = carve<int32_t>(p, nslots);
+    s.rntok = carve<int32_t>(p, nslots);
+    s.rnhat = carve<int32_t>(p, nslots);
+    s.cidx = carve<int32_t>(p, nslots);
+    s.moved = carve<uint32_t>(p, (nslots + 31) / 32);
+    s.rpin = carve<uint8_t>(p, nslots);
+    s.seg_count = carve<int>(p, a.world);
+    s.ulist = carve<int>(p, n);
+    s.inO = carve<uint8_t>(p, n);
+    s.dirty = carve<uint8_t>(p, n);
+    s.bar = carve<uint64_t>(p, 1);
+  }
+  int& s_stop = shv[0];
+  int& s_nU = shv[1];
+  int& s_nmoves = shv[2];
+  int& s_ncand = shv[3];
+
+  // ---- staging ----
+  // Request table: consumed only after Phase 1 + classification, so it streams in behind them:
+  // one thread issues a bulk copy (TMA, 16-byte granules) per segment and array when the segment
+  // arrays are 16-byte aligned (a.bulk, checked on the host), the sub-16-byte tails go through
+  // the loads below; otherwise 4-byte cp.async per element.
+  constexpr int kTabArrays = 5;
+  auto tab_src = [&](int arr, int k) -> const uint8_t* {
+    const void* base = arr == 0 ? (const void*)a.req_id : arr == 1 ? (const void*)a.inst
+                     : arr == 2 ? (const void*)a.n_tok : arr == 3 ? (const void*)a.n_hat : (const void*)a.pinned;
+    return reinterpret_cast<const uint8_t*>(base) + (int64_t)k * a.seg_stride;
+  };
+  auto tab_dst = [&](int arr) -> uint8_t* {
+    return arr == 0 ? (uint8_t*)s.rid : arr == 1 ? (uint8_t*)s.rinst : arr == 2 ? (uint8_t*)s.rntok
+         : arr == 3 ? (uint8_t*)s.rnhat : (uint8_t*)s.rpin;
+  };
+  const int n_arr = a.pinned ? kTabArrays : kTabArrays - 1;
+  const int tail_elems = a.bulk ? ((a.r_cap * 4) & 15) / 4 : 0;   // int32 elements past the last granule
+  const int tail_pin = a.bulk ? (a.r_cap & 15) : 0;
+  if (a.bulk) {
+    if (tid == nthreads - 1) {   // the last thread: it rarely has a synchronous item below
+      mbar_init(s.bar, 1);
+      fence_barrier_init();
+      const uint32_t fl32 = (uint32_t)(a.r_cap * 4) & ~15u, fl8 = (uint32_t)a.r_cap & ~15u;
+      mbar_arrive_expect_tx(s.bar, (uint32_t)a.world * (4 * fl32 + (a.pinned ? fl8 : 0)));
+      for (int k = 0; k < a.world; ++k)
+        for (int arr = 0; arr < n_arr; ++arr) {
+          const uint32_t fl = arr < 4 ? fl32 : fl8;
+          if (fl) bulk_g2s(tab_dst(arr) + (size_t)k * rp * (arr < 4 ? 4 : 1), tab_src(arr, k), fl, s.bar);
+        }
+    }
+  } else {
+    for (int g = tid; g < nslots; g += nthreads) {
+      const int k = g / rp, j = g - k * rp;
+      if (j >= a.r_cap) continue;
+      cp_async4(s.rid + g, seg_ptr(a.req_id, k, a.seg_stride) + j);
+      cp_async4(s.rinst + g, seg_ptr(a.inst, k, a.seg_stride) + j);
+      cp_async4(s.rntok + g, seg_ptr(a.n_tok, k, a.seg_stride) + j);
+      cp_async4(s.rnhat + g, seg_ptr(a.n_hat, k, a.seg_stride) + j);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  PLAN_TS(12);
+  // Synchronous part, one item per thread where it fits, so all loads are in flight together:
+  // loads L, beta, capacities, segment counts, bulk-copy tails, pinned flags (cp.async path).
+  {
+    const int nL = n * H1, nTail = a.world * (4 * tail_elems + (a.pinned ? tail_pin : 0));
+    const int nPin = (!a.bulk && a.pinned) ? nslots : 0;
+    const int total = nL + H1 + n + a.world + nTail + nPin;
+    for (int e = tid; e < total; e += nthreads) {
+      int r = e;
+      if (r < nL) {   // segment k holds instances [k*n_loc, (k+1)*n_loc)
+        const int i = r / H1, t = r - i * H1;
+        const int k = i / a.n_loc, il = i - k * a.n_loc;
+        s.Ls[r] = seg_ptr(a.L, k, a.seg_stride)[(int64_t)il * H1 + t];
+        continue;
+      }
+      r -= nL;
+      if (r < H1) {
+        s.beta[r] = a.beta_q[r];
+        continue;
+      }
+      r -= H1;
+      if (r < n) {
+        if (s.cmem)   // filter (b) capacity: strict needs L_u[0] + N_hat <= C_mem; otherwise
+                      // L_u[0] + reserved + N + N_hat <= C_mem  (readings A17/A18)
+          s.cmem[r] = a.c_mem[r] - (strict ? 0 : (a.reserved ? a.reserved[r] : 0));
+        s.dirty[r] = 1;
+        continue;
+      }
+      r -= n;
+      if (r < a.world) {
+        int c = a.r_cap;
+        if (a.r_count) {
+          c = *seg_ptr(a.r_count, r, a.seg_stride);
+          if (c < 0 || c > a.r_cap) {
+            if (a.err) atomicOr(a.err, 16);
+            c = c < 0 ? 0 : a.r_cap;
+          }
+        }
+        s.seg_count[r] = c;
+        continue;
+      }
+      r -= a.world;
+      if (r < nTail) {
+        const int per = 4 * tail_elems + (a.pinned ? tail_pin : 0);
+        const int k = r / per;
+        int q = r - k * per;
+        if (q < 4 * tail_elems) {
+          const int arr = q / tail_elems, j = (a.r_cap & ~3) + (q - arr * tail_elems);
+          reinterpret_cast<int32_t*>(tab_dst(arr))[(size_t)k * rp + j] =
+              reinterpret_cast<const int32_t*>(tab_src(arr, k))[j];
+        } else {
+          const int j = (a.r_cap & ~15) + (q - 4 * tail_elems);
+          s.rpin[(size_t)k * rp + j] = tab_src(4, k)[j];
+        }
+        continue;
+      }
+      r -= nTail;
+      {   // pinned flags, cp.async path
+        const int k = r / rp, j = r - k * rp;
+        if (j < a.r_cap) s.rpin[r] = seg_ptr(a.pinned, k, a.seg_stride)[j];
+      }
+    }
+  }
+  PLAN_TS(13);
+  if (!a.pinned)
+    for (int g = tid; g < nslots; g += nthreads) s.rpin[g] = 0;
+  for (int w = tid; w < (nslots + 31) / 32; w += nthreads) s.moved[w] = 0u;
+  if (tid == 0) s_nmoves = 0;
+  PLAN_TS(15);
+  __syncthreads();
+  __syncwarp();
+  if (warp == nwarps - 1) {   // B0/B1/B2[T] = sum_{t<=T} beta_t {1, t, t^2}: warp scan (last warp)
+    i128 c0 = 0, c1 = 0, c2 = 0;
+    for (int base = 0; base < H1; base += 32) {
+      const int u = base + lane;
+      const i128 bt = u < H1 ? (i128)s.beta[u] : (i128)0;
+      i128 x0 = bt, x1 = bt * u, x2 = bt * u * u;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off), y2 = shfl_up_i128(x2, off);
+        if (lane >= off) {
+          x0 += y0;
+          x1 += y1;
+          x2 += y2;
+        }
+      }
+      x0 += c0;
+      x1 += c1;
+      x2 += c2;
+      if (u < H1) {
+        s.B[u] = x0;
+        s.B[H1 + u] = x1;
+        s.B[2 * H1 + u] = x2;
+      }
+      c0 = shfl_idx_i128(x0, 31);
+      c1 = shfl_idx_i128(x1, 31);
+      c2 = shfl_idx_i128(x2, 31);
+    }
+  }
+  PLAN_TS(2);
+  const int p1_warps = nwarps - 1;   // Phase-1 warps (the last one builds B in round 0)
+
+  for (int round = 0; round < a.max_moves; ++round) {
+    // ---- Phase 1: InstanceClassification, changed instances only ----
+    // one warp per instance: W_i, T_exec(i) and the prefix sums P0_i / P1_i (warp scans)
+    for (int i = warp; i < n && warp < p1_warps; i += p1_warps) {
+      __syncwarp();
+      if (!s.dirty[i]) continue;
+      const int64_t* Li = s.Ls + (int64_t)i * H1;
+      i128 wpart = 0, c0 = 0, c1 = 0;
+      for (int base = 0; base < H1; base += 32) {
+        const int t = base + lane;
+        const i128 x = t < H1 ? (i128)s.beta[t] * Li[t] : (i128)0;
+        if (t >= 1) wpart += x;
+        i128 x0 = x, x1 = x * t;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off);
+          if (lane >= off) {
+            x0 += y0;
+            x1 += y1;
+          }
+        }
+        x0 += c0;
+        x1 += c1;
+        if (t < H1) {
+          s.P0[(int64_t)i * H1 + t] = x0;
+          s.P1[(int64_t)i * H1 + t] = x1;
+        }
+        c0 = shfl_idx_i128(x0, 31);
+        c1 = shfl_idx_i128(x1, 31);
+      }
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) wpart += shfl_xor_i128(wpart, m);
+      if (lane == 0) {
+        s.Wv[i] = cur_only ? (i128)s.beta[0] * Li[0] : wpart;
+        s.texec[i] = (i128)a.a_ps + (i128)a.b_ps * Li[0];
+      }
+    }
+    __syncthreads();
+    PLAN_TS(3);
+    __syncwarp();
+    if (warp == 0) {   // classification: lanes over instances, ballots build the ordered U list
+      i128 wsum = 0;
+      for (int i = lane; i < n; i += 32) wsum += s.Wv[i];
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) wsum += shfl_xor_i128(wsum, m);
+      const i128 rhs = (i128)(a.theta_den + a.theta_num) * wsum;
+      bool anyO = false;
+      int nU = 0;
+      for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        bool o = false, u = false;
+        if (i < n) {
+          o = (i128)n * a.theta_den * s.Wv[i] > rhs;
+          u = !o && ((i128)n * a.theta_den * (i128)65536 * s.Ls[(int64_t)i * H1] < rhs);
+          s.inO[i] = o ? 1 : 0;
+          s.dirty[i] = 0;   // Phase 1 of this round is done (all warps passed the barrier)
+        }
+        anyO |= __any_sync(0xFFFFFFFFu, o) != 0;
+        const uint32_t um = __ballot_sync(0xFFFFFFFFu, u);
+        if (u) s.ulist[nU + __popc(um & ((1u << lane) - 1u))] = i;
+        nU += __popc(um);
+      }
+      if (lane == 0) {
+        s_nU = nU;
+        s_stop = anyO ? 0 : 1;
+        s_ncand = 0;
+      }
+    }
+    if (round == 0) {   // the request table has landed (the barrier publishes everyone's cp.async)
+      if (a.bulk) mbar_wait(s.bar, 0);
+      else cp_async_wait_all();
+    }
+    __syncthreads();
+    PLAN_TS(4);
+    if (s_stop) break;
+
+    // ---- candidate compaction: requests on overloaded instances, not pinned, not yet moved ----
+    // (round 0 also validates each slot once and marks the slots that can never be candidates)
+    // four consecutive slots per lane (one 16-byte shared load), one atomic per warp
+    for (int base = 0; base < nslots; base += 4 * nthreads) {
+      const int g0 = base + 4 * tid;
+      uint32_t cm = 0;   // candidate bits of slots g0..g0+3
+      if (g0 < nslots) {   // nslots is a multiple of 16 (pitch)
+        int4 sv = *reinterpret_cast<const int4*>(s.rinst + g0);
+        int src4[4] = {sv.x, sv.y, sv.z, sv.w};
+        const uint32_t mv = (s.moved[g0 >> 5] >> (g0 & 31)) & 15u;
+        if (round == 0) {
+          const int k = g0 / rp, j0 = g0 - k * rp, cnt = s.seg_count[k];
+          bool changed = false;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            int src = src4[q];
+            if (j0 + q >= cnt) {
+              src = -1;
+            } else if (src < 0 || src >= n) {
+              if (a.err) atomicOr(a.err, 1);
+              src = -1;
+            } else if (s.rpin[g0 + q]) {
+              src = -1;
+            }
+            changed |= src != src4[q];
+            src4[q] = src;
+          }
+          if (changed) *reinterpret_cast<int4*>(s.rinst + g0) = make_int4(src4[0], src4[1], src4[2], src4[3]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (src4[q] >= 0 && s.inO[src4[q]] && !((mv >> q) & 1u)) cm |= 1u << q;
+      }
+      __syncwarp();
+      const int cntl = __popc(cm);
+      int x = cntl;   // inclusive warp scan of the per-lane counts
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+        if (lane >= off) x += y;
+      }
+      int pos = 0;
+      if (lane == 31 && x) pos = atomicAdd(&s_ncand, x);
+      pos = __shfl_sync(0xFFFFFFFFu, pos, 31) + x - cntl;
+      while (cm) {
+        const int q = __ffs(cm) - 1;
+        cm &= cm - 1;
+        s.cidx[pos++] = g0 + q;
+      }
+    }
+    __syncthreads();
+    PLAN_TS(9);
+
+    // ---- Phase 2 + 3: candidates x targets in U, then block argmax ----
+    Cand best;
+    best.score = 0;
+    best.id = 0;
+    best.dst = 0;
+    best.g = -1;
+    const int nU = s_nU, ncand = s_ncand;
+    for (int c = tid; c < ncand; c += nthreads) {
+      const int g = s.cidx[c];
+      const int src = s.rinst[g];
+      const int32_t N = s.rntok[g], nh = s.rnhat[g];
+      int T = nh - 1 < 0 ? 0 : (nh - 1 > a.H ? a.H : nh - 1);
+      if (cur_only) T = 0;
+      // self = N^2 B0[T] + 2N B1[T] + B2[T];  keep = N P0_src[T] + P1_src[T] - self
+      const i128 self = mul_i32(mul_i32(s.B[T], N), N) + mul_i32(s.B[H1 + T], N) * 2 + s.B[2 * H1 + T];
+      const i128 keep = mul_i32(s.P0[(int64_t)src * H1 + T], N) + s.P1[(int64_t)src * H1 + T] - self;
+      const i128 mig = (i128)a.c0_ps + mul_i32((i128)a.c1_ps, N);
+      const int64_t need_r = strict ? (cur_only ? 0 : (int64_t)nh) : (int64_t)N + (cur_only ? 0 : (int64_t)nh);
+      const int32_t rid = s.rid[g];
+      for (int qq = 0; qq < nU; ++qq) {
+        const int u = s.ulist[qq];
+        if (!cur_only && !(mul_i32(s.texec[u], nh) > mig)) continue;                 // filter (a)
+        if (s.cmem && !(s.Ls[(int64_t)u * H1] + need_r <= s.cmem[u])) continue;       // filter (b)
+        const i128 score = keep - (mul_i32(s.P0[(int64_t)u * H1 + T], N) + s.P1[(int64_t)u * H1 + T]);
+        if (score <= 0) continue;
+        Cand cd;
+        cd.score = score;
+        cd.id = rid;
+        cd.dst = u;
+        cd.g = g;
+        if (cand_better_g(cd, best)) best = cd;
+      }
+    }
+    PLAN_TS(10);
+    __syncwarp();
+    best = warp_argmax_g(best);
+    PLAN_TS(11);
+    if (lane == 0) warp_best[warp] = best;
+    __syncthreads();
+    PLAN_TS(5);
+    __syncwarp();
+    if (warp == 0) {
+      Cand c;
+      if (lane < nwarps) {
+        c = warp_best[lane];
+      } else {
+        c.score = 0; c.id = 0; c.dst = 0; c.g = -1;
+      }
+      c = warp_argmax_g(c);   // every lane holds the winner
+      PLAN_TS(8);
+      if (c.g < 0) {
+        if (lane == 0) s_stop = 1;
+      } else {
+        // ExecuteMigration is out of the path: apply m* to the loads for the next round.
+        const int src = s.rinst[c.g];
+        const int64_t N = s.rntok[c.g], nh = s.rnhat[c.g];
+        for (int t = lane; t < H1; t += 32) {
+          const int64_t ct = (t == 0) ? N : (t < nh ? N + t : 0);
+          s.Ls[(int64_t)src * H1 + t] -= ct;
+          s.Ls[(int64_t)c.dst * H1 + t] += ct;
+        }
+        if (lane == 0) {
+          s.moved[c.g >> 5] |= 1u << (c.g & 31);
+          s.dirty[src] = 1;
+          s.dirty[c.dst] = 1;
+          const i128 gain = (i128)2 * n * c.score;
+          star_move mv;
+          mv.req_id = c.id;
+          mv.src = src;
+          mv.dst = c.dst;
+          mv.round = round;
+          mv.gain_hi = (int64_t)(gain >> 64);
+          mv.gain_lo = (uint64_t)gain;
+          a.moves[s_nmoves] = mv;
+          s_nmoves = s_nmoves + 1;
+        }
+      }
+    }
+    __syncthreads();
+    PLAN_TS(6);
+    if (s_stop) break;
+  }
+  // no copy may still be in flight when the CTA exits (a plan that stopped before round 0's wait)
+  if (a.bulk) mbar_wait(s.bar, 0);
+  else cp_async_wait_all();
+  PLAN_TS(7);
+  if (tid == 0) *a.n_moves = s_nmoves;
+#undef PLAN_TS
+}
+
+}  // namespace star

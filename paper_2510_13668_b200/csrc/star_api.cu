@@ -834,6 +834,13 @@ star_status plan_reschedule_segmented(const star_plan_params* p, const star_plan
   return STAR_OK;
 }
 
+star_status star_plan_timeline(uint64_t* host16) {
+  if (!host16) return fail(STAR_EINVAL, "host16 is NULL");
+  STAR_CUDA(cudaDeviceSynchronize());
+  STAR_CUDA(plan_timeline(host16));
+  return STAR_OK;
+}
+
 size_t star_plan_workspace_bytes(int n_inst, int H, int64_t request_slots) {
   if (n_inst < 1 || H < 0 || request_slots < 0) return 0;
   return plan_large_workspace_bytes(n_inst, H, request_slots);
