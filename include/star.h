@@ -201,6 +201,11 @@ star_status project_instance_load(int R, int n_inst, int inst_base, int H,
  *            lowest req_id, then lowest target (reading A20).  Apply, emit, next round.
  * The whole plan runs in one CTA: per-request warp argmax over target instances of the
  * closed-form score, then a block argmax over requests.
+ * Stream ordering: the plan is launched with programmatic dependent launch.  It reads L and
+ * n_hat only after the preceding kernel in the stream has completed; its static inputs
+ * (req_id, inst, n_tok, pinned, counts, beta_q, c_mem, reserved) may be read while a preceding
+ * kernel of THIS library is still running (none of them writes those arrays).  A preceding
+ * kernel of another library cannot overlap (it does not trigger the dependent launch).
  * ===================================================================================== */
 #define STAR_STRICT_MEM    1u
 #define STAR_CURRENT_ONLY  2u
@@ -252,9 +257,11 @@ star_status plan_reschedule_segmented(const star_plan_params* p, const star_plan
                                       star_stream_t stream);
 
 /* Diagnostics: %globaltimer stamps (ns) of the most recent single-CTA plan launch: [0] entry,
- * [1] after griddepcontrol.wait, [2] inputs staged, [3] prefix sums, [4] classification,
- * [5] candidate argmax, [6] move applied (first round), [7] end.  Synchronises the device. */
-star_status star_plan_timeline(uint64_t* host16);
+ * [1] launched, [12] static inputs staged, [13] after griddepcontrol.wait, [2] inputs staged,
+ * [3] W pass, [4] classification, [9] candidates compacted, [5] candidate argmax, [6] move
+ * applied, [7] end (per-round stamps hold the last round); [32 + k] the same as clock64.
+ * Synchronises the device. */
+star_status star_plan_timeline(uint64_t* host64);
 
 /* Cluster-scale form (NEXT-3: hundreds of instances, up to 2^20 request slots; the paper's
  * budget is <= 300 ms at 256 instances): identical semantics and outputs, but the

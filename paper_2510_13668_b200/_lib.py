@@ -161,9 +161,10 @@ class Predictor:
     def timeline(self, enable: bool = True, fetch: bool = False, layer1: bool = False):
         """Diagnostics: per-CTA phase stamps of the fused tail / layer-1 GEMM (star_predictor_timeline)."""
         if not fetch:
-            _check(lib().star_predictor_timeline(self.handle, int(enable), None, 0, None), "timeline")
+            _check(lib().star_predictor_timeline(self.handle, (2 if layer1 else 1) if enable else 0, None, 0, None),
+                   "timeline")
             return None
-        buf = np.zeros((4 * 148, 16), dtype=np.uint64)
+        buf = np.zeros((4 * 148, 16 if layer1 else 32), dtype=np.uint64)
         n = I()
         _check(lib().star_predictor_timeline(self.handle, 2 if layer1 else 1, buf.ctypes.data_as(P), buf.shape[0],
                                              C.byref(n)), "timeline")

@@ -51,6 +51,7 @@ __device__ __forceinline__ i128 shfl_idx_i128d(i128 v, int src) {
 
 // One warp: P0_i[T] = sum_{t<=T} beta_t L_i[t], P1_i[T] = sum_{t<=T} t beta_t L_i[t].
 __device__ void disp_prefix_row(const DispArgs& a, const uint32_t* sbeta, int i) {
+  __syncwarp();   // reconverge first: shuffles of a diverged warp take a slow path
   const int lane = threadIdx.x & 31, H1 = a.H + 1;
   const int64_t* Li = a.L + (int64_t)i * H1;
   i128 c0 = 0, c1 = 0;
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispArgs a
         }
         if (dkey_less(k, best)) best = k;
       }
+      __syncwarp();
 #pragma unroll
       for (int m = 16; m >= 1; m >>= 1) {
         const DKey o = dkey_shfl(best, m);
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispArgs a
       }
       if (lane == 0) wbest[warp] = best;
       __syncthreads();
+      __syncwarp();
       if (warp == 0) {
         DKey k;
         if (lane < nwarps) {

@@ -56,10 +56,12 @@ struct TailArgs {
   const int32_t* M_dev;  // device-side row count (refresh mode), or nullptr (then M)
 };
 
-// Phase timestamp (diagnostics only; one designated thread per phase).
+// Phase timestamp (diagnostics only; one designated thread per phase).  Row stride
+// kTailTlStride: slots 0-14 phases, 15 the SM id, 16-19 the last finisher's projection finalize.
+constexpr int kTailTlStride = 32;
 #define TAIL_TS(k)                                                                                        \
   do {                                                                                                    \
-    if (p.tl) p.tl[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16 + (k)] = globaltimer_ns(); \
+    if (p.tl) p.tl[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * kTailTlStride + (k)] = globaltimer_ns(); \
   } while (0)
 
 struct TailSmem {
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(192, 1)
     if (p.tl) {
       uint32_t smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      p.tl[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16 + 15] = smid;
+      p.tl[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * kTailTlStride + 15] = smid;
     }
   }
   const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
@@ -453,6 +455,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) dot = fmaf(sw4[c0 + cc + j], fmaxf(z[j] + sb3[c0 + cc + j], 0.0f), dot);
       }
+      __syncwarp();   // reconverge before the collectives (a CTA barrier does not)
       for (int off = 1; off < tpr; off <<= 1) dot += __shfl_xor_sync(0xFFFFFFFFu, dot, off);
       const bool owner = red_g == 0 && grow < Mrows;
       int32_t nh = 0;
@@ -477,6 +480,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (*s_last) {
+          if (te == 0) TAIL_TS(16);
           __threadfence();
           const int nb = p.pa.n_inst * (p.pa.H + 2);
           const uint32_t* hc = p.pa.ws_cnt;
@@ -484,21 +488,41 @@ __global__ void __launch_bounds__(192, 1)
           if (nb * 12 <= 65536) {   // stage the histogram in shared memory (one round trip)
             unsigned long long* ss = reinterpret_cast<unsigned long long*>(sZ3);
             uint32_t* sc = reinterpret_cast<uint32_t*>(ss + nb);
-            for (int k = te; k < nb; k += 128) {
-              ss[k] = __ldcg(p.pa.ws_sum + k);
-              sc[k] = __ldcg(p.pa.ws_cnt + k);
+            constexpr int kB = 8;   // all loads of a batch in flight before any store
+            for (int base = 0; base < nb; base += kB * 128) {
+              unsigned long long vs[kB];
+              uint32_t vc[kB];
+#pragma unroll
+              for (int u = 0; u < kB; ++u) {
+                const int k = base + u * 128 + te;
+                if (k < nb) {
+                  vs[u] = __ldcg(p.pa.ws_sum + k);
+                  vc[u] = __ldcg(p.pa.ws_cnt + k);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < kB; ++u) {
+                const int k = base + u * 128 + te;
+                if (k < nb) {
+                  ss[k] = vs[u];
+                  sc[k] = vc[u];
+                }
+              }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
             hc = sc;
             hs = ss;
           }
+          if (te == 0) TAIL_TS(17);
           proj_finalize(p.pa, hc, hs, sbeta, warp - 2, 4);
           asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (te == 0) TAIL_TS(18);
           for (int k = te; k < nb; k += 128) {
             p.pa.ws_cnt[k] = 0;
             p.pa.ws_sum[k] = 0;
           }
           if (te == 0) *p.pa.ws_arrive = 0;
+          if (te == 0) TAIL_TS(19);
         }
       }
     }

@@ -28,8 +28,8 @@ constexpr int kPlanThreads = 512;
 // diagnostics: %globaltimer stamps of the most recent single-CTA plan (star_plan_timeline)
 __device__ uint64_t g_plan_tl[64];
 
-cudaError_t plan_timeline(uint64_t* host16) {
-  return cudaMemcpyFromSymbol(host16, g_plan_tl, sizeof(uint64_t) * 64);
+cudaError_t plan_timeline(uint64_t* host64) {
+  return cudaMemcpyFromSymbol(host64, g_plan_tl, sizeof(uint64_t) * 64);
 }
 
 
@@ -39,8 +39,8 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a)
   __shared__ Cand warp_best[kPlanThreads / 32];
   __shared__ int shv[4];
   if (threadIdx.x == 0) g_plan_tl[0] = globaltimer_ns();
-  pdl_wait();   // inputs come from the projection / all-gather (PDL launch)
-  pdl_launch_dependents();
+  if constexpr (!kStaged) pdl_wait();   // inputs come from the projection / all-gather (PDL launch)
+  pdl_launch_dependents();   // (the fast path waits itself, after fetching its static inputs)
   if (threadIdx.x == 0) {
     g_plan_tl[1] = globaltimer_ns();
     g_plan_tl[33] = clock64();

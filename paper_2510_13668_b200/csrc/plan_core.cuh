@@ -65,6 +65,7 @@ __device__ __forceinline__ Cand shfl_cand(const Cand& c, int src_lane) {
 }
 
 __device__ __forceinline__ Cand warp_argmax(Cand c) {
+  __syncwarp();   // reconverge first: shuffles of a diverged warp take a slow path
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
@@ -316,6 +317,7 @@ __device__ __forceinline__ void plan_cta(const PlanArgs& a, uint8_t* smraw, cons
     // one warp per instance: W_i (warp reduction) and the Phase-3 prefix sums
     //   P0_i[T] = sum_{t<=T} beta_t L_i[t],  P1_i[T] = sum_{t<=T} t beta_t L_i[t]  (warp scan)
     for (int i = warp; i < n && warp < p1_warps; i += p1_warps) {
+      __syncwarp();
       const int64_t* Li = s.Ls + (int64_t)i * H1;
       i128 wpart = 0, c0 = 0, c1 = 0;
       for (int base = 0; base < H1; base += 32) {
@@ -345,6 +347,7 @@ __device__ __forceinline__ void plan_cta(const PlanArgs& a, uint8_t* smraw, cons
       if (lane == 0) s.Wv[i] = cur_only ? (i128)s.beta[0] * Li[0] : wpart;
     }
     sync(); PLAN_TS(3);
+    __syncwarp();
     if (warp == 0) {   // classification: lanes over instances, ballots build the ordered U list
       i128 wsum = 0;
       for (int i = lane; i < n; i += 32) wsum += s.Wv[i];

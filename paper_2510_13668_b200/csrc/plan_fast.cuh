@@ -1,11 +1,12 @@
 // plan_fast.cuh -- the single-CTA Alg. 1 with the request table in shared
 // memory.  Same arithmetic, filters and candidate order as plan_cta (plan_core.cuh: closed-form
 // score, readings A15-A21); what changes is how the work of a round is laid out:
-//   * staging: the loads (needed by Phase 1) are read synchronously; the request table (needed
-//     only once an instance is overloaded) streams in with cp.async behind Phase 1 and the
-//     classification, so a round that finds no overloaded instance barely waits for it
-//   * Phase 1 recomputes the prefix sums P0/P1, W_i and T_exec(i) only for the instances the
-//     previous move changed (all of them in round 0)
+//   * staging: static inputs are fetched before griddepcontrol.wait (overlapping the predictor
+//     tail), N_hat and the loads after it; the request table (needed only once an instance is
+//     overloaded) streams in with bulk copies behind Phase 1 and the classification
+//   * Phase 1 is split: the W pass (W_i, T_exec(i): one dot product per instance) feeds the
+//     classification; the P pass (prefix sums P0/P1, warp scans) runs only when some instance
+//     is overloaded; both touch only the instances the previous move changed (all in round 0)
 //   * Phases 2-3 first compact the requests of overloaded instances (warp ballots + one shared
 //     counter), so every lane scores a real candidate; the all-slots scan left most lanes of a
 //     warp idle while one lane evaluated a candidate (~4.6k cycles per warp iteration on B200)
@@ -39,7 +40,8 @@ struct FastSmem {
   int* seg_count;  // [world]
   int* ulist;      // [n]
   uint8_t* inO;    // [n]
-  uint8_t* dirty;  // [n]
+  uint8_t* wdirty; // [n] W_i / T_exec(i) stale
+  uint8_t* pdirty; // [n] P0_i / P1_i stale
   uint64_t* bar;   // request-table bulk copies
 };
 
@@ -51,8 +53,8 @@ inline size_t plan_fast_smem_layout(int n, int H, int world, int r_cap) {
   const size_t H1 = (size_t)H + 1, nn = (size_t)n, slots = (size_t)world * plan_fast_pitch(r_cap);
   size_t b = 16 * (2 * nn * H1 + 3 * H1 + 2 * nn) + 8 * (nn * H1 + nn) + 4 * H1;
   b += 4 * 5 * slots + 4 * ((slots + 31) / 32) + slots;
-  b += 4 * (size_t)world + 4 * nn + 2 * nn;
-  return b + 16 * 21;   // mbarrier + alignment slack (each of the 19 arrays starts on 16 bytes)
+  b += 4 * (size_t)world + 4 * nn + 3 * nn;
+  return b + 16 * 22;   // mbarrier + alignment slack (each of the 19 arrays starts on 16 bytes)
 }
 
 // Cand order extended by the slot index, so the winner does not depend on enumeration order.
@@ -154,7 +156,8 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     s.seg_count = carve<int>(p, a.world);
     s.ulist = carve<int>(p, n);
     s.inO = carve<uint8_t>(p, n);
-    s.dirty = carve<uint8_t>(p, n);
+    s.wdirty = carve<uint8_t>(p, n);
+    s.pdirty = carve<uint8_t>(p, n);
     s.bar = carve<uint64_t>(p, 1);
   }
   int& s_stop = shv[0];
@@ -163,11 +166,13 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
   int& s_ncand = shv[3];
 
   // ---- staging ----
-  // Request table: consumed only after Phase 1 + classification, so it streams in behind them:
-  // one thread issues a bulk copy (TMA, 16-byte granules) per segment and array when the segment
-  // arrays are 16-byte aligned (a.bulk, checked on the host), the sub-16-byte tails go through
-  // the loads below; otherwise 4-byte cp.async per element.
-  constexpr int kTabArrays = 5;
+  // Static inputs (request ids, instances, token counts, pins, counts, beta, capacities) are not
+  // written by this library's kernels, so they are fetched BEFORE griddepcontrol.wait, while the
+  // predictor tail is still running; N_hat and the loads L come from the predecessor and are
+  // fetched after it.  The request table is consumed only after the classification, so it
+  // streams in behind it: one thread issues a bulk copy (TMA, 16-byte granules) per segment and
+  // array when the segment arrays are 16-byte aligned (a.bulk, checked on the host), the
+  // sub-16-byte tails go through plain loads; otherwise 4-byte cp.async per element.
   auto tab_src = [&](int arr, int k) -> const uint8_t* {
     const void* base = arr == 0 ? (const void*)a.req_id : arr == 1 ? (const void*)a.inst
                      : arr == 2 ? (const void*)a.n_tok : arr == 3 ? (const void*)a.n_hat : (const void*)a.pinned;
@@ -177,17 +182,18 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     return arr == 0 ? (uint8_t*)s.rid : arr == 1 ? (uint8_t*)s.rinst : arr == 2 ? (uint8_t*)s.rntok
          : arr == 3 ? (uint8_t*)s.rnhat : (uint8_t*)s.rpin;
   };
-  const int n_arr = a.pinned ? kTabArrays : kTabArrays - 1;
-  const int tail_elems = a.bulk ? ((a.r_cap * 4) & 15) / 4 : 0;   // int32 elements past the last granule
-  const int tail_pin = a.bulk ? (a.r_cap & 15) : 0;
+  const int tail_elems = a.bulk ? (a.r_cap & 3) : 0;   // int32 elements past the last 16-byte granule
+  const int tail_pin = (a.bulk && a.pinned) ? (a.r_cap & 15) : 0;
+  const uint32_t fl32 = (uint32_t)(a.r_cap * 4) & ~15u, fl8 = (uint32_t)a.r_cap & ~15u;
+  const int issuer = nthreads - 1;   // the last thread: it rarely has a synchronous item below
   if (a.bulk) {
-    if (tid == nthreads - 1) {   // the last thread: it rarely has a synchronous item below
+    if (tid == issuer) {
       mbar_init(s.bar, 1);
       fence_barrier_init();
-      const uint32_t fl32 = (uint32_t)(a.r_cap * 4) & ~15u, fl8 = (uint32_t)a.r_cap & ~15u;
       mbar_arrive_expect_tx(s.bar, (uint32_t)a.world * (4 * fl32 + (a.pinned ? fl8 : 0)));
       for (int k = 0; k < a.world; ++k)
-        for (int arr = 0; arr < n_arr; ++arr) {
+        for (int arr = 0; arr < 5; ++arr) {
+          if (arr == 3 || (arr == 4 && !a.pinned)) continue;   // N_hat after the wait
           const uint32_t fl = arr < 4 ? fl32 : fl8;
           if (fl) bulk_g2s(tab_dst(arr) + (size_t)k * rp * (arr < 4 ? 4 : 1), tab_src(arr, k), fl, s.bar);
         }
@@ -199,26 +205,15 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
       cp_async4(s.rid + g, seg_ptr(a.req_id, k, a.seg_stride) + j);
       cp_async4(s.rinst + g, seg_ptr(a.inst, k, a.seg_stride) + j);
       cp_async4(s.rntok + g, seg_ptr(a.n_tok, k, a.seg_stride) + j);
-      cp_async4(s.rnhat + g, seg_ptr(a.n_hat, k, a.seg_stride) + j);
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  PLAN_TS(12);
-  // Synchronous part, one item per thread where it fits, so all loads are in flight together:
-  // loads L, beta, capacities, segment counts, bulk-copy tails, pinned flags (cp.async path).
+  // synchronous static items, one per thread where it fits (all loads in flight together)
   {
-    const int nL = n * H1, nTail = a.world * (4 * tail_elems + (a.pinned ? tail_pin : 0));
+    const int nTail = a.world * (3 * tail_elems + tail_pin);
     const int nPin = (!a.bulk && a.pinned) ? nslots : 0;
-    const int total = nL + H1 + n + a.world + nTail + nPin;
+    const int total = H1 + n + a.world + nTail + nPin;
     for (int e = tid; e < total; e += nthreads) {
       int r = e;
-      if (r < nL) {   // segment k holds instances [k*n_loc, (k+1)*n_loc)
-        const int i = r / H1, t = r - i * H1;
-        const int k = i / a.n_loc, il = i - k * a.n_loc;
-        s.Ls[r] = seg_ptr(a.L, k, a.seg_stride)[(int64_t)il * H1 + t];
-        continue;
-      }
-      r -= nL;
       if (r < H1) {
         s.beta[r] = a.beta_q[r];
         continue;
@@ -228,7 +223,8 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
         if (s.cmem)   // filter (b) capacity: strict needs L_u[0] + N_hat <= C_mem; otherwise
                       // L_u[0] + reserved + N + N_hat <= C_mem  (readings A17/A18)
           s.cmem[r] = a.c_mem[r] - (strict ? 0 : (a.reserved ? a.reserved[r] : 0));
-        s.dirty[r] = 1;
+        s.wdirty[r] = 1;
+        s.pdirty[r] = 1;
         continue;
       }
       r -= n;
@@ -246,15 +242,15 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
       }
       r -= a.world;
       if (r < nTail) {
-        const int per = 4 * tail_elems + (a.pinned ? tail_pin : 0);
+        const int per = 3 * tail_elems + tail_pin;
         const int k = r / per;
-        int q = r - k * per;
-        if (q < 4 * tail_elems) {
+        const int q = r - k * per;
+        if (q < 3 * tail_elems) {
           const int arr = q / tail_elems, j = (a.r_cap & ~3) + (q - arr * tail_elems);
           reinterpret_cast<int32_t*>(tab_dst(arr))[(size_t)k * rp + j] =
               reinterpret_cast<const int32_t*>(tab_src(arr, k))[j];
         } else {
-          const int j = (a.r_cap & ~15) + (q - 4 * tail_elems);
+          const int j = (a.r_cap & ~15) + (q - 3 * tail_elems);
           s.rpin[(size_t)k * rp + j] = tab_src(4, k)[j];
         }
         continue;
@@ -266,80 +262,60 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
       }
     }
   }
-  PLAN_TS(13);
   if (!a.pinned)
     for (int g = tid; g < nslots; g += nthreads) s.rpin[g] = 0;
   for (int w = tid; w < (nslots + 31) / 32; w += nthreads) s.moved[w] = 0u;
   if (tid == 0) s_nmoves = 0;
+  PLAN_TS(12);
+  pdl_wait();   // N_hat and L are written by the predecessor (predictor tail / projection / all-gather)
+  PLAN_TS(13);
+  if (a.bulk) {
+    if (tid == issuer)
+      for (int k = 0; k < a.world; ++k)
+        if (fl32) bulk_g2s(tab_dst(3) + (size_t)k * rp * 4, tab_src(3, k), fl32, s.bar);
+  } else {
+    for (int g = tid; g < nslots; g += nthreads) {
+      const int k = g / rp, j = g - k * rp;
+      if (j < a.r_cap) cp_async4(s.rnhat + g, seg_ptr(a.n_hat, k, a.seg_stride) + j);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  {
+    const int nL = n * H1, nTail = a.world * tail_elems;
+    for (int e = tid; e < nL + nTail; e += nthreads) {
+      if (e < nL) {   // segment k holds instances [k*n_loc, (k+1)*n_loc)
+        const int i = e / H1, t = e - i * H1;
+        const int k = i / a.n_loc, il = i - k * a.n_loc;
+        s.Ls[e] = seg_ptr(a.L, k, a.seg_stride)[(int64_t)il * H1 + t];
+      } else {
+        const int r = e - nL, k = r / tail_elems, j = (a.r_cap & ~3) + (r - k * tail_elems);
+        s.rnhat[(size_t)k * rp + j] = reinterpret_cast<const int32_t*>(tab_src(3, k))[j];
+      }
+    }
+  }
   PLAN_TS(15);
   __syncthreads();
   __syncwarp();
-  if (warp == nwarps - 1) {   // B0/B1/B2[T] = sum_{t<=T} beta_t {1, t, t^2}: warp scan (last warp)
-    i128 c0 = 0, c1 = 0, c2 = 0;
-    for (int base = 0; base < H1; base += 32) {
-      const int u = base + lane;
-      const i128 bt = u < H1 ? (i128)s.beta[u] : (i128)0;
-      i128 x0 = bt, x1 = bt * u, x2 = bt * u * u;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off), y2 = shfl_up_i128(x2, off);
-        if (lane >= off) {
-          x0 += y0;
-          x1 += y1;
-          x2 += y2;
-        }
-      }
-      x0 += c0;
-      x1 += c1;
-      x2 += c2;
-      if (u < H1) {
-        s.B[u] = x0;
-        s.B[H1 + u] = x1;
-        s.B[2 * H1 + u] = x2;
-      }
-      c0 = shfl_idx_i128(x0, 31);
-      c1 = shfl_idx_i128(x1, 31);
-      c2 = shfl_idx_i128(x2, 31);
-    }
-  }
   PLAN_TS(2);
-  const int p1_warps = nwarps - 1;   // Phase-1 warps (the last one builds B in round 0)
 
   for (int round = 0; round < a.max_moves; ++round) {
     // ---- Phase 1: InstanceClassification, changed instances only ----
-    // one warp per instance: W_i, T_exec(i) and the prefix sums P0_i / P1_i (warp scans)
-    for (int i = warp; i < n && warp < p1_warps; i += p1_warps) {
+    // W pass: one warp per instance, W_i = sum_{t>=1} beta_t L_i[t] and T_exec(i); the prefix
+    // sums P0/P1 that Phases 2-3 need are built below only when some instance is overloaded.
+    for (int i = warp; i < n; i += nwarps) {
       __syncwarp();
-      if (!s.dirty[i]) continue;
+      const bool d = s.wdirty[i] != 0;
+      __syncwarp();   // every lane has read the flag before lane 0 clears it
+      if (!d) continue;
       const int64_t* Li = s.Ls + (int64_t)i * H1;
-      i128 wpart = 0, c0 = 0, c1 = 0;
-      for (int base = 0; base < H1; base += 32) {
-        const int t = base + lane;
-        const i128 x = t < H1 ? (i128)s.beta[t] * Li[t] : (i128)0;
-        if (t >= 1) wpart += x;
-        i128 x0 = x, x1 = x * t;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off);
-          if (lane >= off) {
-            x0 += y0;
-            x1 += y1;
-          }
-        }
-        x0 += c0;
-        x1 += c1;
-        if (t < H1) {
-          s.P0[(int64_t)i * H1 + t] = x0;
-          s.P1[(int64_t)i * H1 + t] = x1;
-        }
-        c0 = shfl_idx_i128(x0, 31);
-        c1 = shfl_idx_i128(x1, 31);
-      }
+      i128 wpart = 0;
+      for (int t = 1 + lane; t < H1; t += 32) wpart += (i128)s.beta[t] * Li[t];
 #pragma unroll
       for (int m = 16; m >= 1; m >>= 1) wpart += shfl_xor_i128(wpart, m);
       if (lane == 0) {
         s.Wv[i] = cur_only ? (i128)s.beta[0] * Li[0] : wpart;
         s.texec[i] = (i128)a.a_ps + (i128)a.b_ps * Li[0];
+        s.wdirty[i] = 0;
       }
     }
     __syncthreads();
@@ -360,7 +336,6 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
           o = (i128)n * a.theta_den * s.Wv[i] > rhs;
           u = !o && ((i128)n * a.theta_den * (i128)65536 * s.Ls[(int64_t)i * H1] < rhs);
           s.inO[i] = o ? 1 : 0;
-          s.dirty[i] = 0;   // Phase 1 of this round is done (all warps passed the barrier)
         }
         anyO |= __any_sync(0xFFFFFFFFu, o) != 0;
         const uint32_t um = __ballot_sync(0xFFFFFFFFu, u);
@@ -373,14 +348,80 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
         s_ncand = 0;
       }
     }
-    if (round == 0) {   // the request table has landed (the barrier publishes everyone's cp.async)
-      if (a.bulk) mbar_wait(s.bar, 0);
-      else cp_async_wait_all();
-    }
     __syncthreads();
     PLAN_TS(4);
     if (s_stop) break;
+    if (round == 0) {   // the request table must have landed (a stopping plan never waits here)
+      if (a.bulk) {
+        mbar_wait(s.bar, 0);   // the transaction barrier publishes the bulk copies to its waiters
+      } else {
+        cp_async_wait_all();
+        __syncthreads();       // publishes every thread's cp.async
+      }
+    }
 
+    // ---- P pass: P0_i[T] = sum_{t<=T} beta_t L_i[t], P1_i[T] = sum_{t<=T} t beta_t L_i[t] (warp
+    // scans) for the instances whose loads changed; the same warps then join the compaction.
+    // Round 0 also builds B0/B1/B2 here (needed only by the scoring). ----
+    __syncwarp();
+    if (round == 0 && warp == nwarps - 1) {   // B0/B1/B2[T] = sum_{t<=T} beta_t {1, t, t^2}: warp scan (last warp)
+      i128 c0 = 0, c1 = 0, c2 = 0;
+      for (int base = 0; base < H1; base += 32) {
+        const int u = base + lane;
+        const i128 bt = u < H1 ? (i128)s.beta[u] : (i128)0;
+        i128 x0 = bt, x1 = bt * u, x2 = bt * u * u;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off), y2 = shfl_up_i128(x2, off);
+          if (lane >= off) {
+            x0 += y0;
+            x1 += y1;
+            x2 += y2;
+          }
+        }
+        x0 += c0;
+        x1 += c1;
+        x2 += c2;
+        if (u < H1) {
+          s.B[u] = x0;
+          s.B[H1 + u] = x1;
+          s.B[2 * H1 + u] = x2;
+        }
+        c0 = shfl_idx_i128(x0, 31);
+        c1 = shfl_idx_i128(x1, 31);
+        c2 = shfl_idx_i128(x2, 31);
+      }
+    }
+    for (int i = warp; i < n; i += nwarps) {
+      __syncwarp();
+      const bool d = s.pdirty[i] != 0;
+      __syncwarp();
+      if (!d) continue;
+      const int64_t* Li = s.Ls + (int64_t)i * H1;
+      i128 c0 = 0, c1 = 0;
+      for (int base = 0; base < H1; base += 32) {
+        const int t = base + lane;
+        const i128 x = t < H1 ? (i128)s.beta[t] * Li[t] : (i128)0;
+        i128 x0 = x, x1 = x * t;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off);
+          if (lane >= off) {
+            x0 += y0;
+            x1 += y1;
+          }
+        }
+        x0 += c0;
+        x1 += c1;
+        if (t < H1) {
+          s.P0[(int64_t)i * H1 + t] = x0;
+          s.P1[(int64_t)i * H1 + t] = x1;
+        }
+        c0 = shfl_idx_i128(x0, 31);
+        c1 = shfl_idx_i128(x1, 31);
+      }
+      if (lane == 0) s.pdirty[i] = 0;
+    }
     // ---- candidate compaction: requests on overloaded instances, not pinned, not yet moved ----
     // (round 0 also validates each slot once and marks the slots that can never be candidates)
     // four consecutive slots per lane (one 16-byte shared load), one atomic per warp
@@ -497,8 +538,8 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
         }
         if (lane == 0) {
           s.moved[c.g >> 5] |= 1u << (c.g & 31);
-          s.dirty[src] = 1;
-          s.dirty[c.dst] = 1;
+          s.wdirty[src] = s.wdirty[c.dst] = 1;
+          s.pdirty[src] = s.pdirty[c.dst] = 1;
           const i128 gain = (i128)2 * n * c.score;
           star_move mv;
           mv.req_id = c.id;

@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
     }
     seg_count[k] = c;
   }
+  __syncwarp();   // reconverge first: shuffles of a diverged warp take a slow path
   if (warp == nwarps - 1) {   // B0/B1/B2 prefix (warp scan)
     i128 c0 = 0, c1 = 0, c2 = 0;
     for (int base = 0; base < H1; base += 32) {
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
       c2 = shfl_idx_i128(x2, 31);
     }
   }
+  __syncwarp();
   if (warp == 0) {   // Phase 1 from the global W
     i128 wsum = 0;
     for (int i = lane; i < n; i += 32) wsum += w.Wv[i];
@@ -233,6 +235,7 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
   best = warp_argmax(best);
   if (lane == 0) warp_best[warp] = best;
   __syncthreads();
+  __syncwarp();
   if (warp == 0) {
     Cand c;
     if (lane < nwarps) {

@@ -56,6 +56,7 @@ template <bool kShared = false>
 __device__ __forceinline__ void proj_accumulate(const ProjArgs& a, bool valid, int32_t inst, int32_t ntok,
                                                 int32_t nhat, uint32_t* scnt, unsigned long long* ssum,
                                                 uint32_t& errbits) {
+  __syncwarp();   // reconverge first: collectives of a diverged warp take a slow path
   const int i = inst - a.inst_base;
   bool ok = valid;
   if (valid) {
@@ -85,6 +86,7 @@ template <bool kShared>
 __device__ __forceinline__ void proj_accumulate4(const ProjArgs& a, bool valid, const int4& x, const int4& n,
                                                  const int4& h, uint32_t* scnt, unsigned long long* ssum,
                                                  uint32_t& errbits) {
+  __syncwarp();
   const int ins[4] = {x.x - a.inst_base, x.y - a.inst_base, x.z - a.inst_base, x.w - a.inst_base};
   const int nt[4] = {n.x, n.y, n.z, n.w};
   const int nh[4] = {h.x, h.y, h.z, h.w};
@@ -147,6 +149,7 @@ __device__ __forceinline__ void proj_finalize(const ProjArgs& a, const uint32_t*
   const int HB = a.H + 2;
   const int lane = threadIdx.x & 31;
   for (int i = warp; i < a.n_inst; i += nwarps) {
+    __syncwarp();
     const uint32_t* c = cnt + (int64_t)i * HB;
     const unsigned long long* s = sum + (int64_t)i * HB;
     int64_t* Li = a.L + (int64_t)i * (a.H + 1);

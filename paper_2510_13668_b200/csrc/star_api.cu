@@ -450,26 +450,30 @@ star_status star_predictor_layer1_timing(star_predictor* p, int enable) {
 
 star_status star_predictor_timeline(star_predictor* p, int enable, uint64_t* host_out, int max_ctas, int* n_ctas) {
   if (!p) return fail(STAR_EINVAL, "predictor is NULL");
-  if (enable && !p->tl) {
-    const size_t bytes = (size_t)g_num_sms * 4 * 16 * sizeof(uint64_t);
-    STAR_CUDA(cudaMalloc(&p->tl, bytes));
-    STAR_CUDA(cudaMemset(p->tl, 0, bytes));
-  } else if (!enable && p->tl) {
+  const size_t rows = (size_t)g_num_sms * 4;
+  if (enable) {
+    if (!p->tl) {
+      STAR_CUDA(cudaMalloc(&p->tl, rows * kTailTlStride * sizeof(uint64_t)));
+      STAR_CUDA(cudaMemset(p->tl, 0, rows * kTailTlStride * sizeof(uint64_t)));
+    }
+    if (enable == 2 && !p->tl_l1) {
+      STAR_CUDA(cudaMalloc(&p->tl_l1, rows * 16 * sizeof(uint64_t)));
+      STAR_CUDA(cudaMemset(p->tl_l1, 0, rows * 16 * sizeof(uint64_t)));
+    }
+  } else {
     cudaFree(p->tl);
-  cudaFree(p->tl_l1);
-  cudaFree(p->r_idx);
-  cudaFree(p->r_pos);
-  cudaFree(p->r_ntok);
-  cudaFree(p->r_nhat);
-  cudaFree(p->r_M);
-  cudaFree(p->r_h);
-  cudaFree(p->r_ws);
+    cudaFree(p->tl_l1);
     p->tl = nullptr;
+    p->tl_l1 = nullptr;
   }
-  if (host_out && p->tl) {
+  if (host_out) {
     STAR_CUDA(cudaDeviceSynchronize());
-    const int n = p->tl_ctas < max_ctas ? p->tl_ctas : max_ctas;
-    STAR_CUDA(cudaMemcpy(host_out, p->tl, (size_t)n * 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    const bool l1 = enable == 2;
+    const uint64_t* src = l1 ? p->tl_l1 : p->tl;
+    const int have = l1 ? p->tl_l1_ctas : p->tl_ctas;
+    const int n = src ? (have < max_ctas ? have : max_ctas) : 0;
+    const size_t stride = l1 ? 16 : kTailTlStride;
+    if (n > 0) STAR_CUDA(cudaMemcpy(host_out, src, (size_t)n * stride * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     if (n_ctas) *n_ctas = n;
   }
   return STAR_OK;
@@ -834,10 +838,10 @@ star_status plan_reschedule_segmented(const star_plan_params* p, const star_plan
   return STAR_OK;
 }
 
-star_status star_plan_timeline(uint64_t* host16) {
-  if (!host16) return fail(STAR_EINVAL, "host16 is NULL");
+star_status star_plan_timeline(uint64_t* host64) {
+  if (!host64) return fail(STAR_EINVAL, "host64 is NULL");
   STAR_CUDA(cudaDeviceSynchronize());
-  STAR_CUDA(plan_timeline(host16));
+  STAR_CUDA(plan_timeline(host64));
   return STAR_OK;
 }
 

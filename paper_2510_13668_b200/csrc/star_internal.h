@@ -28,7 +28,7 @@ size_t plan_smem_bytes(int n, int H, int world, int r_cap);
 cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg, star_move* moves, int32_t* n_moves,
                         int32_t* err_flag, cudaStream_t stream);
 
-cudaError_t plan_timeline(uint64_t* host16);
+cudaError_t plan_timeline(uint64_t* host64);
 
 // plan_large.cu (multi-CTA plan over a global workspace)
 struct PlanArgs;

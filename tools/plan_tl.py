@@ -26,7 +26,7 @@ for _ in range(5):
     st.run(hd)
 torch.cuda.synchronize()
 tl = _lib.plan_timeline().astype(np.int64)
-names = ["entry", "pdl_wait", "staged", "prefix", "classify", "argmax", "apply", "end"]
+names = ["entry", "launch", "staged", "W pass", "classify", "argmax", "apply", "end"]
 print(cfg, "moves", st.result())
 for k in range(1, 8):
     print(f"{names[k]:9s} +{(tl[k] - tl[k-1]) / 1e3:6.2f} us   (t={(tl[k] - tl[0]) / 1e3:6.2f})")
@@ -41,8 +41,8 @@ print("clock64 deltas (us at 1.965 GHz):", [(names[k], round((cl[k] - cl[k-1]) /
 
 print("blk argmax detail (us): read", round((cl[9] - cl[5]) / 1965.0, 2), "reps", [round((cl[10 + r] - cl[9 + r]) / 1965.0, 3) for r in range(3)])
 
-print("staging detail (us): table issue", round((cl[12] - cl[1]) / 1965.0, 2), "sync loads", round((cl[13] - cl[12]) / 1965.0, 2),
-      "rest", round((cl[15] - cl[13]) / 1965.0, 2), "barrier+B", round((cl[2] - cl[15]) / 1965.0, 2))
+print("staging detail (us): static (pre-wait)", round((cl[12] - cl[1]) / 1965.0, 2), "pdl wait", round((cl[13] - cl[12]) / 1965.0, 2),
+      "post-wait loads", round((cl[15] - cl[13]) / 1965.0, 2), "barrier+B", round((cl[2] - cl[15]) / 1965.0, 2))
 
 print("round detail (us): compaction", round((cl[9] - cl[4]) / 1965.0, 2), "eval(t0)", round((cl[10] - cl[9]) / 1965.0, 2),
       "warp argmax", round((cl[11] - cl[10]) / 1965.0, 2), "to barrier", round((cl[5] - cl[11]) / 1965.0, 2))

@@ -18,7 +18,7 @@ snap = datagen.make_snapshot(0, 8, R // 8)
 nt, ins = torch.from_numpy(snap.n_tok).cuda(), torch.from_numpy(snap.inst).cuda()
 beta = torch.from_numpy(datagen.beta_schedule_q16(50).astype(np.int32)).cuda()
 ws = torch.zeros(star.project_workspace_bytes(8, 50), dtype=torch.uint8, device="cuda")
-pred.timeline(True)
+pred.timeline(True, layer1=True)
 for _ in range(5):
     star.lenpred_forward_project(pred, h, nt, ins, 8, 50, beta, ws)
 torch.cuda.synchronize()
@@ -33,6 +33,12 @@ for k, nm in enumerate(names):
     if len(v):
         print(f"{k:2d} {nm:14s} min {v.min()/1e3:7.2f}  med {np.median(v)/1e3:7.2f}  max {v.max()/1e3:7.2f} us")
 
+last = tl[tl[:, 16] > 0]
+if len(last):
+    r = last[0]
+    print("last finisher (us after its arrival): staged", round((r[17] - r[16]) / 1e3, 2), "finalized",
+          round((r[18] - r[16]) / 1e3, 2), "zeroed", round((r[19] - r[16]) / 1e3, 2), "end", round((r[14] - r[16]) / 1e3, 2),
+          "| arrival at", round((r[16] - t0) / 1e3, 2))
 tl1 = pred.timeline(fetch=True, layer1=True).astype(np.int64)
 names1 = ["entry", "prologue", "prod pdl_wait", "mma kb0", "mma kb16", "mma kb32", "mma kb48", "", "", "mma done",
           "accum ready", "epilogue end", "exit sync"]
