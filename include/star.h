@@ -256,6 +256,21 @@ star_status plan_reschedule_segmented(const star_plan_params* p, const star_plan
                                       star_move* moves, int32_t* n_moves, int32_t* err_flag,
                                       star_stream_t stream);
 
+/* One-rank step (world == 1): lenpred_forward_project (inst_base 0) followed by
+ * plan_reschedule_segmented on this rank's own state; outputs identical to the two calls in
+ * sequence.  The segments (world 1, n_loc == n_inst) normally alias the projection output L and
+ * n_hat.  When the fused tail runs and the plan state fits in its freed stage ring, Alg. 1 is
+ * executed by the projection's last finishing CTA (one launch fewer, no kernel boundary between
+ * the projection and the plan); otherwise the plan kernel follows.  Argument meaning and errors:
+ * lenpred_forward_project and plan_reschedule_segmented. */
+star_status lenpred_forward_project_plan(star_predictor* p, const void* h, int64_t ld_h, int R,
+                                         const int32_t* n_tok, int32_t max_ctx_len, float* y_hat, int32_t* n_hat,
+                                         int n_inst, int H, const int32_t* inst, const uint32_t* beta_q, int64_t* L,
+                                         int64_t* W, int64_t* peak, int64_t* growth, int32_t* count, void* workspace,
+                                         const star_plan_params* pp, const star_plan_segments* sg,
+                                         star_move* moves, int32_t* n_moves, int32_t* err_flag,
+                                         star_stream_t stream);
+
 /* Diagnostics: %globaltimer stamps (ns) of the most recent single-CTA plan launch: [0] entry,
  * [1] launched, [12] static inputs staged, [13] after griddepcontrol.wait, [2] inputs staged,
  * [3] W pass, [4] classification, [9] candidates compacted, [5] candidate argmax, [6] move

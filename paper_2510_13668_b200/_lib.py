@@ -69,6 +69,8 @@ def lib() -> C.CDLL:
         "project_instance_load": ([I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P], I),
         "plan_reschedule": ([C.POINTER(PlanParamsC), P, I, P, P, P, P, P, P, P, P, P], I),
         "plan_reschedule_segmented": ([C.POINTER(PlanParamsC), C.POINTER(PlanSegmentsC), P, P, P, P], I),
+        "lenpred_forward_project_plan": ([P, P, I64, I, P, I32, P, P, I, I, P, P, P, P, P, P, P, P,
+                                          C.POINTER(PlanParamsC), C.POINTER(PlanSegmentsC), P, P, P, P], I),
         "star_dispatch_workspace_bytes": ([I, I], C.c_size_t),
         "star_plan_workspace_bytes": ([I, I, I64], C.c_size_t),
         "star_plan_timeline": ([P], I),
@@ -158,7 +160,7 @@ class Predictor:
         """Library-owned CUDA events around every layer-1 GEMM launch (see star.h)."""
         _check(lib().star_predictor_layer1_timing(self.handle, int(enable)), "layer1_timing")
 
-    def timeline(self, enable: bool = True, fetch: bool = False, layer1: bool = False):
+    def timeline(self, enable: bool = True, fetch: bool = False, layer1: bool = False, raw: bool = False):
         """Diagnostics: per-CTA phase stamps of the fused tail / layer-1 GEMM (star_predictor_timeline)."""
         if not fetch:
             _check(lib().star_predictor_timeline(self.handle, (2 if layer1 else 1) if enable else 0, None, 0, None),
@@ -168,7 +170,7 @@ class Predictor:
         n = I()
         _check(lib().star_predictor_timeline(self.handle, 2 if layer1 else 1, buf.ctypes.data_as(P), buf.shape[0],
                                              C.byref(n)), "timeline")
-        return buf[: n.value]
+        return buf if raw else buf[: n.value]
 
     def layer1_ms(self) -> float:
         ms = C.c_float()
@@ -226,6 +228,30 @@ def lenpred_forward_project(pred: Predictor, h: torch.Tensor, n_tok: torch.Tenso
                                          _ptr(out.count), _ptr(workspace), _ptr(err_flag), _stream(stream)),
            "lenpred_forward_project")
     return y_hat, n_hat, out
+
+
+def lenpred_forward_project_plan(pred: Predictor, h: torch.Tensor, n_tok: torch.Tensor, inst: torch.Tensor,
+                                 n_inst: int, H: int, beta_q: torch.Tensor, workspace: torch.Tensor,
+                                 params: "PlanParams", seg: "PlanSegmentsC", moves: torch.Tensor,
+                                 n_moves: torch.Tensor, n_hat: torch.Tensor, out: "ProjectOut",
+                                 max_ctx_len: int = L_CTX, y_hat: Optional[torch.Tensor] = None,
+                                 err_flag: Optional[torch.Tensor] = None, stream=None):
+    """One-rank step: forward + projection + Alg. 1 (star.h lenpred_forward_project_plan)."""
+    R = h.shape[0]
+    if h.dim() != 2 or h.stride(1) != 1:
+        raise StarError("h must be 2-D with unit column stride")
+    exp = torch.bfloat16 if pred.dt == STAR_BF16 else torch.float32
+    if h.dtype != exp or not h.is_cuda:
+        raise StarError(f"h must be a CUDA {exp} tensor")
+    for n_, t in (("n_tok", n_tok), ("inst", inst), ("beta_q", beta_q), ("n_hat", n_hat)):
+        _req(t, torch.int32, n_)
+    _check(lib().lenpred_forward_project_plan(pred.handle, _ptr(h), h.stride(0), R, _ptr(n_tok), max_ctx_len,
+                                              _ptr(y_hat), _ptr(n_hat), n_inst, H, _ptr(inst), _ptr(beta_q),
+                                              _ptr(out.L), _ptr(out.W), _ptr(out.peak), _ptr(out.growth),
+                                              _ptr(out.count), _ptr(workspace), C.byref(params.c), C.byref(seg),
+                                              _ptr(moves), _ptr(n_moves), _ptr(err_flag), _stream(stream)),
+           "lenpred_forward_project_plan")
+    return moves, n_moves
 
 
 def lenpred_forward_refresh(pred: Predictor, h: torch.Tensor, n_tok: torch.Tensor, gen: torch.Tensor,

@@ -29,6 +29,7 @@
 #pragma once
 #include "lenpred_kernels.cuh"
 #include "project_core.cuh"
+#include "plan_fast.cuh"
 
 namespace star {
 
@@ -54,11 +55,15 @@ struct TailArgs {
   ProjArgs pa;         // R / inst / n_tok / beta_q / outputs / workspace (ws_cnt, ws_sum, ws_arrive)
   uint64_t* tl;        // diagnostics: [ctas][16] %globaltimer phase stamps, or nullptr
   const int32_t* M_dev;  // device-side row count (refresh mode), or nullptr (then M)
+  int plan;            // the projection's last finisher then runs Alg. 1 (one rank: pl reads this
+                       // rank's own record), with the whole CTA, in the freed stage ring
+  PlanArgs pl;
 };
 
 // Phase timestamp (diagnostics only; one designated thread per phase).  Row stride
 // kTailTlStride: slots 0-14 phases, 15 the SM id, 16-19 the last finisher's projection finalize.
 constexpr int kTailTlStride = 32;
+constexpr int kTailPlanTlRow = 4 * 148 - 2;   // rows 590-591 of the [4 * SMs][32] buffer: fused-plan stamps
 #define TAIL_TS(k)                                                                                        \
   do {                                                                                                    \
     if (p.tl) p.tl[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * kTailTlStride + (k)] = globaltimer_ns(); \
@@ -145,6 +150,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     mbar_init(accum, 1);
     mbar_init(w3bar, 1);
+    *s_last = 0;
     mbar_init(a3bar, 4);   // one arrive per epilogue warp
     mbar_init(l3bar, 1);
     mbar_init(pbar, 1);
@@ -533,6 +539,16 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
+  }
+  if (p.plan && *s_last) {   // CTA-uniform: s_last was published by the barrier above
+    // the stage ring is free (every TMA load and MMA of this CTA has completed); the plan's
+    // shared state fits below OFF_W3 - 256 (checked on the host), warp_best / shv above it
+    Cand* wb = reinterpret_cast<Cand*>(smem + S::OFF_W3 - 256);
+    int* shv = reinterpret_cast<int*>(wb + 6);
+    // diagnostics: the plan's stamps go to the two last timeline rows (never a CTA's)
+    uint64_t* ptl = p.tl ? p.tl + (size_t)(gridDim.x * gridDim.y * gridDim.z > 0 ? kTailPlanTlRow : 0) * kTailTlStride
+                         : nullptr;
+    plan_cta_fast<true>(p.pl, smem, (int)threadIdx.x, (int)blockDim.x, wb, shv, ptl);
   }
 }
 

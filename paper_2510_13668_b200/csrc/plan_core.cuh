@@ -32,6 +32,7 @@ struct PlanArgs {
   int32_t* n_moves;
   int32_t* err;
   int bulk;                 // every segment array 16-byte aligned: the table may be bulk-copied
+  const int64_t* W0;        // nullable: W_i of the input L (round 0), e.g. the projection's own
 };
 
 template <typename T>

@@ -118,6 +118,9 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Whole plan by one CTA of `nthreads` threads (multiple of 32).  tl: optional %globaltimer stamps.
+// kFused: called by the predictor tail's last CTA after the projection (no griddepcontrol.wait
+// period to hide the static staging in; the loads are issued together with it instead).
+template <bool kFused = false>
 __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw, const int tid, const int nthreads,
                                               Cand* warp_best, int* shv, uint64_t* tl) {
 #define PLAN_TS(k)                                           \
@@ -186,18 +189,26 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
   const int tail_pin = (a.bulk && a.pinned) ? (a.r_cap & 15) : 0;
   const uint32_t fl32 = (uint32_t)(a.r_cap * 4) & ~15u, fl8 = (uint32_t)a.r_cap & ~15u;
   const int issuer = nthreads - 1;   // the last thread: it rarely has a synchronous item below
-  if (a.bulk) {
-    if (tid == issuer) {
+  // bulk copies of the table arrays (all but N_hat, or only N_hat), by the issuer thread
+  auto issue_table = [&](bool init, bool static_part, bool nhat_part) {
+    if (init) {
       mbar_init(s.bar, 1);
       fence_barrier_init();
       mbar_arrive_expect_tx(s.bar, (uint32_t)a.world * (4 * fl32 + (a.pinned ? fl8 : 0)));
-      for (int k = 0; k < a.world; ++k)
-        for (int arr = 0; arr < 5; ++arr) {
-          if (arr == 3 || (arr == 4 && !a.pinned)) continue;   // N_hat after the wait
-          const uint32_t fl = arr < 4 ? fl32 : fl8;
-          if (fl) bulk_g2s(tab_dst(arr) + (size_t)k * rp * (arr < 4 ? 4 : 1), tab_src(arr, k), fl, s.bar);
-        }
     }
+    if (nhat_part) fence_proxy_async_global();   // N_hat written through the generic proxy
+    for (int k = 0; k < a.world; ++k)
+      for (int arr = 0; arr < 5; ++arr) {
+        if (arr == 4 && !a.pinned) continue;
+        if (arr == 3 ? !nhat_part : !static_part) continue;
+        const uint32_t fl = arr < 4 ? fl32 : fl8;
+        if (fl) bulk_g2s(tab_dst(arr) + (size_t)k * rp * (arr < 4 ? 4 : 1), tab_src(arr, k), fl, s.bar);
+      }
+  };
+  // the fused form issues the whole table only once some instance is overloaded (below)
+  bool table_issued = !(kFused && a.bulk);
+  if (a.bulk) {
+    if (!kFused && tid == issuer) issue_table(true, true, false);
   } else {
     for (int g = tid; g < nslots; g += nthreads) {
       const int k = g / rp, j = g - k * rp;
@@ -207,12 +218,44 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
       cp_async4(s.rntok + g, seg_ptr(a.n_tok, k, a.seg_stride) + j);
     }
   }
-  // synchronous static items, one per thread where it fits (all loads in flight together)
+  // loads L and the N_hat tails, four per thread per batch, all in flight before any store
+  auto load_dynamic = [&]() {
+    const int nL = n * H1, total = nL + a.world * tail_elems;
+    for (int base = 0; base < total; base += 4 * nthreads) {
+      int64_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = base + 4 * tid + u;
+        v[u] = 0;
+        if (e < nL) {   // segment k holds instances [k*n_loc, (k+1)*n_loc)
+          const int i = e / H1, t = e - i * H1;
+          const int k = i / a.n_loc, il = i - k * a.n_loc;
+          v[u] = seg_ptr(a.L, k, a.seg_stride)[(int64_t)il * H1 + t];
+        } else if (e < total) {
+          const int r = e - nL, k = r / tail_elems, j = (a.r_cap & ~3) + (r - k * tail_elems);
+          v[u] = reinterpret_cast<const int32_t*>(tab_src(3, k))[j];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = base + 4 * tid + u;
+        if (e < nL) {
+          s.Ls[e] = v[u];
+        } else if (e < total) {
+          const int r = e - nL, k = r / tail_elems, j = (a.r_cap & ~3) + (r - k * tail_elems);
+          s.rnhat[(size_t)k * rp + j] = (int32_t)v[u];
+        }
+      }
+    }
+  };
+  if constexpr (kFused) load_dynamic();   // no wait period: the L loads on the low threads
+  // synchronous static items, one per thread where it fits (all loads in flight together), on
+  // the high threads (the fused form's L loads occupy the low ones)
   {
     const int nTail = a.world * (3 * tail_elems + tail_pin);
     const int nPin = (!a.bulk && a.pinned) ? nslots : 0;
     const int total = H1 + n + a.world + nTail + nPin;
-    for (int e = tid; e < total; e += nthreads) {
+    for (int e = nthreads - 1 - tid; e < total; e += nthreads) {
       int r = e;
       if (r < H1) {
         s.beta[r] = a.beta_q[r];
@@ -223,7 +266,12 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
         if (s.cmem)   // filter (b) capacity: strict needs L_u[0] + N_hat <= C_mem; otherwise
                       // L_u[0] + reserved + N + N_hat <= C_mem  (readings A17/A18)
           s.cmem[r] = a.c_mem[r] - (strict ? 0 : (a.reserved ? a.reserved[r] : 0));
-        s.wdirty[r] = 1;
+        if (a.W0 && !cur_only) {   // round-0 W_i given (the projection's own, exact in int64)
+          s.Wv[r] = (i128)a.W0[r];
+          s.wdirty[r] = 2;
+        } else {
+          s.wdirty[r] = 1;
+        }
         s.pdirty[r] = 1;
         continue;
       }
@@ -270,9 +318,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
   pdl_wait();   // N_hat and L are written by the predecessor (predictor tail / projection / all-gather)
   PLAN_TS(13);
   if (a.bulk) {
-    if (tid == issuer)
-      for (int k = 0; k < a.world; ++k)
-        if (fl32) bulk_g2s(tab_dst(3) + (size_t)k * rp * 4, tab_src(3, k), fl32, s.bar);
+    if (!kFused && tid == issuer) issue_table(false, false, true);
   } else {
     for (int g = tid; g < nslots; g += nthreads) {
       const int k = g / rp, j = g - k * rp;
@@ -280,19 +326,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  {
-    const int nL = n * H1, nTail = a.world * tail_elems;
-    for (int e = tid; e < nL + nTail; e += nthreads) {
-      if (e < nL) {   // segment k holds instances [k*n_loc, (k+1)*n_loc)
-        const int i = e / H1, t = e - i * H1;
-        const int k = i / a.n_loc, il = i - k * a.n_loc;
-        s.Ls[e] = seg_ptr(a.L, k, a.seg_stride)[(int64_t)il * H1 + t];
-      } else {
-        const int r = e - nL, k = r / tail_elems, j = (a.r_cap & ~3) + (r - k * tail_elems);
-        s.rnhat[(size_t)k * rp + j] = reinterpret_cast<const int32_t*>(tab_src(3, k))[j];
-      }
-    }
-  }
+  if constexpr (!kFused) load_dynamic();
   PLAN_TS(15);
   __syncthreads();
   __syncwarp();
@@ -304,12 +338,19 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     // sums P0/P1 that Phases 2-3 need are built below only when some instance is overloaded.
     for (int i = warp; i < n; i += nwarps) {
       __syncwarp();
-      const bool d = s.wdirty[i] != 0;
+      const int d = s.wdirty[i];
       __syncwarp();   // every lane has read the flag before lane 0 clears it
       if (!d) continue;
       const int64_t* Li = s.Ls + (int64_t)i * H1;
+      if (d == 2) {   // W_i given: T_exec(i) only
+        if (lane == 0) {
+          s.texec[i] = (i128)a.a_ps + (i128)a.b_ps * Li[0];
+          s.wdirty[i] = 0;
+        }
+        continue;
+      }
       i128 wpart = 0;
-      for (int t = 1 + lane; t < H1; t += 32) wpart += (i128)s.beta[t] * Li[t];
+      for (int t = 1 + lane; t < H1; t += 32) wpart += mul_u32((i128)Li[t], s.beta[t]);
 #pragma unroll
       for (int m = 16; m >= 1; m >>= 1) wpart += shfl_xor_i128(wpart, m);
       if (lane == 0) {
@@ -326,15 +367,15 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
       for (int i = lane; i < n; i += 32) wsum += s.Wv[i];
 #pragma unroll
       for (int m = 16; m >= 1; m >>= 1) wsum += shfl_xor_i128(wsum, m);
-      const i128 rhs = (i128)(a.theta_den + a.theta_num) * wsum;
+      const i128 rhs = mul_u32(wsum, (uint32_t)a.theta_den + (uint32_t)a.theta_num);   // den >= 1, num >= 0
       bool anyO = false;
       int nU = 0;
       for (int base = 0; base < n; base += 32) {
         const int i = base + lane;
         bool o = false, u = false;
         if (i < n) {
-          o = (i128)n * a.theta_den * s.Wv[i] > rhs;
-          u = !o && ((i128)n * a.theta_den * (i128)65536 * s.Ls[(int64_t)i * H1] < rhs);
+          o = mul_u32(mul_u32(s.Wv[i], (uint32_t)n), (uint32_t)a.theta_den) > rhs;
+          u = !o && (mul_u32(mul_u32((i128)s.Ls[(int64_t)i * H1], (uint32_t)n), (uint32_t)a.theta_den) << 16) < rhs;
           s.inO[i] = o ? 1 : 0;
         }
         anyO |= __any_sync(0xFFFFFFFFu, o) != 0;
@@ -353,6 +394,10 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     if (s_stop) break;
     if (round == 0) {   // the request table must have landed (a stopping plan never waits here)
       if (a.bulk) {
+        if (!table_issued) {   // fused form: issue it now (CTA-uniform branch)
+          if (tid == issuer) issue_table(true, true, true);
+          table_issued = true;
+        }
         mbar_wait(s.bar, 0);   // the transaction barrier publishes the bulk copies to its waiters
       } else {
         cp_async_wait_all();
@@ -369,7 +414,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
       for (int base = 0; base < H1; base += 32) {
         const int u = base + lane;
         const i128 bt = u < H1 ? (i128)s.beta[u] : (i128)0;
-        i128 x0 = bt, x1 = bt * u, x2 = bt * u * u;
+        i128 x0 = bt, x1 = mul_u32(bt, (uint32_t)u), x2 = mul_u32(x1, (uint32_t)u);
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
           const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off), y2 = shfl_up_i128(x2, off);
@@ -401,8 +446,8 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
       i128 c0 = 0, c1 = 0;
       for (int base = 0; base < H1; base += 32) {
         const int t = base + lane;
-        const i128 x = t < H1 ? (i128)s.beta[t] * Li[t] : (i128)0;
-        i128 x0 = x, x1 = x * t;
+        const i128 x = t < H1 ? mul_u32((i128)Li[t], s.beta[t]) : (i128)0;
+        i128 x0 = x, x1 = mul_u32(x, (uint32_t)t);
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
           const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off);
@@ -558,8 +603,11 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     if (s_stop) break;
   }
   // no copy may still be in flight when the CTA exits (a plan that stopped before round 0's wait)
-  if (a.bulk) mbar_wait(s.bar, 0);
-  else cp_async_wait_all();
+  if (a.bulk) {
+    if (table_issued) mbar_wait(s.bar, 0);
+  } else {
+    cp_async_wait_all();
+  }
   PLAN_TS(7);
   if (tid == 0) *a.n_moves = s_nmoves;
 #undef PLAN_TS

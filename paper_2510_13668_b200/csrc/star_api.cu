@@ -450,7 +450,8 @@ star_status star_predictor_layer1_timing(star_predictor* p, int enable) {
 
 star_status star_predictor_timeline(star_predictor* p, int enable, uint64_t* host_out, int max_ctas, int* n_ctas) {
   if (!p) return fail(STAR_EINVAL, "predictor is NULL");
-  const size_t rows = (size_t)g_num_sms * 4;
+  const size_t rows = (size_t)g_num_sms * 4 > (size_t)kTailPlanTlRow + 2 ? (size_t)g_num_sms * 4
+                                                                        : (size_t)kTailPlanTlRow + 2;
   if (enable) {
     if (!p->tl) {
       STAR_CUDA(cudaMalloc(&p->tl, rows * kTailTlStride * sizeof(uint64_t)));
@@ -471,9 +472,13 @@ star_status star_predictor_timeline(star_predictor* p, int enable, uint64_t* hos
     const bool l1 = enable == 2;
     const uint64_t* src = l1 ? p->tl_l1 : p->tl;
     const int have = l1 ? p->tl_l1_ctas : p->tl_ctas;
+    // copies min(max_ctas, allocated rows) rows (rows past the grid hold auxiliary stamps:
+    // the fused plan's, see TailArgs::tl); *n_ctas = rows that belong to CTAs of the last launch
     const int n = src ? (have < max_ctas ? have : max_ctas) : 0;
+    const int ncopy = src ? (max_ctas < (int)rows ? max_ctas : (int)rows) : 0;
     const size_t stride = l1 ? 16 : kTailTlStride;
-    if (n > 0) STAR_CUDA(cudaMemcpy(host_out, src, (size_t)n * stride * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    if (ncopy > 0)
+      STAR_CUDA(cudaMemcpy(host_out, src, (size_t)ncopy * stride * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     if (n_ctas) *n_ctas = n;
   }
   return STAR_OK;
@@ -492,7 +497,9 @@ star_status star_predictor_layer1_ms(star_predictor* p, float* ms) {
 // standalone projection kernel when `proj` is set).
 static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, int R, const int32_t* n_tok,
                                 int32_t max_ctx_len, float* y_hat, int32_t* n_hat, const ProjArgs* proj,
-                                void* proj_ws, cudaStream_t st) {
+                                void* proj_ws, cudaStream_t st, const PlanArgs* plan = nullptr,
+                                bool* plan_fused = nullptr) {
+  if (plan_fused) *plan_fused = false;
   if (!p) return fail(STAR_EINVAL, "predictor is NULL");
   if (R < 0 || R > p->max_rows) return fail(STAR_ERANGE, "R=%d outside [0, max_rows=%d]", R, p->max_rows);
   star_status s;
@@ -573,6 +580,16 @@ static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, 
     p->tl_ctas = m_tiles * n2 * ts;
     t.project = proj ? 1 : 0;
     if (proj) t.pa = *proj;
+    if (proj && plan && plan->world == 1 &&
+        plan_fast_smem_layout(plan->n, plan->H, 1, plan->r_cap) + 256 <= (size_t)TailSmem::OFF_W3) {
+      t.plan = 1;   // Alg. 1 by the projection's last finisher: no plan launch, no kernel boundary
+      t.pl = *plan;
+      // round-0 W_i from the projection itself when it writes them into the plan's own L record:
+      // W = sum beta_t L[t] in int64 is exact in the projection's validated domain (<= 65536
+      // requests per instance, N <= 2^17, H <= 256: every term < 2^49, the sum < 2^57)
+      if (proj->W && proj->L == plan->L) t.pl.W0 = proj->W;
+      if (plan_fused) *plan_fused = true;
+    }
     cudaError_t e = launch_tail(p->tmA2, p->tmB2, p->tmB3, t, m_tiles, st);
     if (e != cudaSuccess) return cuda_fail(e, "fused tail launch");
     return STAR_OK;
@@ -654,6 +671,52 @@ star_status lenpred_forward_project(star_predictor* p, const void* h, int64_t ld
   ProjArgs pa = make_proj_args(R, n_inst, inst_base, H, inst, n_tok, n_hat, beta_q, L, W, peak, growth, count,
                                workspace, err_flag);
   return forward_impl(p, h, ld_h, R, n_tok, max_ctx_len, y_hat, n_hat, &pa, workspace, st);
+}
+
+static star_status check_plan_params(const star_plan_params* p);
+
+star_status lenpred_forward_project_plan(star_predictor* p, const void* h, int64_t ld_h, int R,
+                                         const int32_t* n_tok, int32_t max_ctx_len, float* y_hat, int32_t* n_hat,
+                                         int n_inst, int H, const int32_t* inst, const uint32_t* beta_q, int64_t* L,
+                                         int64_t* W, int64_t* peak, int64_t* growth, int32_t* count, void* workspace,
+                                         const star_plan_params* pp, const star_plan_segments* sg,
+                                         star_move* moves, int32_t* n_moves, int32_t* err_flag,
+                                         star_stream_t stream_) {
+  if (!p) return fail(STAR_EINVAL, "predictor is NULL");
+  star_status s = check_plan_params(pp);
+  if (s != STAR_OK) return s;
+  if (!sg || !sg->L) return fail(STAR_EINVAL, "segments / L is NULL");
+  if (sg->world != 1 || sg->n_loc != n_inst || pp->n_inst != n_inst || pp->H != H)
+    return fail(STAR_EINVAL, "one-rank step: segments world must be 1 and n_inst / H must match the plan");
+  if (!n_moves || (pp->max_moves > 0 && !moves)) return fail(STAR_EINVAL, "moves / n_moves is NULL");
+  if (sg->r_cap < R) return fail(STAR_EINVAL, "segment r_cap=%d < R=%d", sg->r_cap, R);
+  if (sg->r_cap > 0 && (!sg->req_id || !sg->inst || !sg->n_tok || !sg->n_hat))
+    return fail(STAR_EINVAL, "request arrays must be non-NULL");
+  const size_t smem = plan_smem_bytes(pp->n_inst, pp->H, 1, sg->r_cap) + 2048;
+  if (smem > (size_t)kMaxSmemBytes)
+    return fail(STAR_ENOTSUP, "plan state (%zu B) exceeds shared memory: n_inst*(H+1) too large", smem);
+  if (R < 0 || R > p->max_rows) return fail(STAR_ERANGE, "R=%d outside [0, max_rows=%d]", R, p->max_rows);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+  bool fused = false;
+  if (R > 0) {
+    if (n_inst < 1 || n_inst > (1 << 16)) return fail(STAR_ERANGE, "n_inst=%d outside [1, 65536]", n_inst);
+    if (H < 0 || H > 256) return fail(STAR_ERANGE, "H=%d outside [0, 256]", H);
+    if (!L || !beta_q || !workspace || !n_hat) return fail(STAR_EINVAL, "L, beta_q, workspace and n_hat must be non-NULL");
+    if (max_ctx_len < 0) return fail(STAR_EINVAL, "max_ctx_len < 0");
+    if (!h || !inst || !n_tok) return fail(STAR_EINVAL, "h, inst and n_tok must be non-NULL");
+    if (ld_h < p->d) return fail(STAR_EINVAL, "ld_h=%lld < d=%d", (long long)ld_h, p->d);
+    ProjArgs pa = make_proj_args(R, n_inst, 0, H, inst, n_tok, n_hat, beta_q, L, W, peak, growth, count, workspace,
+                                 err_flag);
+    const PlanArgs pl = make_plan_args(pp, sg, moves, n_moves, err_flag);
+    s = forward_impl(p, h, ld_h, R, n_tok, max_ctx_len, y_hat, n_hat, &pa, workspace, st, &pl, &fused);
+  } else {
+    s = lenpred_forward_project(p, h, ld_h, 0, n_tok, max_ctx_len, y_hat, n_hat, n_inst, 0, H, inst, beta_q, L, W,
+                                peak, growth, count, workspace, err_flag, stream_);
+  }
+  if (s != STAR_OK || fused) return s;
+  cudaError_t e = launch_plan(pp, sg, moves, n_moves, err_flag, st);
+  if (e != cudaSuccess) return cuda_fail(e, "plan_kernel launch");
+  return STAR_OK;
 }
 
 star_status lenpred_forward_refresh(star_predictor* p, const void* h, int64_t ld_h, int R, const int32_t* n_tok,

@@ -2,6 +2,7 @@
 
     lenpred_forward_project (predictor fused with project_instance_load) -> all-gather(records)
     -> plan_reschedule_segmented
+    (one rank: lenpred_forward_project_plan, the plan run by the fused tail's last CTA)
 
 Sharding follows the paper's deployment unit (one decode instance per GPU, PAPER.md:488;
 SURVEY.md §8(e)): the n decode instances are split into contiguous blocks of n_loc = n/W per
@@ -174,6 +175,13 @@ class Step:
             if self.world > 1:
                 exchange(self.send, self.recv, self.group)
             _lib.plan_reschedule_segmented(self.params, self.seg, self.moves, self.n_moves, self.err, stream=stream)
+            return self.moves, self.n_moves
+        if self.world == 1:
+            # one rank: forward + projection + Alg. 1 (the plan runs in the fused tail's last CTA)
+            _lib.lenpred_forward_project_plan(self.pred, h[:R], v["n_tok"][:R], v["inst"][:R], self.n_loc, self.H,
+                                              self.params.beta_q, self.ws, self.params, self.seg, self.moves,
+                                              self.n_moves, v["n_hat"][:max(R, 1)], self.proj_out,
+                                              max_ctx_len=self.max_ctx_len, err_flag=self.err, stream=stream)
             return self.moves, self.n_moves
         # predictor fused with the projection of its own N_hat (2 launches for bf16 predictors)
         _lib.lenpred_forward_project(self.pred, h[:R], v["n_tok"][:R], v["inst"][:R], self.n_loc, self.H,

@@ -450,3 +450,51 @@ def test_refresh_schedule_on_device(star, oracle_mod):
         assert np.array_equal(gl2[due], gen[due])
         g_last, nhat_last = gl2, nl2
     pred.close()
+
+
+# ============================================================================ one-rank step (fused plan)
+@pytest.mark.parametrize("cfg,R,seed", [("C2", 2048, 0), ("C4", 4096, 1), ("TGT", 4096, 2), ("C2", 1000, 3),
+                                        ("C1", 128, 4), ("C4", 777, 5)])
+def test_step_world1_fused_plan_equals_oracle(star, oracle_mod, cfg, R, seed):
+    """Step.run at world 1 (lenpred_forward_project_plan: Alg. 1 run by the fused tail's last CTA
+    when it fits) == the separate calls == the oracle plan on the GPU's own N_hat, bit for bit."""
+    from paper_2510_13668_b200.step import Step
+    c = datagen.CONFIGS[cfg]
+    n = c["n_inst"]
+    snap = datagen.make_snapshot(seed, n, (R + n - 1) // n, skewed=c.get("skewed", False), pinned_frac=0.05)
+    sl = slice(0, R)
+    ids, inst, n_tok, pin = snap.req_id[sl], snap.inst[sl], snap.n_tok[sl], snap.pinned[sl]
+    pw = datagen.make_predictor_weights(seed, c["d"], c["dtype"])
+    scale = np.maximum(snap.true_rem[sl], 1).astype(np.float32) / 60.0   # long-tailed self-predictions
+    h = datagen.make_hidden(seed, R, c["d"], c["dtype"], scale=scale)
+    tdt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
+    W, b = _weights_dev(pw, False)
+    pred = star.Predictor(*W, *b, max_rows=R)
+    params_h = datagen.make_plan_params(snap, H=50, mem_factor=c.get("mem_factor", 1.10),
+                                        max_moves=max(c["max_moves"], 4))
+    params = star.PlanParams.from_host(params_h)
+    st = Step(pred, params, n, r_cap=R)
+    st.load_requests(*(torch.from_numpy(np.ascontiguousarray(a)) for a in (ids, inst, n_tok)),
+                     pinned=torch.from_numpy(np.ascontiguousarray(pin)))
+    hd = _dev(h, tdt)
+    st.run(hd)
+    torch.cuda.synchronize()
+    got = st.result()
+    nh = st.v["n_hat"][:R].cpu().numpy()
+    L = st.v["L"].cpu().numpy()
+    assert st.err.item() == 0
+    # the fused projection equals the oracle projection of the GPU's own N_hat ...
+    ref_p = oracle_mod.project(inst, n_tok, nh, n, 50, params_h.beta_q)
+    assert np.array_equal(L, ref_p["L"])
+    # ... and the plan equals the oracle plan on that state
+    ref = oracle_mod.plan(params_h, ref_p["L"], ids, inst, n_tok, nh, pin)
+    assert got == ref
+    # the separate calls (projection, then the plan kernel) give the same moves
+    moves2, nm2 = star.plan_reschedule_segmented(params, st.seg)
+    torch.cuda.synchronize()
+    assert star.decode_moves(moves2, nm2) == got
+    # repeated step: identical (workspace re-armed, plan state rebuilt)
+    st.run(hd)
+    torch.cuda.synchronize()
+    assert st.result() == got
+    pred.close()

@@ -55,3 +55,11 @@ print("per-CTA (us from own prologue), leader CTAs 0,2,64:")
 for cta in (0, 2, 64):
     r = tl1[cta].astype(np.int64)
     print(cta, [round((r[k] - r[1]) / 1e3, 2) if r[k] else None for k in (2, 3, 4, 5, 6, 9, 10, 11, 12)])
+
+# same-SM deltas (the globaltimer offset differs between SMs): tail griddepcontrol.wait release
+# minus the layer-1 CTA exit on that SM; the smallest delta ~ the gap after the last layer-1 exit
+l1_exit = {int(r[15]): int(r[12]) for r in tl1 if r[12]}
+d = [int(r[2]) - l1_exit[int(r[15])] for r in tl if r[2] and int(r[15]) in l1_exit]
+if d:
+    d = np.array(d) / 1e3
+    print(f"tail wait release - layer-1 exit on the same SM: min {d.min():.2f} med {np.median(d):.2f} max {d.max():.2f} us (n={len(d)})")
