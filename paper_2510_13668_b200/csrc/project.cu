@@ -24,6 +24,58 @@ namespace star {
 constexpr int kProjThreads = 1024;
 constexpr int kProjMaxSmemBins = 16384;   // n_inst*(H+2) handled in shared memory (<= 192 KB)
 
+// Grid-wide merge of the per-CTA histograms (shared-memory bins -> global workspace atomics) and
+// the last-arriving CTA's finalize; leaves the workspace zeroed.  Every thread of the CTA calls it
+// after a __syncthreads that follows its own accumulation.
+template <bool SMEM_BINS>
+__device__ __forceinline__ void proj_merge_finalize(const ProjArgs& a, uint32_t* scnt, unsigned long long* ssum,
+                                                    const uint32_t* sbeta, int* s_last) {
+  const int nb = a.n_inst * (a.H + 2);
+  if (gridDim.x == 1) {
+    proj_finalize(a, scnt, ssum, sbeta, threadIdx.x >> 5, blockDim.x >> 5);
+    if (!SMEM_BINS) {  // leave the workspace zeroed
+      __syncthreads();
+      for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+        a.ws_sum[k] = 0;
+        a.ws_cnt[k] = 0;
+      }
+    }
+    return;
+  }
+  if (SMEM_BINS) {
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+      if (scnt[k]) {
+        atomicAdd(a.ws_cnt + k, scnt[k]);
+        atomicAdd(a.ws_sum + k, ssum[k]);
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) *s_last = (atomicAdd(a.ws_arrive, 1u) == gridDim.x - 1) ? 1 : 0;
+  __syncthreads();
+  if (!*s_last) return;
+  __threadfence();
+  if (SMEM_BINS) {
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+      scnt[k] = __ldcg(a.ws_cnt + k);
+      ssum[k] = __ldcg(a.ws_sum + k);
+      a.ws_cnt[k] = 0;
+      a.ws_sum[k] = 0;
+    }
+    __syncthreads();
+    proj_finalize(a, scnt, ssum, sbeta, threadIdx.x >> 5, blockDim.x >> 5);
+  } else {
+    proj_finalize(a, a.ws_cnt, a.ws_sum, sbeta, threadIdx.x >> 5, blockDim.x >> 5);
+    __syncthreads();
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+      a.ws_sum[k] = 0;
+      a.ws_cnt[k] = 0;
+    }
+  }
+  if (threadIdx.x == 0) *a.ws_arrive = 0;
+}
+
 // SMEM_BINS: histogram lives in shared memory (else directly in the global workspace).
 template <bool SMEM_BINS>
 __global__ void __launch_bounds__(kProjThreads) project_kernel(const ProjArgs a) {
@@ -98,48 +150,258 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const ProjArgs a)
   if (errbits && a.err) atomicOr(a.err, (int)errbits);
   __syncthreads();
 
-  if (gridDim.x == 1) {
-    proj_finalize(a, scnt, ssum, sbeta, threadIdx.x >> 5, blockDim.x >> 5);
-    if (!SMEM_BINS) {  // leave the workspace zeroed
-      __syncthreads();
-      for (int k = threadIdx.x; k < nb; k += blockDim.x) {
-        a.ws_sum[k] = 0;
-        a.ws_cnt[k] = 0;
+  proj_merge_finalize<SMEM_BINS>(a, scnt, ssum, sbeta, &s_last);
+}
+
+// ---------------------------------------------------------------------------------------
+// Bandwidth form for large batches (R >= kStreamMinRows, 16-byte aligned arrays, the histogram
+// in shared memory): each CTA (two per SM when the histogram is small) streams its contiguous
+// slice of the three arrays through a 3-stage shared-memory ring with bulk copies
+// (cp.async.bulk, one producer thread, transaction mbarriers), so the bytes in flight per SM (up
+// to 2 x 3 x 24 KB) do not depend on registers.  16 consumer warps each take one int4 of every
+// array per stage (4 requests per lane) and release the stage with one arrive per warp.
+// The per-request aggregation is the branch-light proj_acc4_stream (ncu: the general
+// proj_accumulate4 spent ~270 warp-instructions per 128 requests, mostly compares, branches and
+// reconvergence, and capped the kernel at ~45% of HBM): validity as bit masks, hot requests
+// (N_hat > H, ~78% of a long-tailed CoT batch) reduced per distinct instance with ballot +
+// REDUX (one round for an instance-grouped batch), cold requests added straight to their bin.
+// Bins are 32-bit in shared memory with the token sum split as S = lo + hi * 2^12 (lo adds N mod
+// 2^12, hi adds N >> 12 <= 32), so no bin can wrap while a CTA sees at most 2^20 requests
+// (checked at launch) and no periodic flush (a CTA-wide barrier) is needed; the bins are merged
+// into the 64-bit global workspace once at the end.
+constexpr int kStreamWarps = 16;                          // consumer warps
+constexpr int kStreamThreads = (kStreamWarps + 1) * 32;   // + the producer warp
+constexpr int kStreamVec = kStreamWarps * 32;             // int4 per array per stage (2048 requests)
+constexpr int kStreamStages = 3;
+constexpr uint32_t kStreamArrBytes = kStreamVec * 16u;    // 8 KB
+constexpr uint32_t kStreamStageBytes = 3u * kStreamArrBytes;
+constexpr size_t kStreamRingBytes = (size_t)kStreamStages * kStreamStageBytes + 2 * kStreamStages * 8;
+constexpr int kStreamMaxBins = 8192;                      // 96 KB of 32-bit bins next to the 72 KB ring
+constexpr int64_t kStreamMaxPerCta = 1 << 20;             // requests per CTA (32-bit split-sum bins)
+constexpr int64_t kStreamMinRows = 1 << 18;
+
+// Warp-uniform running total of hot requests (N_hat > H) of one instance, kept in registers
+// across stages: an instance-grouped stream touches the shared hot bin only when the instance
+// changes (and once at the end).
+struct HotAcc {
+  int inst = -1;
+  uint32_t c = 0;
+  unsigned long long s = 0;
+};
+__device__ __forceinline__ void hot_acc_push(HotAcc& acc, int HB, int H, uint32_t* cnt, uint32_t* slo,
+                                             uint32_t* shi) {
+  if (acc.inst >= 0 && (threadIdx.x & 31) == 0) {
+    const int key = acc.inst * HB + H + 1;
+    atomicAdd(cnt + key, acc.c);
+    atomicAdd(slo + key, (uint32_t)(acc.s & 0xFFFu));
+    atomicAdd(shi + key, (uint32_t)(acc.s >> 12));
+  }
+  acc.inst = -1;
+  acc.c = 0;
+  acc.s = 0;
+}
+
+// Four requests per lane; every lane of the warp calls it.  Bins: count and token sum, 32-bit.
+// Written for issue slots (the kernel is issue-bound once the stream is decoupled): one OR of
+// three range tests per request, the detailed error bits only in a warp that saw a bad request,
+// the lane's hot merge through selects.
+__device__ __forceinline__ void proj_acc4_stream(const ProjArgs& a, bool valid, const int4& x, const int4& n,
+                                                 const int4& h, uint32_t* cnt, uint32_t* slo, uint32_t* shi,
+                                                 uint32_t& errbits, HotAcc& acc) {
+  const int HB = a.H + 2;
+  const int ins[4] = {x.x - a.inst_base, x.y - a.inst_base, x.z - a.inst_base, x.w - a.inst_base};
+  const int nt[4] = {n.x, n.y, n.z, n.w};
+  const int nh[4] = {h.x, h.y, h.z, h.w};
+  // range checks for the four requests at once (unsigned max over the lane's four values):
+  // instance < n_inst, N - 1 < 2^17 (N in [1, 2^17]), N_hat >= 0
+  const unsigned mi = max(max((unsigned)ins[0], (unsigned)ins[1]), max((unsigned)ins[2], (unsigned)ins[3]));
+  const unsigned mn = max(max((unsigned)(nt[0] - 1), (unsigned)(nt[1] - 1)),
+                          max((unsigned)(nt[2] - 1), (unsigned)(nt[3] - 1)));
+  const unsigned sh = (unsigned)(nh[0] | nh[1] | nh[2] | nh[3]) >> 31;
+  const bool lane_bad = valid && (mi >= (unsigned)a.n_inst || mn >= (1u << 17) || sh);
+  uint32_t okm = valid ? 15u : 0u;
+  if (__any_sync(0xFFFFFFFFu, lane_bad)) {   // rare: per-request checks and error bits
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t e = ((unsigned)ins[j] >= (unsigned)a.n_inst ? 1u : 0u) |
+                         ((unsigned)(nt[j] - 1) >= (1u << 17) ? 2u : 0u) | (nh[j] < 0 ? 4u : 0u);
+      if (valid && e) {
+        errbits |= e;
+        okm &= ~(1u << j);
       }
     }
-    return;
   }
-  if (SMEM_BINS) {
-    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
-      if (scnt[k]) {
-        atomicAdd(a.ws_cnt + k, scnt[k]);
-        atomicAdd(a.ws_sum + k, ssum[k]);
+  uint32_t hot = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) hot |= nh[j] > a.H ? (1u << j) : 0u;
+  hot &= okm;
+  const uint32_t cold = okm & ~hot;
+  // lane merge: hot requests of the lane's first hot instance (all four when the lane's
+  // requests share one instance, the common case of an instance-grouped batch)
+  int li = -1;
+  uint32_t same = 0, ls = 0;
+  if (ins[0] == ins[1] && ins[0] == ins[2] && ins[0] == ins[3]) {
+    li = hot ? ins[0] : -1;
+    same = hot;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ls += ((hot >> j) & 1u) ? (uint32_t)nt[j] : 0u;
+  } else {
+    li = (hot & 1u) ? ins[0] : (hot & 2u) ? ins[1] : (hot & 4u) ? ins[2] : (hot & 8u) ? ins[3] : -1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool sj = ((hot >> j) & 1u) && ins[j] == li;
+      same |= sj ? (1u << j) : 0u;
+      ls += sj ? (uint32_t)nt[j] : 0u;
+    }
+  }
+  const uint32_t lc = __popc(same);
+  const uint32_t direct = cold | (hot & ~same);   // to their bins one by one
+  if (__any_sync(0xFFFFFFFFu, direct != 0)) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if ((direct >> j) & 1u) {
+        const int key = ins[j] * HB + ((hot >> j) & 1u ? a.H + 1 : nh[j]);
+        atomicAdd(cnt + key, 1u);
+        atomicAdd(slo + key, (uint32_t)nt[j] & 0xFFFu);
+        atomicAdd(shi + key, (uint32_t)nt[j] >> 12);
       }
     }
   }
+  // one ballot + REDUX round per distinct lane instance (one for an instance-grouped batch)
+  __syncwarp();
+  uint32_t pend = __ballot_sync(0xFFFFFFFFu, li >= 0);
+  while (pend) {   // warp-uniform
+    const int ki = __shfl_sync(0xFFFFFFFFu, li, __ffs(pend) - 1);
+    const bool mine = li == ki;
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, mine);
+    const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, mine ? lc : 0u);
+    const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, mine ? ls : 0u);   // <= 128 * 2^17
+    if (ki != acc.inst) {
+      hot_acc_push(acc, HB, a.H, cnt, slo, shi);
+      acc.inst = ki;
+    }
+    acc.c += wc;
+    acc.s += ws;
+    pend &= ~m;
+  }
+}
+
+__global__ void __launch_bounds__(kStreamThreads, 2) project_stream_kernel(const ProjArgs a) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int nb = a.n_inst * (a.H + 2);
+  int4* ring = reinterpret_cast<int4*>(sm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)kStreamStages * kStreamStageBytes);
+  uint64_t* empty = full + kStreamStages;
+  uint32_t* scnt = reinterpret_cast<uint32_t*>(empty + kStreamStages);
+  uint32_t* slo = scnt + nb;
+  uint32_t* shi = slo + nb;
+  __shared__ int s_last;
+  __shared__ uint32_t sbeta[257];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+    scnt[k] = 0;
+    slo[k] = 0;
+    shi[k] = 0;
+  }
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kStreamStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kStreamWarps);
+    }
+    fence_barrier_init();
+  }
+  pdl_wait();   // inputs may come from the previous kernel (PDL launch)
+  for (int t = threadIdx.x; t <= a.H; t += blockDim.x) sbeta[t] = a.beta_q[t];
+  __syncthreads();   // zeroed bins, barriers and beta visible
+
+  const int64_t nvec = a.R / 4;
+  const int64_t per = (nvec + gridDim.x - 1) / gridDim.x;
+  const int64_t v_beg = (int64_t)blockIdx.x * per;
+  const int64_t v_end = v_beg + per < nvec ? v_beg + per : nvec;
+  const int64_t nchunks = v_end > v_beg ? (v_end - v_beg + kStreamVec - 1) / kStreamVec : 0;
+  uint32_t errbits = 0;
+  HotAcc acc;
+  if (warp == kStreamWarps) {
+    // ---------------- producer: one thread, bulk copies into the ring ----------------
+    if (lane == 0) {
+      const int4* src[3] = {reinterpret_cast<const int4*>(a.inst), reinterpret_cast<const int4*>(a.n_tok),
+                            reinterpret_cast<const int4*>(a.n_hat)};
+      for (int64_t c = 0; c < nchunks; ++c) {
+        const int st = (int)(c % kStreamStages);
+        const uint32_t ph = (uint32_t)(c / kStreamStages) & 1u;
+        mbar_wait(&empty[st], ph ^ 1u);
+        const int64_t v0 = v_beg + c * kStreamVec;
+        const int nv = (int)(v_end - v0 < kStreamVec ? v_end - v0 : kStreamVec);
+        const uint32_t bytes = (uint32_t)nv * 16u;
+        mbar_arrive_expect_tx(&full[st], 3u * bytes);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) bulk_g2s(ring + ((size_t)st * 3 + k) * kStreamVec, src[k] + v0, bytes, &full[st]);
+      }
+    }
+  } else {
+    // ---------------- consumers: one int4 of each array per lane per stage ----------------
+    const int j = warp * 32 + lane;
+    const int nch = (int)nchunks;
+    const int last_nv = (int)(v_end - v_beg - (int64_t)(nch - 1) * kStreamVec);   // vectors in the last chunk
+    int st = 0;
+    uint32_t ph = 0;
+    for (int c = 0; c < nch; ++c) {
+      mbar_wait(&full[st], ph);
+      const bool valid = c + 1 < nch || j < last_nv;
+      // (lanes past the last chunk's end read stale ring data, masked by `valid`)
+      const int4* sx = ring + (size_t)st * 3 * kStreamVec + j;
+      const int4 x = sx[0], n = sx[kStreamVec], h = sx[2 * kStreamVec];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);   // this warp's reads of the stage are done
+      proj_acc4_stream(a, valid, x, n, h, scnt, slo, shi, errbits, acc);
+      if (++st == kStreamStages) {
+        st = 0;
+        ph ^= 1u;
+      }
+    }
+    // the R % 4 trailing requests (CTA 0, warp 0), one per lane
+    if (blockIdx.x == 0 && warp == 0) {
+      const int64_t r = nvec * 4 + lane;
+      if (r < a.R) {
+        const int i = a.inst[r] - a.inst_base, nt = a.n_tok[r], nh = a.n_hat[r];
+        const bool in_rng = (unsigned)i < (unsigned)a.n_inst, nt_ok = (unsigned)(nt - 1) < (1u << 17), nh_ok = nh >= 0;
+        errbits |= (in_rng ? 0u : 1u) | (nt_ok ? 0u : 2u) | (nh_ok ? 0u : 4u);
+        if (in_rng && nt_ok && nh_ok) {
+          const int key = i * (a.H + 2) + (nh > a.H + 1 ? a.H + 1 : nh);
+          atomicAdd(scnt + key, 1u);
+          atomicAdd(slo + key, (uint32_t)nt & 0xFFFu);
+          atomicAdd(shi + key, (uint32_t)nt >> 12);
+        }
+      }
+    }
+    hot_acc_push(acc, a.H + 2, a.H, scnt, slo, shi);
+  }
+  if (errbits && a.err) atomicOr(a.err, (int)errbits);
+  __syncthreads();
+  for (int k = threadIdx.x; k < nb; k += blockDim.x) {   // merge into the 64-bit global workspace
+    const uint32_t c = scnt[k];
+    if (c) {
+      atomicAdd(a.ws_cnt + k, c);
+      atomicAdd(a.ws_sum + k, (unsigned long long)slo[k] + ((unsigned long long)shi[k] << 12));
+    }
+  }
+  // grid-wide arrival; the last CTA finalises from the global workspace and re-zeroes it
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = (atomicAdd(a.ws_arrive, 1u) == gridDim.x - 1) ? 1 : 0;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (SMEM_BINS) {
-    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
-      scnt[k] = __ldcg(a.ws_cnt + k);
-      ssum[k] = __ldcg(a.ws_sum + k);
-      a.ws_cnt[k] = 0;
-      a.ws_sum[k] = 0;
-    }
-    __syncthreads();
-    proj_finalize(a, scnt, ssum, sbeta, threadIdx.x >> 5, blockDim.x >> 5);
-  } else {
-    proj_finalize(a, a.ws_cnt, a.ws_sum, sbeta, threadIdx.x >> 5, blockDim.x >> 5);
-    __syncthreads();
-    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
-      a.ws_sum[k] = 0;
-      a.ws_cnt[k] = 0;
-    }
+  uint32_t* fc = reinterpret_cast<uint32_t*>(sm);                       // the ring is free now
+  unsigned long long* fs = reinterpret_cast<unsigned long long*>(sm + ((size_t)nb * 4 + 15) / 16 * 16);
+  for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+    fc[k] = __ldcg(a.ws_cnt + k);
+    fs[k] = __ldcg(a.ws_sum + k);
+    a.ws_cnt[k] = 0;
+    a.ws_sum[k] = 0;
   }
+  __syncthreads();
+  proj_finalize(a, fc, fs, sbeta, warp, blockDim.x >> 5);
   if (threadIdx.x == 0) *a.ws_arrive = 0;
 }
 
@@ -186,6 +448,30 @@ cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_
   ProjArgs a = make_proj_args(R, n_inst, inst_base, H, inst, n_tok, n_hat, beta_q, L, W, peak, growth, count,
                               workspace, err_flag);
   const size_t nb = (size_t)n_inst * (size_t)(H + 2);
+  if (workspace && a.vec_ok && (int64_t)R >= kStreamMinRows && nb <= (size_t)kStreamMaxBins &&
+      (int64_t)R <= kStreamMaxPerCta * g_num_sms) {
+    const size_t smem = kStreamRingBytes + nb * 12;
+    static int attr_bytes = 0;
+    if ((int)smem > attr_bytes) {
+      cudaError_t e = cudaFuncSetAttribute(project_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr_bytes = (int)smem;
+    }
+    // two CTAs per SM (2 x 72 KB in flight, 32 consumer warps) when both fit in shared memory
+    const int grid = g_num_sms * (smem <= (size_t)113 * 1024 ? 2 : 1);
+    if (grid_out) *grid_out = grid;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(kStreamThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, project_stream_kernel, a);
+  }
   const bool smem_bins = nb <= (size_t)kProjMaxSmemBins;
   int grid = 1;
   if (workspace && R > project_single_cta_max_rows() / 8) {

@@ -60,8 +60,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
   const uint64_t t0 = globaltimer_ns();
-  while (!mbar_try_wait(a, parity)) {
-    if (globaltimer_ns() - t0 > 2000000000ull) __trap();
+  for (uint32_t it = 1;; ++it) {   // try_wait suspends in hardware; the clock is read every 64 tries
+    if (mbar_try_wait(a, parity)) return;
+    if ((it & 63u) == 0 && globaltimer_ns() - t0 > 2000000000ull) __trap();
   }
 }
 

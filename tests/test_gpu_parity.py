@@ -58,7 +58,8 @@ def test_quantizer_bitexact(star, oracle_mod):
 # ============================================================================ projection
 @pytest.mark.parametrize("seed,n,R,H", [(0, 1, 0, 50), (1, 1, 1, 50), (2, 8, 2048, 50), (3, 8, 4096, 50),
                                        (4, 3, 1001, 7), (5, 5, 333, 0), (6, 64, 12345, 50), (7, 2, 77, 256),
-                                       (8, 8, 300_000, 50), (9, 300, 50_000, 50)])
+                                       (8, 8, 300_000, 50), (9, 300, 50_000, 50), (10, 32, 1_000_003, 50),
+                                       (11, 32, (1 << 20) + 1, 20), (12, 150, 600_001, 50)])
 def test_projection_bitexact(star, oracle_mod, seed, n, R, H):
     snap = datagen.make_snapshot(seed, n, max(R // n, 1))
     g = datagen.rng(seed)

@@ -15,6 +15,11 @@ inst = torch.from_numpy((np.tile(snap.inst, reps) + shift).astype(np.int32)).cud
 ntok = torch.from_numpy(np.tile(snap.n_tok, reps)).cuda()
 nhat = torch.from_numpy(np.tile(snap.true_rem.astype(np.int32), reps)).cuda()
 n = 8 * n_per
+dist = sys.argv[3] if len(sys.argv) > 3 else "real"
+if dist == "hot":
+    nhat = torch.full_like(nhat, 1000)
+elif dist == "cold":
+    nhat = torch.randint(0, 51, nhat.shape, dtype=torch.int32, device=nhat.device)
 if len(sys.argv) > 2 and sys.argv[2] == "grouped":   # instance-major layout (each instance's batch contiguous)
     order = torch.argsort(inst, stable=True)
     inst, ntok, nhat = inst[order].contiguous(), ntok[order].contiguous(), nhat[order].contiguous()
