@@ -53,6 +53,7 @@ struct GemmArgs {
   float* head_ws;        // [tiles][splits][128] per-owner partial dots (EPI_HEAD)
   uint64_t* tl;          // diagnostics: [ctas][16] %globaltimer phase stamps, or nullptr
   const int32_t* M_dev;  // device-side row count (refresh mode: rows selected on the device), or nullptr
+  int* l1_cnt;           // CTA-pair split-K: [cta tiles][2] arrival / done counters (zeroed, self re-arming)
 };
 
 // Quantizer (readings A8-A10): cap = max(0, L_ctx - N(r)) (no n_tok -> L_ctx);
@@ -163,6 +164,13 @@ __global__ void __launch_bounds__(192, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  uint64_t* tl = p.tl ? p.tl + (((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16 : nullptr;
+  if (tl && threadIdx.x == 0) {
+    tl[0] = globaltimer_ns();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tl[15] = smid;
+  }
   const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
   const int splits = p.splits;
   const int kb0 = split * p.kb_per_split;
@@ -189,10 +197,12 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tl && threadIdx.x == 0) tl[1] = globaltimer_ns();
   // PDL: the prologue above overlapped the previous kernel's tail; from here on we read
   // (and overwrite) memory it may own.
   pdl_wait();
   pdl_launch_dependents();
+  if (tl && threadIdx.x == 0) tl[2] = globaltimer_ns();
 
   const int OW = BN / splits;                 // columns owned by each split
   const int own0 = split * OW;                // first owned column (tile-relative)
@@ -228,6 +238,7 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t ph = (uint32_t)(i / S::STAGES) & 1u;
         mbar_wait(&full[s], ph);
         tc_fence_after();
+        if (tl && i == 0) tl[3] = globaltimer_ns();
         const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * S::A_BYTES));
         const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * S::B_BYTES));
 #pragma unroll
@@ -238,12 +249,14 @@ __global__ void __launch_bounds__(192, 1)
         umma_commit(&empty[s]);
       }
       umma_commit(accum);
+      if (tl) tl[9] = globaltimer_ns();
     }
     __syncwarp();
   } else {
     // ---------------- epilogue phase 1: wait for the accumulator, publish partials --------
     mbar_wait(accum, 0);
     tc_fence_after();
+    if (tl && threadIdx.x == 64) tl[10] = globaltimer_ns();
     if (splits > 1) {
       for (int o = 0; o < splits; ++o) {
         if (o == split) continue;
@@ -261,7 +274,9 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   }
+  if (tl && threadIdx.x == 64) tl[7] = globaltimer_ns();
   if (splits > 1) cluster_sync_all();   // partials of every split of this tile are visible
+  if (tl && threadIdx.x == 64) tl[8] = globaltimer_ns();
 
   float head_acc = 0.0f;
   if (warp >= 2) {
@@ -277,21 +292,36 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
       } else {
+        // every other split's partial of these 16 columns is loaded before any is summed (the
+        // loads overlap instead of paying one L2 round trip per split); the sum runs in the
+        // fixed split order 0..S-1
+        float4 pv[7][4];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) f[j] = 0.0f;
-        for (int s = 0; s < splits; ++s) {
-          if (s == split) {
-            uint32_t v[16];
-            tmem_ld_32x32b_x16(trow + (uint32_t)(own0 + c), v);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) f[j] += __uint_as_float(v[j]);
-          } else {
+        for (int k = 0; k < 7; ++k) {
+          if (k < splits - 1) {
+            const int s = k < split ? k : k + 1;
             const float4* src =
                 reinterpret_cast<const float4*>(wsb + (int64_t)(s * splits + split) * OW * BM) + row_in_tile;
 #pragma unroll
+            for (int j = 0; j < 4; ++j) pv[k][j] = __ldcg(src + (c / 4 + j) * BM);
+          }
+        }
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(trow + (uint32_t)(own0 + c), v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) f[j] = 0.0f;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          if (s >= splits) break;
+          if (s == split) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) f[j] += __uint_as_float(v[j]);
+          } else {
+#pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const float4 x = __ldcg(src + (c / 4 + j) * BM);
+              float4 x = pv[s < 7 ? s : 6][j];
+              if (s > split) x = pv[s > 0 ? s - 1 : 0][j];
               f[4 * j] += x.x;
               f[4 * j + 1] += x.y;
               f[4 * j + 2] += x.z;
@@ -312,6 +342,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
     if (stage_base && lane == 0) bulk_wait_all();
+    if (tl && threadIdx.x == 64) tl[11] = globaltimer_ns();
     if (p.epi == EPI_HEAD && splits > 1) p.head_ws[((int64_t)tile_id * splits + split) * BM + row_in_tile] = head_acc;
   }
   if (p.epi == EPI_HEAD && splits > 1) cluster_sync_all();   // per-owner partial dots visible
@@ -327,6 +358,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (tl && threadIdx.x == 0) tl[12] = globaltimer_ns();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<S::TMEM_COLS>(tmem);
@@ -376,7 +408,7 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();       // 0 = leader (issues the MMAs), 1 = peer
-  uint64_t* tl = p.tl ? p.tl + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 : nullptr;
+  uint64_t* tl = p.tl ? p.tl + (((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16 : nullptr;
   if (tl && threadIdx.x == 0) {
     tl[0] = globaltimer_ns();
     uint32_t smid;
@@ -385,7 +417,9 @@ __global__ void __launch_bounds__(192, 1)
   }
   const int m_row0 = blockIdx.x * 128;           // this CTA's 128 rows (pair covers 256)
   const int n_tile = blockIdx.y;
-  const int nkb = p.num_kb;
+  const int split = blockIdx.z, splits = p.splits;
+  const int kb0 = split * p.kb_per_split;
+  const int nkb = min(p.num_kb, kb0 + p.kb_per_split) - kb0;   // >= 1 (host guarantees)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -418,7 +452,7 @@ __global__ void __launch_bounds__(192, 1)
       const int pre = nkb < S::STAGES ? nkb : S::STAGES;
       for (int i = 0; i < pre; ++i) {
         if (rank == 0) mbar_arrive_expect_tx(&full[i], 2 * S::STAGE_BYTES);
-        tma_load_2d_pair(sB + i * S::B_BYTES, &tmB, full0 + (uint32_t)(i * 8), i * BK, b_row, pol_b);
+        tma_load_2d_pair(sB + i * S::B_BYTES, &tmB, full0 + (uint32_t)(i * 8), (kb0 + i) * BK, b_row, pol_b);
       }
       pdl_wait();
       if (tl) tl[2] = globaltimer_ns();
@@ -428,12 +462,12 @@ __global__ void __launch_bounds__(192, 1)
         if (i >= pre) {
           mbar_wait(&empty[s], ph ^ 1u);
           if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * S::STAGE_BYTES);
-          tma_load_2d_pair(sB + s * S::B_BYTES, &tmB, full0 + (uint32_t)(s * 8), i * BK, b_row, pol_b);
+          tma_load_2d_pair(sB + s * S::B_BYTES, &tmB, full0 + (uint32_t)(s * 8), (kb0 + i) * BK, b_row, pol_b);
         }
-        tma_load_2d_pair(sA + s * S::A_BYTES, &tmA, full0 + (uint32_t)(s * 8), i * BK, m_row0, pol_a);
+        tma_load_2d_pair(sA + s * S::A_BYTES, &tmA, full0 + (uint32_t)(s * 8), (kb0 + i) * BK, m_row0, pol_a);
         if (i + kPrefetchKB < nkb) {   // pull a later K block into L2 so its TMA load is an L2 hit
-          tma_prefetch_2d(&tmA, (i + kPrefetchKB) * BK, m_row0);
-          tma_prefetch_2d(&tmB, (i + kPrefetchKB) * BK, b_row);
+          tma_prefetch_2d(&tmA, (kb0 + i + kPrefetchKB) * BK, m_row0);
+          tma_prefetch_2d(&tmB, (kb0 + i + kPrefetchKB) * BK, b_row);
         }
       }
     }
@@ -468,8 +502,108 @@ __global__ void __launch_bounds__(192, 1)
     mbar_wait(accum, 0);
     tc_fence_after();
     if (tl && threadIdx.x == 64) tl[10] = globaltimer_ns();
-    uint8_t* stage_base = smem + (q * (BN / 64)) * 4096;
     float head_acc = 0.0f;
+    if (splits > 1) {
+      // ---- split-K: the S CTAs computing this CTA's 128 x BN block over disjoint K ranges meet
+      // through an arrival counter in global memory (the grid is one wave of <= 148 CTAs, every
+      // CTA resident, so the wait cannot starve).  Each split publishes the columns the other
+      // splits own (fp32, lane-contiguous [col/4][row][4]), then reduces its own BN/S columns in
+      // the fixed split order 0..S-1 (deterministic) and runs the epilogue on them.
+      const int OW = BN / splits, own0 = split * OW;
+      const int row_in_tile = q * 32 + lane;
+      const int cta_tile = blockIdx.y * gridDim.x + blockIdx.x;
+      float* wsb = p.ws + (int64_t)cta_tile * splits * BN * 128;
+      for (int o = 0; o < splits; ++o) {
+        if (o == split) continue;
+        float4* dst = reinterpret_cast<float4*>(wsb + (int64_t)(split * splits + o) * OW * 128) + row_in_tile;
+#pragma unroll 1
+        for (int c = 0; c < OW; c += 32) {
+          uint32_t v[16], u[16];
+          tmem_ld_32x32b_x16(trow + (uint32_t)(o * OW + c), v);
+          tmem_ld_32x32b_x16(trow + (uint32_t)(o * OW + c + 16), u);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            dst[(c / 4 + j) * 128] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                 __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+            dst[(c / 4 + 4 + j) * 128] = make_float4(__uint_as_float(u[4 * j]), __uint_as_float(u[4 * j + 1]),
+                                                     __uint_as_float(u[4 * j + 2]), __uint_as_float(u[4 * j + 3]));
+          }
+        }
+      }
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (tl && threadIdx.x == 64) tl[7] = globaltimer_ns();
+      if (threadIdx.x == 64) {
+        int* ctr = p.l1_cnt + 2 * cta_tile;
+        atomicAdd(ctr, 1);
+        int seen;
+        do {
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
+          if (seen < splits) __nanosleep(64);
+        } while (seen < splits);
+        if (tl) tl[8] = globaltimer_ns();
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      uint8_t* stage_base = (OW % 64 == 0) ? smem + (q * (OW / 64)) * 4096 : nullptr;
+#pragma unroll 1
+      for (int c = 0; c < OW; c += 16) {
+        float4 pv[7][4];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+          if (k < splits - 1) {
+            const int s = k < split ? k : k + 1;
+            const float4* src =
+                reinterpret_cast<const float4*>(wsb + (int64_t)(s * splits + split) * OW * 128) + row_in_tile;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pv[k][j] = __ldcg(src + (c / 4 + j) * 128);
+          }
+        }
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(trow + (uint32_t)(own0 + c), v);
+        tmem_ld_wait();
+        float f[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) f[j] = 0.0f;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          if (s >= splits) break;
+          if (s == split) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) f[j] += __uint_as_float(v[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float4 x = pv[s < 7 ? s : 6][j];
+              if (s > split) x = pv[s > 0 ? s - 1 : 0][j];
+              f[4 * j] += x.x;
+              f[4 * j + 1] += x.y;
+              f[4 * j + 2] += x.z;
+              f[4 * j + 3] += x.w;
+            }
+          }
+        }
+        uint8_t* stage = stage_base ? stage_base + (c / 64) * 4096 : nullptr;
+        epilogue16<false>(p, row, n0 + own0 + c, f, head_acc, stage, (c % 64) / 8);
+        if (stage && (c % 64) == 48) {
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, stage, n0 + own0 + (c / 64) * 64, m_row0 + q * 32);
+            bulk_commit();
+          }
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 64) {   // the last split to finish re-arms the counter for the next launch
+        int* ctr = p.l1_cnt + 2 * cta_tile;
+        if (atomicAdd(ctr + 1, 1) == splits - 1) {
+          ctr[0] = 0;
+          ctr[1] = 0;
+        }
+      }
+    } else {
+    uint8_t* stage_base = smem + (q * (BN / 64)) * 4096;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       uint32_t v[16], u[16];
@@ -493,6 +627,7 @@ __global__ void __launch_bounds__(192, 1)
           bulk_commit();
         }
       }
+    }
     }
     if (lane == 0) bulk_wait_all();
     if (tl && threadIdx.x == 64) tl[11] = globaltimer_ns();

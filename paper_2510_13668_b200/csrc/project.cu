@@ -14,6 +14,7 @@
 // Multi-CTA grids merge through a global workspace; the last CTA to arrive finalises and
 // re-zeroes the workspace.  Pass 2 (one CTA) is a suffix scan per instance.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "project_core.cuh"
 #include "ptx.cuh"
@@ -154,12 +155,13 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const ProjArgs a)
 }
 
 // ---------------------------------------------------------------------------------------
-// Bandwidth form for large batches (R >= kStreamMinRows, 16-byte aligned arrays, the histogram
-// in shared memory): each CTA (two per SM when the histogram is small) streams its contiguous
-// slice of the three arrays through a 3-stage shared-memory ring with bulk copies
-// (cp.async.bulk, one producer thread, transaction mbarriers), so the bytes in flight per SM (up
-// to 2 x 3 x 24 KB) do not depend on registers.  16 consumer warps each take one int4 of every
-// array per stage (4 requests per lane) and release the stage with one arrive per warp.
+// Bandwidth form for large batches (R >= kStreamMinRows, 16-byte aligned arrays, workspace):
+// project_ldg_kernel streams each CTA's contiguous slice of the three arrays with ld.global.nc
+// int4 loads (two CTAs per SM), aggregates into a shared-memory histogram window and merges it
+// into the 64-bit global workspace; project_finalize_kernel (PDL-launched) then finalises every
+// instance in parallel, one warp per instance, and re-zeroes the workspace.  (Measured on this
+// B200, tools/read_bench.cu: per-CTA-contiguous int4 loads reach 4.7-5.0 TB/s, cp.async.bulk
+// rings cap at ~4.4 TB/s; a finalize by the last-arriving CTA cost ~10-30 us at 8-256 instances.)
 // The per-request aggregation is the branch-light proj_acc4_stream (ncu: the general
 // proj_accumulate4 spent ~270 warp-instructions per 128 requests, mostly compares, branches and
 // reconvergence, and capped the kernel at ~45% of HBM): validity as bit masks, hot requests
@@ -167,18 +169,33 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const ProjArgs a)
 // REDUX (one round for an instance-grouped batch), cold requests added straight to their bin.
 // Bins are 32-bit in shared memory with the token sum split as S = lo + hi * 2^12 (lo adds N mod
 // 2^12, hi adds N >> 12 <= 32), so no bin can wrap while a CTA sees at most 2^20 requests
-// (checked at launch) and no periodic flush (a CTA-wide barrier) is needed; the bins are merged
-// into the 64-bit global workspace once at the end.
-constexpr int kStreamWarps = 16;                          // consumer warps
-constexpr int kStreamThreads = (kStreamWarps + 1) * 32;   // + the producer warp
-constexpr int kStreamVec = kStreamWarps * 32;             // int4 per array per stage (2048 requests)
-constexpr int kStreamStages = 3;
-constexpr uint32_t kStreamArrBytes = kStreamVec * 16u;    // 8 KB
-constexpr uint32_t kStreamStageBytes = 3u * kStreamArrBytes;
-constexpr size_t kStreamRingBytes = (size_t)kStreamStages * kStreamStageBytes + 2 * kStreamStages * 8;
-constexpr int kStreamMaxBins = 8192;                      // 96 KB of 32-bit bins next to the 72 KB ring
+// (checked at launch) and no periodic flush (a CTA-wide barrier) is needed.
+constexpr int kStreamWinBins = 3072;                      // 36 KB window of 32-bit bins
 constexpr int64_t kStreamMaxPerCta = 1 << 20;             // requests per CTA (32-bit split-sum bins)
 constexpr int64_t kStreamMinRows = 1 << 18;
+
+// Shared-memory bins cover a WINDOW of instances [wbase, wbase + wn) (all of them when the
+// histogram fits; otherwise the instances around the first request of the CTA's slice, which for
+// an instance-grouped batch is every instance the slice touches).  A request of an instance
+// outside the window is added straight to the 64-bit global workspace (correct for any order,
+// slow only for inputs that are neither grouped nor small in instance count).
+struct BinWin {
+  int wbase, wn, HB;
+};
+__device__ __forceinline__ void bin_add(const ProjArgs& a, const BinWin& w, int inst, int b, uint32_t c,
+                                        unsigned long long s, uint32_t* cnt, uint32_t* slo, uint32_t* shi) {
+  const int wi = inst - w.wbase;
+  if ((unsigned)wi < (unsigned)w.wn) {
+    const int key = wi * w.HB + b;
+    atomicAdd(cnt + key, c);
+    atomicAdd(slo + key, (uint32_t)(s & 0xFFFu));
+    atomicAdd(shi + key, (uint32_t)(s >> 12));
+  } else {
+    const int key = inst * w.HB + b;
+    atomicAdd(a.ws_cnt + key, c);
+    atomicAdd(a.ws_sum + key, s);
+  }
+}
 
 // Warp-uniform running total of hot requests (N_hat > H) of one instance, kept in registers
 // across stages: an instance-grouped stream touches the shared hot bin only when the instance
@@ -188,14 +205,9 @@ struct HotAcc {
   uint32_t c = 0;
   unsigned long long s = 0;
 };
-__device__ __forceinline__ void hot_acc_push(HotAcc& acc, int HB, int H, uint32_t* cnt, uint32_t* slo,
-                                             uint32_t* shi) {
-  if (acc.inst >= 0 && (threadIdx.x & 31) == 0) {
-    const int key = acc.inst * HB + H + 1;
-    atomicAdd(cnt + key, acc.c);
-    atomicAdd(slo + key, (uint32_t)(acc.s & 0xFFFu));
-    atomicAdd(shi + key, (uint32_t)(acc.s >> 12));
-  }
+__device__ __forceinline__ void hot_acc_push(const ProjArgs& a, const BinWin& w, HotAcc& acc, uint32_t* cnt,
+                                             uint32_t* slo, uint32_t* shi) {
+  if (acc.inst >= 0 && (threadIdx.x & 31) == 0) bin_add(a, w, acc.inst, a.H + 1, acc.c, acc.s, cnt, slo, shi);
   acc.inst = -1;
   acc.c = 0;
   acc.s = 0;
@@ -206,9 +218,8 @@ __device__ __forceinline__ void hot_acc_push(HotAcc& acc, int HB, int H, uint32_
 // three range tests per request, the detailed error bits only in a warp that saw a bad request,
 // the lane's hot merge through selects.
 __device__ __forceinline__ void proj_acc4_stream(const ProjArgs& a, bool valid, const int4& x, const int4& n,
-                                                 const int4& h, uint32_t* cnt, uint32_t* slo, uint32_t* shi,
-                                                 uint32_t& errbits, HotAcc& acc) {
-  const int HB = a.H + 2;
+                                                 const int4& h, const BinWin& w, uint32_t* cnt, uint32_t* slo,
+                                                 uint32_t* shi, uint32_t& errbits, HotAcc& acc) {
   const int ins[4] = {x.x - a.inst_base, x.y - a.inst_base, x.z - a.inst_base, x.w - a.inst_base};
   const int nt[4] = {n.x, n.y, n.z, n.w};
   const int nh[4] = {h.x, h.y, h.z, h.w};
@@ -259,12 +270,7 @@ __device__ __forceinline__ void proj_acc4_stream(const ProjArgs& a, bool valid, 
   if (__any_sync(0xFFFFFFFFu, direct != 0)) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      if ((direct >> j) & 1u) {
-        const int key = ins[j] * HB + ((hot >> j) & 1u ? a.H + 1 : nh[j]);
-        atomicAdd(cnt + key, 1u);
-        atomicAdd(slo + key, (uint32_t)nt[j] & 0xFFFu);
-        atomicAdd(shi + key, (uint32_t)nt[j] >> 12);
-      }
+      if ((direct >> j) & 1u) bin_add(a, w, ins[j], (hot >> j) & 1u ? a.H + 1 : nh[j], 1u, (uint32_t)nt[j], cnt, slo, shi);
     }
   }
   // one ballot + REDUX round per distinct lane instance (one for an instance-grouped batch)
@@ -277,7 +283,7 @@ __device__ __forceinline__ void proj_acc4_stream(const ProjArgs& a, bool valid, 
     const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, mine ? lc : 0u);
     const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, mine ? ls : 0u);   // <= 128 * 2^17
     if (ki != acc.inst) {
-      hot_acc_push(acc, HB, a.H, cnt, slo, shi);
+      hot_acc_push(a, w, acc, cnt, slo, shi);
       acc.inst = ki;
     }
     acc.c += wc;
@@ -286,123 +292,133 @@ __device__ __forceinline__ void proj_acc4_stream(const ProjArgs& a, bool valid, 
   }
 }
 
-__global__ void __launch_bounds__(kStreamThreads, 2) project_stream_kernel(const ProjArgs a) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  const int nb = a.n_inst * (a.H + 2);
-  int4* ring = reinterpret_cast<int4*>(sm);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)kStreamStages * kStreamStageBytes);
-  uint64_t* empty = full + kStreamStages;
-  uint32_t* scnt = reinterpret_cast<uint32_t*>(empty + kStreamStages);
-  uint32_t* slo = scnt + nb;
-  uint32_t* shi = slo + nb;
-  __shared__ int s_last;
+// Each CTA adds its window bins (split 32-bit sums) into the 64-bit global workspace.
+__device__ __forceinline__ void window_merge(const ProjArgs& a, const BinWin& w, const uint32_t* scnt,
+                                             const uint32_t* slo, const uint32_t* shi) {
+  const int nbw = w.wn * w.HB, wofs = w.wbase * w.HB;
+  for (int k = threadIdx.x; k < nbw; k += blockDim.x) {
+    const uint32_t c = scnt[k];
+    if (c) {
+      atomicAdd(a.ws_cnt + wofs + k, c);
+      atomicAdd(a.ws_sum + wofs + k, (unsigned long long)slo[k] + ((unsigned long long)shi[k] << 12));
+    }
+  }
+}
+
+// Finalize of the bandwidth form: one warp per instance straight from the (L2-resident) global
+// workspace -- the bins of an instance are two coalesced loads per lane, the suffix scan runs on
+// shuffles -- then the warp re-zeroes its instance's bins.  PDL: waits for the merging kernel.
+constexpr int kFinWarps = 8;
+__global__ void __launch_bounds__(kFinWarps * 32) project_finalize_kernel(const ProjArgs a) {
   __shared__ uint32_t sbeta[257];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+  for (int t = threadIdx.x; t <= a.H; t += blockDim.x) sbeta[t] = a.beta_q[t];
+  pdl_wait();
+  __syncthreads();
+  const int HB = a.H + 2;
+  const int i0 = blockIdx.x * kFinWarps;
+  ProjArgs ab = a;
+  ab.n_inst = a.n_inst - i0 < kFinWarps ? a.n_inst - i0 : kFinWarps;
+  ab.L = a.L + (int64_t)i0 * (a.H + 1);
+  ab.W = a.W ? a.W + i0 : nullptr;
+  ab.peak = a.peak ? a.peak + i0 : nullptr;
+  ab.growth = a.growth ? a.growth + i0 : nullptr;
+  ab.count = a.count ? a.count + i0 : nullptr;
+  const int64_t o = (int64_t)i0 * HB;
+  proj_finalize(ab, a.ws_cnt + o, a.ws_sum + o, sbeta, warp, kFinWarps);
+  __syncthreads();
+  if (warp < ab.n_inst) {
+    for (int b = lane; b < HB; b += 32) {
+      a.ws_cnt[o + (int64_t)warp * HB + b] = 0;
+      a.ws_sum[o + (int64_t)warp * HB + b] = 0;
+    }
+  }
+}
+
+// Bandwidth kernel: the three arrays are read with ld.global.nc int4 loads, software-pipelined
+// two iterations deep (the next iteration's 3 x 16 B per lane are in flight while the current
+// ones are aggregated), one int4 of each array (4 requests) per lane per iteration.
+constexpr int kLdgThreads = 512;
+__global__ void __launch_bounds__(kLdgThreads, 2) project_ldg_kernel(const ProjArgs a, const int win_n) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int HB = a.H + 2;
+  const int nbw = win_n * HB;
+  uint32_t* scnt = reinterpret_cast<uint32_t*>(sm);
+  uint32_t* slo = scnt + nbw;
+  uint32_t* shi = slo + nbw;
+  __shared__ int s_wbase;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = threadIdx.x; k < nbw; k += blockDim.x) {
     scnt[k] = 0;
     slo[k] = 0;
     shi[k] = 0;
   }
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < kStreamStages; ++st) {
-      mbar_init(&full[st], 1);
-      mbar_init(&empty[st], kStreamWarps);
-    }
-    fence_barrier_init();
-  }
-  pdl_wait();   // inputs may come from the previous kernel (PDL launch)
-  for (int t = threadIdx.x; t <= a.H; t += blockDim.x) sbeta[t] = a.beta_q[t];
-  __syncthreads();   // zeroed bins, barriers and beta visible
-
   const int64_t nvec = a.R / 4;
   const int64_t per = (nvec + gridDim.x - 1) / gridDim.x;
   const int64_t v_beg = (int64_t)blockIdx.x * per;
   const int64_t v_end = v_beg + per < nvec ? v_beg + per : nvec;
-  const int64_t nchunks = v_end > v_beg ? (v_end - v_beg + kStreamVec - 1) / kStreamVec : 0;
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    int wb = 0;
+    if (win_n < a.n_inst && v_beg < v_end) {
+      wb = __ldg(a.inst + v_beg * 4) - a.inst_base;
+      wb = wb > a.n_inst - win_n ? a.n_inst - win_n : wb;
+      wb = wb < 0 ? 0 : wb;
+    }
+    s_wbase = wb;
+  }
+  __syncthreads();
+  const BinWin w{s_wbase, win_n, HB};
+  const int4* vi = reinterpret_cast<const int4*>(a.inst);
+  const int4* vn = reinterpret_cast<const int4*>(a.n_tok);
+  const int4* vh = reinterpret_cast<const int4*>(a.n_hat);
+  const int64_t stride = (int64_t)kLdgThreads;   // vectors per CTA sweep (16 warps x 32 lanes)
   uint32_t errbits = 0;
   HotAcc acc;
-  if (warp == kStreamWarps) {
-    // ---------------- producer: one thread, bulk copies into the ring ----------------
-    if (lane == 0) {
-      const int4* src[3] = {reinterpret_cast<const int4*>(a.inst), reinterpret_cast<const int4*>(a.n_tok),
-                            reinterpret_cast<const int4*>(a.n_hat)};
-      for (int64_t c = 0; c < nchunks; ++c) {
-        const int st = (int)(c % kStreamStages);
-        const uint32_t ph = (uint32_t)(c / kStreamStages) & 1u;
-        mbar_wait(&empty[st], ph ^ 1u);
-        const int64_t v0 = v_beg + c * kStreamVec;
-        const int nv = (int)(v_end - v0 < kStreamVec ? v_end - v0 : kStreamVec);
-        const uint32_t bytes = (uint32_t)nv * 16u;
-        mbar_arrive_expect_tx(&full[st], 3u * bytes);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) bulk_g2s(ring + ((size_t)st * 3 + k) * kStreamVec, src[k] + v0, bytes, &full[st]);
-      }
-    }
-  } else {
-    // ---------------- consumers: one int4 of each array per lane per stage ----------------
-    const int j = warp * 32 + lane;
-    const int nch = (int)nchunks;
-    const int last_nv = (int)(v_end - v_beg - (int64_t)(nch - 1) * kStreamVec);   // vectors in the last chunk
-    int st = 0;
-    uint32_t ph = 0;
-    for (int c = 0; c < nch; ++c) {
-      mbar_wait(&full[st], ph);
-      const bool valid = c + 1 < nch || j < last_nv;
-      // (lanes past the last chunk's end read stale ring data, masked by `valid`)
-      const int4* sx = ring + (size_t)st * 3 * kStreamVec + j;
-      const int4 x = sx[0], n = sx[kStreamVec], h = sx[2 * kStreamVec];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);   // this warp's reads of the stage are done
-      proj_acc4_stream(a, valid, x, n, h, scnt, slo, shi, errbits, acc);
-      if (++st == kStreamStages) {
-        st = 0;
-        ph ^= 1u;
-      }
-    }
-    // the R % 4 trailing requests (CTA 0, warp 0), one per lane
-    if (blockIdx.x == 0 && warp == 0) {
-      const int64_t r = nvec * 4 + lane;
-      if (r < a.R) {
-        const int i = a.inst[r] - a.inst_base, nt = a.n_tok[r], nh = a.n_hat[r];
-        const bool in_rng = (unsigned)i < (unsigned)a.n_inst, nt_ok = (unsigned)(nt - 1) < (1u << 17), nh_ok = nh >= 0;
-        errbits |= (in_rng ? 0u : 1u) | (nt_ok ? 0u : 2u) | (nh_ok ? 0u : 4u);
-        if (in_rng && nt_ok && nh_ok) {
-          const int key = i * (a.H + 2) + (nh > a.H + 1 ? a.H + 1 : nh);
-          atomicAdd(scnt + key, 1u);
-          atomicAdd(slo + key, (uint32_t)nt & 0xFFFu);
-          atomicAdd(shi + key, (uint32_t)nt >> 12);
-        }
-      }
-    }
-    hot_acc_push(acc, a.H + 2, a.H, scnt, slo, shi);
+  const int4 z = make_int4(0, 0, 0, 0);
+  int64_t ga = v_beg + threadIdx.x, gb = ga + stride;
+  int4 xa = z, na = z, ha = z, xb = z, nb = z, hb = z;
+  if (ga < v_end) {
+    xa = ld_stream_int4(vi + ga);
+    na = ld_stream_int4(vn + ga);
+    ha = ld_stream_int4(vh + ga);
   }
+  if (gb < v_end) {
+    xb = ld_stream_int4(vi + gb);
+    nb = ld_stream_int4(vn + gb);
+    hb = ld_stream_int4(vh + gb);
+  }
+  // warp-uniform trip conditions: the warp's first vector of the sweep is inside the slice
+  for (int64_t base = v_beg + warp * 32; base < v_end; base += 2 * stride) {
+    proj_acc4_stream(a, ga < v_end, xa, na, ha, w, scnt, slo, shi, errbits, acc);
+    ga += 2 * stride;
+    if (ga < v_end) {
+      xa = ld_stream_int4(vi + ga);
+      na = ld_stream_int4(vn + ga);
+      ha = ld_stream_int4(vh + ga);
+    }
+    if (base + stride < v_end) proj_acc4_stream(a, gb < v_end, xb, nb, hb, w, scnt, slo, shi, errbits, acc);
+    gb += 2 * stride;
+    if (gb < v_end) {
+      xb = ld_stream_int4(vi + gb);
+      nb = ld_stream_int4(vn + gb);
+      hb = ld_stream_int4(vh + gb);
+    }
+  }
+  if (blockIdx.x == 0 && warp == 0) {   // the R % 4 trailing requests, one per lane
+    const int64_t r = nvec * 4 + lane;
+    if (r < a.R) {
+      const int i = a.inst[r] - a.inst_base, nt = a.n_tok[r], nh = a.n_hat[r];
+      const bool in_rng = (unsigned)i < (unsigned)a.n_inst, nt_ok = (unsigned)(nt - 1) < (1u << 17), nh_ok = nh >= 0;
+      errbits |= (in_rng ? 0u : 1u) | (nt_ok ? 0u : 2u) | (nh_ok ? 0u : 4u);
+      if (in_rng && nt_ok && nh_ok) bin_add(a, w, i, nh > a.H + 1 ? a.H + 1 : nh, 1u, (uint32_t)nt, scnt, slo, shi);
+    }
+  }
+  hot_acc_push(a, w, acc, scnt, slo, shi);
   if (errbits && a.err) atomicOr(a.err, (int)errbits);
   __syncthreads();
-  for (int k = threadIdx.x; k < nb; k += blockDim.x) {   // merge into the 64-bit global workspace
-    const uint32_t c = scnt[k];
-    if (c) {
-      atomicAdd(a.ws_cnt + k, c);
-      atomicAdd(a.ws_sum + k, (unsigned long long)slo[k] + ((unsigned long long)shi[k] << 12));
-    }
-  }
-  // grid-wide arrival; the last CTA finalises from the global workspace and re-zeroes it
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(a.ws_arrive, 1u) == gridDim.x - 1) ? 1 : 0;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  uint32_t* fc = reinterpret_cast<uint32_t*>(sm);                       // the ring is free now
-  unsigned long long* fs = reinterpret_cast<unsigned long long*>(sm + ((size_t)nb * 4 + 15) / 16 * 16);
-  for (int k = threadIdx.x; k < nb; k += blockDim.x) {
-    fc[k] = __ldcg(a.ws_cnt + k);
-    fs[k] = __ldcg(a.ws_sum + k);
-    a.ws_cnt[k] = 0;
-    a.ws_sum[k] = 0;
-  }
-  __syncthreads();
-  proj_finalize(a, fc, fs, sbeta, warp, blockDim.x >> 5);
-  if (threadIdx.x == 0) *a.ws_arrive = 0;
+  window_merge(a, w, scnt, slo, shi);
+  pdl_launch_dependents();   // after this CTA's merge: the finalize kernel's wait covers it
 }
 
 size_t project_workspace_bytes(int n_inst, int H) {
@@ -448,21 +464,16 @@ cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_
   ProjArgs a = make_proj_args(R, n_inst, inst_base, H, inst, n_tok, n_hat, beta_q, L, W, peak, growth, count,
                               workspace, err_flag);
   const size_t nb = (size_t)n_inst * (size_t)(H + 2);
-  if (workspace && a.vec_ok && (int64_t)R >= kStreamMinRows && nb <= (size_t)kStreamMaxBins &&
-      (int64_t)R <= kStreamMaxPerCta * g_num_sms) {
-    const size_t smem = kStreamRingBytes + nb * 12;
-    static int attr_bytes = 0;
-    if ((int)smem > attr_bytes) {
-      cudaError_t e = cudaFuncSetAttribute(project_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      attr_bytes = (int)smem;
-    }
-    // two CTAs per SM (2 x 72 KB in flight, 32 consumer warps) when both fit in shared memory
-    const int grid = g_num_sms * (smem <= (size_t)113 * 1024 ? 2 : 1);
+  if (workspace && a.vec_ok && (int64_t)R >= kStreamMinRows && (int64_t)R <= kStreamMaxPerCta * 2 * g_num_sms &&
+      H + 2 <= kStreamWinBins) {
+    // shared-memory window: every instance when the histogram fits, else a window of instances
+    const int win_n = nb <= (size_t)kStreamWinBins ? n_inst : kStreamWinBins / (H + 2);
+    const size_t smem = (size_t)win_n * (H + 2) * 12;
+    const int grid = g_num_sms * 2;   // two 512-thread CTAs per SM
     if (grid_out) *grid_out = grid;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid, 1, 1);
-    cfg.blockDim = dim3(kStreamThreads, 1, 1);
+    cfg.blockDim = dim3(kLdgThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
@@ -470,7 +481,12 @@ cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, project_stream_kernel, a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, project_ldg_kernel, a, win_n);
+    if (e != cudaSuccess) return e;
+    cfg.gridDim = dim3((n_inst + kFinWarps - 1) / kFinWarps, 1, 1);
+    cfg.blockDim = dim3(kFinWarps * 32, 1, 1);
+    cfg.dynamicSmemBytes = 0;
+    return cudaLaunchKernelEx(&cfg, project_finalize_kernel, a);
   }
   const bool smem_bins = nb <= (size_t)kProjMaxSmemBins;
   int grid = 1;

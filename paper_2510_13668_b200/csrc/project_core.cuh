@@ -144,10 +144,50 @@ __device__ __forceinline__ void proj_accumulate4(const ProjArgs& a, bool valid, 
 // shuffle scan plus a carry, then L[t] = SS[t+1] + t*CC[t+1] for t = 1..H, and warp reductions
 // of L0, count, growth, W = sum beta_t L[t], peak.  beta comes from shared memory.
 // `warp` / `nwarps`: this warp's index among the warps taking part (whole warps only).
+// Many instances (n_inst > 2 * nwarps): one LANE per instance instead, a sequential suffix sum
+// from the top bin (the warp form costs a dependent chain of shuffles per instance, ~1.5 us, and a
+// warp walks n_inst / nwarps instances one after the other).
+__device__ __forceinline__ void proj_finalize_lanes(const ProjArgs& a, const uint32_t* cnt,
+                                                    const unsigned long long* sum, const uint32_t* sbeta, int tid,
+                                                    int nthreads) {
+  const int HB = a.H + 2;
+  for (int i = tid; i < a.n_inst; i += nthreads) {
+    const uint32_t* c = cnt + (int64_t)i * HB;
+    const unsigned long long* s = sum + (int64_t)i * HB;
+    int64_t* Li = a.L + (int64_t)i * (a.H + 1);
+    int64_t ss = 0, cc = 0, grow = 0, w = 0, peak = 0;
+    for (int b = HB - 1; b >= 1; --b) {   // b = H+1 .. 1: SS[b], CC[b] suffix sums
+      const int64_t cv = (int64_t)c[b];
+      ss += (int64_t)s[b];
+      cc += cv;
+      grow += cv * (b < a.H ? b : a.H);
+      if (b >= 2) {   // t = b - 1 in [1, H]: L[t] = SS[t+1] + t * CC[t+1]
+        const int t = b - 1;
+        const int64_t lt = ss + (int64_t)t * cc;
+        Li[t] = lt;
+        w += (int64_t)sbeta[t] * lt;
+        peak = lt > peak ? lt : peak;
+      }
+    }
+    ss += (int64_t)s[0];
+    cc += (int64_t)c[0];
+    Li[0] = ss;
+    if (a.W) a.W[i] = w;
+    if (a.peak) a.peak[i] = ss > peak ? ss : peak;
+    if (a.growth) a.growth[i] = grow;
+    if (a.count) a.count[i] = (int32_t)cc;
+    if (cc > 65536 && a.err) atomicOr(a.err, 8);
+  }
+}
+
 __device__ __forceinline__ void proj_finalize(const ProjArgs& a, const uint32_t* cnt, const unsigned long long* sum,
                               const uint32_t* sbeta, int warp, int nwarps) {
   const int HB = a.H + 2;
   const int lane = threadIdx.x & 31;
+  if (a.n_inst > 2 * nwarps) {
+    proj_finalize_lanes(a, cnt, sum, sbeta, warp * 32 + lane, nwarps * 32);
+    return;
+  }
   for (int i = warp; i < a.n_inst; i += nwarps) {
     __syncwarp();
     const uint32_t* c = cnt + (int64_t)i * HB;

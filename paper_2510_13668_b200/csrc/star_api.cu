@@ -158,7 +158,7 @@ static cudaError_t launch_pair_gemm(const CUtensorMap& a, const CUtensorMap& b, 
     attr = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((m_tiles + 1) & ~1, p.N / 256, 1);
+  cfg.gridDim = dim3((m_tiles + 1) & ~1, p.N / 256, p.splits);   // splits: K ranges (one wave, <= SMs)
   cfg.blockDim = dim3(192, 1, 1);
   cfg.dynamicSmemBytes = PairSmem<256>::BYTES;
   cfg.stream = st;
@@ -280,6 +280,7 @@ struct star_predictor {
   float* head_ws = nullptr;   // split-K head partial dots
   float* ws3 = nullptr;       // fused tail: layer-3 partials [m_tiles][16][64][128]
   int* tail_cnt = nullptr;    // fused tail: per (m-tile, split) arrival counters
+  int* l1_cnt = nullptr;      // layer-1 CTA-pair split-K: per CTA tile arrival / done counters
   uint64_t* tl = nullptr;     // diagnostics: fused-tail phase timeline [ctas][16]
   int tl_ctas = 0;            // CTAs of the most recent timed tail launch
   // refresh cadence (NEXT-1) scratch: compacted rows and their hidden states
@@ -318,6 +319,7 @@ static void free_pred(star_predictor* p) {
   cudaFree(p->head_ws);
   cudaFree(p->ws3);
   cudaFree(p->tail_cnt);
+  cudaFree(p->l1_cnt);
   cudaFree(p->tl);
   cudaFree(p->tl_l1);
   cudaFree(p->r_idx);
@@ -373,6 +375,7 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
   ok &= alloc(reinterpret_cast<void**>(&p->head_ws), (size_t)g_num_sms * 128 * 4);
   ok &= alloc(reinterpret_cast<void**>(&p->ws3), (size_t)((max_rows + 127) / 128) * 16 * 64 * 128 * 4);
   ok &= alloc(reinterpret_cast<void**>(&p->tail_cnt), (size_t)((max_rows + 127) / 128) * 8 * sizeof(int));
+  ok &= alloc(reinterpret_cast<void**>(&p->l1_cnt), (size_t)2 * g_num_sms * sizeof(int));
   if (!f32) {
     ok &= alloc(reinterpret_cast<void**>(&p->r_idx), (size_t)max_rows * 4);
     ok &= alloc(reinterpret_cast<void**>(&p->r_pos), (size_t)max_rows * 4);
@@ -395,6 +398,7 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
     return fail(STAR_ENOMEM, "device allocation failed");
   }
   cudaError_t e = cudaMemsetAsync(p->tail_cnt, 0, (size_t)((max_rows + 127) / 128) * 8 * sizeof(int), stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p->l1_cnt, 0, (size_t)2 * g_num_sms * sizeof(int), stream);
   if (e == cudaSuccess && f32) {
     tf32x3_split_kernel<<<1024, 256, 0, stream>>>(static_cast<const float*>(W1), d, m1, d, p->W1s, 1);
     tf32x3_split_kernel<<<256, 256, 0, stream>>>(static_cast<const float*>(W2), m1, m2, m1, p->W2s, 1);
@@ -538,20 +542,38 @@ static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, 
     g.out = p->Z1;
     g.ld_out = (int64_t)p->m1 * kx;
     g.bias = p->b1;
-    // CTA pairs when the unsplit pair grid already fills most of the SMs
-    const bool pair = !f32 && p->bn1 == 256 && ((m_tiles + 1) & ~1) * (p->m1 / 256) >= (g_num_sms * 5) / 8;
+    // CTA pairs (bf16): split K over the pairs until one wave of <= SMs CTAs is filled
+    int pair_splits = 0;
+    if (!f32 && p->bn1 == 256) {
+      const int pairs = ((m_tiles + 1) / 2) * (p->m1 / 256);
+      pair_splits = 1;
+      // split-K pairs only for one pair row (129..256 requests: measured 12.5 us vs 13.2 us for the
+      // 1-CTA split-4 kernel at d = 4096); at 257..1024 rows the 1-CTA split-K kernel is faster
+      // (tools/gemm_bench.cu), at <= 128 rows as well (no padding rows)
+      if (m_tiles == 2)
+        while (pair_splits < 8 && pairs * pair_splits * 2 * 2 <= g_num_sms && num_kb / (pair_splits * 2) >= 4)
+          pair_splits *= 2;
+      if (pairs * pair_splits * 2 < (g_num_sms * 5) / 8) pair_splits = 0;   // too few CTAs either way
+    }
+    const bool pair = pair_splits > 0;
     if (pair) {
-      g.splits = 1;
-      g.kb_per_split = num_kb;
+      g.splits = pair_splits;
+      g.kb_per_split = (num_kb + pair_splits - 1) / pair_splits;
       g.tma_store = 1;
+      g.l1_cnt = p->l1_cnt;
       g.tl = p->tl_l1;
-      p->tl_l1_ctas = ((m_tiles + 1) & ~1) * (p->m1 / 256);
+      p->tl_l1_ctas = ((m_tiles + 1) & ~1) * (p->m1 / 256) * pair_splits;
+    }
+    if (!pair) {   // diagnostics timeline of the 1-CTA layer-1 kernel (rows: m x n x split CTAs)
+      g.tl = p->tl_l1;
+      p->tl_l1_ctas = m_tiles * (p->m1 / p->bn1) * g.splits;
     }
     if (p->ev0) record_timing_event(p->ev0, st);
     cudaError_t e = pair ? launch_pair_gemm(p->tmA1, p->tmB1p, tmC1, g, m_tiles, st)
                          : launch_gemm(p->bn1, f32, p->tmA1, p->tmB1, tmC1, g, m_tiles, st);
     if (e != cudaSuccess) return cuda_fail(e, "layer-1 GEMM launch");
     if (p->ev1) record_timing_event(p->ev1, st);
+    g.tl = nullptr;
   }
   // ---- fused tail: layer 2 -> layer 3 -> head -> quantizer [-> projection] ----
   const int n2 = p->m2 / 256;

@@ -101,7 +101,11 @@ class Step:
 
     def __init__(self, predictor: _lib.Predictor, params: _lib.PlanParams, n_inst: int, r_cap: int,
                  rank: int = 0, world: int = 1, group=None, device: Optional[torch.device] = None,
-                 max_ctx_len: int = _lib.L_CTX, refresh_k: Optional[int] = None):
+                 max_ctx_len: int = _lib.L_CTX, refresh_k: Optional[int] = None,
+                 gathered: Optional[torch.Tensor] = None):
+        """gathered: (single-GPU measurement of one rank of a W-rank job) a caller-owned buffer of
+        world * nbytes holding the OTHER ranks' records as the all-gather would deliver them; this
+        rank's record is written in place at slot `rank` and no collective is issued."""
         if n_inst % world:
             raise ValueError(f"n_inst={n_inst} must be divisible by world={world}")
         self.pred, self.params = predictor, params
@@ -112,9 +116,17 @@ class Step:
         self.max_ctx_len = max_ctx_len
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         self.layout = RecordLayout(self.n_loc, self.H, r_cap)
-        self.send = torch.zeros(self.layout.nbytes, dtype=torch.uint8, device=self.device)
-        self.recv = (torch.zeros(world * self.layout.nbytes, dtype=torch.uint8, device=self.device)
-                     if world > 1 else self.send)
+        self.emulated = gathered is not None
+        if self.emulated:
+            nb = self.layout.nbytes
+            if gathered.dtype != torch.uint8 or gathered.numel() != world * nb:
+                raise ValueError(f"gathered must be a uint8 buffer of world*nbytes = {world * nb}")
+            self.recv = gathered
+            self.send = gathered[rank * nb:(rank + 1) * nb]
+        else:
+            self.send = torch.zeros(self.layout.nbytes, dtype=torch.uint8, device=self.device)
+            self.recv = (torch.zeros(world * self.layout.nbytes, dtype=torch.uint8, device=self.device)
+                         if world > 1 else self.send)
         self.v = self.layout.views(self.send)
         self.seg = self.layout.segments(self.recv.data_ptr(), world)
         self.ws = torch.zeros(_lib.project_workspace_bytes(self.n_loc, self.H), dtype=torch.uint8, device=self.device)
@@ -172,7 +184,7 @@ class Step:
             _lib.project_instance_load(v["inst"], v["n_tok"], v["n_hat"], self.n_loc, self.H, self.params.beta_q,
                                        inst_base=self.rank * self.n_loc, out=self.proj_out, workspace=self.ws,
                                        err_flag=self.err, R=R, stream=stream)
-            if self.world > 1:
+            if self.world > 1 and not self.emulated:
                 exchange(self.send, self.recv, self.group)
             _lib.plan_reschedule_segmented(self.params, self.seg, self.moves, self.n_moves, self.err, stream=stream)
             return self.moves, self.n_moves
@@ -188,7 +200,7 @@ class Step:
                                      self.params.beta_q, self.ws, inst_base=self.rank * self.n_loc,
                                      max_ctx_len=self.max_ctx_len, n_hat=v["n_hat"][:max(R, 1)],
                                      out=self.proj_out, err_flag=self.err, want_y=False, stream=stream)
-        if self.world > 1:
+        if self.world > 1 and not self.emulated:
             exchange(self.send, self.recv, self.group)
         _lib.plan_reschedule_segmented(self.params, self.seg, self.moves, self.n_moves, self.err, stream=stream)
         return self.moves, self.n_moves

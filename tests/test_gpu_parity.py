@@ -85,6 +85,38 @@ def test_projection_bitexact(star, oracle_mod, seed, n, R, H):
     assert int(ws.sum().item()) == 0   # workspace left zeroed
 
 
+@pytest.mark.parametrize("seed,n,R,H,grouped,base", [(20, 256, (1 << 20) + 3, 50, True, 0),
+                                                    (21, 200, 300_001, 50, False, 0),
+                                                    (22, 96, 500_000, 50, True, 1000),
+                                                    (23, 40, 400_002, 256, True, 0),
+                                                    (24, 64, 262_144, 50, False, 0)])
+def test_projection_stream_window(star, oracle_mod, seed, n, R, H, grouped, base):
+    """Bandwidth form (R >= 2^18): shared-memory bins over a window of instances, requests of
+    instances outside the window added to the global workspace; grouped and interleaved orders,
+    a nonzero inst_base, H = 256 -- bit-exact against the oracle."""
+    g = datagen.rng(seed)
+    snap = datagen.make_snapshot(seed, 8, 256)
+    idx = g.integers(0, snap.R, R)
+    inst = g.integers(0, n, R).astype(np.int32)
+    if grouped:
+        inst = np.sort(inst).astype(np.int32)
+    n_tok, n_hat = snap.n_tok[idx], snap.true_rem[idx].astype(np.int32)
+    n_hat = np.where(g.random(R) < 0.2, g.integers(0, H + 3, R), n_hat).astype(np.int32)
+    beta = datagen.beta_schedule_q16(H)
+    ref = oracle_mod.project(inst, n_tok, n_hat, n, H, beta)
+    ws = torch.zeros(star.project_workspace_bytes(n, H), dtype=torch.uint8, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for _ in range(2):   # the workspace is left zeroed and reused
+        out = star.project_instance_load(_dev(inst + base), _dev(n_tok), _dev(n_hat), n, H,
+                                         _dev(beta.astype(np.int32)), inst_base=base, workspace=ws, err_flag=err)
+        torch.cuda.synchronize()
+        assert err.item() == 0
+        assert np.array_equal(out.L.cpu().numpy(), ref["L"])
+        for k in ("W", "peak", "growth", "count"):
+            assert np.array_equal(getattr(out, k).cpu().numpy(), ref[k]), k
+    assert int(ws.sum().item()) == 0
+
+
 def test_projection_inst_base_and_errors(star, oracle_mod):
     inst = np.array([4, 5, 4, 9, 5], np.int32)
     n_tok = np.array([3, 4, 5, 6, 0], np.int32)   # inst 9 out of range, N=0 invalid
@@ -498,4 +530,54 @@ def test_step_world1_fused_plan_equals_oracle(star, oracle_mod, cfg, R, seed):
     st.run(hd)
     torch.cuda.synchronize()
     assert st.result() == got
+    pred.close()
+
+
+# ============================================================================ W-rank step, one GPU
+@pytest.mark.parametrize("cfg,world,r_per,seed", [("TGT", 8, 512, 0), ("C2", 4, 256, 1), ("C4", 2, 300, 2)])
+def test_step_gathered_ranks_plan_equals_oracle(star, oracle_mod, cfg, world, r_per, seed):
+    """Every rank of a W-rank job on one GPU (Step(gathered=...): the ranks' records written into
+    one shared gathered buffer, as the all-gather delivers them): each rank's fused projection of
+    its own N_hat equals the oracle's, and every rank's plan over the gathered records equals the
+    oracle plan on the concatenated state, bit for bit."""
+    from paper_2510_13668_b200.step import RecordLayout, Step, split_snapshot_by_rank
+    c = datagen.CONFIGS[cfg]
+    n = c["n_inst"]
+    snap = datagen.make_snapshot(seed, n, r_per, skewed=c.get("skewed", False), pinned_frac=0.05)
+    pw = datagen.make_predictor_weights(seed, c["d"], c["dtype"])
+    tdt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
+    W, b = _weights_dev(pw, False)
+    params_h = datagen.make_plan_params(snap, H=50, mem_factor=c.get("mem_factor", 1.10),
+                                        max_moves=max(c["max_moves"], 2))
+    params = star.PlanParams.from_host(params_h)
+    idxs = [split_snapshot_by_rank(snap.inst, n, world, k) for k in range(world)]
+    r_cap = max(len(i) for i in idxs)
+    pred = star.Predictor(*W, *b, max_rows=r_cap)
+    buf = torch.zeros(world * RecordLayout(n // world, 50, r_cap).nbytes, dtype=torch.uint8, device="cuda")
+    steps = []
+    for k, idx in enumerate(idxs):
+        scale = np.maximum(snap.true_rem[idx], 1).astype(np.float32) / 60.0
+        h = datagen.make_hidden(seed * 100 + k, len(idx), c["d"], c["dtype"], scale=scale)
+        st = Step(pred, params, n, r_cap=r_cap, rank=k, world=world, gathered=buf)
+        st.load_requests(*(torch.from_numpy(np.ascontiguousarray(a[idx])) for a in (snap.req_id, snap.inst,
+                                                                                      snap.n_tok)),
+                         pinned=torch.from_numpy(np.ascontiguousarray(snap.pinned[idx])))
+        st.run(_dev(h, tdt))
+        steps.append(st)
+    torch.cuda.synchronize()
+    order = np.concatenate(idxs)
+    nh = np.concatenate([st.v["n_hat"][:len(i)].cpu().numpy() for st, i in zip(steps, idxs)])
+    ids, inst, n_tok, pin = (a[order] for a in (snap.req_id, snap.inst, snap.n_tok, snap.pinned))
+    ref_p = oracle_mod.project(inst, n_tok, nh, n, 50, params_h.beta_q)
+    for k, st in enumerate(steps):
+        assert st.err.item() == 0
+        loc = slice(k * (n // world), (k + 1) * (n // world))
+        assert np.array_equal(st.v["L"].cpu().numpy(), ref_p["L"][loc])
+    ref = oracle_mod.plan(params_h, ref_p["L"], ids, inst, n_tok, nh, pin)
+    # the last rank ran with every record in place; re-plan on the final buffer from every rank
+    for st in steps:
+        moves, nm = star.plan_reschedule_segmented(params, st.seg)
+        torch.cuda.synchronize()
+        assert star.decode_moves(moves, nm) == ref
+    assert steps[-1].result() == ref
     pred.close()

@@ -140,6 +140,38 @@ int main(int argc, char** argv) {
     const float w = time_batch(split, nrep, flush, 0), c = time_batch(split, 1, flush, fb);
     printf("M=%d K=%d N=%d  1-CTA split %d: %.2f us warm (%.0f TF/s), %.2f us cold\n", M, K, N, S, w, flop / w / 1e6, c);
   }
+  // ---- CTA-pair kernel with split-K (arrival counters in global memory) ----
+  int* cnt;
+  cudaMalloc(&cnt, 4096 * sizeof(int));
+  cudaMemset(cnt, 0, 4096 * sizeof(int));
+  for (int S : {2, 4, 8}) {
+    const int pairs = ((m_tiles + 1) / 2) * (N / 256);
+    if (pairs * S > 74 || (K / 64) / S < 2) continue;
+    GemmArgs gs = g;
+    gs.splits = S;
+    gs.kb_per_split = (K / 64 + S - 1) / S;
+    gs.ws = ws;
+    gs.l1_cnt = cnt;
+    auto psplit = [&]() {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3((m_tiles + 1) & ~1, N / 256, S);
+      cfg.blockDim = dim3(192, 1, 1);
+      cfg.dynamicSmemBytes = PairSmem<256>::BYTES;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      cudaLaunchKernelEx(&cfg, umma_pair_gemm_kernel<256>, tA, tB128, tC, gs);
+    };
+    const float w = time_batch(psplit, nrep, flush, 0), c = time_batch(psplit, 1, flush, fb);
+    printf("M=%d K=%d N=%d  pair split %d: %.2f us warm (%.0f TF/s), %.2f us cold  [%s]\n", M, K, N, S, w,
+           flop / w / 1e6, c, cudaGetErrorString(cudaDeviceSynchronize()));
+  }
   float tp_w = time_batch(pair, nrep, flush, 0), tp_c = time_batch(pair, 1, flush, fb);
   float ts_w = time_batch(single, nrep, flush, 0), ts_c = time_batch(single, 1, flush, fb);
   printf("M=%d K=%d N=%d  pair: %.2f us warm (%.0f TF/s), %.2f us cold   1-CTA: %.2f us warm (%.0f TF/s), %.2f us cold\n",

@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import datagen  # noqa: E402
 import paper_2510_13668_b200 as star  # noqa: E402
 
-R = 1 << 24
+R = 1 << (int(sys.argv[4]) if len(sys.argv) > 4 else 24)
 n_per = int(sys.argv[1]) if len(sys.argv) > 1 else 32   # instance multiplier: n_inst = 8 * n_per
 snap = datagen.make_snapshot(0, 8, 256)
 reps = R // snap.R
@@ -32,9 +32,12 @@ for _ in range(3):
     fn()
 torch.cuda.synchronize()
 ts = []
-for _ in range(10):
+for _ in range(10):   # 10 launches back to back per span: device time (inputs beyond L2 stream from HBM)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(); fn(); e1.record(); e1.synchronize()
-    ts.append(e0.elapsed_time(e1))
+    e0.record()
+    for _ in range(10):
+        fn()
+    e1.record(); e1.synchronize()
+    ts.append(e0.elapsed_time(e1) / 10)
 t = float(np.median(ts)) * 1e-3
-print(f"n_inst={n} {sys.argv[2:] }: {t*1e6:.1f} us, {12*R/t/1e9:.0f} GB/s, err={err.item()}")
+print(f"n_inst={n} R=2^{R.bit_length()-1} {sys.argv[2:3]} {os.environ.get('STAR_PROJ_BULK', '0')}: {t*1e6:.1f} us, {12*R/t/1e9:.0f} GB/s, err={err.item()}")

@@ -40,7 +40,8 @@ if len(last):
           round((r[18] - r[16]) / 1e3, 2), "zeroed", round((r[19] - r[16]) / 1e3, 2), "end", round((r[14] - r[16]) / 1e3, 2),
           "| arrival at", round((r[16] - t0) / 1e3, 2))
 tl1 = pred.timeline(fetch=True, layer1=True).astype(np.int64)
-names1 = ["entry", "prologue", "prod pdl_wait", "mma kb0", "mma kb16", "mma kb32", "mma kb48", "", "", "mma done",
+names1 = ["entry", "prologue", "prod pdl_wait", "mma kb0", "mma kb16", "mma kb32", "mma kb48", "splitK published",
+          "splitK met", "mma done",
           "accum ready", "epilogue end", "exit sync"]
 t0 = tl1[:, 0].min()
 print(f"layer 1: ctas={tl1.shape[0]}")
@@ -51,6 +52,14 @@ for k, nm in enumerate(names1):
     v = v[v > 0] - t0
     if len(v):
         print(f"{k:2d} {nm:14s} min {v.min()/1e3:7.2f}  med {np.median(v)/1e3:7.2f}  max {v.max()/1e3:7.2f} us")
+print("same-CTA phase offsets from the CTA's own entry (robust to the per-GPC timer offset):")
+for k, nm in enumerate(names1):
+    if not nm or k == 0:
+        continue
+    ok = (tl1[:, k] > 0) & (tl1[:, 0] > 0)
+    if ok.any():
+        v = (tl1[ok, k] - tl1[ok, 0]) / 1e3
+        print(f"{k:2d} {nm:16s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f} us (n={ok.sum()})")
 print("per-CTA (us from own prologue), leader CTAs 0,2,64:")
 for cta in (0, 2, 64):
     r = tl1[cta].astype(np.int64)
