@@ -348,11 +348,32 @@ def tgt_rank_timing(star, Step, dev, flush, seed=0, reps=200, world=8):
         if i >= 10:
             ts.append(e0.elapsed_time(e1) * 1e3)
     n_moves = int(st.n_moves.item())
+    # stage split (event nodes between the stages: each costs ~2 us and blocks the PDL overlap, so
+    # the stages sum to more than the step)
+    es = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)]
+    v = st.v
+    gs = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gs):
+        if flush is not None:
+            flush.fill_(1.0)
+        es[0].record()
+        star.lenpred_forward_project(pred, h, v["n_tok"][:st.R], v["inst"][:st.R], st.n_loc, st.H, params.beta_q,
+                                     st.ws, inst_base=0, n_hat=v["n_hat"][:st.R], out=st.proj_out, err_flag=st.err,
+                                     want_y=False)
+        es[1].record()
+        star.plan_reschedule_segmented(params, st.seg, st.moves, st.n_moves, st.err)
+        es[2].record()
+    acc = np.zeros(2)
+    for _ in range(50):
+        gs.replay()
+        es[2].synchronize()
+        acc += [es[k].elapsed_time(es[k + 1]) * 1e3 / 50 for k in range(2)]
     pred.close()
     return {"workload": "TGT, one rank of W=8: 1 instance x 512 requests, d=4096 bf16; Alg. 1 over the 8 gathered "
                         "records (4096 requests)",
             "us_per_step_p50": round(float(np.median(ts)), 2), "us_per_step_p99": round(float(np.percentile(ts, 99)), 2),
             "target_us": 50.0, "launches_per_step": launches, "moves": n_moves,
+            "stage_us": {"predict+project": round(acc[0], 2), "plan_4096_gathered": round(acc[1], 2)},
             "l2": "flushed before every step" if flush is not None else "warm",
             "note": "one GPU: the other 7 ranks' records are pre-computed into the gathered buffer; the NCCL "
                     "all-gather (8 x %d B) is not in the timed span" % (buf.numel() // world)}

@@ -82,6 +82,8 @@ struct GemmSmem {
   static constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
   static constexpr uint32_t BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
   static_assert(STAGES * STAGE_BYTES >= 4u * (BN / 64 > 0 ? BN / 64 : 1) * 4096u, "epilogue staging fits");
+  // split-K: [0, 32 KB) epilogue staging, [32 KB, +(S-1) x OW x 512 B <= 7/8 x BN x 512 B) partner partials
+  static_assert(STAGES * STAGE_BYTES >= 32768u + (uint32_t)BN * 448u, "split-K partials fit");
 };
 
 // Fused epilogue on 16 consecutive columns [col0, col0+16) of one row.
@@ -161,6 +163,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* empty = full + S::STAGES;
   uint64_t* accum = empty + S::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* pbar = accum + 2;   // split-K: the partner partial blocks' bulk copies
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -190,6 +193,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(accum, 1);
+    mbar_init(pbar, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<S::TMEM_COLS>(tmem_slot);
@@ -272,6 +276,7 @@ __global__ void __launch_bounds__(192, 1)
                                                 __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
         }
       }
+      fence_proxy_async_global();   // the owners read these blocks with bulk copies
     }
   }
   if (tl && threadIdx.x == 64) tl[7] = globaltimer_ns();
@@ -281,6 +286,18 @@ __global__ void __launch_bounds__(192, 1)
   float head_acc = 0.0f;
   if (warp >= 2) {
     // ---------------- epilogue phase 2: reduce owned columns (fixed split order) + epilogue ----
+    if (splits > 1) {   // partner partials -> shared memory [32 KB, ...) (the ring is free now)
+      const uint32_t pblk = (uint32_t)OW * BM * 4u;
+      if (threadIdx.x == 64) {
+        fence_proxy_async_global();
+        mbar_arrive_expect_tx(pbar, (uint32_t)(splits - 1) * pblk);
+        for (int s = 0, k = 0; s < splits; ++s) {
+          if (s == split) continue;
+          bulk_g2s(smem + 32768 + (size_t)(k++) * pblk, wsb + (int64_t)(s * splits + split) * OW * BM, pblk, pbar);
+        }
+      }
+      mbar_wait(pbar, 0);
+    }
     uint8_t* stage_base = p.tma_store ? smem + (q * (OW / 64)) * 4096 : nullptr;
 #pragma unroll 1
     for (int c = 0; c < OW; c += 16) {
@@ -292,36 +309,23 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
       } else {
-        // every other split's partial of these 16 columns is loaded before any is summed (the
-        // loads overlap instead of paying one L2 round trip per split); the sum runs in the
-        // fixed split order 0..S-1
-        float4 pv[7][4];
-#pragma unroll
-        for (int k = 0; k < 7; ++k) {
-          if (k < splits - 1) {
-            const int s = k < split ? k : k + 1;
-            const float4* src =
-                reinterpret_cast<const float4*>(wsb + (int64_t)(s * splits + split) * OW * BM) + row_in_tile;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) pv[k][j] = __ldcg(src + (c / 4 + j) * BM);
-          }
-        }
+        // the S-1 partner partial blocks of the owned columns (OW x 128 fp32 each, contiguous)
+        // came into shared memory by bulk copy (one L2 round trip); sum in split order 0..S-1
+        const float* sP = reinterpret_cast<const float*>(smem + 32768);
         uint32_t v[16];
         tmem_ld_32x32b_x16(trow + (uint32_t)(own0 + c), v);
         tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 16; ++j) f[j] = 0.0f;
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          if (s >= splits) break;
+        for (int s = 0, k = 0; s < splits; ++s) {
           if (s == split) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) f[j] += __uint_as_float(v[j]);
           } else {
+            const float4* src = reinterpret_cast<const float4*>(sP + (int64_t)(k++) * OW * BM) + row_in_tile;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              float4 x = pv[s < 7 ? s : 6][j];
-              if (s > split) x = pv[s > 0 ? s - 1 : 0][j];
+              const float4 x = src[(c / 4 + j) * BM];
               f[4 * j] += x.x;
               f[4 * j + 1] += x.y;
               f[4 * j + 2] += x.z;

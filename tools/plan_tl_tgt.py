@@ -1,0 +1,23 @@
+"""Standalone plan kernel phase timeline at the per-rank north-star point (development tool):
+one rank of W=8 at TGT on one GPU (bench.tgt_rank_timing), then star_plan_timeline."""
+import os, sys
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_2510_13668_b200 as star  # noqa: E402
+from paper_2510_13668_b200 import _lib  # noqa: E402
+from paper_2510_13668_b200.step import Step  # noqa: E402
+
+r = bench.tgt_rank_timing(star, Step, torch.device("cuda", 0), None, reps=20)
+print({k: r[k] for k in ("us_per_step_p50", "stage_us", "moves")})
+tl = _lib.plan_timeline().astype(np.int64)
+names = ["entry", "launch", "staged", "W pass", "classify", "argmax", "apply", "end"]
+for k in range(1, 8):
+    if tl[k]:
+        print(f"{names[k]:9s} t={(tl[k] - tl[0]) / 1e3:6.2f} us")
+cl = tl[32:48]
+print("staging detail (us): static (pre-wait)", round((cl[12] - cl[1]) / 1965.0, 2), "pdl wait",
+      round((cl[13] - cl[12]) / 1965.0, 2), "post-wait loads", round((cl[15] - cl[13]) / 1965.0, 2),
+      "barrier", round((cl[2] - cl[15]) / 1965.0, 2))
+print("raw globaltimer offsets (us):", [(k, round((tl[k] - tl[0]) / 1e3, 2)) for k in range(16) if tl[k]])
