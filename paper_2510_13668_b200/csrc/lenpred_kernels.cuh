@@ -54,6 +54,7 @@ struct GemmArgs {
   uint64_t* tl;          // diagnostics: [ctas][16] %globaltimer phase stamps, or nullptr
   const int32_t* M_dev;  // device-side row count (refresh mode: rows selected on the device), or nullptr
   int* l1_cnt;           // CTA-pair split-K: [cta tiles][2] arrival / done counters (zeroed, self re-arming)
+  int prefetch;          // CTA-pair L2 prefetch: 0 = every CTA, 1 = none, 2 = one CTA per tile row / column
 };
 
 // Quantizer (readings A8-A10): cap = max(0, L_ctx - N(r)) (no n_tok -> L_ctx);
@@ -451,12 +452,13 @@ __global__ void __launch_bounds__(192, 1)
       const uint64_t pol_b = policy_evict_last();
       const uint32_t full0 = mapa_shared(smem_u32(&full[0]), 0);   // leader's full[0]
       const int b_row = n_tile * BN + (int)rank * (BN / 2);
+      auto kcol = [&](int i) { return (kb0 + i) * BK; };
       // the weights do not depend on the previous kernel: their first stages go out before
       // griddepcontrol.wait (PDL overlap)
       const int pre = nkb < S::STAGES ? nkb : S::STAGES;
       for (int i = 0; i < pre; ++i) {
         if (rank == 0) mbar_arrive_expect_tx(&full[i], 2 * S::STAGE_BYTES);
-        tma_load_2d_pair(sB + i * S::B_BYTES, &tmB, full0 + (uint32_t)(i * 8), (kb0 + i) * BK, b_row, pol_b);
+        tma_load_2d_pair(sB + i * S::B_BYTES, &tmB, full0 + (uint32_t)(i * 8), kcol(i), b_row, pol_b);
       }
       pdl_wait();
       if (tl) tl[2] = globaltimer_ns();
@@ -466,12 +468,14 @@ __global__ void __launch_bounds__(192, 1)
         if (i >= pre) {
           mbar_wait(&empty[s], ph ^ 1u);
           if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * S::STAGE_BYTES);
-          tma_load_2d_pair(sB + s * S::B_BYTES, &tmB, full0 + (uint32_t)(s * 8), (kb0 + i) * BK, b_row, pol_b);
+          tma_load_2d_pair(sB + s * S::B_BYTES, &tmB, full0 + (uint32_t)(s * 8), kcol(i), b_row, pol_b);
         }
-        tma_load_2d_pair(sA + s * S::A_BYTES, &tmA, full0 + (uint32_t)(s * 8), (kb0 + i) * BK, m_row0, pol_a);
-        if (i + kPrefetchKB < nkb) {   // pull a later K block into L2 so its TMA load is an L2 hit
-          tma_prefetch_2d(&tmA, (kb0 + i + kPrefetchKB) * BK, m_row0);
-          tma_prefetch_2d(&tmB, (kb0 + i + kPrefetchKB) * BK, b_row);
+        tma_load_2d_pair(sA + s * S::A_BYTES, &tmA, full0 + (uint32_t)(s * 8), kcol(i), m_row0, pol_a);
+        if (i + kPrefetchKB < nkb && p.prefetch != 1) {   // pull a later K block into L2 (TMA hits L2)
+          // prefetch 2: one prefetch per tile row / column (the pair column n_tile 0 fetches A,
+          // the pair row 0 fetches B) instead of one per consumer
+          if (p.prefetch != 2 || n_tile == 0) tma_prefetch_2d(&tmA, kcol(i + kPrefetchKB), m_row0);
+          if (p.prefetch != 2 || blockIdx.x < 2) tma_prefetch_2d(&tmB, kcol(i + kPrefetchKB), b_row);
         }
       }
     }

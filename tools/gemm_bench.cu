@@ -172,6 +172,13 @@ int main(int argc, char** argv) {
     printf("M=%d K=%d N=%d  pair split %d: %.2f us warm (%.0f TF/s), %.2f us cold  [%s]\n", M, K, N, S, w,
            flop / w / 1e6, c, cudaGetErrorString(cudaDeviceSynchronize()));
   }
+  for (int pf : {0, 1, 2}) {
+    g.prefetch = pf;
+    const float w = time_batch(pair, nrep, flush, 0), c = time_batch(pair, 1, flush, fb);
+    printf("M=%d K=%d N=%d  pair prefetch=%d: %.2f us warm (%.0f TF/s), %.2f us cold\n", M, K, N, pf, w,
+           flop / w / 1e6, c);
+  }
+  g.prefetch = 2;
   float tp_w = time_batch(pair, nrep, flush, 0), tp_c = time_batch(pair, 1, flush, fb);
   float ts_w = time_batch(single, nrep, flush, 0), ts_c = time_batch(single, 1, flush, fb);
   printf("M=%d K=%d N=%d  pair: %.2f us warm (%.0f TF/s), %.2f us cold   1-CTA: %.2f us warm (%.0f TF/s), %.2f us cold\n",
