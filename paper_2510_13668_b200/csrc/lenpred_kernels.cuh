@@ -390,9 +390,12 @@ struct PairSmem {
   static constexpr int STAGES = (int)((196u * 1024u) / STAGE_BYTES) > 8 ? 8 : (int)((196u * 1024u) / STAGE_BYTES);
   static constexpr uint32_t BYTES = 1024 + STAGES * STAGE_BYTES + 256;
   static_assert(STAGES * STAGE_BYTES >= 4u * (BN / 64) * 4096u, "epilogue staging fits");
+  static_assert(STAGES * STAGE_BYTES >= 32768u + (uint32_t)BN * 448u, "split-K partials fit");
 };
 
-template <int BN>
+// kSplit: the split-K instantiation (grid.z > 1).  A separate instantiation because merely
+// compiling the split-K epilogue into the unsplit kernel cost the C2 step ~2 us (measured A/B).
+template <int BN, bool kSplit = false>
 __global__ void __launch_bounds__(192, 1)
     umma_pair_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmC, const GemmArgs p) {
@@ -409,6 +412,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* empty = full + S::STAGES;
   uint64_t* accum = empty + S::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* pbar = accum + 2;   // split-K: the partner partial blocks' bulk copies
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -435,6 +439,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(accum, 1);
+    mbar_init(pbar, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_pair<BN>(tmem_slot);
@@ -511,7 +516,7 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_after();
     if (tl && threadIdx.x == 64) tl[10] = globaltimer_ns();
     float head_acc = 0.0f;
-    if (splits > 1) {
+    if (kSplit) {
       // ---- split-K: the S CTAs computing this CTA's 128 x BN block over disjoint K ranges meet
       // through an arrival counter in global memory (the grid is one wave of <= 148 CTAs, every
       // CTA resident, so the wait cannot starve).  Each split publishes the columns the other
@@ -539,6 +544,7 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       }
+      fence_proxy_async_global();   // the owners read these blocks with bulk copies
       __threadfence();
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (tl && threadIdx.x == 64) tl[7] = globaltimer_ns();
@@ -551,39 +557,35 @@ __global__ void __launch_bounds__(192, 1)
           if (seen < splits) __nanosleep(64);
         } while (seen < splits);
         if (tl) tl[8] = globaltimer_ns();
+        // the S-1 partner blocks of the owned columns -> shared memory [32 KB, ...) (ring is free)
+        const uint32_t pblk = (uint32_t)OW * 128u * 4u;
+        fence_proxy_async_global();
+        mbar_arrive_expect_tx(pbar, (uint32_t)(splits - 1) * pblk);
+        for (int s = 0, k = 0; s < splits; ++s) {
+          if (s == split) continue;
+          bulk_g2s(smem + 32768 + (size_t)(k++) * pblk, wsb + (int64_t)(s * splits + split) * OW * 128, pblk, pbar);
+        }
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      mbar_wait(pbar, 0);
       uint8_t* stage_base = (OW % 64 == 0) ? smem + (q * (OW / 64)) * 4096 : nullptr;
 #pragma unroll 1
       for (int c = 0; c < OW; c += 16) {
-        float4 pv[7][4];
-#pragma unroll
-        for (int k = 0; k < 7; ++k) {
-          if (k < splits - 1) {
-            const int s = k < split ? k : k + 1;
-            const float4* src =
-                reinterpret_cast<const float4*>(wsb + (int64_t)(s * splits + split) * OW * 128) + row_in_tile;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) pv[k][j] = __ldcg(src + (c / 4 + j) * 128);
-          }
-        }
+        const float* sP = reinterpret_cast<const float*>(smem + 32768);
         uint32_t v[16];
         tmem_ld_32x32b_x16(trow + (uint32_t)(own0 + c), v);
         tmem_ld_wait();
         float f[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) f[j] = 0.0f;
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          if (s >= splits) break;
+        for (int s = 0, k = 0; s < splits; ++s) {   // fixed split order (deterministic)
           if (s == split) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) f[j] += __uint_as_float(v[j]);
           } else {
+            const float4* src = reinterpret_cast<const float4*>(sP + (int64_t)(k++) * OW * 128) + row_in_tile;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              float4 x = pv[s < 7 ? s : 6][j];
-              if (s > split) x = pv[s > 0 ? s - 1 : 0][j];
+              const float4 x = src[(c / 4 + j) * 128];
               f[4 * j] += x.x;
               f[4 * j + 1] += x.y;
               f[4 * j + 2] += x.z;

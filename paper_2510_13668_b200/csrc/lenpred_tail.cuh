@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(192, 1)
             hs = ss;
           }
           if (te == 0) TAIL_TS(17);
-          proj_finalize(p.pa, hc, hs, sbeta, warp - 2, 4);
+          proj_finalize<false>(p.pa, hc, hs, sbeta, warp - 2, 4);
           asm volatile("bar.sync 1, 128;" ::: "memory");
           if (te == 0) TAIL_TS(18);
           for (int k = te; k < nb; k += 128) {

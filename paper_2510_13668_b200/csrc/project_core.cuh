@@ -180,11 +180,14 @@ __device__ __forceinline__ void proj_finalize_lanes(const ProjArgs& a, const uin
   }
 }
 
+// kLanes: allow the lane-per-instance form (the fused tail, whose projection covers one rank's
+// few instances, instantiates the warp form only and keeps its register budget).
+template <bool kLanes = true>
 __device__ __forceinline__ void proj_finalize(const ProjArgs& a, const uint32_t* cnt, const unsigned long long* sum,
                               const uint32_t* sbeta, int warp, int nwarps) {
   const int HB = a.H + 2;
   const int lane = threadIdx.x & 31;
-  if (a.n_inst > 2 * nwarps) {
+  if (kLanes && a.n_inst > 2 * nwarps) {
     proj_finalize_lanes(a, cnt, sum, sbeta, warp * 32 + lane, nwarps * 32);
     return;
   }

@@ -152,8 +152,11 @@ static cudaError_t launch_pair_gemm(const CUtensorMap& a, const CUtensorMap& b, 
                                    int m_tiles, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(umma_pair_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(umma_pair_gemm_kernel<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)PairSmem<256>::BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(umma_pair_gemm_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)PairSmem<256>::BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -171,7 +174,8 @@ static cudaError_t launch_pair_gemm(const CUtensorMap& a, const CUtensorMap& b, 
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, umma_pair_gemm_kernel<256>, a, b, c, p);
+  return p.splits > 1 ? cudaLaunchKernelEx(&cfg, umma_pair_gemm_kernel<256, true>, a, b, c, p)
+                      : cudaLaunchKernelEx(&cfg, umma_pair_gemm_kernel<256, false>, a, b, c, p);
 }
 
 // Timing events must be real event-record nodes inside a captured graph (External flag);

@@ -79,6 +79,8 @@ int main(int argc, char** argv) {
   // ---- CTA-pair kernel ----
   cudaFuncSetAttribute(umma_pair_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)PairSmem<256>::BYTES);
+  cudaFuncSetAttribute(umma_pair_gemm_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)PairSmem<256>::BYTES);
   auto pair = [&]() {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((m_tiles + 1) & ~1, N / 256, 1);
@@ -166,7 +168,7 @@ int main(int argc, char** argv) {
       at[1].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = at;
       cfg.numAttrs = 2;
-      cudaLaunchKernelEx(&cfg, umma_pair_gemm_kernel<256>, tA, tB128, tC, gs);
+      cudaLaunchKernelEx(&cfg, umma_pair_gemm_kernel<256, true>, tA, tB128, tC, gs);
     };
     const float w = time_batch(psplit, nrep, flush, 0), c = time_batch(psplit, 1, flush, fb);
     printf("M=%d K=%d N=%d  pair split %d: %.2f us warm (%.0f TF/s), %.2f us cold  [%s]\n", M, K, N, S, w,
