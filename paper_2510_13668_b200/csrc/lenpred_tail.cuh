@@ -82,6 +82,9 @@ struct TailSmem {
   static constexpr uint32_t BYTES = 1024 + OFF_CONST + CONST_BYTES;
 };
 
+// kPlan: the instantiation with the fused Alg. 1 (one rank); the others do not carry the plan's
+// code (its mere presence in a kernel measurably changes the code generated for the rest).
+template <bool kPlan>
 __global__ void __launch_bounds__(192, 1)
     tail_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmW3, const TailArgs p) {
@@ -540,7 +543,7 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
-  if (p.plan && *s_last) {   // CTA-uniform: s_last was published by the barrier above
+  if (kPlan && p.plan && *s_last) {   // CTA-uniform: s_last was published by the barrier above
     // the stage ring is free (every TMA load and MMA of this CTA has completed); the plan's
     // shared state fits below OFF_W3 - 256 (checked on the host), warp_best / shv above it
     Cand* wb = reinterpret_cast<Cand*>(smem + S::OFF_W3 - 256);

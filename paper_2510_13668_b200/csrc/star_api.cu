@@ -234,7 +234,10 @@ static cudaError_t launch_tail(const CUtensorMap& a, const CUtensorMap& b, const
                                int m_tiles, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TailSmem::BYTES);
+    cudaError_t e = cudaFuncSetAttribute(tail_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)TailSmem::BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(tail_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TailSmem::BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -252,7 +255,8 @@ static cudaError_t launch_tail(const CUtensorMap& a, const CUtensorMap& b, const
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, tail_kernel, a, b, w3, t);
+  return t.plan ? cudaLaunchKernelEx(&cfg, tail_kernel<true>, a, b, w3, t)
+                : cudaLaunchKernelEx(&cfg, tail_kernel<false>, a, b, w3, t);
 }
 
 // Split count of the fused tail: S = 4 when m_tiles * n2 * 4 CTAs fit one wave, else 2
