@@ -613,7 +613,10 @@ static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, 
     p->tl_ctas = m_tiles * n2 * ts;
     t.project = proj ? 1 : 0;
     if (proj) t.pa = *proj;
-    if (proj && plan && plan->world == 1 &&
+    // fused only for a single-round plan: the fused form runs on the tail's 192 threads, where a
+    // multi-round plan (C4, max_moves = 4: ~17 us per round) is slower than the 512-thread plan
+    // kernel it would save the launch of
+    if (proj && plan && plan->world == 1 && plan->max_moves <= 1 &&
         plan_fast_smem_layout(plan->n, plan->H, 1, plan->r_cap) + 256 <= (size_t)TailSmem::OFF_W3) {
       t.plan = 1;   // Alg. 1 by the projection's last finisher: no plan launch, no kernel boundary
       t.pl = *plan;

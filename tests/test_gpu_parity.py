@@ -130,6 +130,41 @@ def test_projection_inst_base_and_errors(star, oracle_mod):
     assert err.item() & 1 and err.item() & 2
 
 
+@pytest.mark.parametrize("R,n,grouped", [(300_003, 8, True), (400_000, 200, False)])
+def test_projection_bandwidth_form_errors(star, oracle_mod, R, n, grouped):
+    """Bandwidth form (R >= 2^18) with invalid rows (instance out of range, N = 0, N > 2^17,
+    N_hat < 0) scattered through the batch, incl. the R % 4 tail: every invalid row is skipped
+    and flagged in err_flag (bits 1 / 2 / 4), the valid rows project bit-exactly."""
+    g = datagen.rng(R)
+    snap = datagen.make_snapshot(3, 8, 256)
+    idx = g.integers(0, snap.R, R)
+    inst = g.integers(0, n, R).astype(np.int32)
+    if grouped:
+        inst = np.sort(inst).astype(np.int32)
+    n_tok, n_hat = snap.n_tok[idx].copy(), snap.true_rem[idx].astype(np.int32)
+    bad = g.choice(R - 3, 40, replace=False)
+    bad = np.concatenate([bad, [R - 1, R - 2]])   # two in the R % 4 tail
+    kinds = np.arange(len(bad)) % 4
+    inst[bad[kinds == 0]] = n + 5
+    n_tok[bad[kinds == 1]] = 0
+    n_tok[bad[kinds == 2]] = (1 << 17) + 1
+    n_hat[bad[kinds == 3]] = -3
+    ok = np.ones(R, bool)
+    ok[bad] = False
+    beta = datagen.beta_schedule_q16(50)
+    ref = oracle_mod.project(inst[ok], n_tok[ok], n_hat[ok], n, 50, beta)
+    ws = torch.zeros(star.project_workspace_bytes(n, 50), dtype=torch.uint8, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = star.project_instance_load(_dev(inst), _dev(n_tok), _dev(n_hat), n, 50, _dev(beta.astype(np.int32)),
+                                     workspace=ws, err_flag=err)
+    torch.cuda.synchronize()
+    assert err.item() & 7 == 7
+    assert np.array_equal(out.L.cpu().numpy(), ref["L"])
+    for k in ("W", "peak", "growth", "count"):
+        assert np.array_equal(getattr(out, k).cpu().numpy(), ref[k]), k
+    assert int(ws.sum().item()) == 0
+
+
 # ============================================================================ plan
 def _plan_gpu(star, params_h, L, snap, n_hat):
     pp = star.PlanParams.from_host(params_h)
