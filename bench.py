@@ -544,35 +544,64 @@ def run_star(args):
         v = step.v
         pred.layer1_timing(False)
         step.capture(h_dev)   # public API: Step.capture / Step.replay (one graph launch per step)
-        e2e_ms = []
-        for i in range(max(args.warmup, 3) + args.steps):
-            if flush is not None:
-                flush.fill_(1.0)
+        # Pipelined serving loop: step i+1's hidden states travel host -> device (PCIe, the e2e
+        # bottleneck: 16.8 MB per C2 step) on copy streams into one of two staging buffers while
+        # step i computes; the compute stream then moves the staged rows into the step's input
+        # (device-to-device) and copies the small request arrays and the moves itself.  The
+        # whole K-step loop is timed between two events (per-step = total / K); the L2 flush
+        # stays in every step (it overlaps the next step's host copy).
+        NCS = 2   # h split in row blocks over 2 copy streams (measured: 1 -> 386 us, 2 -> 341 us, 4 -> 348 us per C2 step)
+        cstreams = [torch.cuda.Stream(device=dev) for _ in range(NCS)]
+        hstage = [torch.empty_like(h_dev), torch.empty_like(h_dev)]
+        copied = [[torch.cuda.Event() for _ in range(NCS)] for _ in range(2)]
+        rows = [(R * k // NCS, R * (k + 1) // NCS) for k in range(NCS)]
+        consumed = [torch.cuda.Event(), torch.cuda.Event()]
+        moves_h = [torch.empty_like(step.moves, device="cpu").pin_memory() for _ in range(2)]
+        nm_h = [torch.empty(1, dtype=torch.int32).pin_memory() for _ in range(2)]
+
+        def e2e_loop(n):
             s, e = ev(), ev()
             s.record(stream)
-            h_dev.copy_(h_pin, non_blocking=True)
-            v["req_id"][:R].copy_(req_pin[0], non_blocking=True)
-            v["inst"][:R].copy_(req_pin[1], non_blocking=True)
-            v["n_tok"][:R].copy_(req_pin[2], non_blocking=True)
-            v["pinned"][:R].copy_(req_pin[3], non_blocking=True)
-            step.replay()
-            moves_h.copy_(step.moves, non_blocking=True)
-            nm_h.copy_(step.n_moves, non_blocking=True)
+            for cs in cstreams:
+                cs.wait_event(s)
+            for i in range(n):
+                b = i & 1
+                for k, cs in enumerate(cstreams):
+                    if i >= 2:
+                        cs.wait_event(consumed[b])   # step i-2 has moved its rows out of hstage[b]
+                    with torch.cuda.stream(cs):
+                        hstage[b][rows[k][0]:rows[k][1]].copy_(h_pin[rows[k][0]:rows[k][1]], non_blocking=True)
+                        copied[b][k].record(cs)
+                if flush is not None:
+                    flush.fill_(1.0)
+                for k in range(NCS):
+                    stream.wait_event(copied[b][k])
+                h_dev.copy_(hstage[b])
+                consumed[b].record(stream)
+                v["req_id"][:R].copy_(req_pin[0], non_blocking=True)
+                v["inst"][:R].copy_(req_pin[1], non_blocking=True)
+                v["n_tok"][:R].copy_(req_pin[2], non_blocking=True)
+                v["pinned"][:R].copy_(req_pin[3], non_blocking=True)
+                step.replay()
+                moves_h[b].copy_(step.moves, non_blocking=True)
+                nm_h[b].copy_(step.n_moves, non_blocking=True)
             e.record(stream)
             e.synchronize()
-            if i >= max(args.warmup, 3):
-                e2e_ms.append(s.elapsed_time(e))
+            return s.elapsed_time(e)
+
+        e2e_loop(max(args.warmup, 3))
+        e2e_ms = [e2e_loop(args.steps)]
         te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
         e2e_ms_step = float(te.item()) / args.steps
         h2d = h_pin.numel() * h_pin.element_size() + sum(t.numel() * t.element_size() for t in req_pin)
-        d2h = moves_h.numel() + 4
+        d2h = moves_h[0].numel() + 4
         e2e = {"value": R_total / (e2e_ms_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms_step,
-               "path": "Step public API (Step.capture/replay of lenpred_forward_project -> all-gather -> "
-                       "plan_reschedule_segmented through the C ABI): pinned-host h + request arrays -> device, "
-                       "moves -> pinned host, every step"}
+               "path": "Step public API (Step.capture/replay of the step through the C ABI): every step "
+                       "pinned-host h + request arrays -> device and moves -> pinned host; the next step's "
+                       "h copy (copy stream, double-buffered) overlaps the current step's compute"}
 
     # ---- roofline: the layer-1 tcgen05 GEMM (dominant kernel), timed live inside the step ----
     peaks = load_peaks()
@@ -583,7 +612,8 @@ def run_star(args):
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get(f"{args.config}/w{world}/layer1")
-    pair = c["dtype"] == "bf16" and ((R + 127) // 128 + 1) // 2 * 2 * 8 >= 148 * 5 // 8
+    m_tiles = (R + 127) // 128
+    pair = c["dtype"] == "bf16" and (m_tiles == 2 or (m_tiles + 1) // 2 * 2 * 8 >= 148 * 5 // 8)
     roofline = {"kernel": ("umma_pair_gemm_kernel<256> (tcgen05 cta_group::2 + TMA)" if pair else
                            "umma_gemm_kernel (tcgen05 + TMA, cluster split-K)") + " = predictor layer 1",
                 "bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
