@@ -239,19 +239,17 @@ def _ncu_traffic(key):
     return None
 
 
-def projection_sweep(star, snap, params, dev, peaks, R=1 << 24, reps=10):
-    """Bandwidth-scale evidence for the projection kernel (SURVEY §8(d)): the standalone
-    project_instance_load over R = 2^24 requests (the C2 snapshot tiled; 12 B/request, 201 MB,
-    beyond L2), timed with CUDA events; algorithmic bytes = 12 B x R (+ outputs)."""
+def _projection_point(star, snap, params, dev, R, reps=10):
+    """Per-launch time of the standalone projection over R instance-grouped requests (R / 65536
+    instances of 65536, the documented per-instance bound; the C2 snapshot tiled), 10 launches
+    back to back per event span (no host latency in the span); inputs beyond L2 stream from HBM."""
     import torch
     reps_tile = (R + snap.R - 1) // snap.R
-    # 256 instances x 65536 requests (the documented per-instance bound): tile k of the snapshot
-    # goes to instances 8*(k % 32) + inst
-    n = snap.n_inst * 32
-    shift = (np.arange(reps_tile, dtype=np.int64) % 32 * snap.n_inst).repeat(snap.R)[:R]
+    per = R // 65536 // snap.n_inst          # tiles per instance group: tile k -> instances 8*(k % per) + inst
+    n = snap.n_inst * per
+    shift = (np.arange(reps_tile, dtype=np.int64) % per * snap.n_inst).repeat(snap.R)[:R]
     inst_h = (np.tile(snap.inst, reps_tile)[:R] + shift).astype(np.int32)
-    # instance-grouped (each instance's batch contiguous: the layout of a worker's running batch)
-    order = np.argsort(inst_h, kind="stable")
+    order = np.argsort(inst_h, kind="stable")   # instance-grouped (a worker's running batch)
     inst = torch.from_numpy(inst_h[order]).to(dev)
     ntok = torch.from_numpy(np.tile(snap.n_tok, reps_tile)[:R][order]).to(dev)
     nhat = torch.from_numpy(np.tile(snap.true_rem.astype(np.int32), reps_tile)[:R][order]).to(dev)
@@ -262,8 +260,6 @@ def projection_sweep(star, snap, params, dev, peaks, R=1 << 24, reps=10):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
-    # inputs (201 MB) exceed the 126 MB L2, so every launch streams from HBM; K launches back to
-    # back per timed span keep the GPU queue full (no host launch latency in the span)
     K = 10
     ts = []
     for _ in range(reps):
@@ -274,13 +270,25 @@ def projection_sweep(star, snap, params, dev, peaks, R=1 << 24, reps=10):
         e1.record()
         e1.synchronize()
         ts.append(e0.elapsed_time(e1) / 1e3 / K)
-    t_med = float(np.median(ts))
-    algo = 12.0 * R + n * (H + 5) * 8.0
+    del inst, ntok, nhat, ws
+    return float(np.median(ts)), n, 12.0 * R + n * (H + 5) * 8.0
+
+
+def projection_sweep(star, snap, params, dev, peaks, R=1 << 24):
+    """Bandwidth-scale evidence for the projection kernel (SURVEY §8(d)): the standalone
+    project_instance_load over R = 2^24 requests (201 MB, beyond L2) -- the headline point -- and
+    2^25 (403 MB); algorithmic bytes = 12 B x R (+ outputs)."""
+    t_med, n, algo = _projection_point(star, snap, params, dev, R)
     gbs = algo / t_med / 1e9
+    sweep = [{"requests": R, "instances": n, "us": round(t_med * 1e6, 2), "GBps": round(gbs, 1),
+              "frac": round(gbs / peaks["hbm_gbs"], 4)}]
+    t2, n2, algo2 = _projection_point(star, snap, params, dev, 2 * R)
+    sweep.append({"requests": 2 * R, "instances": n2, "us": round(t2 * 1e6, 2), "GBps": round(algo2 / t2 / 1e9, 1),
+                  "frac": round(algo2 / t2 / 1e9 / peaks["hbm_gbs"], 4)})
     return {"kernel": "project_ldg_kernel (standalone, windowed histogram, 2 CTAs/SM)", "bound": "hbm", "requests": R,
             "algorithmic_bytes": algo, "avg_launch_us": t_med * 1e6, "achieved": gbs, "peak": peaks["hbm_gbs"],
             "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"], "traffic": _ncu_traffic("sweep/project"),
-            "instances": n,
+            "instances": n, "sweep": sweep,
             "note": "inputs beyond L2 (201 MB; the C2 snapshot tiled over 256 instances x 65536 requests, "
                     "instance-grouped as a worker's batch is); the in-step projection is fused into the "
                     "predictor tail"}
@@ -635,6 +643,27 @@ def run_star(args):
             "launches_per_step": launches,
             "clocks": clocks, "e2e": e2e, "wall_s_timed": wall,
             "step_us_p50": float(np.median(step_ms)) * 1e3, "step_us_p99": float(np.percentile(step_ms, 99)) * 1e3}
+    try:
+        line["plan_stats"] = {"moves_per_step": len(step.result()), "max_moves": c["max_moves"]}
+    except Exception as ex:
+        line["plan_stats"] = {"error": str(ex)}
+    if world > 1 and not args.profile:
+        try:   # NCCL floor: a 1-byte-per-rank all-gather on the same process group, device-timed
+            one = torch.zeros(1, dtype=torch.uint8, device=dev)
+            allb = torch.zeros(world, dtype=torch.uint8, device=dev)
+            for _ in range(5):
+                torch.distributed.all_gather_into_tensor(allb, one, group=group)
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            for _ in range(50):
+                torch.distributed.all_gather_into_tensor(allb, one, group=group)
+            e1.record(stream)
+            e1.synchronize()
+            tf = torch.tensor([e0.elapsed_time(e1) / 50 * 1e3], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(tf, op=torch.distributed.ReduceOp.MAX)
+            line["nccl_floor_us"] = round(float(tf.item()), 2)
+        except Exception as ex:
+            line["nccl_floor_us"] = {"error": str(ex)}
     if rank == 0 and not args.profile and not args.no_sweep:
         try:
             line["roofline_projection"] = projection_sweep(star, snap, params_h_dev(star, params_h, dev), dev, peaks)
