@@ -788,9 +788,14 @@ def refresh_step_timing(star, Step, pred, params, c, snap, idx, h_dev, dev, flus
     torch.cuda.current_stream().wait_stream(s_)
     torch.cuda.synchronize()
     st.set_generation(torch.from_numpy(gen), torch.from_numpy(g_last), torch.from_numpy(nhat_last))
-    g = torch.cuda.CUDAGraph()
+    g = torch.cuda.CUDAGraph(keep_graph=True)
     with torch.cuda.graph(g):
         st.run(h_dev)
+    try:
+        launches = count_kernel_nodes(g)
+    except Exception:
+        launches = None
+    g.instantiate()
     ts, nref = [], []
     for i in range(reps + 5):
         st.set_generation(torch.from_numpy(gen + i))   # one token per step; the cadence state evolves
@@ -806,7 +811,7 @@ def refresh_step_timing(star, Step, pred, params, c, snap, idx, h_dev, dev, flus
             nref.append(int(st.n_refreshed.item()))
     t = float(np.median(ts))
     return {"k": k, "us_per_step": round(t, 2), "requests_per_s": R / (t * 1e-6),
-            "rows_repredicted_per_step": float(np.mean(nref)), "launches_per_step": 7,
+            "rows_repredicted_per_step": float(np.mean(nref)), "launches_per_step": launches,
             "note": "paper's deployment mode (k = 20, PAPER.md:463-469): due rows re-predicted, the rest "
                     "aged; projection + plan over all requests every step"}
 

@@ -89,9 +89,12 @@ __global__ void __launch_bounds__(256) refresh_gather_kernel(const uint8_t* __re
 __global__ void __launch_bounds__(256) refresh_scatter_kernel(int R, const int32_t* __restrict__ pos,
                                                               const int32_t* __restrict__ nhat_c,
                                                               const int32_t* __restrict__ gen, int32_t* g_last,
-                                                              int32_t* nhat_last, int32_t* __restrict__ n_hat) {
+                                                              int32_t* nhat_last, int32_t* __restrict__ n_hat,
+                                                              const int32_t* __restrict__ M_dev,
+                                                              int32_t* __restrict__ n_refreshed) {
   pdl_wait();
   pdl_launch_dependents();
+  if (n_refreshed && blockIdx.x == 0 && threadIdx.x == 0) *n_refreshed = *M_dev;   // (no memcpy node in the chain)
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
     const int p = pos[r];
     const int g = gen[r];
@@ -137,12 +140,14 @@ cudaError_t launch_refresh_gather(int R, const void* h, int64_t ld_bytes, int ro
 }
 
 cudaError_t launch_refresh_scatter(int R, const int32_t* pos, const int32_t* nhat_c, const int32_t* gen,
-                                   int32_t* g_last, int32_t* nhat_last, int32_t* n_hat, cudaStream_t st) {
+                                   int32_t* g_last, int32_t* nhat_last, int32_t* n_hat, const int32_t* M_dev,
+                                   int32_t* n_refreshed, cudaStream_t st) {
   cudaLaunchAttribute at[1];
   int grid = (R + 255) / 256;
   grid = grid < 1 ? 1 : (grid > 4 * g_num_sms ? 4 * g_num_sms : grid);
   cudaLaunchConfig_t cfg = pdl_cfg(dim3(grid), dim3(256), st, at);
-  return cudaLaunchKernelEx(&cfg, refresh_scatter_kernel, R, pos, nhat_c, gen, g_last, nhat_last, n_hat);
+  return cudaLaunchKernelEx(&cfg, refresh_scatter_kernel, R, pos, nhat_c, gen, g_last, nhat_last, n_hat, M_dev,
+                            n_refreshed);
 }
 
 }  // namespace star

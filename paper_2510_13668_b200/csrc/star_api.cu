@@ -826,12 +826,9 @@ star_status lenpred_forward_refresh(star_predictor* p, const void* h, int64_t ld
   t.project = 0;
   if ((e = launch_tail(p->tmA2, p->tmB2, p->tmB3, t, m_tiles, st)) != cudaSuccess)
     return cuda_fail(e, "refresh tail launch");
-  if ((e = launch_refresh_scatter(R, p->r_pos, p->r_nhat, gen, g_last, nhat_last, n_hat, st)) != cudaSuccess)
+  if ((e = launch_refresh_scatter(R, p->r_pos, p->r_nhat, gen, g_last, nhat_last, n_hat, p->r_M, n_refreshed, st)) !=
+      cudaSuccess)
     return cuda_fail(e, "refresh_scatter launch");
-  if (n_refreshed) {
-    if ((e = cudaMemcpyAsync(n_refreshed, p->r_M, sizeof(int32_t), cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
-      return cuda_fail(e, "n_refreshed copy");
-  }
   return STAR_OK;
 }
 

@@ -44,7 +44,8 @@ cudaError_t launch_refresh_select(int R, const int32_t* gen, const int32_t* g_la
 cudaError_t launch_refresh_gather(int R, const void* h, int64_t ld_bytes, int row_bytes, const int32_t* idx,
                                   const int32_t* M_dev, void* hc, cudaStream_t st);
 cudaError_t launch_refresh_scatter(int R, const int32_t* pos, const int32_t* nhat_c, const int32_t* gen,
-                                   int32_t* g_last, int32_t* nhat_last, int32_t* n_hat, cudaStream_t st);
+                                   int32_t* g_last, int32_t* nhat_last, int32_t* n_hat, const int32_t* M_dev,
+                                   int32_t* n_refreshed, cudaStream_t st);
 
 // dispatch.cu
 size_t dispatch_workspace_bytes(int n, int H);
