@@ -97,3 +97,37 @@ def test_gathered_records_give_the_cluster_plan(world, n_inst, r_per, seed):
         assert loads_ok, f"rank {rank}: gathered loads != cluster projection"
         assert plan_ok, f"rank {rank}: plan on gathered records != cluster plan"
         assert hash_ok, f"rank {rank}: plans differ across ranks"
+
+
+def test_step_gathered_buffer_layout():
+    """Step(gathered=...) (one rank of a W-rank job measured on one GPU): rank k's record is a
+    view of slot k of the caller's gathered buffer -- exactly where the all-gather would put it --
+    so load_requests writes the bytes the exchange would deliver; a wrong-sized buffer is rejected."""
+    from paper_2510_13668_b200.step import RecordLayout, Step
+
+    class _P:   # the layout needs H / max_moves / beta_q only
+        pass
+    snap = datagen.make_snapshot(4, 8, 16)
+    params_h = datagen.make_plan_params(snap)
+    pp = _P()
+    pp.H, pp.max_moves = params_h.H, 1
+    pp.beta_q = torch.zeros(params_h.H + 1, dtype=torch.int32)
+    world, r_cap = 8, 32
+    lay = RecordLayout(1, params_h.H, r_cap)
+    buf = torch.zeros(world * lay.nbytes, dtype=torch.uint8)
+    cpu = torch.device("cpu")
+    for k in range(world):
+        st = Step(None, pp, 8, r_cap=r_cap, rank=k, world=world, device=cpu, gathered=buf)
+        assert st.recv is buf and st.send.data_ptr() == buf.data_ptr() + k * lay.nbytes
+        idx = np.nonzero(snap.inst == k)[0]
+        st.load_requests(*(torch.from_numpy(np.ascontiguousarray(a[idx])) for a in (snap.req_id, snap.inst,
+                                                                                      snap.n_tok)))
+    # the gathered buffer now decodes to every rank's requests in rank order
+    for k in range(world):
+        v = lay.views(buf[k * lay.nbytes:(k + 1) * lay.nbytes])
+        idx = np.nonzero(snap.inst == k)[0]
+        assert int(v["count"].item()) == len(idx)
+        assert np.array_equal(v["req_id"][:len(idx)].numpy(), snap.req_id[idx])
+        assert np.array_equal(v["inst"][:len(idx)].numpy(), snap.inst[idx])
+    with pytest.raises(ValueError):
+        Step(None, pp, 8, r_cap=r_cap, rank=0, world=world, device=cpu, gathered=buf[:-1])
