@@ -116,13 +116,18 @@ class ClockSampler:
         except Exception as e:  # pragma: no cover
             self.err = str(e)
 
+    def sample(self):
+        if not self.ok:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+        except Exception:
+            pass
+
     def _run(self):
         while not self.stop_ev.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
-            except Exception:
-                pass
+            self.sample()
             time.sleep(0.005)
 
     def start(self):
@@ -482,8 +487,10 @@ def run_star(args):
         clk.start()
     t0 = time.perf_counter()
     step_ms = []
-    for _ in range(args.steps):
+    for i in range(args.steps):
         timed(g, step_ms, None)
+        if clk and i % 25 == 0:   # also sample from this thread (between steps, outside the event span)
+            clk.sample()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
