@@ -395,7 +395,9 @@ struct PairSmem {
 
 // kSplit: the split-K instantiation (grid.z > 1).  A separate instantiation because merely
 // compiling the split-K epilogue into the unsplit kernel cost the C2 step ~2 us (measured A/B).
-template <int BN, bool kSplit = false>
+// kNU: N = 2048 as 9 pair tiles of 224 (x7) and 240 (x2) columns instead of 8 x 256, so that
+// 8 m-pairs occupy 144 of the 148 SMs (72 pairs) instead of 128; the epilogue stores directly.
+template <int BN, bool kSplit = false, bool kNU = false>
 __global__ void __launch_bounds__(192, 1)
     umma_pair_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmC, const GemmArgs p) {
@@ -403,6 +405,8 @@ __global__ void __launch_bounds__(192, 1)
   constexpr int BK = 64;
   constexpr uint32_t IDESC = umma_idesc(false, 256, BN);
   static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN");
+  static_assert(!(kNU && kSplit), "non-uniform N tiles are an unsplit form");
+  const uint32_t idesc = kNU ? umma_idesc(false, 256, blockIdx.y < 7 ? 224u : 240u) : IDESC;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -456,7 +460,9 @@ __global__ void __launch_bounds__(192, 1)
       const uint64_t pol_a = policy_evict_first();
       const uint64_t pol_b = policy_evict_last();
       const uint32_t full0 = mapa_shared(smem_u32(&full[0]), 0);   // leader's full[0]
-      const int b_row = n_tile * BN + (int)rank * (BN / 2);
+      const int nw_p = kNU ? (n_tile < 7 ? 224 : 240) : BN;
+      const int n0_p = kNU ? n_tile * 224 + (n_tile > 7 ? (n_tile - 7) * 16 : 0) : n_tile * BN;
+      const int b_row = n0_p + (int)rank * (nw_p / 2);
       auto kcol = [&](int i) { return (kb0 + i) * BK; };
       // the weights do not depend on the previous kernel: their first stages go out before
       // griddepcontrol.wait (PDL overlap)
@@ -498,7 +504,7 @@ __global__ void __launch_bounds__(192, 1)
         const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * S::B_BYTES));
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
-          umma_pair(tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC, (i | k) != 0 ? 1u : 0u);
+          umma_pair(tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (i | k) != 0 ? 1u : 0u);
         umma_commit_pair(&empty[s], (uint16_t)3);
       }
       umma_commit_pair(accum, (uint16_t)3);
@@ -510,7 +516,7 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;
     const int row = m_row0 + q * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    const int n0 = n_tile * BN;
+    const int n0 = kNU ? n_tile * 224 + (n_tile > 7 ? (n_tile - 7) * 16 : 0) : n_tile * BN;
     pdl_wait();   // Z1 may still be read by the previous kernel
     mbar_wait(accum, 0);
     tc_fence_after();
@@ -610,6 +616,24 @@ __global__ void __launch_bounds__(192, 1)
         if (atomicAdd(ctr + 1, 1) == splits - 1) {
           ctr[0] = 0;
           ctr[1] = 0;
+        }
+      }
+    } else if (kNU) {   // 224- or 240-column tile: 16-column chunks, direct 32-byte row stores
+      const int nw = n_tile < 7 ? 224 : 240;
+#pragma unroll 1
+      for (int c = 0; c < nw; c += 32) {
+        uint32_t v[16], u[16];
+        tmem_ld_32x32b_x16(trow + (uint32_t)c, v);
+        if (c + 16 < nw) tmem_ld_32x32b_x16(trow + (uint32_t)(c + 16), u);
+        tmem_ld_wait();
+        float f[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
+        epilogue16<false>(p, row, n0 + c, f, head_acc, nullptr, 0);
+        if (c + 16 < nw) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(u[j]);
+          epilogue16<false>(p, row, n0 + c + 16, f, head_acc, nullptr, 0);
         }
       }
     } else {

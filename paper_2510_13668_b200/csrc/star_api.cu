@@ -149,7 +149,7 @@ static cudaError_t launch_gemm(int BN, bool tf32, const CUtensorMap& a, const CU
 
 // CTA-pair layer-1 GEMM: grid (m tiles rounded up to even, n tiles), clusters of 2 along M, PDL.
 static cudaError_t launch_pair_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmArgs& p,
-                                   int m_tiles, cudaStream_t st) {
+                                   int m_tiles, cudaStream_t st, bool nu = false) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(umma_pair_gemm_kernel<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -157,11 +157,15 @@ static cudaError_t launch_pair_gemm(const CUtensorMap& a, const CUtensorMap& b, 
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(umma_pair_gemm_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)PairSmem<256>::BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(umma_pair_gemm_kernel<256, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)PairSmem<256>::BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((m_tiles + 1) & ~1, p.N / 256, p.splits);   // splits: K ranges (one wave, <= SMs)
+  // nu: N = 2048 as 9 tiles of 224 / 240 columns; splits: K ranges (one wave, <= SMs)
+  cfg.gridDim = dim3((m_tiles + 1) & ~1, nu ? 9 : p.N / 256, p.splits);
   cfg.blockDim = dim3(192, 1, 1);
   cfg.dynamicSmemBytes = PairSmem<256>::BYTES;
   cfg.stream = st;
@@ -174,6 +178,7 @@ static cudaError_t launch_pair_gemm(const CUtensorMap& a, const CUtensorMap& b, 
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
+  if (nu) return cudaLaunchKernelEx(&cfg, umma_pair_gemm_kernel<256, false, true>, a, b, c, p);
   return p.splits > 1 ? cudaLaunchKernelEx(&cfg, umma_pair_gemm_kernel<256, true>, a, b, c, p)
                       : cudaLaunchKernelEx(&cfg, umma_pair_gemm_kernel<256, false>, a, b, c, p);
 }
@@ -575,12 +580,15 @@ static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, 
       g.tl = p->tl_l1;
       p->tl_l1_ctas = ((m_tiles + 1) & ~1) * (p->m1 / 256) * pair_splits;
     }
+    // unsplit pairs over N = 2048: 9 non-uniform column tiles when they still fit one wave
+    const bool nu = pair && pair_splits == 1 && p->m1 == 2048 && ((m_tiles + 1) / 2) * 9 * 2 <= g_num_sms;
+    if (nu) p->tl_l1_ctas = ((m_tiles + 1) & ~1) * 9;
     if (!pair) {   // diagnostics timeline of the 1-CTA layer-1 kernel (rows: m x n x split CTAs)
       g.tl = p->tl_l1;
       p->tl_l1_ctas = m_tiles * (p->m1 / p->bn1) * g.splits;
     }
     if (p->ev0) record_timing_event(p->ev0, st);
-    cudaError_t e = pair ? launch_pair_gemm(p->tmA1, p->tmB1p, tmC1, g, m_tiles, st)
+    cudaError_t e = pair ? launch_pair_gemm(p->tmA1, p->tmB1p, tmC1, g, m_tiles, st, nu)
                          : launch_gemm(p->bn1, f32, p->tmA1, p->tmB1, tmC1, g, m_tiles, st);
     if (e != cudaSuccess) return cuda_fail(e, "layer-1 GEMM launch");
     if (p->ev1) record_timing_event(p->ev1, st);
