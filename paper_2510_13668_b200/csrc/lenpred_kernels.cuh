@@ -157,7 +157,9 @@ __global__ void __launch_bounds__(192, 1)
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (128B-swizzle atoms) by pointer arithmetic on the shared array itself, so
+  // the compiler keeps the shared address space (LDS/STS, not generic LD/ST through an integer)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S::STAGES * S::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + S::STAGES * S::B_BYTES);
@@ -409,7 +411,9 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t idesc = kNU ? umma_idesc(false, 256, blockIdx.y < 7 ? 224u : 240u) : IDESC;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (128B-swizzle atoms) by pointer arithmetic on the shared array itself, so
+  // the compiler keeps the shared address space (LDS/STS, not generic LD/ST through an integer)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S::STAGES * S::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + S::STAGES * S::B_BYTES);

@@ -94,7 +94,9 @@ __global__ void __launch_bounds__(192, 1)
   constexpr uint32_t IDESC3 = umma_idesc(false, BM, 64);
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (128B-swizzle atoms) by pointer arithmetic on the shared array itself, so
+  // the compiler keeps the shared address space (LDS/STS, not generic LD/ST through an integer)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S::STAGES * S::A_BYTES;
   uint8_t* sW3 = smem + S::OFF_W3;

@@ -104,7 +104,9 @@ __device__ __forceinline__ i128 mul_i32(i128 a, int32_t b) {
 
 template <class T>
 __device__ __forceinline__ T* carve(uint8_t*& p, size_t count) {
-  p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+  // align by pointer arithmetic (an integer round trip would lose the shared address space and
+  // turn every access to the plan state into a generic LD/ST)
+  p += (16u - (uint32_t)(reinterpret_cast<uintptr_t>(p) & 15u)) & 15u;
   T* r = reinterpret_cast<T*>(p);
   p += sizeof(T) * count;
   return r;
