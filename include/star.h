@@ -171,7 +171,11 @@ star_status star_predictor_layer1_ms(star_predictor* p, float* ms);
  * the caller once at allocation; each call leaves it zeroed again.  May be NULL when
  * R <= star_project_single_cta_max_rows(): then one CTA does the whole reduction.
  * Implementation: vectorised coalesced int4 loads, warp-aggregated (match_any + redux) shared-
- * memory histogram over (instance, min(N_hat, H+1)), suffix scan -> L, W, peak, growth.
+ * memory histogram over (instance, min(N_hat, H+1)), suffix scan -> L, W, peak, growth.  From
+ * 2^18 requests (16-byte aligned arrays, workspace given) the bandwidth form runs as two launches:
+ * a streaming kernel (two CTAs per SM, per-CTA contiguous slices, shared-memory bins for a window
+ * of instances -- fastest when each instance's requests are contiguous -- merged into the
+ * workspace) and a PDL-launched finalize kernel (one warp per instance).
  * ===================================================================================== */
 size_t star_project_workspace_bytes(int n_inst, int H);
 int star_project_single_cta_max_rows(void);
@@ -259,9 +263,10 @@ star_status plan_reschedule_segmented(const star_plan_params* p, const star_plan
 /* One-rank step (world == 1): lenpred_forward_project (inst_base 0) followed by
  * plan_reschedule_segmented on this rank's own state; outputs identical to the two calls in
  * sequence.  The segments (world 1, n_loc == n_inst) normally alias the projection output L and
- * n_hat.  When the fused tail runs and the plan state fits in its freed stage ring, Alg. 1 is
- * executed by the projection's last finishing CTA (one launch fewer, no kernel boundary between
- * the projection and the plan); otherwise the plan kernel follows.  Argument meaning and errors:
+ * n_hat.  When the fused tail runs, the plan has a single round (max_moves <= 1) and its state
+ * fits in the tail's freed stage ring, Alg. 1 is executed by the projection's last finishing CTA
+ * (one launch fewer, no kernel boundary between the projection and the plan); otherwise the
+ * 512-thread plan kernel follows (faster for several rounds).  Argument meaning and errors:
  * lenpred_forward_project and plan_reschedule_segmented. */
 star_status lenpred_forward_project_plan(star_predictor* p, const void* h, int64_t ld_h, int R,
                                          const int32_t* n_tok, int32_t max_ctx_len, float* y_hat, int32_t* n_hat,
