@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   if (warp == 1) tmem_alloc_pair<BN>(tmem_slot);
   tc_fence_before();
-  cluster_sync_all();   // barriers of both CTAs initialised before any cross-CTA signal
+  cluster_sync_relaxed();   // barriers of both CTAs initialised (fence.mbarrier_init released them)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(192, 1)
     if (tl && threadIdx.x == 64) tl[11] = globaltimer_ns();
   }
   tc_fence_before();
-  cluster_sync_all();   // the pair's MMAs and TMEM reads are done before the pair frees TMEM
+  cluster_sync_relaxed();   // the pair's MMAs and TMEM reads are done before the pair frees TMEM
   if (tl && threadIdx.x == 0) tl[12] = globaltimer_ns();
   if (warp == 1) {
     tc_fence_after();

@@ -122,6 +122,13 @@ __device__ __forceinline__ void cluster_sync_all() {   // every thread of every 
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Execution-only cluster barrier (no release of prior memory writes: no MEMBAR.GPU wait for this
+// thread's outstanding stores).  For barrier-init handoffs (fence.mbarrier_init already released
+// the inits) and tcgen05-ordered handoffs (tcgen05.fence::before/after_thread_sync around it).
+__device__ __forceinline__ void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
 // Programmatic dependent launch: wait until the previous grid in the stream has completed
 // (and its memory is visible); allow the next grid to start its prologue.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
