@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       fence_proxy_async_global();   // the owners read these blocks with bulk copies
-      __threadfence();
+      fence_acq_rel_gpu();
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (tl && threadIdx.x == 64) tl[7] = globaltimer_ns();
       if (threadIdx.x == 64) {

@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(192, 1)
       d4[1] = make_float4(z[4], z[5], z[6], z[7]);
     }
     // ---- the last of the n2 tiles to finish a row group completes it (arrival counter) ----
-    __threadfence();
+    fence_acq_rel_gpu();
     asm volatile("bar.sync 1, 128;" ::: "memory");
     if (te == 0) {
       int* ctr = p.cnt + m_tile * splits + split;
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(192, 1)
     asm volatile("bar.sync 1, 128;" ::: "memory");
     if (te == 0) TAIL_TS(13);
     if (*s_last) {
-      __threadfence();
+      fence_acq_rel_gpu();
       // ---- Z3 = relu(sum over n-tiles + b3); y = w4 . Z3 + b4; N_hat = q(y) ----
       float dot = 0.0f;
 #pragma unroll 1
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(192, 1)
         uint32_t errbits = 0;
         proj_accumulate(p.pa, owner, my_inst, my_ntok, nh, p.pa.ws_cnt, p.pa.ws_sum, errbits);
         if (errbits && p.pa.err) atomicOr(p.pa.err, (int)errbits);
-        __threadfence();
+        fence_acq_rel_gpu();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (te == 0) {
           const unsigned int finishers = gridDim.x * (unsigned)splits;   // one per (m-tile, row group)
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(192, 1)
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (*s_last) {
           if (te == 0) TAIL_TS(16);
-          __threadfence();
+          fence_acq_rel_gpu();
           const int nb = p.pa.n_inst * (p.pa.H + 2);
           const uint32_t* hc = p.pa.ws_cnt;
           const unsigned long long* hs = p.pa.ws_sum;

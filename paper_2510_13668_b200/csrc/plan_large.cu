@@ -246,14 +246,14 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
     c = warp_argmax(c);
     if (lane == 0) {
       w.cta_best[blockIdx.x] = c;
-      __threadfence();
+      fence_acq_rel_gpu();
       s_last = (atomicAdd(w.ctr, 1u) == gridDim.x - 1) ? 1 : 0;
     }
   }
   __syncthreads();
   if (!s_last || warp != 0) return;
   // ---- last CTA: m* over the CTA candidates (a total order, so the reduction order is free) ----
-  __threadfence();
+  fence_acq_rel_gpu();
   Cand c;
   c.score = 0; c.id = 0; c.dst = 0; c.g = -1;
   for (int b = lane; b < (int)gridDim.x; b += 32) {   // written by other CTAs before fence + arrival: L2 reads

@@ -51,12 +51,12 @@ __device__ __forceinline__ void proj_merge_finalize(const ProjArgs& a, uint32_t*
       }
     }
   }
-  __threadfence();
+  fence_acq_rel_gpu();
   __syncthreads();
   if (threadIdx.x == 0) *s_last = (atomicAdd(a.ws_arrive, 1u) == gridDim.x - 1) ? 1 : 0;
   __syncthreads();
   if (!*s_last) return;
-  __threadfence();
+  fence_acq_rel_gpu();
   if (SMEM_BINS) {
     for (int k = threadIdx.x; k < nb; k += blockDim.x) {
       scnt[k] = __ldcg(a.ws_cnt + k);

@@ -122,6 +122,11 @@ __device__ __forceinline__ void cluster_sync_all() {   // every thread of every 
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Release / acquire fence at GPU scope for the arrival-counter hand-offs (writes; fence; relaxed
+// atomic  ->  relaxed atomic; fence; reads).  __threadfence() is fence.sc.gpu (MEMBAR.SC.GPU),
+// stronger than the message-passing pattern needs.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 // Execution-only cluster barrier (no release of prior memory writes: no MEMBAR.GPU wait for this
 // thread's outstanding stores).  For barrier-init handoffs (fence.mbarrier_init already released
 // the inits) and tcgen05-ordered handoffs (tcgen05.fence::before/after_thread_sync around it).
