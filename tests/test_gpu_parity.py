@@ -258,7 +258,10 @@ def _predict(star, pw, h, biases=False, n_tok=None, max_rows=None):
 @pytest.mark.parametrize("d,dtype,R,biases", [(896, "f32", 128, False), (896, "f32", 333, True),
                                               (4096, "bf16", 300, False), (4096, "bf16", 129, True),
                                               (5120, "bf16", 257, False), (1024, "bf16", 1, False),
-                                              (896, "bf16", 640, False)])
+                                              (896, "bf16", 640, False),
+                                              # layer 1 as 9 non-uniform column tiles (6-8 row pairs):
+                                              # odd m-tile count (phantom rows) and a ragged last tile
+                                              (4096, "bf16", 1300, True), (4096, "bf16", 1537, False)])
 def test_predictor_parity(star, oracle_mod, d, dtype, R, biases):
     pw = datagen.make_predictor_weights(d, d, dtype, biases=biases)
     h = datagen.make_hidden(d + 1, R, d, dtype)
