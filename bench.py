@@ -385,6 +385,7 @@ def tgt_rank_timing(star, Step, dev, flush, seed=0, reps=200, world=8):
     return {"workload": "TGT, one rank of W=8: 1 instance x 512 requests, d=4096 bf16; Alg. 1 over the 8 gathered "
                         "records (4096 requests)",
             "us_per_step_p50": round(float(np.median(ts)), 2), "us_per_step_p99": round(float(np.percentile(ts, 99)), 2),
+            "us_per_step_min": round(float(np.min(ts)), 2), "us_per_step_p10": round(float(np.percentile(ts, 10)), 2),
             "target_us": 50.0, "launches_per_step": launches, "moves": n_moves,
             "stage_us": {"predict+project": round(acc[0], 2), "plan_4096_gathered": round(acc[1], 2)},
             "l2": "flushed before every step" if flush is not None else "warm",
