@@ -446,21 +446,29 @@ def run_star(args):
     use_graph = not args.no_graph
     launches = None
     g = g_l1 = None
+    graph_error = None
     if use_graph:
-        pred.layer1_timing(False)
-        g = torch.cuda.CUDAGraph(keep_graph=True)
-        with torch.cuda.graph(g):
-            step.run(h_dev)
         try:
-            launches = count_kernel_nodes(g)
-        except Exception:
+            pred.layer1_timing(False)
+            g = torch.cuda.CUDAGraph(keep_graph=True)
+            with torch.cuda.graph(g):
+                step.run(h_dev)
+            try:
+                launches = count_kernel_nodes(g)
+            except Exception:
+                launches = None
+            g.instantiate()
+            # a second graph of the same step with the library's layer-1 event pair (roofline pass)
+            pred.layer1_timing(True)
+            g_l1 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_l1):
+                step.run(h_dev)
+        except Exception as ex:   # e.g. a collective that cannot be captured: time the eager step instead
+            graph_error = f"{type(ex).__name__}: {ex}"
+            torch.cuda.synchronize()
+            g = g_l1 = None
+            use_graph = False
             launches = None
-        g.instantiate()
-        # a second graph of the same step with the library's layer-1 event pair (roofline pass)
-        pred.layer1_timing(True)
-        g_l1 = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_l1):
-            step.run(h_dev)
 
     def timed(graph, store, l1):
         if flush is not None:
@@ -574,7 +582,10 @@ def run_star(args):
         nm_h = torch.empty(1, dtype=torch.int32).pin_memory()
         v = step.v
         pred.layer1_timing(False)
-        step.capture(h_dev)   # public API: Step.capture / Step.replay (one graph launch per step)
+        if use_graph:
+            step.capture(h_dev)   # public API: Step.capture / Step.replay (one graph launch per step)
+        else:
+            step.replay = lambda: step.run(h_dev)   # eager fallback (graph capture failed above)
         # Pipelined serving loop: step i+1's hidden states travel host -> device (PCIe, the e2e
         # bottleneck: 16.8 MB per C2 step) on copy streams into one of two staging buffers while
         # step i computes; the compute stream then moves the staged rows into the step's input
@@ -667,6 +678,8 @@ def run_star(args):
             "clocks": clocks, "e2e": e2e, "wall_s_timed": wall,
             "step_us_p50": float(np.median(step_ms)) * 1e3, "step_us_p99": float(np.percentile(step_ms, 99)) * 1e3,
             "step_us_warm_l2": warm_us, "requests_per_s_per_gpu": value / world}
+    if graph_error:
+        line["graph_error"] = graph_error
     try:
         line["plan_stats"] = {"moves_per_step": len(step.result()), "max_moves": c["max_moves"]}
     except Exception as ex:
