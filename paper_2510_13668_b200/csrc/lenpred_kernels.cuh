@@ -55,6 +55,7 @@ struct GemmArgs {
   const int32_t* M_dev;  // device-side row count (refresh mode: rows selected on the device), or nullptr
   int* l1_cnt;           // CTA-pair split-K: [cta tiles][2] arrival / done counters (zeroed, self re-arming)
   int prefetch;          // CTA-pair L2 prefetch: 0 = every CTA, 1 = none, 2 = one CTA per tile row / column
+  int mn_swap;           // 1-CTA kernel: grid (n tiles, m tiles, splits) instead of (m, n, splits)
 };
 
 // Quantizer (readings A8-A10): cap = max(0, L_ctx - N(r)) (no n_tok -> L_ctx);
@@ -177,7 +178,10 @@ __global__ void __launch_bounds__(192, 1)
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     tl[15] = smid;
   }
-  const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
+  // mn_swap: grid (n, m, S) -- m-tiles vary slowest, so with a device-side row count the real
+  // (low) m-tiles are launched first instead of interleaved with the tiles that leave at once
+  const int m_tile = p.mn_swap ? blockIdx.y : blockIdx.x, n_tile = p.mn_swap ? blockIdx.x : blockIdx.y;
+  const int split = blockIdx.z;
   const int splits = p.splits;
   const int kb0 = split * p.kb_per_split;
   const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);

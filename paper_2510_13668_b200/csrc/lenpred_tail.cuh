@@ -55,6 +55,7 @@ struct TailArgs {
   ProjArgs pa;         // R / inst / n_tok / beta_q / outputs / workspace (ws_cnt, ws_sum, ws_arrive)
   uint64_t* tl;        // diagnostics: [ctas][16] %globaltimer phase stamps, or nullptr
   const int32_t* M_dev;  // device-side row count (refresh mode), or nullptr (then M)
+  int mn_swap;           // grid (n2 tiles, m tiles, splits): real m-tiles launch first (refresh mode)
   int plan;            // the projection's last finisher then runs Alg. 1 (one rank: pl reads this
                        // rank's own record), with the whole CTA, in the freed stage ring
   PlanArgs pl;
@@ -130,7 +131,8 @@ __global__ void __launch_bounds__(192, 1)
       p.tl[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * kTailTlStride + 15] = smid;
     }
   }
-  const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
+  const int m_tile = p.mn_swap ? blockIdx.y : blockIdx.x, n_tile = p.mn_swap ? blockIdx.x : blockIdx.y;
+  const int split = blockIdx.z;
   const int splits = p.splits;
   const int OW = BN / splits;                  // owned Z2 columns (128 or 64)
   const int OWK = OW / 64;                     // layer-3 K blocks (2 or 1)
@@ -486,7 +488,7 @@ __global__ void __launch_bounds__(192, 1)
         fence_acq_rel_gpu();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (te == 0) {
-          const unsigned int finishers = gridDim.x * (unsigned)splits;   // one per (m-tile, row group)
+          const unsigned int finishers = (p.mn_swap ? gridDim.y : gridDim.x) * (unsigned)splits;   // per (m-tile, row group)
           *s_last = (atomicAdd(p.pa.ws_arrive, 1u) == finishers - 1) ? 1 : 0;
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");

@@ -119,7 +119,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, con
   // dependent launch lets the prologue overlap the previous kernel; the kernel calls
   // griddepcontrol.wait before touching memory.
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(m_tiles, p.N / BN, p.splits);
+  cfg.gridDim = p.mn_swap ? dim3(p.N / BN, m_tiles, p.splits) : dim3(m_tiles, p.N / BN, p.splits);
   cfg.blockDim = dim3(192, 1, 1);
   cfg.dynamicSmemBytes = GemmSmem<BN>::BYTES;
   cfg.stream = st;
@@ -247,7 +247,7 @@ static cudaError_t launch_tail(const CUtensorMap& a, const CUtensorMap& b, const
     attr = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(m_tiles, t.n2_tiles, t.splits);
+  cfg.gridDim = t.mn_swap ? dim3(t.n2_tiles, m_tiles, t.splits) : dim3(m_tiles, t.n2_tiles, t.splits);
   cfg.blockDim = dim3(192, 1, 1);
   cfg.dynamicSmemBytes = TailSmem::BYTES;
   cfg.stream = st;
@@ -801,6 +801,7 @@ star_status lenpred_forward_refresh(star_predictor* p, const void* h, int64_t ld
     g.kb_per_split = (g.num_kb + 3) / 4;
   }
   g.ws = p->r_ws;
+  g.mn_swap = 1;   // the device-side row count leaves most m-tiles empty: launch the real ones first
   g.epi = EPI_RELU_BF16;
   g.tma_store = (p->bn1 / g.splits) % 64 == 0 ? 1 : 0;
   g.out = p->Z1;
@@ -815,6 +816,7 @@ star_status lenpred_forward_refresh(star_predictor* p, const void* h, int64_t ld
   TailArgs t{};
   t.M = R;
   t.M_dev = p->r_M;
+  t.mn_swap = 1;
   t.num_kb = num_kb2;
   t.splits = ts;
   t.kb_per_split = (num_kb2 + ts - 1) / ts;
