@@ -138,6 +138,21 @@ star_status lenpred_forward_refresh(star_predictor* p, const void* h, int64_t ld
                                     int32_t* g_last, int32_t* nhat_last, int32_t k, int32_t* n_hat,
                                     int32_t* n_refreshed, star_stream_t stream);
 
+/* lenpred_forward_refresh followed by project_instance_load(R, n_inst, inst_base, H, inst, n_tok,
+ * n_hat, beta_q, L, W, peak, growth, count, workspace, err_flag) on the resulting N_hat -- the
+ * cadence-k step of one worker -- with identical outputs bit for bit.  For
+ * R <= 8192 and n_inst * (H + 2) bins that fit one CTA's shared memory, the aging scatter and the
+ * projection run as ONE kernel (one CTA: shared-memory histogram, suffix-scan finalize; the
+ * workspace is not touched); otherwise the two kernels follow each other.  Argument meaning,
+ * layouts and errors: lenpred_forward_refresh and project_instance_load. */
+star_status lenpred_forward_refresh_project(star_predictor* p, const void* h, int64_t ld_h, int R,
+                                            const int32_t* n_tok, int32_t max_ctx_len, const int32_t* gen,
+                                            int32_t* g_last, int32_t* nhat_last, int32_t k, int32_t* n_hat,
+                                            int32_t* n_refreshed, int n_inst, int inst_base, int H,
+                                            const int32_t* inst, const uint32_t* beta_q, int64_t* L, int64_t* W,
+                                            int64_t* peak, int64_t* growth, int32_t* count, void* workspace,
+                                            int32_t* err_flag, star_stream_t stream);
+
 /* The quantizer alone, on a caller-given fp32 y_hat (the exact device function the forward
  * epilogue uses).  Lets quantizer parity be tested on identical fp32 inputs. */
 star_status lenpred_quantize(const float* y_hat, const int32_t* n_tok, int R, int32_t max_ctx_len,

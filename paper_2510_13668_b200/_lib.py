@@ -64,6 +64,8 @@ def lib() -> C.CDLL:
         "lenpred_quantize": ([P, P, I, I32, P, P], I),
         "lenpred_forward_project": ([P, P, I64, I, P, I32, P, P, I, I, I, P, P, P, P, P, P, P, P, P, P], I),
         "lenpred_forward_refresh": ([P, P, I64, I, P, I32, P, P, P, I32, P, P, P], I),
+        "lenpred_forward_refresh_project": ([P, P, I64, I, P, I32, P, P, P, I32, P, P, I, I, I, P, P, P, P, P, P, P,
+                                             P, P, P], I),
         "star_project_workspace_bytes": ([I, I], C.c_size_t),
         "star_project_single_cta_max_rows": ([], I),
         "project_instance_load": ([I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P], I),
@@ -270,6 +272,32 @@ def lenpred_forward_refresh(pred: Predictor, h: torch.Tensor, n_tok: torch.Tenso
                                          _ptr(g_last), _ptr(nhat_last), int(k), _ptr(n_hat), _ptr(n_refreshed),
                                          _stream(stream)), "lenpred_forward_refresh")
     return n_hat[:R]
+
+
+def lenpred_forward_refresh_project(pred: Predictor, h: torch.Tensor, n_tok: torch.Tensor, gen: torch.Tensor,
+                                    g_last: torch.Tensor, nhat_last: torch.Tensor, k: int, inst: torch.Tensor,
+                                    n_inst: int, H: int, beta_q: torch.Tensor, workspace: torch.Tensor,
+                                    inst_base: int = 0, max_ctx_len: int = L_CTX,
+                                    n_hat: Optional[torch.Tensor] = None, n_refreshed: Optional[torch.Tensor] = None,
+                                    out: Optional["ProjectOut"] = None, err_flag: Optional[torch.Tensor] = None,
+                                    R: Optional[int] = None, stream=None):
+    """Cadence-k step of one worker (star.h lenpred_forward_refresh_project): refresh + projection."""
+    R = h.shape[0] if R is None else R
+    if h.dim() != 2 or h.stride(1) != 1 or h.dtype != torch.bfloat16 or not h.is_cuda:
+        raise StarError("h must be a 2-D CUDA bf16 tensor with unit column stride")
+    for n_, t in (("n_tok", n_tok), ("gen", gen), ("g_last", g_last), ("nhat_last", nhat_last), ("inst", inst),
+                  ("beta_q", beta_q)):
+        _req(t, torch.int32, n_)
+    if n_hat is None:
+        n_hat = torch.empty(max(R, 1), dtype=torch.int32, device=h.device)
+    if out is None:
+        out = ProjectOut(n_inst, H, h.device)
+    _check(lib().lenpred_forward_refresh_project(
+        pred.handle, _ptr(h), h.stride(0), R, _ptr(n_tok), max_ctx_len, _ptr(gen), _ptr(g_last), _ptr(nhat_last),
+        int(k), _ptr(n_hat), _ptr(n_refreshed), n_inst, inst_base, H, _ptr(inst), _ptr(beta_q), _ptr(out.L),
+        _ptr(out.W), _ptr(out.peak), _ptr(out.growth), _ptr(out.count), _ptr(workspace), _ptr(err_flag),
+        _stream(stream)), "lenpred_forward_refresh_project")
+    return n_hat[:R], out
 
 
 def lenpred_quantize(y_hat: torch.Tensor, n_tok: Optional[torch.Tensor] = None, max_ctx_len: int = L_CTX,

@@ -12,8 +12,12 @@
 //                           device-side row count (CTAs beyond M exit at once)
 //   refresh_scatter_kernel  per row: refreshed -> new N_hat, g_last = g, N_hat_last = N_hat;
 //                           else the aged value
+//   refresh_scatter_project_kernel  the scatter fused with the per-instance projection of the
+//                           resulting N_hat (one CTA, shared-memory histogram + finalize): one
+//                           launch and one N_hat round trip fewer per step
 #include <cstdint>
 #include <cuda_runtime.h>
+#include "project_core.cuh"
 #include "ptx.cuh"
 #include "star_internal.h"
 
@@ -111,6 +115,53 @@ __global__ void __launch_bounds__(256) refresh_scatter_kernel(int R, const int32
   }
 }
 
+constexpr int kScatProjThreads = 1024;
+__global__ void __launch_bounds__(kScatProjThreads) refresh_scatter_project_kernel(
+    const ProjArgs a, const int32_t* __restrict__ pos, const int32_t* __restrict__ nhat_c,
+    const int32_t* __restrict__ gen, int32_t* g_last, int32_t* nhat_last, const int32_t* __restrict__ M_dev,
+    int32_t* __restrict__ n_refreshed) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int nb = a.n_inst * (a.H + 2);
+  unsigned long long* ssum = reinterpret_cast<unsigned long long*>(sm);
+  uint32_t* scnt = reinterpret_cast<uint32_t*>(ssum + nb);
+  __shared__ uint32_t sbeta[257];
+  for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+    ssum[k] = 0;
+    scnt[k] = 0;
+  }
+  pdl_wait();
+  pdl_launch_dependents();
+  for (int t = threadIdx.x; t <= a.H; t += blockDim.x) sbeta[t] = a.beta_q[t];
+  if (n_refreshed && threadIdx.x == 0) *n_refreshed = *M_dev;
+  __syncthreads();
+  uint32_t errbits = 0;
+  int32_t* n_hat = const_cast<int32_t*>(a.n_hat);
+  for (int base = 0; base < a.R; base += blockDim.x) {   // CTA-uniform trip count: whole warps call
+    const int r = base + (int)threadIdx.x;
+    const bool valid = r < a.R;
+    int nh = 0, ins = 0, nt = 0;
+    if (valid) {
+      const int p = pos[r];
+      const int g = gen[r];
+      if (p >= 0) {                       // re-predicted this step
+        nh = nhat_c[p];
+        g_last[r] = g;
+        nhat_last[r] = nh;
+      } else {                            // aged (reading A27)
+        const int aged = nhat_last[r] - (g - g_last[r]);
+        nh = aged > 0 ? aged : 0;
+      }
+      n_hat[r] = nh;
+      ins = a.inst[r];
+      nt = a.n_tok[r];
+    }
+    proj_accumulate<true>(a, valid, ins, nt, nh, scnt, ssum, errbits);
+  }
+  if (errbits && a.err) atomicOr(a.err, (int)errbits);
+  __syncthreads();
+  proj_finalize(a, scnt, ssum, sbeta, threadIdx.x >> 5, blockDim.x >> 5);
+}
+
 static cudaLaunchConfig_t pdl_cfg(dim3 grid, dim3 block, cudaStream_t st, cudaLaunchAttribute* at) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
@@ -147,6 +198,26 @@ cudaError_t launch_refresh_scatter(int R, const int32_t* pos, const int32_t* nha
   grid = grid < 1 ? 1 : (grid > 4 * g_num_sms ? 4 * g_num_sms : grid);
   cudaLaunchConfig_t cfg = pdl_cfg(dim3(grid), dim3(256), st, at);
   return cudaLaunchKernelEx(&cfg, refresh_scatter_kernel, R, pos, nhat_c, gen, g_last, nhat_last, n_hat, M_dev,
+                            n_refreshed);
+}
+
+size_t refresh_scatter_project_smem(int n_inst, int H) { return (size_t)n_inst * (H + 2) * 12; }
+
+cudaError_t launch_refresh_scatter_project(const ProjArgs& a, const int32_t* pos, const int32_t* nhat_c,
+                                           const int32_t* gen, int32_t* g_last, int32_t* nhat_last,
+                                           const int32_t* M_dev, int32_t* n_refreshed, cudaStream_t st) {
+  const size_t smem = refresh_scatter_project_smem(a.n_inst, a.H);
+  static int attr = 48 * 1024;
+  if ((int)smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(refresh_scatter_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = (int)smem;
+  }
+  cudaLaunchAttribute at[1];
+  cudaLaunchConfig_t cfg = pdl_cfg(dim3(1), dim3(kScatProjThreads), st, at);
+  cfg.dynamicSmemBytes = smem;
+  return cudaLaunchKernelEx(&cfg, refresh_scatter_project_kernel, a, pos, nhat_c, gen, g_last, nhat_last, M_dev,
                             n_refreshed);
 }
 

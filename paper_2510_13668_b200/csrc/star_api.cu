@@ -763,9 +763,10 @@ star_status lenpred_forward_project_plan(star_predictor* p, const void* h, int64
   return STAR_OK;
 }
 
-star_status lenpred_forward_refresh(star_predictor* p, const void* h, int64_t ld_h, int R, const int32_t* n_tok,
-                                    int32_t max_ctx_len, const int32_t* gen, int32_t* g_last, int32_t* nhat_last,
-                                    int32_t k, int32_t* n_hat, int32_t* n_refreshed, star_stream_t stream_) {
+static star_status refresh_impl(star_predictor* p, const void* h, int64_t ld_h, int R, const int32_t* n_tok,
+                                int32_t max_ctx_len, const int32_t* gen, int32_t* g_last, int32_t* nhat_last,
+                                int32_t k, int32_t* n_hat, int32_t* n_refreshed, const ProjArgs* proj,
+                                star_stream_t stream_) {
   if (!p) return fail(STAR_EINVAL, "predictor is NULL");
   if (p->f32 || p->bn2 != 256 || p->m3 != 64)
     return fail(STAR_ENOTSUP, "refresh mode needs a bf16 predictor (m2 %% 256 == 0, m3 == 64)");
@@ -836,10 +837,49 @@ star_status lenpred_forward_refresh(star_predictor* p, const void* h, int64_t ld
   t.project = 0;
   if ((e = launch_tail(p->tmA2, p->tmB2, p->tmB3, t, m_tiles, st)) != cudaSuccess)
     return cuda_fail(e, "refresh tail launch");
+  if (proj && R <= 8192 && refresh_scatter_project_smem(proj->n_inst, proj->H) <= (size_t)200 * 1024) {
+    // aging scatter fused with the projection of the resulting N_hat (one CTA)
+    if ((e = launch_refresh_scatter_project(*proj, p->r_pos, p->r_nhat, gen, g_last, nhat_last, p->r_M, n_refreshed,
+                                            st)) != cudaSuccess)
+      return cuda_fail(e, "refresh_scatter_project launch");
+    return STAR_OK;
+  }
   if ((e = launch_refresh_scatter(R, p->r_pos, p->r_nhat, gen, g_last, nhat_last, n_hat, p->r_M, n_refreshed, st)) !=
       cudaSuccess)
     return cuda_fail(e, "refresh_scatter launch");
+  if (proj) {
+    const ProjArgs& a = *proj;
+    if ((e = launch_project(a.R, a.n_inst, a.inst_base, a.H, a.inst, a.n_tok, a.n_hat, a.beta_q, a.L, a.W, a.peak,
+                            a.growth, a.count, a.ws_sum, a.err, st, nullptr)) != cudaSuccess)
+      return cuda_fail(e, "projection launch");
+  }
   return STAR_OK;
+}
+
+star_status lenpred_forward_refresh(star_predictor* p, const void* h, int64_t ld_h, int R, const int32_t* n_tok,
+                                    int32_t max_ctx_len, const int32_t* gen, int32_t* g_last, int32_t* nhat_last,
+                                    int32_t k, int32_t* n_hat, int32_t* n_refreshed, star_stream_t stream_) {
+  return refresh_impl(p, h, ld_h, R, n_tok, max_ctx_len, gen, g_last, nhat_last, k, n_hat, n_refreshed, nullptr,
+                      stream_);
+}
+
+star_status lenpred_forward_refresh_project(star_predictor* p, const void* h, int64_t ld_h, int R,
+                                            const int32_t* n_tok, int32_t max_ctx_len, const int32_t* gen,
+                                            int32_t* g_last, int32_t* nhat_last, int32_t k, int32_t* n_hat,
+                                            int32_t* n_refreshed, int n_inst, int inst_base, int H,
+                                            const int32_t* inst, const uint32_t* beta_q, int64_t* L, int64_t* W,
+                                            int64_t* peak, int64_t* growth, int32_t* count, void* workspace,
+                                            int32_t* err_flag, star_stream_t stream_) {
+  if (n_inst < 1 || n_inst > (1 << 16)) return fail(STAR_ERANGE, "n_inst=%d outside [1, 65536]", n_inst);
+  if (H < 0 || H > 256) return fail(STAR_ERANGE, "H=%d outside [0, 256]", H);
+  if (!L || !beta_q || !workspace) return fail(STAR_EINVAL, "L, beta_q and workspace must be non-NULL");
+  if (R > 0 && (!inst || !n_tok)) return fail(STAR_EINVAL, "inst and n_tok must be non-NULL");
+  if (R == 0)
+    return project_instance_load(0, n_inst, inst_base, H, inst, n_tok, n_hat, beta_q, L, W, peak, growth, count,
+                                 workspace, err_flag, stream_);
+  const ProjArgs a = make_proj_args(R, n_inst, inst_base, H, inst, n_tok, n_hat, beta_q, L, W, peak, growth, count,
+                                    workspace, err_flag);
+  return refresh_impl(p, h, ld_h, R, n_tok, max_ctx_len, gen, g_last, nhat_last, k, n_hat, n_refreshed, &a, stream_);
 }
 
 star_status lenpred_quantize(const float* y_hat, const int32_t* n_tok, int R, int32_t max_ctx_len, int32_t* n_hat,

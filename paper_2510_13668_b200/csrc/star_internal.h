@@ -46,6 +46,11 @@ cudaError_t launch_refresh_gather(int R, const void* h, int64_t ld_bytes, int ro
 cudaError_t launch_refresh_scatter(int R, const int32_t* pos, const int32_t* nhat_c, const int32_t* gen,
                                    int32_t* g_last, int32_t* nhat_last, int32_t* n_hat, const int32_t* M_dev,
                                    int32_t* n_refreshed, cudaStream_t st);
+struct ProjArgs;
+size_t refresh_scatter_project_smem(int n_inst, int H);
+cudaError_t launch_refresh_scatter_project(const ProjArgs& a, const int32_t* pos, const int32_t* nhat_c,
+                                           const int32_t* gen, int32_t* g_last, int32_t* nhat_last,
+                                           const int32_t* M_dev, int32_t* n_refreshed, cudaStream_t st);
 
 // dispatch.cu
 size_t dispatch_workspace_bytes(int n, int H);

@@ -177,13 +177,12 @@ class Step:
         v, R = self.v, self.R
         if self.refresh_k is not None:
             # cadence k: re-predict only the due rows, age the rest, then project all of them
-            _lib.lenpred_forward_refresh(self.pred, h[:R], v["n_tok"][:R], self.gen[:R], self.g_last[:R],
-                                         self.nhat_last[:R], self.refresh_k, max_ctx_len=self.max_ctx_len,
-                                         n_hat=v["n_hat"][:max(R, 1)], n_refreshed=self.n_refreshed,
-                                         stream=stream)
-            _lib.project_instance_load(v["inst"], v["n_tok"], v["n_hat"], self.n_loc, self.H, self.params.beta_q,
-                                       inst_base=self.rank * self.n_loc, out=self.proj_out, workspace=self.ws,
-                                       err_flag=self.err, R=R, stream=stream)
+            _lib.lenpred_forward_refresh_project(self.pred, h[:R], v["n_tok"][:R], self.gen[:R], self.g_last[:R],
+                                                 self.nhat_last[:R], self.refresh_k, v["inst"][:R], self.n_loc,
+                                                 self.H, self.params.beta_q, self.ws,
+                                                 inst_base=self.rank * self.n_loc, max_ctx_len=self.max_ctx_len,
+                                                 n_hat=v["n_hat"][:max(R, 1)], n_refreshed=self.n_refreshed,
+                                                 out=self.proj_out, err_flag=self.err, R=R, stream=stream)
             if self.world > 1 and not self.emulated:
                 exchange(self.send, self.recv, self.group)
             _lib.plan_reschedule_segmented(self.params, self.seg, self.moves, self.n_moves, self.err, stream=stream)

@@ -490,6 +490,48 @@ def test_refresh_step_parity(star, oracle_mod, R, k, seed):
     pred.close()
 
 
+@pytest.mark.parametrize("R,k,seed,n", [(2048, 20, 0, 8), (777, 7, 1, 3), (64, 1, 2, 1), (5000, 20, 3, 64)])
+def test_refresh_project_fused_equals_separate(star, oracle_mod, R, k, seed, n):
+    """lenpred_forward_refresh_project (aging scatter fused with the projection, one CTA) ==
+    lenpred_forward_refresh + project_instance_load, bit for bit (N_hat, cadence state, L, W, peak,
+    growth, count), and == the oracle projection of that N_hat."""
+    from paper_2510_13668_b200 import _lib
+    c = datagen.CONFIGS["C2"]
+    g = datagen.rng(seed)
+    snap = datagen.make_snapshot(seed, n, (R + n - 1) // n)
+    n_tok, inst = snap.n_tok[:R].copy(), snap.inst[:R].astype(np.int32)
+    pw = datagen.make_predictor_weights(seed, c["d"], "bf16")
+    scale = np.exp(g.normal(0.0, 1.5, R)).astype(np.float32)
+    h = _dev(datagen.make_hidden(seed, R, c["d"], "bf16", scale=scale), torch.bfloat16)
+    gen = g.integers(0, 5000, R).astype(np.int32)
+    g_last = np.where(g.random(R) < 0.1, -1, gen - g.integers(0, 2 * k + 1, R)).astype(np.int32)
+    nhat_last = g.integers(0, 30000, R).astype(np.int32)
+    W, _ = _weights_dev(pw)
+    pred = star.Predictor(*W, max_rows=R)
+    beta = datagen.beta_schedule_q16(50)
+    bq = _dev(beta.astype(np.int32))
+    res = []
+    for fused in (True, False):
+        gl_d, nl_d = _dev(g_last), _dev(nhat_last)
+        ws = torch.zeros(star.project_workspace_bytes(n, 50), dtype=torch.uint8, device="cuda")
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        if fused:
+            nh, out = _lib.lenpred_forward_refresh_project(pred, h, _dev(n_tok), _dev(gen), gl_d, nl_d, k,
+                                                           _dev(inst), n, 50, bq, ws, err_flag=err)
+        else:
+            nh = star.lenpred_forward_refresh(pred, h, _dev(n_tok), _dev(gen), gl_d, nl_d, k)
+            out = star.project_instance_load(_dev(inst), _dev(n_tok), nh, n, 50, bq, workspace=ws, err_flag=err)
+        torch.cuda.synchronize()
+        assert err.item() == 0 and int(ws.sum().item()) == 0
+        res.append([nh.cpu().numpy(), gl_d.cpu().numpy(), nl_d.cpu().numpy()] +
+                   [getattr(out, k_).cpu().numpy() for k_ in ("L", "W", "peak", "growth", "count")])
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
+    ref = oracle_mod.project(inst, n_tok, res[0][0], n, 50, beta)
+    assert np.array_equal(res[0][3], ref["L"]) and np.array_equal(res[0][4], ref["W"])
+    pred.close()
+
+
 def test_refresh_schedule_on_device(star, oracle_mod):
     """45 decode steps (gen += 1 per step), k = 20: every row refreshes at its first step and then
     every 20 generated tokens; in between the device ages it exactly like the oracle."""
