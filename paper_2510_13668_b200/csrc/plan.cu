@@ -37,7 +37,7 @@ template <bool kStaged>
 __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a) {
   extern __shared__ __align__(16) uint8_t smraw[];
   __shared__ Cand warp_best[kPlanThreads / 32];
-  __shared__ int shv[4];
+  __shared__ int shv[8];
   if (threadIdx.x == 0) g_plan_tl[0] = globaltimer_ns();
   if constexpr (!kStaged) pdl_wait();   // inputs come from the projection / all-gather (PDL launch)
   pdl_launch_dependents();   // (the fast path waits itself, after fetching its static inputs)

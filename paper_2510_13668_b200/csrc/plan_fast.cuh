@@ -169,6 +169,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
   int& s_nU = shv[1];
   int& s_nmoves = shv[2];
   int& s_ncand = shv[3];
+  int& s_reuse = shv[4];   // round > 0 with an unchanged overloaded set: last round's candidates stand
 
   // ---- staging ----
   // Static inputs (request ids, instances, token counts, pins, counts, beta, capacities) are not
@@ -370,17 +371,19 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
 #pragma unroll
       for (int m = 16; m >= 1; m >>= 1) wsum += shfl_xor_i128(wsum, m);
       const i128 rhs = mul_u32(wsum, (uint32_t)a.theta_den + (uint32_t)a.theta_num);   // den >= 1, num >= 0
-      bool anyO = false;
+      bool anyO = false, chO = false;
       int nU = 0;
       for (int base = 0; base < n; base += 32) {
         const int i = base + lane;
-        bool o = false, u = false;
+        bool o = false, u = false, ch = false;
         if (i < n) {
           o = mul_u32(mul_u32(s.Wv[i], (uint32_t)n), (uint32_t)a.theta_den) > rhs;
           u = !o && (mul_u32(mul_u32((i128)s.Ls[(int64_t)i * H1], (uint32_t)n), (uint32_t)a.theta_den) << 16) < rhs;
+          ch = s.inO[i] != (o ? 1 : 0);
           s.inO[i] = o ? 1 : 0;
         }
         anyO |= __any_sync(0xFFFFFFFFu, o) != 0;
+        chO |= __any_sync(0xFFFFFFFFu, ch) != 0;
         const uint32_t um = __ballot_sync(0xFFFFFFFFu, u);
         if (u) s.ulist[nU + __popc(um & ((1u << lane) - 1u))] = i;
         nU += __popc(um);
@@ -388,7 +391,10 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
       if (lane == 0) {
         s_nU = nU;
         s_stop = anyO ? 0 : 1;
-        s_ncand = 0;
+        // the candidate set is {valid, unpinned, source in O, not moved}: with O unchanged it is
+        // last round's list minus the request just moved (skipped in the evaluation below)
+        s_reuse = (round > 0 && !chO) ? 1 : 0;
+        if (!s_reuse) s_ncand = 0;
       }
     }
     __syncthreads();
@@ -472,7 +478,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     // ---- candidate compaction: requests on overloaded instances, not pinned, not yet moved ----
     // (round 0 also validates each slot once and marks the slots that can never be candidates)
     // four consecutive slots per lane (one 16-byte shared load), one atomic per warp
-    for (int base = 0; base < nslots; base += 4 * nthreads) {
+    for (int base = 0; base < (s_reuse ? 0 : nslots); base += 4 * nthreads) {
       const int g0 = base + 4 * tid;
       uint32_t cm = 0;   // candidate bits of slots g0..g0+3
       if (g0 < nslots) {   // nslots is a multiple of 16 (pitch)
@@ -531,6 +537,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     const int nU = s_nU, ncand = s_ncand;
     for (int c = tid; c < ncand; c += nthreads) {
       const int g = s.cidx[c];
+      if ((s.moved[g >> 5] >> (g & 31)) & 1u) continue;   // moved earlier in this call (reused list)
       const int src = s.rinst[g];
       const int32_t N = s.rntok[g], nh = s.rnhat[g];
       int T = nh - 1 < 0 ? 0 : (nh - 1 > a.H ? a.H : nh - 1);
