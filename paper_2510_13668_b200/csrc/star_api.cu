@@ -383,7 +383,12 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
   bool ok = true;
   ok &= alloc(&p->Z1, (size_t)max_rows * m1 * esz * kx);
   ok &= alloc(&p->Z2, (size_t)max_rows * m2 * esz * kx);
-  p->ws_floats = (size_t)g_num_sms * 128 * 256;
+  // split-K partials (128 x 256 fp32 per CTA tile and split): layer-1 split-K and CTA-pair grids
+  // stay within one wave (<= SMs tiles x splits); the fused tail needs m_tiles x (m2/256) x S with
+  // S = 4 (S = 2 only bounds the grid to one wave for the plain forward; the refresh grid may
+  // run every m-tile with the S chosen for its row estimate)
+  const size_t tail_tiles = (size_t)((max_rows + 127) / 128) * (m2 / 256 > 0 ? m2 / 256 : 1) * 4;
+  p->ws_floats = (tail_tiles > (size_t)g_num_sms ? tail_tiles : (size_t)g_num_sms) * 128 * 256;
   ok &= alloc(reinterpret_cast<void**>(&p->ws), p->ws_floats * 4);
   ok &= alloc(reinterpret_cast<void**>(&p->head_ws), (size_t)g_num_sms * 128 * 4);
   ok &= alloc(reinterpret_cast<void**>(&p->ws3), (size_t)((max_rows + 127) / 128) * 16 * 64 * 128 * 4);

@@ -326,7 +326,7 @@ def test_fused_step_projection_equals_oracle(star, oracle_mod):
 # ============================================================================ fused forward+projection
 @pytest.mark.parametrize("cfg,R,seed", [("C2", 2048, 0), ("C2", 2047, 1), ("C2", 1, 2), ("C2", 100, 3),
                                         ("C3", 4096, 4), ("TGT", 512, 5), ("C2", 256, 6), ("C1", 128, 7),
-                                        ("C4", 4096, 8), ("C2", 3000, 9)])
+                                        ("C4", 4096, 8), ("C2", 3000, 9), ("C2", 8192, 10)])
 def test_fused_forward_project_equals_standalone(star, oracle_mod, cfg, R, seed):
     """lenpred_forward_project == lenpred_forward + project_instance_load, bit for bit (y_hat,
     N_hat, L, W, peak, growth, count), and its projection equals the oracle projection of the
@@ -490,7 +490,8 @@ def test_refresh_step_parity(star, oracle_mod, R, k, seed):
     pred.close()
 
 
-@pytest.mark.parametrize("R,k,seed,n", [(2048, 20, 0, 8), (777, 7, 1, 3), (64, 1, 2, 1), (5000, 20, 3, 64)])
+@pytest.mark.parametrize("R,k,seed,n", [(2048, 20, 0, 8), (777, 7, 1, 3), (64, 1, 2, 1), (5000, 20, 3, 64),
+                                        (6000, 20, 4, 8)])
 def test_refresh_project_fused_equals_separate(star, oracle_mod, R, k, seed, n):
     """lenpred_forward_refresh_project (aging scatter fused with the projection, one CTA) ==
     lenpred_forward_refresh + project_instance_load, bit for bit (N_hat, cadence state, L, W, peak,
@@ -505,6 +506,8 @@ def test_refresh_project_fused_equals_separate(star, oracle_mod, R, k, seed, n):
     h = _dev(datagen.make_hidden(seed, R, c["d"], "bf16", scale=scale), torch.bfloat16)
     gen = g.integers(0, 5000, R).astype(np.int32)
     g_last = np.where(g.random(R) < 0.1, -1, gen - g.integers(0, 2 * k + 1, R)).astype(np.int32)
+    if R >= 6000:   # first step of a batch: no prediction yet, every row due (the grid runs every m-tile)
+        g_last[:] = -1
     nhat_last = g.integers(0, 30000, R).astype(np.int32)
     W, _ = _weights_dev(pw)
     pred = star.Predictor(*W, max_rows=R)
