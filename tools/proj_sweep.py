@@ -40,4 +40,4 @@ for _ in range(10):   # 10 launches back to back per span: device time (inputs b
     e1.record(); e1.synchronize()
     ts.append(e0.elapsed_time(e1) / 10)
 t = float(np.median(ts)) * 1e-3
-print(f"n_inst={n} R=2^{R.bit_length()-1} {sys.argv[2:3]} {os.environ.get('STAR_PROJ_BULK', '0')}: {t*1e6:.1f} us, {12*R/t/1e9:.0f} GB/s, err={err.item()}")
+print(f"n_inst={n} R=2^{R.bit_length()-1} {sys.argv[2:3]}: {t*1e6:.1f} us, {12*R/t/1e9:.0f} GB/s, err={err.item()}")
