@@ -680,6 +680,16 @@ def run_star(args):
             "step_us_warm_l2": warm_us, "requests_per_s_per_gpu": value / world}
     if graph_error:
         line["graph_error"] = graph_error
+    # the paper's own figures (other hardware, context only), next to this run's
+    line["paper_context"] = {
+        "predictor_latency_ms": {"batch1": 1.33, "batch10": 1.40, "hw": "RTX 4090D (PAPER.md:306, 466)"},
+        "decode_iteration_ms": {"value": 18.23, "hw": "RTX 4090D, R1-Distill-Qwen-7B W8A8 (PAPER.md:466)"},
+        "overhead_pct": {"k1": 7.68, "k20": 0.38, "source": "PAPER.md:466-469"},
+        "mae_tokens": {"value": 3873.21, "source": "PAPER.md:280-287, 305 (trained weights not available here)"},
+        "p99_tpot_ms_sharegpt": {"vllm": 96.3, "vllm_rescheduling": 28.3, "star": 24.3,
+                                 "hw": "4x RTX 4090D (PAPER.md:488, 577)"},
+        "goodput_x_vs_vllm": {"sharegpt": 1.93, "max": 2.24, "source": "PAPER.md:15, 571, 652"},
+        "this_run_step_ms": ms_per_step}
     try:
         line["plan_stats"] = {"moves_per_step": len(step.result()), "max_moves": c["max_moves"]}
     except Exception as ex:
