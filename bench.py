@@ -8,9 +8,10 @@ per-instance loads -> (NCCL all-gather of the per-rank records when N > 1) -> Al
     python bench.py [--gpus N --steps K --warmup W] [--config C2] [--impl star|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
 
-Defaults: N=1, workload BASELINE.json configs[1] ("C2": 8 instances x 256 requests, hidden 4096,
-bf16, long-tailed CoT lengths).  Sharding: the 8 instances are split in contiguous blocks over
-the N ranks (strong scaling: total work fixed).  The step is one CUDA graph
+Defaults: N=1, workload TGT, the north-star point (8 instances x 512 requests, hidden 4096, bf16,
+long-tailed CoT lengths, instance 0 overloaded so Alg. 1 moves a request every step).  Sharding:
+the 8 instances are split in contiguous blocks over the N ranks (one decode instance per GPU at
+N = 8; total work fixed).  The step is one CUDA graph
 [L2 flush (256 MB write) -> event -> step -> event]: the events are graph nodes on the step's
 stream, so the timed span excludes the flush and host launch latency; the reported time is the
 max over ranks of the summed per-step times.  Prints ONE JSON line.
@@ -43,7 +44,7 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["star", "reference"], default="star")
-    ap.add_argument("--config", default="C2", choices=CONFIG_ORDER)
+    ap.add_argument("--config", default="TGT", choices=CONFIG_ORDER)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
@@ -87,13 +88,15 @@ def make_workload(cfg_name, world, rank, seed):
     return c, snap, params, idx, pw, h
 
 
-def config_block(cfg_name, c, world, graph, flush):
+def config_block(cfg_name, c, world):
+    """The workload (identical in both arms; timing details are separate keys of the line)."""
     return {"workload": f"{cfg_name}: {c['desc']}", "n_inst": c["n_inst"], "requests_per_instance": c["r_per_inst"],
             "total_requests": c["n_inst"] * c["r_per_inst"], "hidden": c["d"], "m1_m2_m3": [2048, 512, 64],
-            "H": 50, "max_moves": c["max_moves"], "instances_per_gpu": c["n_inst"] // world,
+            "dtype": c["dtype"], "H": 50, "max_moves": c["max_moves"], "skewed": bool(c.get("skewed", False)),
+            "instances_per_gpu": c["n_inst"] // world,
             "parallelism": f"instance-sharded x{world} (one NCCL all-gather of per-rank records)",
-            "l2": "flushed before every timed step (256 MB write, outside the timed span)" if flush else "warm",
-            "cuda_graph": graph, "n_hat_source": "GPU predictor (hidden rows scaled so predictions are long-tailed)"}
+            "l2": "GPU arm: flushed before every timed step (256 MB write, outside the timed span)",
+            "n_hat_source": "the arm's own predictor (hidden rows scaled so predictions are long-tailed)"}
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -146,76 +149,98 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ oracle timing
-def oracle_step_sample(snap, params, idx_all, pw, h_rows, nthreads):
-    """Times the oracle (as it stands) on: predictor over the given hidden rows, projection and
-    plan over the whole snapshot.  Returns (t_pred, n_rows, t_proj, t_plan)."""
+def oracle_full_step(snap, params, pw, h_all, nthreads):
+    """One whole step of the oracle (as it stands) on the whole workload: Eq. 2 over EVERY
+    running request's hidden row (fp64 loops, OpenMP over rows), the quantizer, the projection
+    and Alg. 1 over the whole snapshot.  Returns (t_pred, t_proj, t_plan, n_moves) in seconds."""
     import oracle
     t0 = time.perf_counter()
-    oracle.lenpred_weights(h_rows, pw, nthreads=nthreads)
+    y = oracle.lenpred_weights(h_all, pw, nthreads=nthreads)
+    n_hat = oracle.quantize(y.astype(np.float32), snap.n_tok)
     t1 = time.perf_counter()
-    n_hat = snap.true_rem
     P = oracle.project(snap.inst, snap.n_tok, n_hat, snap.n_inst, params.H, params.beta_q)
     t2 = time.perf_counter()
-    oracle.plan(params, P["L"], snap.req_id, snap.inst, snap.n_tok, n_hat, snap.pinned)
+    moves = oracle.plan(params, P["L"], snap.req_id, snap.inst, snap.n_tok, n_hat, snap.pinned)
     t3 = time.perf_counter()
-    return t1 - t0, h_rows.shape[0], t2 - t1, t3 - t2
+    return t1 - t0, t2 - t1, t3 - t2, len(moves)
+
+
+def oracle_workload(cfg_name, seed):
+    """The GPU arm's workload at N = 1 (all ranks' hidden rows in instance-rank order)."""
+    import datagen   # (no product import on this path)
+    c = datagen.CONFIGS[cfg_name]
+    snap = datagen.make_snapshot(seed, c["n_inst"], c["r_per_inst"], skewed=c.get("skewed", False))
+    params = datagen.make_plan_params(snap, H=50, mem_factor=c.get("mem_factor", 1.10), max_moves=c["max_moves"])
+    idx = np.arange(snap.R)   # N = 1: one rank owns every instance
+    pw = datagen.make_predictor_weights(seed, c["d"], c["dtype"])
+    h = datagen.make_hidden(seed * 1000, len(idx), c["d"], c["dtype"])
+    # long-tailed self-predictions, as in the GPU arm: rows scaled by true_rem / median(y_hat),
+    # the median taken from this arm's own predictor (untimed setup)
+    import oracle
+    y0 = oracle.lenpred_weights(h, pw)
+    scale = np.maximum(snap.true_rem[idx], 1).astype(np.float32) / max(float(np.median(y0)), 1e-3)
+    h = datagen.round_to_dtype(h * scale[:, None], c["dtype"])
+    return c, snap, params, pw, h
 
 
 def cpu_baseline(cfg_name, seed, budget_s):
-    import datagen
-    c, snap, params, idx, pw, _ = make_workload(cfg_name, 1, 0, seed)
-    R_total = snap.R
+    """The oracle timed on the host cores: whole steps of the bench workload (no extrapolation),
+    as many as fit in the budget (at least one)."""
+    import oracle
+    oracle.build()
+    c, snap, params, pw, h = oracle_workload(cfg_name, seed)
     cores = os.cpu_count() or 1
-    h1 = datagen.make_hidden(seed + 99, 1, c["d"], c["dtype"])
-    tp, _, _, _ = oracle_step_sample(snap, params, idx, pw, h1, cores)   # calibration
-    rows = int(max(cores, min(R_total, budget_s / max(tp, 1e-4) * 0.8)))
-    rows = max(1, min(rows, R_total))
-    h = datagen.make_hidden(seed + 98, rows, c["d"], c["dtype"])
-    t_pred, n_rows, t_proj, t_plan = oracle_step_sample(snap, params, idx, pw, h, cores)
-    t_step = t_pred * (R_total / n_rows) + t_proj + t_plan
-    return {"value": R_total / t_step, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": (f"oracle predictor (fp64 loops, OpenMP {cores} threads) on {n_rows} of {R_total} hidden rows "
-                       f"({t_pred:.2f} s, extrapolated linearly); projection ({t_proj * 1e3:.1f} ms) and plan "
-                       f"({t_plan * 1e3:.1f} ms) single-threaded on the full snapshot"),
-            "s_per_step_extrapolated": t_step}
+    ts = []
+    t_beg = time.perf_counter()
+    while not ts or (time.perf_counter() - t_beg + ts[-1] <= budget_s and len(ts) < 20):
+        tp, tj, tl, nm = oracle_full_step(snap, params, pw, h, cores)
+        ts.append(tp + tj + tl)
+    t_step = float(np.mean(ts))
+    return {"value": snap.R / t_step, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": (f"{len(ts)} whole step(s) of the bench workload ({snap.R} requests): oracle Eq. 2 on every "
+                       f"hidden row (fp64 loops, OpenMP {cores} threads, {tp:.2f} s), quantizer, projection "
+                       f"({tj * 1e3:.1f} ms) and Alg. 1 ({tl * 1e3:.1f} ms, {nm} move(s)) single-threaded"),
+            "s_per_step": t_step}
 
 
 # ------------------------------------------------------------------------------ reference arm
 def run_reference(args):
+    """Reference arm: the plain CPU oracle (the paper ships no code) timed as it stands on the
+    host cores; every step is a WHOLE step of the same workload (no sampling, no extrapolation)."""
     rank, _, world = dist_env()
     if rank != 0:
         return 0
-    import datagen
     import oracle
     oracle.build()
-    c, snap, params, idx, pw, _ = make_workload(args.config, 1, 0, args.seed)
-    R_total = snap.R
+    c, snap, params, pw, h = oracle_workload(args.config, args.seed)
     cores = os.cpu_count() or 1
-    per_step_budget = max(0.05, min(2.0, 150.0 / max(args.steps + args.warmup, 1)))
-    h1 = datagen.make_hidden(args.seed + 99, 1, c["d"], c["dtype"])
-    tp, _, tproj, tplan = oracle_step_sample(snap, params, idx, pw, h1, cores)
-    rows = int(max(1, min(R_total, (per_step_budget - tproj - tplan) / max(tp, 1e-4))))
-    h = datagen.make_hidden(args.seed + 98, rows, c["d"], c["dtype"])
     for _ in range(args.warmup):
-        oracle_step_sample(snap, params, idx, pw, h, cores)
-    est = []
+        oracle_full_step(snap, params, pw, h, cores)
+    ts, parts = [], np.zeros(3)
+    nm = 0
     t_wall0 = time.perf_counter()
     for _ in range(args.steps):
-        t_pred, n_rows, t_proj, t_plan = oracle_step_sample(snap, params, idx, pw, h, cores)
-        est.append(t_pred * (R_total / n_rows) + t_proj + t_plan)
+        tp, tj, tl, nm = oracle_full_step(snap, params, pw, h, cores)
+        ts.append(tp + tj + tl)
+        parts += (tp, tj, tl)
     wall = time.perf_counter() - t_wall0
-    t_step = float(np.mean(est))
-    value = R_total / t_step
-    sample = (f"each step: oracle predictor on {rows} of {R_total} rows (OpenMP {cores} threads, extrapolated "
-              f"linearly to all rows) + projection and plan on the full snapshot")
+    t_step = wall / max(args.steps, 1)
+    value = snap.R / t_step
+    sample = (f"every step is the whole workload ({snap.R} requests): oracle Eq. 2 on every hidden row (fp64 "
+              f"loops, OpenMP {cores} threads), quantizer, projection and Alg. 1 single-threaded "
+              f"({nm} move(s) per step)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(args.config, c, 1, False, False),
+            "config": config_block(args.config, c, args.gpus),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "stage_ms": {"predict": round(parts[0] / args.steps * 1e3, 2),
+                         "project": round(parts[1] / args.steps * 1e3, 3),
+                         "plan": round(parts[2] / args.steps * 1e3, 3)},
             "wall_s_timed": wall,
-            "note": "The paper ships no code; the reference arm is the plain CPU oracle written from the paper."}
+            "note": "The paper ships no code; the reference arm is the plain CPU oracle written from the paper, "
+                    "timed over whole steps (wall clock of the K timed steps / K)."}
     print(json.dumps(line))
     return 0
 
@@ -387,10 +412,14 @@ def tgt_rank_timing(star, Step, dev, flush, seed=0, reps=200, world=8):
             "us_per_step_p50": round(float(np.median(ts)), 2), "us_per_step_p99": round(float(np.percentile(ts, 99)), 2),
             "us_per_step_min": round(float(np.min(ts)), 2), "us_per_step_p10": round(float(np.percentile(ts, 10)), 2),
             "target_us": 50.0, "launches_per_step": launches, "moves": n_moves,
+            "exchange_budget_us": round(50.0 - float(np.median(ts)), 2),
+            "exchange_estimate_us": "5-15 (SURVEY.md 8(d): NCCL all-gather of 8 x %d B over NVLink; unmeasured here, "
+                                    "one GPU)" % (buf.numel() // world),
             "stage_us": {"predict+project": round(acc[0], 2), "plan_4096_gathered": round(acc[1], 2)},
             "l2": "flushed before every step" if flush is not None else "warm",
             "note": "one GPU: the other 7 ranks' records are pre-computed into the gathered buffer; the NCCL "
-                    "all-gather (8 x %d B) is not in the timed span" % (buf.numel() // world)}
+                    "all-gather (8 x %d B) is NOT in the timed span: the span plus the all-gather must fit "
+                    "50 us, i.e. the all-gather has exchange_budget_us" % (buf.numel() // world)}
 
 
 def run_star(args):
@@ -671,7 +700,8 @@ def run_star(args):
             "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "us_per_step": ms_per_step * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": c["dtype"],
             "data": "synthetic (seeded datagen: N(0,1) hidden states, He-normal weights, long-tailed CoT lengths)",
-            "config": config_block(args.config, c, world, use_graph, flush is not None),
+            "config": config_block(args.config, c, world), "cuda_graph": use_graph,
+            "l2_flushed": flush is not None,
             "roofline": roofline, "stage_us": stage,
             "gpu_launches": (launches if launches is not None else 3 + (world > 1)) * args.steps,
             "launches_per_step": launches,

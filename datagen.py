@@ -17,7 +17,8 @@ Recipe (PAPER.md citations):
   * running snapshot: L_out length-biased (long requests occupy slots longer),
     g ~ U{0..L_out-1}, N = p + g, true remaining = L_out - g (STAR-Oracle N̂).
   * instance assignment round-robin; "skewed": instance 0 gets 2x the share
-    of near-cap requests (config C4).
+    of near-cap requests (configs C3, C4, TGT: the overloaded instance puts Alg. 1 past Phase 1,
+    PAPER.md:428-451, so every planned step scores candidates and moves a request).
   * plan params: H=50, beta_q[t] = round(65536*0.95^t) (SPEC.md:122 reading A6),
     theta = 1/10, T_exec = 5 ms + 10 ns/token, C_mig = c1 * N with
     c1 = KV bytes/token * 8 / bandwidth (Llama-3-8B bf16 KV 131072 B/token over 900 GB/s).
@@ -281,10 +282,12 @@ CONFIGS = {
                desc="2 decode instances x 64 requests, hidden 896 (Qwen2.5-0.5B-shaped), fp32, 1 reschedule round"),
     "C2": dict(n_inst=8, r_per_inst=256, d=4096, dtype="bf16", max_moves=1,
                desc="8 instances x 256 requests, hidden 4096 (Llama-3-8B-shaped), bf16, long-tailed CoT lengths"),
-    "C3": dict(n_inst=8, r_per_inst=512, d=5120, dtype="bf16", max_moves=1,
-               desc="8 instances x 512 requests, hidden 5120 (Qwen-32B-shaped), per-step prediction + rebalance"),
+    "C3": dict(n_inst=8, r_per_inst=512, d=5120, dtype="bf16", max_moves=1, skewed=True,
+               desc="8 instances x 512 requests, hidden 5120 (Qwen-32B-shaped), per-step prediction + rebalance "
+                    "(instance 0 holds 2x the near-cap share, so Alg. 1 moves a request every step)"),
     "C4": dict(n_inst=4, r_per_inst=1024, d=4096, dtype="bf16", max_moves=4, skewed=True, mem_factor=1.02,
                desc="4 instances x 1024 requests, hidden 4096, skewed arrivals near KV-OOM"),
-    "TGT": dict(n_inst=8, r_per_inst=512, d=4096, dtype="bf16", max_moves=1,
-                desc="north-star target: 8 instances x 512 requests, hidden 4096, bf16"),
+    "TGT": dict(n_inst=8, r_per_inst=512, d=4096, dtype="bf16", max_moves=1, skewed=True,
+                desc="north-star target: 8 instances x 512 requests, hidden 4096, bf16, skewed (instance 0 holds "
+                     "2x the near-cap share: overloaded, so Alg. 1 reaches Phases 2-3 and moves a request)"),
 }

@@ -565,11 +565,7 @@ __global__ void __launch_bounds__(192, 1)
       if (threadIdx.x == 64) {
         int* ctr = p.l1_cnt + 2 * cta_tile;
         atomicAdd(ctr, 1);
-        int seen;
-        do {
-          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
-          if (seen < splits) __nanosleep(64);
-        } while (seen < splits);
+        spin_wait_geq(ctr, splits);   // co-residency checked on the host; traps after ~2 s
         if (tl) tl[8] = globaltimer_ns();
         // the S-1 partner blocks of the owned columns -> shared memory [32 KB, ...) (ring is free)
         const uint32_t pblk = (uint32_t)OW * 128u * 4u;

@@ -99,17 +99,12 @@ cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg,
   const size_t smem = staged ? plan_fast_smem_layout(a.n, a.H, a.world, a.r_cap)
                              : plan_smem_layout(a.n, a.H, a.world, a.r_cap, false);
   auto kern = staged ? plan_kernel<true> : plan_kernel<false>;
-  static int attr_bytes[2] = {48 * 1024, 48 * 1024};
-  if ((int)smem > attr_bytes[staged]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 48 * 1024) {
+    cudaError_t e = func_attr((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_bytes[staged] = (int)smem;
   }
-  static bool carve[2] = {false, false};
-  if (!carve[staged]) {   // same L1/shared split as the GEMM kernels before it: no SM reconfiguration
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    carve[staged] = true;
-  }
+  // same L1/shared split as the GEMM kernels before it: no SM reconfiguration
+  func_attr((const void*)kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(1, 1, 1);
   cfg.blockDim = dim3(kPlanThreads, 1, 1);

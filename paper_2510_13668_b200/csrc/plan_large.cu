@@ -335,11 +335,9 @@ cudaError_t launch_plan_large(const PlanArgs& a, void* workspace, cudaStream_t s
   scan_grid = scan_grid < 1 ? 1 : (scan_grid > 2 * g_num_sms ? 2 * g_num_sms : scan_grid);
   const size_t H1 = (size_t)a.H + 1;
   const size_t smem = 16 * 3 * H1 + 4 * (size_t)a.n + 4 * (size_t)a.world + (size_t)a.n + 16;
-  static size_t attr = 48 * 1024;
-  if (smem > attr) {
-    e = cudaFuncSetAttribute(plan_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 48 * 1024) {
+    e = func_attr((const void*)plan_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
   }
   cudaLaunchConfig_t cs{};
   cs.gridDim = dim3(scan_grid, 1, 1);

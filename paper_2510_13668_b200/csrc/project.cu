@@ -517,18 +517,13 @@ cudaError_t launch_project(int R, int n_inst, int inst_base, int H, const int32_
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (smem_bins) {
-    static int attr_bytes = 48 * 1024;
-    if ((int)smem > attr_bytes) {
-      cudaError_t e = cudaFuncSetAttribute(project_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
+    if (smem > 48 * 1024) {
+      cudaError_t e = func_attr((const void*)project_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem);
       if (e != cudaSuccess) return e;
-      attr_bytes = (int)smem;
     }
-    static bool carve = false;
-    if (!carve) {   // streaming kernel: prefer shared memory (several CTAs per SM), L1 is bypassed
-      cudaFuncSetAttribute(project_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      carve = true;
-    }
+    // streaming kernel: prefer shared memory (several CTAs per SM), L1 is bypassed
+    func_attr((const void*)project_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return cudaLaunchKernelEx(&cfg, project_kernel<true>, a);
   }
   return cudaLaunchKernelEx(&cfg, project_kernel<false>, a);

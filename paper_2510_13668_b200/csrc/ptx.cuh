@@ -66,6 +66,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Spins until the global counter reaches `target` (acquire).  The CTAs that bump it must be
+// co-resident (the host sizes such grids to one wave); if they are not (MPS, green contexts,
+// another persistent kernel holding SMs), the wait traps after ~2 s instead of hanging the GPU.
+__device__ __forceinline__ void spin_wait_geq(const int* ctr, int target) {
+  int seen;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
+  if (seen >= target) return;
+  const uint64_t t0 = globaltimer_ns();
+  for (uint32_t it = 1;; ++it) {
+    __nanosleep(64);
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
+    if (seen >= target) return;
+    if ((it & 63u) == 0 && globaltimer_ns() - t0 > 2000000000ull) __trap();
+  }
+}
+
 // ------------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

@@ -207,12 +207,10 @@ cudaError_t launch_refresh_scatter_project(const ProjArgs& a, const int32_t* pos
                                            const int32_t* gen, int32_t* g_last, int32_t* nhat_last,
                                            const int32_t* M_dev, int32_t* n_refreshed, cudaStream_t st) {
   const size_t smem = refresh_scatter_project_smem(a.n_inst, a.H);
-  static int attr = 48 * 1024;
-  if ((int)smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(refresh_scatter_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  if (smem > 48 * 1024) {
+    cudaError_t e = func_attr((const void*)refresh_scatter_project_kernel,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = (int)smem;
   }
   cudaLaunchAttribute at[1];
   cudaLaunchConfig_t cfg = pdl_cfg(dim3(1), dim3(kScatProjThreads), st, at);

@@ -7,8 +7,10 @@
 #include <cstdio>
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 
 #include "lenpred_kernels.cuh"
 #include "lenpred_tail.cuh"
@@ -72,6 +74,22 @@ static star_status ensure_device() {
   return STAR_OK;
 }
 
+cudaError_t func_attr(const void* func, cudaFuncAttribute attr, int value) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int>, int> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_tuple(dev, func, (int)attr);
+  auto it = done.find(key);
+  const bool grow = attr == cudaFuncAttributeMaxDynamicSharedMemorySize;
+  if (it != done.end() && (grow ? it->second >= value : true)) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, attr, value);
+  if (e == cudaSuccess) done[key] = value;
+  return e;
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -107,12 +125,10 @@ static star_status make_tmap(CUtensorMap* m, const void* base, bool f32, uint64_
 template <int BN, bool TF32>
 static cudaError_t launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmArgs& p,
                                  int m_tiles, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(umma_gemm_kernel<BN, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)GemmSmem<BN>::BYTES);
+  {
+    cudaError_t e = func_attr((const void*)umma_gemm_kernel<BN, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)GemmSmem<BN>::BYTES);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   // grid (m tiles, n tiles, K splits); the splits of one output tile form a cluster along z
   // (co-scheduled, so they can exchange partials behind a cluster barrier).  Programmatic
@@ -150,18 +166,16 @@ static cudaError_t launch_gemm(int BN, bool tf32, const CUtensorMap& a, const CU
 // CTA-pair layer-1 GEMM: grid (m tiles rounded up to even, n tiles), clusters of 2 along M, PDL.
 static cudaError_t launch_pair_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmArgs& p,
                                    int m_tiles, cudaStream_t st, bool nu = false) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(umma_pair_gemm_kernel<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)PairSmem<256>::BYTES);
+  {
+    cudaError_t e = func_attr((const void*)umma_pair_gemm_kernel<256, false>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairSmem<256>::BYTES);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(umma_pair_gemm_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)PairSmem<256>::BYTES);
+      e = func_attr((const void*)umma_pair_gemm_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    (int)PairSmem<256>::BYTES);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(umma_pair_gemm_kernel<256, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)PairSmem<256>::BYTES);
+      e = func_attr((const void*)umma_pair_gemm_kernel<256, false, true>,
+                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairSmem<256>::BYTES);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   cudaLaunchConfig_t cfg{};
   // nu: N = 2048 as 9 tiles of 224 / 240 columns; splits: K ranges (one wave, <= SMs)
@@ -237,14 +251,13 @@ static void plan_splits(int tiles, int num_kb, int bn, bool tf32, int* splits, i
 // (m_tiles, n2, S), one cluster per layer-2 tile (its S split-K CTAs), PDL.
 static cudaError_t launch_tail(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& w3, const TailArgs& t,
                                int m_tiles, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tail_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)TailSmem::BYTES);
+  {
+    cudaError_t e = func_attr((const void*)tail_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)TailSmem::BYTES);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(tail_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TailSmem::BYTES);
+      e = func_attr((const void*)tail_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    (int)TailSmem::BYTES);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = t.mn_swap ? dim3(t.n2_tiles, m_tiles, t.splits) : dim3(m_tiles, t.n2_tiles, t.splits);

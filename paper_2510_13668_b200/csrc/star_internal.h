@@ -11,6 +11,11 @@ namespace star {
 constexpr int kMaxSmemBytes = 227 * 1024;
 extern int g_num_sms;   // set once by ensure_device()
 
+// Function attributes belong to each device's context: set them per (device, kernel, attribute),
+// under a lock.  cudaFuncAttributeMaxDynamicSharedMemorySize is raised to at least `value`;
+// any other attribute is set to `value` once.  (star_api.cu)
+cudaError_t func_attr(const void* func, cudaFuncAttribute attr, int value);
+
 // project.cu
 size_t project_workspace_bytes(int n_inst, int H);
 int project_single_cta_max_rows();

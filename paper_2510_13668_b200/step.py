@@ -102,12 +102,15 @@ class Step:
     def __init__(self, predictor: _lib.Predictor, params: _lib.PlanParams, n_inst: int, r_cap: int,
                  rank: int = 0, world: int = 1, group=None, device: Optional[torch.device] = None,
                  max_ctx_len: int = _lib.L_CTX, refresh_k: Optional[int] = None,
-                 gathered: Optional[torch.Tensor] = None):
+                 gathered: Optional[torch.Tensor] = None, force_collective: bool = False):
         """gathered: (single-GPU measurement of one rank of a W-rank job) a caller-owned buffer of
         world * nbytes holding the OTHER ranks' records as the all-gather would deliver them; this
         rank's record is written in place at slot `rank` and no collective is issued."""
         if n_inst % world:
             raise ValueError(f"n_inst={n_inst} must be divisible by world={world}")
+        # force_collective: take the W > 1 path (separate plan launch after an all-gather over
+        # `group`) even at world 1 -- exercises the exchange on a one-GPU box
+        self.force_collective = bool(force_collective) and group is not None
         self.pred, self.params = predictor, params
         self.n_inst, self.world, self.rank, self.group = n_inst, world, rank, group
         self.n_loc = n_inst // world
@@ -126,7 +129,7 @@ class Step:
         else:
             self.send = torch.zeros(self.layout.nbytes, dtype=torch.uint8, device=self.device)
             self.recv = (torch.zeros(world * self.layout.nbytes, dtype=torch.uint8, device=self.device)
-                         if world > 1 else self.send)
+                         if world > 1 or self.force_collective else self.send)
         self.v = self.layout.views(self.send)
         self.seg = self.layout.segments(self.recv.data_ptr(), world)
         self.ws = torch.zeros(_lib.project_workspace_bytes(self.n_loc, self.H), dtype=torch.uint8, device=self.device)
@@ -161,6 +164,11 @@ class Step:
             v["pinned"][:R].zero_()
         v["count"].fill_(R)
         self.R = R
+        if self.refresh_k is not None:
+            # new occupants: no prediction yet (a slot must not inherit the previous request's
+            # cadence state, reading A27); set_generation() may install an explicit state after
+            self.g_last[:R].fill_(-1)
+            self.nhat_last[:R].zero_()
 
     def set_generation(self, gen, g_last=None, nhat_last=None, non_blocking=False):
         """Refresh mode: tokens generated so far per slot (and optionally the cadence state)."""
@@ -183,11 +191,10 @@ class Step:
                                                  inst_base=self.rank * self.n_loc, max_ctx_len=self.max_ctx_len,
                                                  n_hat=v["n_hat"][:max(R, 1)], n_refreshed=self.n_refreshed,
                                                  out=self.proj_out, err_flag=self.err, R=R, stream=stream)
-            if self.world > 1 and not self.emulated:
-                exchange(self.send, self.recv, self.group)
+            self._exchange(stream)
             _lib.plan_reschedule_segmented(self.params, self.seg, self.moves, self.n_moves, self.err, stream=stream)
             return self.moves, self.n_moves
-        if self.world == 1:
+        if self.world == 1 and not self.force_collective:
             # one rank: forward + projection + Alg. 1 (the plan runs in the fused tail's last CTA)
             _lib.lenpred_forward_project_plan(self.pred, h[:R], v["n_tok"][:R], v["inst"][:R], self.n_loc, self.H,
                                               self.params.beta_q, self.ws, self.params, self.seg, self.moves,
@@ -199,10 +206,21 @@ class Step:
                                      self.params.beta_q, self.ws, inst_base=self.rank * self.n_loc,
                                      max_ctx_len=self.max_ctx_len, n_hat=v["n_hat"][:max(R, 1)],
                                      out=self.proj_out, err_flag=self.err, want_y=False, stream=stream)
-        if self.world > 1 and not self.emulated:
-            exchange(self.send, self.recv, self.group)
+        self._exchange(stream)
         _lib.plan_reschedule_segmented(self.params, self.seg, self.moves, self.n_moves, self.err, stream=stream)
         return self.moves, self.n_moves
+
+    def _exchange(self, stream=None):
+        """The all-gather, ordered on the SAME stream as the kernels around it: the NCCL collective
+        is enqueued on `stream` (torch.distributed uses the current stream), so it reads the record
+        only after the predictor/projection wrote it and the plan reads `recv` only after it landed."""
+        if (self.world == 1 and not self.force_collective) or self.emulated:
+            return
+        if stream is None:
+            exchange(self.send, self.recv, self.group)
+        else:
+            with torch.cuda.stream(stream):
+                exchange(self.send, self.recv, self.group)
 
     def capture(self, h: torch.Tensor):
         """Captures run(h) into a CUDA graph (one launch per step)."""
