@@ -73,10 +73,12 @@ def load_peaks():
 
 
 # ------------------------------------------------------------------------------ workload
-def make_workload(cfg_name, world, rank, seed):
+def make_workload(cfg_name, world, rank, seed, r_per=None):
     import datagen
     from paper_2510_13668_b200.step import split_snapshot_by_rank
-    c = datagen.CONFIGS[cfg_name]
+    c = dict(datagen.CONFIGS[cfg_name])
+    if r_per is not None:
+        c["r_per_inst"] = r_per
     n_inst, r_per = c["n_inst"], c["r_per_inst"]
     if n_inst % world:
         raise SystemExit(f"config {cfg_name} has {n_inst} instances; --gpus {world} must divide it")
@@ -269,17 +271,18 @@ def _ncu_traffic(key):
     return None
 
 
-def _projection_point(star, snap, params, dev, R, reps=10):
-    """Per-launch time of the standalone projection over R instance-grouped requests (R / 65536
-    instances of 65536, the documented per-instance bound; the C2 snapshot tiled), 10 launches
-    back to back per event span (no host latency in the span); inputs beyond L2 stream from HBM."""
+def _projection_point(star, snap, params, dev, R, reps=10, grouped=True):
+    """Per-launch time of the standalone projection over R requests of R / 65536 instances (the
+    documented per-instance bound; the C2 snapshot tiled), 10 launches back to back per event span
+    (no host latency in the span); inputs beyond L2 stream from HBM.  grouped: requests sorted by
+    instance (a worker's running batch); otherwise shuffled (every instance interleaved)."""
     import torch
     reps_tile = (R + snap.R - 1) // snap.R
-    per = R // 65536 // snap.n_inst          # tiles per instance group: tile k -> instances 8*(k % per) + inst
+    per = max(R // 65536 // snap.n_inst, 1)   # tiles per instance group: tile k -> instances 8*(k % per) + inst
     n = snap.n_inst * per
     shift = (np.arange(reps_tile, dtype=np.int64) % per * snap.n_inst).repeat(snap.R)[:R]
     inst_h = (np.tile(snap.inst, reps_tile)[:R] + shift).astype(np.int32)
-    order = np.argsort(inst_h, kind="stable")   # instance-grouped (a worker's running batch)
+    order = np.argsort(inst_h, kind="stable") if grouped else np.random.default_rng(1).permutation(R)
     inst = torch.from_numpy(inst_h[order]).to(dev)
     ntok = torch.from_numpy(np.tile(snap.n_tok, reps_tile)[:R][order]).to(dev)
     nhat = torch.from_numpy(np.tile(snap.true_rem.astype(np.int32), reps_tile)[:R][order]).to(dev)
@@ -306,22 +309,30 @@ def _projection_point(star, snap, params, dev, R, reps=10):
 
 def projection_sweep(star, snap, params, dev, peaks, R=1 << 24):
     """Bandwidth-scale evidence for the projection kernel: the standalone
-    project_instance_load over R = 2^24 requests (201 MB, beyond L2) -- the headline point -- and
-    2^25 (403 MB); algorithmic bytes = 12 B x R (+ outputs)."""
-    t_med, n, algo = _projection_point(star, snap, params, dev, R)
-    gbs = algo / t_med / 1e9
-    sweep = [{"requests": R, "instances": n, "us": round(t_med * 1e6, 2), "GBps": round(gbs, 1),
-              "frac": round(gbs / peaks["hbm_gbs"], 4)}]
-    t2, n2, algo2 = _projection_point(star, snap, params, dev, 2 * R)
-    sweep.append({"requests": 2 * R, "instances": n2, "us": round(t2 * 1e6, 2), "GBps": round(algo2 / t2 / 1e9, 1),
-                  "frac": round(algo2 / t2 / 1e9 / peaks["hbm_gbs"], 4)})
+    project_instance_load over R = 2^20 ... 2^26 requests (12.6 MB ... 805 MB), instance-grouped
+    and shuffled; algorithmic bytes = 12 B x R (+ outputs).  Headline point: 2^24 grouped."""
+    sweep = []
+    head = None
+    for lg in (20, 22, 24, 25, 26):
+        for grouped in (True, False):
+            Rk = 1 << lg
+            t, n, algo = _projection_point(star, snap, params, dev, Rk, grouped=grouped)
+            gbs = algo / t / 1e9
+            pt = {"requests": Rk, "instances": n, "order": "grouped" if grouped else "shuffled",
+                  "bins": n * (params.H + 2), "us": round(t * 1e6, 2), "GBps": round(gbs, 1),
+                  "frac": round(gbs / peaks["hbm_gbs"], 4)}
+            sweep.append(pt)
+            if Rk == R and grouped:
+                head = (t, n, algo, gbs)
+    t_med, n, algo, gbs = head
     return {"kernel": "project_ldg_kernel (standalone, windowed histogram, 2 CTAs/SM)", "bound": "hbm", "requests": R,
             "algorithmic_bytes": algo, "avg_launch_us": t_med * 1e6, "achieved": gbs, "peak": peaks["hbm_gbs"],
             "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"], "traffic": _ncu_traffic("sweep/project"),
             "instances": n, "sweep": sweep,
-            "note": "inputs beyond L2 (201 MB; the C2 snapshot tiled over 256 instances x 65536 requests, "
-                    "instance-grouped as a worker's batch is); the in-step projection is fused into the "
-                    "predictor tail"}
+            "note": "headline: 2^24 requests (201 MB, beyond L2), the C2 snapshot tiled over 256 instances x 65536 "
+                    "requests, instance-grouped as a worker's batch is; 'shuffled' = every instance interleaved "
+                    "(beyond the 3072-bin shared-memory window the kernel falls back to global 64-bit atomics); "
+                    "the in-step projection is fused into the predictor tail"}
 
 
 def longtail_hidden(star, pred, h_np, snap, idx, tdt, dev):
@@ -336,18 +347,19 @@ def longtail_hidden(star, pred, h_np, snap, idx, tdt, dev):
     return torch.from_numpy((h_np * scale[:, None]).astype(np.float32)).to(tdt).to(dev)
 
 
-def tgt_rank_timing(star, Step, dev, flush, seed=0, reps=200, world=8):
+def tgt_rank_timing(star, Step, dev, flush, seed=0, reps=200, world=8, cfg="TGT", r_per=None, stages=True):
     """North-star target point, one rank of the W = 8 job (8 instances x 512 requests, d = 4096,
     bf16; one instance per GPU): this rank's predictor + fused projection over its 512 requests,
     then Alg. 1 over the 8 gathered records (4096 requests).  Measured on ONE GPU: the other 7
     ranks' records are computed first with the same library calls and sit in the gathered buffer
-    as the all-gather would deliver them; the NCCL all-gather itself is not in the timed span."""
+    as the all-gather would deliver them; the NCCL all-gather itself is not in the timed span.
+    (cfg="C5", r_per=R: the same per-rank measurement at R requests per instance.)"""
     import torch
     from paper_2510_13668_b200.step import RecordLayout
     steps, hs = [], []
     buf = pred = params = None
     for k in range(world):
-        c, snap, params_h, idx, pw, h_np = make_workload("TGT", world, k, seed)
+        c, snap, params_h, idx, pw, h_np = make_workload(cfg, world, k, seed, r_per=r_per)
         tdt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
         if pred is None:
             W = [torch.from_numpy(x).to(tdt).to(dev) for x in (pw.W1, pw.W2, pw.W3)]
@@ -386,6 +398,11 @@ def tgt_rank_timing(star, Step, dev, flush, seed=0, reps=200, world=8):
         if i >= 10:
             ts.append(e0.elapsed_time(e1) * 1e3)
     n_moves = int(st.n_moves.item())
+    if not stages:
+        pred.close()
+        return {"requests_per_instance": c["r_per_inst"], "us_per_step_p50": round(float(np.median(ts)), 2),
+                "us_per_step_min": round(float(np.min(ts)), 2), "launches_per_step": launches, "moves": n_moves,
+                "rank_requests_per_s": round(c["r_per_inst"] / (float(np.median(ts)) * 1e-6), 1)}
     # stage split (event nodes between the stages: each costs ~2 us and blocks the PDL overlap, so
     # the stages sum to more than the step)
     es = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)]
@@ -756,6 +773,23 @@ def run_star(args):
             line["tgt_rank"] = tgt_rank_timing(star, Step, dev, flush, seed=args.seed)
         except Exception as ex:
             line["tgt_rank"] = {"error": str(ex)}
+    if world == 1 and not args.profile and not args.no_sweep:
+        try:   # C5 (BASELINE.json configs[4]) at N = 1: the per-rank step of a W = 8 job vs R per instance
+            import datagen
+            line["c5_rank_sweep"] = {
+                "workload": "C5: one rank of W = 8 (one instance per GPU), R requests per instance, d = 4096 bf16, "
+                            "skewed; predictor + fused projection over this rank's R rows, Alg. 1 over the 8 "
+                            "gathered records (8R requests); L2 flushed before every step; the NCCL all-gather "
+                            "is not in the span",
+                "points": [tgt_rank_timing(star, Step, dev, flush, seed=args.seed, reps=60, cfg="C5", r_per=r,
+                                           stages=False) for r in datagen.CONFIGS["C5"]["r_sweep"]]}
+        except Exception as ex:
+            line["c5_rank_sweep"] = {"error": str(ex)}
+        try:
+            import episode
+            line["c4_episode"] = episode.run_episode(star, Step, steps=200, dev=dev)
+        except Exception as ex:
+            line["c4_episode"] = {"error": str(ex)}
     if rank == 0 and not args.profile and not args.no_sweep:
         try:
             line["next_rows"] = next_rows_timing(star, dev)
@@ -840,9 +874,52 @@ def next_rows_timing(star, dev, seed=0):
         star.dispatch_requests(star.DISPATCH_PROJECTED, L1, beta_d, ntok_d, nhat_d, assign=assign, workspace=dws)
     out["dispatch_projected_64_arrivals_onto_256_us"] = device_us(disp)
     del flush
+    out["kv_migration"] = kv_migration_timing(star, dev)
     out["note"] = ("paper: scheduler <= 300 ms at 256 instances (PAPER.md:460); NEXT rows of SURVEY 8(f), "
-                   "bit-exact vs the oracle in tests/test_gpu_parity.py")
+                   "bit-exact vs the oracle in tests/test_gpu_parity.py, tests/test_gpu_migrate.py")
     return out
+
+
+def kv_migration_timing(star, dev, layers=32, blocks_per_layer=1024, n_tok=13_700, reps=5):
+    """NEXT-4 (ExecuteMigration's KV copy): one request of the snapshot's mean
+    running length (~13.7K tokens) in a Llama-3-8B-shaped paged pool (32 layers; block = 16 tokens
+    x 8 KV heads x 128 x K,V x bf16 = 64 KB per layer), fragmented block tables.  Pack (pool ->
+    staging), unpack (staging -> pool) and direct block-to-block migrate on ONE GPU; HBM GB/s =
+    (read + write bytes) / CUDA-event time, against the measured copy peak (read + write).  The
+    NVLink hop needs two GPUs: unmeasured here."""
+    import torch
+    bb = 16 * 8 * 128 * 2 * 2
+    n = (n_tok + 15) // 16
+    g = np.random.default_rng(3)
+    src = torch.empty((layers, blocks_per_layer, bb), dtype=torch.uint8, device=dev)
+    dst = torch.empty_like(src)
+    st = torch.from_numpy(g.permutation(blocks_per_layer)[:n].astype(np.int32)).to(dev)
+    dt = torch.from_numpy(g.permutation(blocks_per_layer)[:n].astype(np.int32)).to(dev)
+    stg = torch.empty((layers, n, bb), dtype=torch.uint8, device=dev)
+    moved = layers * n * bb
+    peak = load_peaks()["hbm_gbs"]
+    res = {"request_tokens": n_tok, "blocks": n, "layers": layers, "block_bytes": bb, "bytes_moved": moved}
+    for name, fn in (("pack", lambda: star.kv_pack(src, st, staging=stg)),
+                     ("unpack", lambda: star.kv_unpack(stg, dst, dt)),
+                     ("migrate", lambda: star.kv_migrate(src, st, dst, dt))):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        t = float(np.median(ts))
+        res[name] = {"us": round(t * 1e6, 1), "GBps": round(2 * moved / t / 1e9, 1),
+                     "frac_hbm": round(2 * moved / t / 1e9 / peak, 4)}
+    res["nvlink"] = ("unmeasured (one GPU); at NVLink 5's 900 GB/s per direction the transfer of this request "
+                     "takes %.2f ms, at the paper's 25 Gbps %.0f ms (PAPER.md:647)" % (moved / 900e9 * 1e3,
+                                                                                     moved * 8 / 25e9 * 1e3))
+    del src, dst, stg
+    return res
 
 
 def refresh_step_timing(star, Step, pred, params, c, snap, idx, h_dev, dev, flush, k=20, reps=50):

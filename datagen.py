@@ -287,6 +287,10 @@ CONFIGS = {
                     "(instance 0 holds 2x the near-cap share, so Alg. 1 moves a request every step)"),
     "C4": dict(n_inst=4, r_per_inst=1024, d=4096, dtype="bf16", max_moves=4, skewed=True, mem_factor=1.02,
                desc="4 instances x 1024 requests, hidden 4096, skewed arrivals near KV-OOM"),
+    "C5": dict(n_inst=8, r_per_inst=512, d=4096, dtype="bf16", max_moves=1, skewed=True,
+               r_sweep=(64, 128, 256, 512, 1024, 2048),
+               desc="scaling sweep: one instance per GPU, 64-2048 requests per instance, hidden 4096, bf16, "
+                    "skewed (r_per_inst is the sweep variable)"),
     "TGT": dict(n_inst=8, r_per_inst=512, d=4096, dtype="bf16", max_moves=1, skewed=True,
                 desc="north-star target: 8 instances x 512 requests, hidden 4096, bf16, skewed (instance 0 holds "
                      "2x the near-cap share: overloaded, so Alg. 1 reaches Phases 2-3 and moves a request)"),

@@ -338,6 +338,43 @@ star_status dispatch_requests(int policy, int n_inst, int H, const uint32_t* bet
                               const int32_t* n_hat, int32_t counter, int32_t* assign, void* workspace,
                               star_stream_t stream);
 
+/* =====================================================================================
+ * KV-cache migration  (NEXT-4; Alg. 1 line 10 "ExecuteMigration(m*)"; §5.4: "the
+ * paused request's KV cache is transfered to the target instance without blocking the execution
+ * of other requests"; transfer time vs bandwidth, Fig. 9)
+ * A paged KV pool is n_layers x n_blocks blocks of block_bytes bytes (block b of layer l at
+ * base + l*layer_stride + b*block_bytes; e.g. vLLM's K and V of block_size tokens of one layer);
+ * a request owns the n blocks its block table lists (int32 block ids, device memory).
+ *   kv_pack     copies the request's blocks into a contiguous staging buffer laid out
+ *               [n_layers][n][block_bytes] (layer-major, table order);
+ *   kv_unpack   copies a staging buffer into the blocks `table` lists (the destination's
+ *               freshly allocated blocks);
+ *   kv_migrate  copies block src_table[j] of src to block dst_table[j] of dst for every layer and
+ *               j, with no staging.  src->base may be a PEER device's pointer (cudaDeviceEnablePeerAccess):
+ *               the kernel runs on the calling (destination) device and pulls over NVLink.
+ * Requirements: bases, block_bytes and layer_stride 16-byte aligned, layer_stride >= n_blocks *
+ * block_bytes, equal n_layers and block_bytes for kv_migrate.  A block id outside [0, n_blocks)
+ * sets STAR_ERRF_BLOCK in *err_flag and that (layer, block) copy is skipped.  Asynchronous on
+ * `stream`, no allocation, graph capturable; n = 0 enqueues nothing.  Overlap with decode by
+ * issuing on a separate (low-priority) stream.
+ * ===================================================================================== */
+#define STAR_ERRF_BLOCK 4  /* KV block id outside the pool */
+
+typedef struct {
+  void* base;            /* device pointer of layer 0, block 0 */
+  int n_layers;
+  int64_t layer_stride;  /* bytes between consecutive layers */
+  int64_t n_blocks;      /* blocks per layer */
+  int64_t block_bytes;   /* bytes of one block of one layer */
+} star_kv_pool;
+
+star_status kv_pack(const star_kv_pool* src, const int32_t* table, int n, void* staging, int32_t* err_flag,
+                    star_stream_t stream);
+star_status kv_unpack(const void* staging, const star_kv_pool* dst, const int32_t* table, int n, int32_t* err_flag,
+                      star_stream_t stream);
+star_status kv_migrate(const star_kv_pool* src, const int32_t* src_table, const star_kv_pool* dst,
+                       const int32_t* dst_table, int n, int32_t* err_flag, star_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -194,3 +194,37 @@ def refresh_step(h, pw, n_tok, gen, g_last, nhat_last, k, l_ctx=32768):
     for r in np.nonzero(~due)[0]:
         n_hat[r] = max(0, int(nhat_last[r]) - int(gen[r] - g_last[r]))
     return n_hat, g_last, nhat_last, due
+
+
+# ----------------------------------------------------------------------------- KV migration (NEXT-4)
+# ExecuteMigration(m*) (Alg. 1 line 10; §5.4) moves the request's
+# KV cache: for every layer l and every block j of the request, block src_table[j] of the source
+# pool becomes block dst_table[j] of the destination pool.  Plain loops over (l, j) with slice
+# copies; a pool is a numpy array [n_layers][n_blocks][block_bytes] (uint8).
+def kv_pack(pool, table):
+    """staging[l][j] = pool[l][table[j]]."""
+    pool = np.asarray(pool)
+    n_layers, _, bb = pool.shape
+    out = np.zeros((n_layers, len(table), bb), dtype=pool.dtype)
+    for layer in range(n_layers):
+        for j, b in enumerate(table):
+            out[layer, j, :] = pool[layer, int(b), :]
+    return out
+
+
+def kv_unpack(staging, pool, table):
+    """Returns a copy of pool with pool[l][table[j]] = staging[l][j]."""
+    pool = np.array(pool, copy=True)
+    for layer in range(pool.shape[0]):
+        for j, b in enumerate(table):
+            pool[layer, int(b), :] = staging[layer, j, :]
+    return pool
+
+
+def kv_migrate(src_pool, src_table, dst_pool, dst_table):
+    """Returns a copy of dst_pool with dst[l][dst_table[j]] = src[l][src_table[j]]."""
+    dst = np.array(dst_pool, copy=True)
+    for layer in range(dst.shape[0]):
+        for j in range(len(src_table)):
+            dst[layer, int(dst_table[j]), :] = src_pool[layer, int(src_table[j]), :]
+    return dst

@@ -5,6 +5,7 @@ Public API (names follow the C ABI in include/star.h):
     project_instance_load                              per-instance projected loads
     PlanParams, plan_reschedule, plan_reschedule_segmented   Alg. 1 plan
     step.Step                                          one decode-step pass over ranks (NCCL)
+    kv_pack, kv_unpack, kv_migrate                     ExecuteMigration's paged-KV copy (NEXT-4)
 Importing the package does not load the CUDA library; the first call does, and raises
 StarError if it is missing (there is no CPU fallback).
 """
@@ -14,8 +15,10 @@ from ._lib import (DISPATCH_CURRENT_LOAD, DISPATCH_PROJECTED, DISPATCH_ROUND_ROB
                    lenpred_forward_refresh,
                    lenpred_quantize, plan_reschedule,
                    plan_reschedule_segmented, project_instance_load, plan_reschedule_large,
-                   plan_reschedule_segmented_ws, plan_workspace_bytes, project_workspace_bytes, version)
+                   plan_reschedule_segmented_ws, plan_workspace_bytes, project_workspace_bytes, version,
+                   kv_migrate, kv_pack, kv_unpack)
 
 __all__ = ["Predictor", "lenpred_forward", "lenpred_forward_project", "lenpred_forward_project_plan", "lenpred_quantize", "project_instance_load", "PlanParams",
            "plan_reschedule", "plan_reschedule_segmented", "decode_moves", "alloc_moves", "StarError",
-           "project_workspace_bytes", "version", "dispatch_requests", "STRICT_MEM", "CURRENT_ONLY", "L_CTX", "ProjectOut"]
+           "project_workspace_bytes", "version", "dispatch_requests", "STRICT_MEM", "CURRENT_ONLY", "L_CTX", "ProjectOut",
+           "kv_pack", "kv_unpack", "kv_migrate"]

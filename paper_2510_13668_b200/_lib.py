@@ -38,6 +38,10 @@ class PlanSegmentsC(C.Structure):
                 ("req_id", P), ("inst", P), ("n_tok", P), ("n_hat", P), ("pinned", P)]
 
 
+class KvPoolC(C.Structure):
+    _fields_ = [("base", P), ("n_layers", I), ("layer_stride", I64), ("n_blocks", I64), ("block_bytes", I64)]
+
+
 MOVE_DTYPE = np.dtype([("req_id", "<i4"), ("src", "<i4"), ("dst", "<i4"), ("round", "<i4"),
                        ("gain_hi", "<i8"), ("gain_lo", "<u8")])
 MOVE_BYTES = 32
@@ -78,6 +82,9 @@ def lib() -> C.CDLL:
         "star_plan_timeline": ([P], I),
         "plan_reschedule_segmented_ws": ([C.POINTER(PlanParamsC), C.POINTER(PlanSegmentsC), P, P, P, P, P], I),
         "dispatch_requests": ([I, I, I, P, P, P, P, I, P, P, I32, P, P, P], I),
+        "kv_pack": ([C.POINTER(KvPoolC), P, I, P, P, P], I),
+        "kv_unpack": ([P, C.POINTER(KvPoolC), P, I, P, P], I),
+        "kv_migrate": ([C.POINTER(KvPoolC), P, C.POINTER(KvPoolC), P, I, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -470,3 +477,46 @@ def plan_timeline():
     buf = np.zeros(64, dtype=np.uint64)
     _check(lib().star_plan_timeline(buf.ctypes.data_as(P)), "star_plan_timeline")
     return buf
+
+
+# ================================================================ KV migration (NEXT-4)
+def kv_pool(pool: torch.Tensor) -> KvPoolC:
+    """Describes a paged KV pool tensor [n_layers, n_blocks, block_bytes] (any dtype; the last
+    dimension is taken in bytes).  Layers may be strided (a view into a larger allocation)."""
+    if not pool.is_cuda or pool.dim() != 3 or pool.stride(2) != 1 or pool.stride(1) != pool.shape[2]:
+        raise StarError("pool must be a CUDA tensor [n_layers, n_blocks, block] with contiguous blocks")
+    es = pool.element_size()
+    return KvPoolC(pool.data_ptr(), pool.shape[0], pool.stride(0) * es, pool.shape[1], pool.shape[2] * es)
+
+
+def kv_pack(pool: torch.Tensor, table: torch.Tensor, staging: Optional[torch.Tensor] = None,
+            err_flag: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """staging[l, j] = pool[l, table[j]] (star.h kv_pack)."""
+    _req(table, torch.int32, "table")
+    n = int(table.shape[0])
+    if staging is None:
+        staging = torch.empty((pool.shape[0], n, pool.shape[2]), dtype=pool.dtype, device=pool.device)
+    d = kv_pool(pool)
+    _check(lib().kv_pack(C.byref(d), _ptr(table), n, _ptr(staging), _ptr(err_flag), _stream(stream)), "kv_pack")
+    return staging
+
+
+def kv_unpack(staging: torch.Tensor, pool: torch.Tensor, table: torch.Tensor, err_flag: Optional[torch.Tensor] = None,
+              stream=None) -> None:
+    """pool[l, table[j]] = staging[l, j] (star.h kv_unpack)."""
+    _req(table, torch.int32, "table")
+    d = kv_pool(pool)
+    _check(lib().kv_unpack(_ptr(staging), C.byref(d), _ptr(table), int(table.shape[0]), _ptr(err_flag),
+                           _stream(stream)), "kv_unpack")
+
+
+def kv_migrate(src_pool: torch.Tensor, src_table: torch.Tensor, dst_pool: torch.Tensor, dst_table: torch.Tensor,
+               err_flag: Optional[torch.Tensor] = None, stream=None) -> None:
+    """dst_pool[l, dst_table[j]] = src_pool[l, src_table[j]] (star.h kv_migrate)."""
+    _req(src_table, torch.int32, "src_table")
+    _req(dst_table, torch.int32, "dst_table")
+    if src_table.shape[0] != dst_table.shape[0]:
+        raise StarError("src_table and dst_table must have the same length")
+    s, d = kv_pool(src_pool), kv_pool(dst_pool)
+    _check(lib().kv_migrate(C.byref(s), _ptr(src_table), C.byref(d), _ptr(dst_table), int(src_table.shape[0]),
+                            _ptr(err_flag), _stream(stream)), "kv_migrate")

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(HERE, "libstar.so")
-SOURCES = ["star_api.cu", "project.cu", "plan.cu", "plan_large.cu", "dispatch.cu", "refresh.cu"]
+SOURCES = ["star_api.cu", "project.cu", "plan.cu", "plan_large.cu", "dispatch.cu", "refresh.cu", "migrate.cu"]
 HEADERS = ["ptx.cuh", "lenpred_kernels.cuh", "lenpred_tail.cuh", "project_core.cuh", "plan_core.cuh", "plan_fast.cuh", "star_internal.h"]
 
 NVCC_FLAGS = [
@@ -67,7 +67,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         vmap = os.path.join(BUILD, "star.map")   # export the C ABI only (include/star.h)
         with open(vmap, "w") as f:
             f.write("{\n  global:\n    star_*;\n    lenpred_*;\n    project_instance_load;\n"
-                    "    plan_reschedule*;\n    dispatch_requests;\n  local: *;\n};\n")
+                    "    plan_reschedule*;\n    dispatch_requests;\n    kv_pack;\n    kv_unpack;\n    kv_migrate;\n"
+                    "  local: *;\n};\n")
         cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
                "-Xlinker", "--version-script=" + vmap]
         r = subprocess.run(cmd, capture_output=True, text=True)

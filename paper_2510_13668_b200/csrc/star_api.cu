@@ -1057,4 +1057,37 @@ star_status plan_reschedule(const star_plan_params* p, const int64_t* L, int R_t
   return plan_reschedule_segmented(p, &sg, moves, n_moves, err_flag, stream);
 }
 
+star_status kv_pack(const star_kv_pool* src, const int32_t* table, int n, void* staging, int32_t* err_flag,
+                    star_stream_t stream) {
+  star_status s = ensure_device();
+  if (s != STAR_OK) return s;
+  std::string msg;
+  if (!src) return fail(STAR_EINVAL, "kv_pack: src is NULL");
+  s = kv_copy_checked(src, table, nullptr, nullptr, n, nullptr, staging, err_flag,
+                      reinterpret_cast<cudaStream_t>(stream), &msg);
+  return s == STAR_OK ? s : fail(s, "kv_pack: %s", msg.c_str());
+}
+
+star_status kv_unpack(const void* staging, const star_kv_pool* dst, const int32_t* table, int n, int32_t* err_flag,
+                      star_stream_t stream) {
+  star_status s = ensure_device();
+  if (s != STAR_OK) return s;
+  std::string msg;
+  if (!dst) return fail(STAR_EINVAL, "kv_unpack: dst is NULL");
+  s = kv_copy_checked(nullptr, nullptr, dst, table, n, const_cast<void*>(staging), nullptr, err_flag,
+                      reinterpret_cast<cudaStream_t>(stream), &msg);
+  return s == STAR_OK ? s : fail(s, "kv_unpack: %s", msg.c_str());
+}
+
+star_status kv_migrate(const star_kv_pool* src, const int32_t* src_table, const star_kv_pool* dst,
+                       const int32_t* dst_table, int n, int32_t* err_flag, star_stream_t stream) {
+  star_status s = ensure_device();
+  if (s != STAR_OK) return s;
+  std::string msg;
+  if (!src || !dst) return fail(STAR_EINVAL, "kv_migrate: src and dst must be non-NULL");
+  s = kv_copy_checked(src, src_table, dst, dst_table, n, nullptr, nullptr, err_flag,
+                      reinterpret_cast<cudaStream_t>(stream), &msg);
+  return s == STAR_OK ? s : fail(s, "kv_migrate: %s", msg.c_str());
+}
+
 }  // extern "C"

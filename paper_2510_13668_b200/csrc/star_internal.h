@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 #include "../../include/star.h"
 #include "project_core.cuh"
@@ -56,6 +57,11 @@ size_t refresh_scatter_project_smem(int n_inst, int H);
 cudaError_t launch_refresh_scatter_project(const ProjArgs& a, const int32_t* pos, const int32_t* nhat_c,
                                            const int32_t* gen, int32_t* g_last, int32_t* nhat_last,
                                            const int32_t* M_dev, int32_t* n_refreshed, cudaStream_t st);
+
+// migrate.cu (KV migration, NEXT-4): src/dst NULL select the staging side
+star_status kv_copy_checked(const star_kv_pool* src, const int32_t* src_table, const star_kv_pool* dst,
+                            const int32_t* dst_table, int n, void* staging_in, void* staging_out, int32_t* err_flag,
+                            cudaStream_t stream, std::string* msg);
 
 // dispatch.cu
 size_t dispatch_workspace_bytes(int n, int H);

@@ -496,3 +496,33 @@ def test_refresh_schedule_and_aging(oracle_mod):
         assert nh[0] >= 0
         prev = int(nh[0])
     assert fires == -(-L_out // k)
+
+
+# ============================================================================ KV migration (NEXT-4)
+def test_kv_oracle_hand_example(oracle_mod):
+    """2 layers x 4 blocks of 2 bytes; the request owns blocks [3, 0] at the source and gets blocks
+    [1, 2] at the destination (worked by hand)."""
+    src = np.arange(16, dtype=np.uint8).reshape(2, 4, 2)      # layer l, block b holds (8l+2b, 8l+2b+1)
+    stg = oracle_mod.kv_pack(src, [3, 0])
+    assert stg.tolist() == [[[6, 7], [0, 1]], [[14, 15], [8, 9]]]
+    dst = np.full((2, 4, 2), 255, np.uint8)
+    out = oracle_mod.kv_unpack(stg, dst, [1, 2])
+    assert out.tolist() == [[[255, 255], [6, 7], [0, 1], [255, 255]], [[255, 255], [14, 15], [8, 9], [255, 255]]]
+    assert np.array_equal(oracle_mod.kv_migrate(src, [3, 0], dst, [1, 2]), out)
+
+
+def test_kv_oracle_invariants(oracle_mod):
+    g = np.random.default_rng(0)
+    pool = g.integers(0, 256, (3, 10, 32), dtype=np.uint8)
+    ident = list(range(10))
+    assert np.array_equal(oracle_mod.kv_pack(pool, ident), pool)                     # identity table
+    perm = g.permutation(10)
+    stg = oracle_mod.kv_pack(pool, perm)
+    back = oracle_mod.kv_unpack(stg, np.zeros_like(pool), perm)                       # round trip
+    assert np.array_equal(back, pool)
+    # untouched destination blocks keep their bytes; the bytes moved are conserved as a multiset
+    dst = g.integers(0, 256, (3, 10, 32), dtype=np.uint8)
+    out = oracle_mod.kv_migrate(pool, perm[:4], dst, [9, 0, 5, 2])
+    keep = [b for b in range(10) if b not in (9, 0, 5, 2)]
+    assert np.array_equal(out[:, keep], dst[:, keep])
+    assert np.array_equal(np.sort(out[:, [9, 0, 5, 2]].ravel()), np.sort(pool[:, perm[:4]].ravel()))
