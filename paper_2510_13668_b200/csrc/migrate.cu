@@ -124,6 +124,7 @@ star_status kv_copy_checked(const star_kv_pool* src, const int32_t* src_table, c
     *msg = "block table is NULL";
     return STAR_EINVAL;
   }
+  if (n == 0) return STAR_OK;   // nothing to copy (staging may be an empty allocation)
   void* stg = staging_in ? staging_in : staging_out;
   if (!(src && dst) && (!stg || (reinterpret_cast<uintptr_t>(stg) & 15))) {
     *msg = "staging must be a 16-byte aligned device buffer of n_layers * n * block_bytes bytes";

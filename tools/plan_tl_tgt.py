@@ -21,3 +21,15 @@ print("staging detail (us): static (pre-wait)", round((cl[12] - cl[1]) / 1965.0,
       round((cl[13] - cl[12]) / 1965.0, 2), "post-wait loads", round((cl[15] - cl[13]) / 1965.0, 2),
       "barrier", round((cl[2] - cl[15]) / 1965.0, 2))
 print("raw globaltimer offsets (us):", [(k, round((tl[k] - tl[0]) / 1e3, 2)) for k in range(16) if tl[k]])
+order = [1, 12, 13, 15, 2, 3, 4, 9, 10, 11, 5, 8, 6, 7]
+lbl = {1: "launch", 12: "static staged", 13: "pdl_wait", 15: "dyn loads", 2: "staged", 3: "W pass", 4: "classify",
+       9: "compaction", 10: "evaluate", 11: "warp argmax", 5: "block bar", 8: "final argmax", 6: "apply", 7: "end"}
+prev = None
+for k in order:
+    if cl[k - 0 if k < 16 else k]:
+        pass
+for k in order:
+    c = tl[32 + k]
+    if c:
+        print(f"  clk {lbl[k]:14s} {(c - tl[33]) / 1965.0:7.2f} us" + ("" if prev is None else f"  (+{(c - prev) / 1965.0:.2f})"))
+        prev = c
