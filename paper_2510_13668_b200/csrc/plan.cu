@@ -14,7 +14,9 @@
 // its requests against every target in U (filters (a)/(b) applied) and keeps the best; a
 // warp-shuffle + shared-memory argmax over requests then picks m* with the key
 // (gain desc, req_id asc, dst asc) (reading A20).  Greedy rounds (reading A21).
+#include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "plan_core.cuh"
 #include "plan_fast.cuh"
@@ -49,6 +51,37 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(const PlanArgs a)
     plan_cta_fast(a, smraw, (int)threadIdx.x, (int)blockDim.x, warp_best, shv, g_plan_tl);
   else
     plan_cta<CtaSync, false>(a, smraw, (int)threadIdx.x, (int)blockDim.x, CtaSync{}, warp_best, shv, g_plan_tl);
+}
+
+// Alg. 1 on a thread-block cluster of kCl CTAs (plan_fast.cuh: candidate compaction and scoring
+// split over the CTAs, the round's argmax in distributed shared memory).
+static_assert(offsetof(Cand, id) == 16 && offsetof(Cand, dst) == 20 && offsetof(Cand, g) == 24,
+              "plan_cta_fast reads peers' Cand fields at these offsets");
+template <int kCl>
+__global__ void __launch_bounds__(kPlanThreads, 1) plan_cluster_kernel(const PlanArgs a) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  __shared__ Cand warp_best[kPlanThreads / 32];
+  __shared__ Cand cl_best[2];
+  __shared__ int shv[8];
+  const bool lead = cluster_ctarank() == 0;
+  if (lead && threadIdx.x == 0) g_plan_tl[0] = globaltimer_ns();
+  pdl_launch_dependents();
+  if (lead && threadIdx.x == 0) {
+    g_plan_tl[1] = globaltimer_ns();
+    g_plan_tl[33] = clock64();
+  }
+  plan_cta_fast<false, kCl>(a, smraw, (int)threadIdx.x, (int)blockDim.x, warp_best, shv, g_plan_tl, cl_best);
+}
+
+// Cluster size of the staged plan: STAR_PLAN_CLUSTER (1, 2, 4 or 8; read once) for A/B
+// measurements, default 8.
+static int plan_cluster_size() {
+  static int v = [] {
+    const char* e = getenv("STAR_PLAN_CLUSTER");
+    const int x = e ? atoi(e) : 8;
+    return (x == 1 || x == 2 || x == 4 || x == 8) ? x : 8;
+  }();
+  return v;
 }
 
 // Minimum dynamic shared memory (request table read from global memory).
@@ -98,7 +131,10 @@ cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg,
   const bool staged = plan_fast_smem_layout(a.n, a.H, a.world, a.r_cap) <= lim;
   const size_t smem = staged ? plan_fast_smem_layout(a.n, a.H, a.world, a.r_cap)
                              : plan_smem_layout(a.n, a.H, a.world, a.r_cap, false);
-  auto kern = staged ? plan_kernel<true> : plan_kernel<false>;
+  const int ncl = staged ? plan_cluster_size() : 1;
+  auto kern = !staged ? plan_kernel<false>
+            : ncl == 8 ? plan_cluster_kernel<8> : ncl == 4 ? plan_cluster_kernel<4>
+            : ncl == 2 ? plan_cluster_kernel<2> : plan_kernel<true>;
   if (smem > 48 * 1024) {
     cudaError_t e = func_attr((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -106,15 +142,19 @@ cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg,
   // same L1/shared split as the GEMM kernels before it: no SM reconfiguration
   func_attr((const void*)kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(1, 1, 1);
+  cfg.gridDim = dim3(ncl, 1, 1);
   cfg.blockDim = dim3(kPlanThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = (unsigned)ncl;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = ncl > 1 ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 

@@ -122,9 +122,18 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // Whole plan by one CTA of `nthreads` threads (multiple of 32).  tl: optional %globaltimer stamps.
 // kFused: called by the predictor tail's last CTA after the projection (no griddepcontrol.wait
 // period to hide the static staging in; the loads are issued together with it instead).
-template <bool kFused = false>
+// kCl > 1: the plan runs on a thread-block cluster of kCl CTAs.  Every CTA stages the whole state
+// and runs the (cheap, per-instance) Phase-1 / prefix-sum work itself; the candidate compaction
+// and scoring -- the instruction-bound part, one int128 score per (request, target) -- are split
+// over the CTAs (4-slot groups interleaved by CTA rank, so the requests of an overloaded instance
+// spread over every SM); each round's CTA winners meet in distributed shared memory and every
+// CTA takes the same argmax (a total order), applies m* to its own copy of the loads and goes on.
+// Only CTA 0 writes the move list.  cl_best: [2] shared Cands (round-parity double buffer).
+template <bool kFused = false, int kCl = 1>
 __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw, const int tid, const int nthreads,
-                                              Cand* warp_best, int* shv, uint64_t* tl) {
+                                              Cand* warp_best, int* shv, uint64_t* tl, Cand* cl_best = nullptr) {
+  const int crank = kCl > 1 ? (int)cluster_ctarank() : 0;
+  if (kCl > 1 && crank != 0) tl = nullptr;
 #define PLAN_TS(k)                                           \
   do {                                                       \
     if (tl && tid == 0) {                                    \
@@ -477,9 +486,10 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     }
     // ---- candidate compaction: requests on overloaded instances, not pinned, not yet moved ----
     // (round 0 also validates each slot once and marks the slots that can never be candidates)
-    // four consecutive slots per lane (one 16-byte shared load), one atomic per warp
-    for (int base = 0; base < (s_reuse ? 0 : nslots); base += 4 * nthreads) {
-      const int g0 = base + 4 * tid;
+    // four consecutive slots per lane (one 16-byte shared load), one atomic per warp; in a
+    // cluster, CTA `crank` takes the 4-slot groups with (group index mod kCl) == crank
+    for (int base = 0; base < (s_reuse ? 0 : nslots); base += 4 * nthreads * kCl) {
+      const int g0 = base + 4 * (tid * kCl + crank);
       uint32_t cm = 0;   // candidate bits of slots g0..g0+3
       if (g0 < nslots) {   // nslots is a multiple of 16 (pitch)
         int4 sv = *reinterpret_cast<const int4*>(s.rinst + g0);
@@ -570,14 +580,36 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     __syncthreads();
     PLAN_TS(5);
     __syncwarp();
+    Cand c;
+    c.score = 0; c.id = 0; c.dst = 0; c.g = -1;
     if (warp == 0) {
-      Cand c;
-      if (lane < nwarps) {
-        c = warp_best[lane];
-      } else {
-        c.score = 0; c.id = 0; c.dst = 0; c.g = -1;
+      if (lane < nwarps) c = warp_best[lane];
+      c = warp_argmax_g(c);   // every lane holds the CTA's winner
+      if (kCl > 1 && lane == 0) cl_best[round & 1] = c;
+    }
+    if constexpr (kCl > 1) {
+      // cluster argmax: every CTA published its winner; meet (all threads), then warp 0 of every
+      // CTA reads all kCl winners from distributed shared memory and takes the same argmax
+      cluster_sync_all();
+      if (warp == 0) {
+        Cand o;
+        o.score = 0; o.id = 0; o.dst = 0; o.g = -1;
+        if (lane < kCl) {
+          const uint32_t ra = mapa_shared(smem_u32(cl_best + (round & 1)), (uint32_t)lane);
+          uint64_t lo, hi;
+          int32_t id, dst, g;
+          asm volatile("ld.shared::cluster.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(ra) : "memory");
+          asm volatile("ld.shared::cluster.v2.s32 {%0, %1}, [%2];" : "=r"(id), "=r"(dst) : "r"(ra + 16u) : "memory");
+          asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(g) : "r"(ra + 24u) : "memory");
+          o.score = (i128)(((unsigned __int128)hi << 64) | lo);
+          o.id = id;
+          o.dst = dst;
+          o.g = g;
+        }
+        c = warp_argmax_g(o);
       }
-      c = warp_argmax_g(c);   // every lane holds the winner
+    }
+    if (warp == 0) {
       PLAN_TS(8);
       if (c.g < 0) {
         if (lane == 0) s_stop = 1;
@@ -594,6 +626,8 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
           s.moved[c.g >> 5] |= 1u << (c.g & 31);
           s.wdirty[src] = s.wdirty[c.dst] = 1;
           s.pdirty[src] = s.pdirty[c.dst] = 1;
+        }
+        if (lane == 0 && crank == 0) {
           const i128 gain = (i128)2 * n * c.score;
           star_move mv;
           mv.req_id = c.id;
@@ -618,7 +652,8 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     cp_async_wait_all();
   }
   PLAN_TS(7);
-  if (tid == 0) *a.n_moves = s_nmoves;
+  if (tid == 0 && crank == 0) *a.n_moves = s_nmoves;
+  if constexpr (kCl > 1) cluster_sync_all();   // no CTA leaves while a peer may still read its cl_best
 #undef PLAN_TS
 }
 

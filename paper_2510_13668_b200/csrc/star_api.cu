@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -13,6 +14,7 @@
 #include <tuple>
 
 #include "lenpred_kernels.cuh"
+#include "lenpred_small.cuh"
 #include "lenpred_tail.cuh"
 #include "plan_core.cuh"
 #include "star_internal.h"
@@ -247,6 +249,51 @@ static void plan_splits(int tiles, int num_kb, int bn, bool tf32, int* splits, i
 }
 
 
+// The one-launch small-batch predictor (lenpred_small.cuh) needs all of its CTAs resident at
+// once (phases hand off through counters): 32 clusters of 4 CTAs of ~220 KB shared memory.
+// STAR_SMALL=0 disables it (A/B measurements).
+static bool small_path_available() {
+  const char* e = getenv("STAR_SMALL");
+  if (e && atoi(e) == 0) return false;
+  if (func_attr((const void*)lenpred_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                (int)SmallSmem::BYTES) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(4, 8, 4);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = SmallSmem::BYTES;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 4;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)lenpred_small_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return ncl >= 32;
+}
+
+static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, int32_t max_ctx, float* y_hat,
+                                int32_t* n_hat, const ProjArgs* proj, cudaStream_t st);
+
+// Whether a one-rank single-round plan runs in the fused tail's last CTA (STAR_PLAN_FUSE=1, read
+// once) instead of the cluster plan kernel launched after it (default).  Measured at TGT with a
+// move (Alg. 1 past Phase 1): 117.3 us fused (192 threads score the candidates) vs 99.4 us with
+// the 8-CTA plan kernel; without candidates (C2) the two are within 0.4 us.
+static bool plan_fuse_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("STAR_PLAN_FUSE");
+    return e ? atoi(e) != 0 : false;
+  }();
+  return v;
+}
+
 // Fused tail (layer 2 -> layer 3 -> head -> quantizer [-> projection]) launch: grid
 // (m_tiles, n2, S), one cluster per layer-2 tile (its S split-K CTAs), PDL.
 static cudaError_t launch_tail(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& w3, const TailArgs& t,
@@ -320,6 +367,11 @@ struct star_predictor {
   CUtensorMap tmA1, tmB1, tmA2, tmB2, tmA3, tmB3;
   CUtensorMap tmC1, tmC2;     // TMA-store maps of Z1 / Z2 (bf16, 64 x 32 boxes)
   CUtensorMap tmB1p;          // W1 with 128-row boxes (CTA-pair kernel: each CTA loads half of B)
+  // one-launch predictor for <= 512 rows (lenpred_small.cuh)
+  CUtensorMap tmW2s;          // W2 with 64-row boxes
+  int* small_cnt = nullptr;   // its phase counters (zero between launches)
+  bool small_ok = false;      // shape supported and 32 clusters of 4 co-resident
+  uint64_t* tl_small = nullptr;
   const void* last_h = nullptr;
   int64_t last_ld = 0;
   int last_R = -1;
@@ -348,6 +400,8 @@ static void free_pred(star_predictor* p) {
   cudaFree(p->l1_cnt);
   cudaFree(p->tl);
   cudaFree(p->tl_l1);
+  cudaFree(p->small_cnt);
+  cudaFree(p->tl_small);
   cudaFree(p->r_idx);
   cudaFree(p->r_pos);
   cudaFree(p->r_ntok);
@@ -458,6 +512,21 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
     free_pred(p);
     return st;
   }
+  if (!f32 && m1 == 2048 && m2 == 512 && d % 256 == 0) {
+    if ((st = make_tmap(&p->tmW2s, W2, false, (uint64_t)m1, m2, (uint64_t)m1 * 2, 64)) != STAR_OK) {
+      free_pred(p);
+      return st;
+    }
+    p->small_ok = small_path_available();
+    if (p->small_ok) {
+      if (cudaMalloc(reinterpret_cast<void**>(&p->small_cnt), 64 * sizeof(int)) != cudaSuccess ||
+          cudaMemset(p->small_cnt, 0, 64 * sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        free_pred(p);
+        return fail(STAR_ENOMEM, "device allocation failed");
+      }
+    }
+  }
   *out = p;
   return STAR_OK;
 }
@@ -555,6 +624,11 @@ static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, 
     p->last_ld = ld_h;
     p->last_R = R;
   }
+  if (!f32 && p->small_ok && R >= 1 && R <= 512) {   // one launch: Eq. 2 + quantizer (+ projection)
+    cudaError_t e = launch_small(p, R, n_tok, max_ctx_len, y_hat, n_hat, proj, st);
+    if (e != cudaSuccess) return cuda_fail(e, "lenpred_small_kernel launch");
+    return STAR_OK;
+  }
   GemmArgs g{};
   g.M = R;
   g.max_ctx = max_ctx_len;
@@ -642,7 +716,7 @@ static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, 
     // fused only for a single-round plan: the fused form runs on the tail's 192 threads, where a
     // multi-round plan (C4, max_moves = 4: ~17 us per round) is slower than the 512-thread plan
     // kernel it would save the launch of
-    if (proj && plan && plan->world == 1 && plan->max_moves <= 1 &&
+    if (proj && plan && plan->world == 1 && plan->max_moves <= 1 && plan_fuse_enabled() &&
         plan_fast_smem_layout(plan->n, plan->H, 1, plan->r_cap) + 256 <= (size_t)TailSmem::OFF_W3) {
       t.plan = 1;   // Alg. 1 by the projection's last finisher: no plan launch, no kernel boundary
       t.pl = *plan;
@@ -1091,3 +1165,42 @@ star_status kv_migrate(const star_kv_pool* src, const int32_t* src_table, const 
 }
 
 }  // extern "C"
+
+namespace star {
+static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, int32_t max_ctx, float* y_hat,
+                                int32_t* n_hat, const ProjArgs* proj, cudaStream_t st) {
+  SmallArgs a{};
+  a.M = R;
+  a.kb1 = p->d / 64;
+  a.b1 = p->b1;
+  a.b2 = p->b2;
+  a.b3 = p->b3;
+  a.w4 = p->w4;
+  a.b4 = p->b4;
+  a.n_tok = n_tok;
+  a.max_ctx = max_ctx;
+  a.y_hat = y_hat;
+  a.n_hat = n_hat;
+  a.Z1 = static_cast<__nv_bfloat16*>(p->Z1);
+  a.Z2 = static_cast<__nv_bfloat16*>(p->Z2);
+  a.cnt = p->small_cnt;
+  a.project = proj ? 1 : 0;
+  if (proj) a.pa = *proj;
+  a.tl = p->tl_small;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(4, 8, (R + 127) / 128);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = SmallSmem::BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 4;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, lenpred_small_kernel, p->tmA1, p->tmB1, p->tmA2, p->tmW2s, p->tmA3, p->tmB3, a);
+}
+}  // namespace star
