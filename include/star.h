@@ -171,6 +171,11 @@ star_status star_predictor_layer1_timing(star_predictor* p, int enable);
  * frees the buffers.  Not for the hot path. */
 star_status star_predictor_timeline(star_predictor* p, int enable, uint64_t* host_out, int max_ctas, int* n_ctas);
 star_status star_predictor_layer1_ms(star_predictor* p, float* ms);
+/* Which kernels a forward of R rows runs: *path = 1 for the one-launch small-batch predictor
+ * (bf16, m1 = 2048, m2 = 512, d % 256 == 0, 1 <= R <= 512, and its 128 CTAs co-resident on this
+ * device; the layer-1 timing events then bracket that whole launch), 0 for the layer-1 GEMM +
+ * fused tail (bf16) or the 3 GEMMs (fp32). */
+star_status star_predictor_path(star_predictor* p, int R, int* path);
 
 /* =====================================================================================
  * Projected per-instance load  (readings A4-A6)

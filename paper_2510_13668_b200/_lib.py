@@ -63,6 +63,7 @@ def lib() -> C.CDLL:
         "star_predictor_destroy": ([P], I),
         "star_predictor_layer1_timing": ([P, I], I),
         "star_predictor_layer1_ms": ([P, C.POINTER(C.c_float)], I),
+        "star_predictor_path": ([P, I, C.POINTER(I)], I),
         "star_predictor_timeline": ([P, I, P, I, C.POINTER(I)], I),
         "lenpred_forward": ([P, P, I64, I, P, I32, P, P, P], I),
         "lenpred_quantize": ([P, P, I, I32, P, P], I),
@@ -185,6 +186,12 @@ class Predictor:
         ms = C.c_float()
         _check(lib().star_predictor_layer1_ms(self.handle, C.byref(ms)), "layer1_ms")
         return float(ms.value)
+
+    def path(self, R: int) -> int:
+        """1 if a forward of R rows runs the one-launch small-batch kernel, else 0 (star.h)."""
+        v = C.c_int()
+        _check(lib().star_predictor_path(self.handle, int(R), C.byref(v)), "star_predictor_path")
+        return int(v.value)
 
 
 def lenpred_forward(pred: Predictor, h: torch.Tensor, n_tok: Optional[torch.Tensor] = None,

@@ -545,32 +545,32 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     best.dst = 0;
     best.g = -1;
     const int nU = s_nU, ncand = s_ncand;
-    for (int c = tid; c < ncand; c += nthreads) {
+    // one (candidate, target) pair per thread: the scoring is a dependent chain of int128 steps,
+    // so spreading the pairs (not the candidates) over the threads shortens each thread's chain
+    const int npairs = ncand * nU;
+    for (int pi = tid; pi < npairs; pi += nthreads) {
+      const int c = pi / nU, qq = pi - c * nU;
       const int g = s.cidx[c];
       if ((s.moved[g >> 5] >> (g & 31)) & 1u) continue;   // moved earlier in this call (reused list)
       const int src = s.rinst[g];
       const int32_t N = s.rntok[g], nh = s.rnhat[g];
+      const int u = s.ulist[qq];
+      if (!cur_only && !(mul_i32(s.texec[u], nh) > (i128)a.c0_ps + mul_i32((i128)a.c1_ps, N))) continue;  // filter (a)
+      const int64_t need_r = strict ? (cur_only ? 0 : (int64_t)nh) : (int64_t)N + (cur_only ? 0 : (int64_t)nh);
+      if (s.cmem && !(s.Ls[(int64_t)u * H1] + need_r <= s.cmem[u])) continue;                         // filter (b)
       int T = nh - 1 < 0 ? 0 : (nh - 1 > a.H ? a.H : nh - 1);
       if (cur_only) T = 0;
-      // self = N^2 B0[T] + 2N B1[T] + B2[T];  keep = N P0_src[T] + P1_src[T] - self
+      // score = N (P0_src[T] - P0_u[T]) + (P1_src[T] - P1_u[T]) - (N^2 B0[T] + 2N B1[T] + B2[T])
       const i128 self = mul_i32(mul_i32(s.B[T], N), N) + mul_i32(s.B[H1 + T], N) * 2 + s.B[2 * H1 + T];
-      const i128 keep = mul_i32(s.P0[(int64_t)src * H1 + T], N) + s.P1[(int64_t)src * H1 + T] - self;
-      const i128 mig = (i128)a.c0_ps + mul_i32((i128)a.c1_ps, N);
-      const int64_t need_r = strict ? (cur_only ? 0 : (int64_t)nh) : (int64_t)N + (cur_only ? 0 : (int64_t)nh);
-      const int32_t rid = s.rid[g];
-      for (int qq = 0; qq < nU; ++qq) {
-        const int u = s.ulist[qq];
-        if (!cur_only && !(mul_i32(s.texec[u], nh) > mig)) continue;                 // filter (a)
-        if (s.cmem && !(s.Ls[(int64_t)u * H1] + need_r <= s.cmem[u])) continue;       // filter (b)
-        const i128 score = keep - (mul_i32(s.P0[(int64_t)u * H1 + T], N) + s.P1[(int64_t)u * H1 + T]);
-        if (score <= 0) continue;
-        Cand cd;
-        cd.score = score;
-        cd.id = rid;
-        cd.dst = u;
-        cd.g = g;
-        if (cand_better_g(cd, best)) best = cd;
-      }
+      const i128 score = mul_i32(s.P0[(int64_t)src * H1 + T] - s.P0[(int64_t)u * H1 + T], N) +
+                         (s.P1[(int64_t)src * H1 + T] - s.P1[(int64_t)u * H1 + T]) - self;
+      if (score <= 0) continue;
+      Cand cd;
+      cd.score = score;
+      cd.id = s.rid[g];
+      cd.dst = u;
+      cd.g = g;
+      if (cand_better_g(cd, best)) best = cd;
     }
     PLAN_TS(10);
     __syncwarp();

@@ -588,6 +588,12 @@ star_status star_predictor_timeline(star_predictor* p, int enable, uint64_t* hos
   return STAR_OK;
 }
 
+star_status star_predictor_path(star_predictor* p, int R, int* path) {
+  if (!p || !path) return fail(STAR_EINVAL, "predictor / path is NULL");
+  *path = (!p->f32 && p->small_ok && R >= 1 && R <= 512) ? 1 : 0;
+  return STAR_OK;
+}
+
 star_status star_predictor_layer1_ms(star_predictor* p, float* ms) {
   if (!p || !ms) return fail(STAR_EINVAL, "predictor / ms is NULL");
   if (!p->ev0) return fail(STAR_EINVAL, "layer-1 timing is not enabled");
@@ -625,8 +631,10 @@ static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, 
     p->last_R = R;
   }
   if (!f32 && p->small_ok && R >= 1 && R <= 512) {   // one launch: Eq. 2 + quantizer (+ projection)
+    if (p->ev0) record_timing_event(p->ev0, st);
     cudaError_t e = launch_small(p, R, n_tok, max_ctx_len, y_hat, n_hat, proj, st);
     if (e != cudaSuccess) return cuda_fail(e, "lenpred_small_kernel launch");
+    if (p->ev1) record_timing_event(p->ev1, st);
     return STAR_OK;
   }
   GemmArgs g{};

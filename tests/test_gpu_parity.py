@@ -289,7 +289,9 @@ def test_predictor_full_size_all_rows(star, oracle_mod, cfg, R):
                                  skewed=c.get("skewed", False))
     scale = np.maximum(snap.true_rem[:R], 1).astype(np.float32) / 60.0   # long-tailed, as in the bench
     h = datagen.make_hidden(0, R, c["d"], c["dtype"], scale=scale)
-    _, y, nh = _predict(star, pw, h, n_tok=snap.n_tok[:R])
+    pred, y, nh = _predict(star, pw, h, n_tok=snap.n_tok[:R])
+    # the per-rank sizes run the one-launch small-batch kernel on a B200, the rest the 2-launch path
+    assert pred.path(R) == (1 if R <= 512 else 0)
     ref = oracle_mod.lenpred_weights(h, pw)
     err = _rel_err(y, ref)
     assert err <= TOL[c["dtype"]], f"max rel err {err:.3e} over all {R} rows"
@@ -674,4 +676,49 @@ def test_step_gathered_ranks_plan_equals_oracle(star, oracle_mod, cfg, world, r_
         torch.cuda.synchronize()
         assert star.decode_moves(moves, nm) == ref
     assert steps[-1].result() == ref
+    pred.close()
+
+
+# ============================================================================ one-launch small-batch predictor
+@pytest.mark.parametrize("d,R,biases,n,ld_pad", [(4096, 512, True, 1, 0), (4096, 384, False, 3, 64), (4096, 129, False, 8, 0),
+                                                 (5120, 511, True, 2, 0), (1024, 64, False, 1, 0), (4096, 1, True, 1, 8),
+                                                 (4096, 256, False, 300, 0), (2048, 200, True, 5, 0)])
+def test_small_path_forward_project(star, oracle_mod, d, R, biases, n, ld_pad):
+    """The one-launch predictor (<= 512 rows: layers 1-3, head, quantizer and the projection in
+    one persistent kernel, DSMEM split-K reductions): every row within the bf16 tolerance of the
+    fp64 oracle, N_hat == the oracle quantizer of its y_hat, L/W/peak/growth/count == the oracle
+    projection of that N_hat bit for bit; repeated launches (counters re-armed) are bit-identical,
+    also with a row stride > d and max_rows > R."""
+    pw = datagen.make_predictor_weights(d + R, d, "bf16", biases=biases)
+    snap = datagen.make_snapshot(R + n, n, (R + n - 1) // n)
+    n_tok, inst = snap.n_tok[:R].copy(), snap.inst[:R].astype(np.int32)
+    scale = np.maximum(snap.true_rem[:R], 1).astype(np.float32) / 60.0
+    h = datagen.make_hidden(d + R, R, d, "bf16", scale=scale)
+    hpad = np.zeros((R, d + ld_pad), np.float32)
+    hpad[:, :d] = h
+    hd = _dev(hpad, torch.bfloat16)[:, :d]
+    W, b = _weights_dev(pw, biases)
+    pred = star.Predictor(*W, *b, max_rows=max(R, 600))
+    assert pred.path(R) == 1
+    beta = datagen.beta_schedule_q16(50)
+    bq = _dev(beta.astype(np.int32))
+    ws = torch.zeros(star.project_workspace_bytes(n, 50), dtype=torch.uint8, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    runs = []
+    for _ in range(3):
+        y, nh, out = star.lenpred_forward_project(pred, hd, _dev(n_tok), _dev(inst), n, 50, bq, ws, err_flag=err)
+        torch.cuda.synchronize()
+        runs.append([y.cpu().numpy(), nh[:R].cpu().numpy()] +
+                    [getattr(out, k).cpu().numpy() for k in ("L", "W", "peak", "growth", "count")])
+    for r in runs[1:]:
+        for a_, b_ in zip(runs[0], r):
+            assert np.array_equal(a_, b_)
+    y, nh = runs[0][0], runs[0][1]
+    ref = oracle_mod.lenpred_weights(h, pw)
+    assert _rel_err(y, ref) <= TOL["bf16"]
+    assert np.array_equal(nh, oracle_mod.quantize(y, n_tok))
+    rp = oracle_mod.project(inst, n_tok, nh, n, 50, beta)
+    for k, v in zip(("L", "W", "peak", "growth", "count"), runs[0][2:]):
+        assert np.array_equal(v, rp[k]), k
+    assert err.item() == 0 and int(ws.sum().item()) == 0
     pred.close()
