@@ -250,7 +250,7 @@ static void plan_splits(int tiles, int num_kb, int bn, bool tf32, int* splits, i
 
 
 // The one-launch small-batch predictor (lenpred_small.cuh) needs all of its CTAs resident at
-// once (phases hand off through counters): 32 clusters of 4 CTAs of ~220 KB shared memory.
+// once (phases hand off through counters): 64 clusters of 2 CTAs of ~218 KB shared memory.
 // STAR_SMALL=0 disables it (A/B measurements).
 static bool small_path_available() {
   const char* e = getenv("STAR_SMALL");
@@ -261,12 +261,12 @@ static bool small_path_available() {
     return false;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(4, 8, 4);
+  cfg.gridDim = dim3(2, 16, 4);
   cfg.blockDim = dim3(192, 1, 1);
   cfg.dynamicSmemBytes = SmallSmem::BYTES;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 4;
+  at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
@@ -276,7 +276,7 @@ static bool small_path_available() {
     cudaGetLastError();
     return false;
   }
-  return ncl >= 32;
+  return ncl >= 64;
 }
 
 static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, int32_t max_ctx, float* y_hat,
@@ -368,7 +368,7 @@ struct star_predictor {
   CUtensorMap tmC1, tmC2;     // TMA-store maps of Z1 / Z2 (bf16, 64 x 32 boxes)
   CUtensorMap tmB1p;          // W1 with 128-row boxes (CTA-pair kernel: each CTA loads half of B)
   // one-launch predictor for <= 512 rows (lenpred_small.cuh)
-  CUtensorMap tmW2s;          // W2 with 64-row boxes
+  CUtensorMap tmW2s;          // W2 with 32-row boxes
   int* small_cnt = nullptr;   // its phase counters (zero between launches)
   bool small_ok = false;      // shape supported and 32 clusters of 4 co-resident
   uint64_t* tl_small = nullptr;
@@ -513,7 +513,7 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
     return st;
   }
   if (!f32 && m1 == 2048 && m2 == 512 && d % 256 == 0) {
-    if ((st = make_tmap(&p->tmW2s, W2, false, (uint64_t)m1, m2, (uint64_t)m1 * 2, 64)) != STAR_OK) {
+    if ((st = make_tmap(&p->tmW2s, W2, false, (uint64_t)m1, m2, (uint64_t)m1 * 2, 32)) != STAR_OK) {
       free_pred(p);
       return st;
     }
@@ -1194,21 +1194,22 @@ static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, 
   a.cnt = p->small_cnt;
   a.project = proj ? 1 : 0;
   if (proj) a.pa = *proj;
-  a.tl = p->tl_small;
+  a.tl = p->tl;   // diagnostics (star_predictor_timeline): [CTAs][32] phase stamps
+  if (p->tl) p->tl_ctas = 2 * 16 * ((R + 127) / 128);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(4, 8, (R + 127) / 128);
+  cfg.gridDim = dim3(2, 16, (R + 127) / 128);
   cfg.blockDim = dim3(192, 1, 1);
   cfg.dynamicSmemBytes = SmallSmem::BYTES;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 4;
+  at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, lenpred_small_kernel, p->tmA1, p->tmB1, p->tmA2, p->tmW2s, p->tmA3, p->tmB3, a);
+  return cudaLaunchKernelEx(&cfg, lenpred_small_kernel, p->tmA1, p->tmB1p, p->tmA2, p->tmW2s, p->tmA3, p->tmB3, a);
 }
 }  // namespace star
