@@ -53,6 +53,7 @@ struct GemmArgs {
   float* head_ws;        // [tiles][splits][128] per-owner partial dots (EPI_HEAD)
   uint64_t* tl;          // diagnostics: [ctas][16] %globaltimer phase stamps, or nullptr
   const int32_t* M_dev;  // device-side row count (refresh mode: rows selected on the device), or nullptr
+  int skip_le;           // refresh mode: leave when M_dev <= skip_le (the one-launch small path ran them)
   int* l1_cnt;           // CTA-pair split-K: [cta tiles][2] arrival / done counters (zeroed, self re-arming)
   int prefetch;          // CTA-pair L2 prefetch: 0 = every CTA, 1 = none, 2 = one CTA per tile row / column
   int mn_swap;           // 1-CTA kernel: grid (n tiles, m tiles, splits) instead of (m, n, splits)
@@ -189,7 +190,8 @@ __global__ void __launch_bounds__(192, 1)
 
   if (p.M_dev) {   // refresh mode: tiles beyond the device-side row count leave before any setup
     pdl_wait();
-    if (m_tile * BM >= __ldcg(p.M_dev)) return;   // the whole cluster (same m-tile) leaves
+    const int md = __ldcg(p.M_dev);
+    if (m_tile * BM >= md || md <= p.skip_le) return;   // the whole cluster (same m-tile) leaves
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);

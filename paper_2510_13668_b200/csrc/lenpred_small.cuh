@@ -53,6 +53,8 @@ struct SmallArgs {
   int project;
   ProjArgs pa;
   uint64_t* tl;          // diagnostics: [ctas][32] %globaltimer phase stamps (slot 15 = SM id), or nullptr
+  const int32_t* M_dev;  // refresh mode: the row count comes from the device (<= 512 runs here,
+                         // more rows leave the whole grid to the 2-launch path), or nullptr (then M)
 };
 
 struct SmallSmem {
@@ -165,7 +167,14 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = blockIdx.x, n = blockIdx.y, m = blockIdx.z;
   const int partner = rank ^ 1;
-  const int m_tiles = gridDim.z;
+  int M = p.M, m_tiles = gridDim.z;
+  if (p.M_dev) {   // refresh mode: the count was produced on the device by the previous kernels
+    pdl_wait();
+    M = __ldcg(p.M_dev);
+    if (M > 128 * (int)gridDim.z) return;   // too many rows: the 2-launch path runs them
+    m_tiles = (M + 127) / 128;
+    if (m >= m_tiles) return;               // both CTAs of the cluster (same m) leave before setup
+  }
   const bool l3 = n == 0;   // this cluster also runs layer 3 + head for m-tile m
   int* z1_cnt = p.cnt;       // [4][2]: Z1 column halves published
   int* z2_cnt = p.cnt + 8;   // [4]
@@ -361,7 +370,7 @@ __global__ void __launch_bounds__(192, 1)
       reduce16(trow, 64 * rank + c, recv, c, rank, row, f);
       relu_bf16_16(f, p.b1, n * 128 + 64 * rank + c, w[c / 16]);
     }
-    if (grow < p.M) {   // the row's 64 owned columns: 128 contiguous bytes
+    if (grow < M) {   // the row's 64 owned columns: 128 contiguous bytes
       uint4* d = reinterpret_cast<uint4*>(p.Z1 + (int64_t)grow * 2048 + n * 128 + 64 * rank);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -398,7 +407,7 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t w2[8];
       reduce16(trow, 128 + 16 * rank, reinterpret_cast<const float*>(smem + S::R2), 0, rank, row, f);
       relu_bf16_16(f, p.b2, n * 32 + 16 * rank, w2);
-      if (grow < p.M) {
+      if (grow < M) {
         uint4* d = reinterpret_cast<uint4*>(p.Z2 + (int64_t)grow * 512 + n * 32 + 16 * rank);
         d[0] = make_uint4(w2[0], w2[1], w2[2], w2[3]);
         d[1] = make_uint4(w2[4], w2[5], w2[6], w2[7]);
@@ -450,7 +459,7 @@ __global__ void __launch_bounds__(192, 1)
       const float* D = reinterpret_cast<const float*>(smem + S::DOT);
       float y = D[row] + D[128 + row];   // rank order (deterministic)
       y += p.b4 ? __ldg(p.b4) : 0.0f;
-      const bool owner = grow < p.M;
+      const bool owner = grow < M;
       int32_t nh = 0, ntok = 0, inst = 0;
       if (owner) {
         if (p.n_tok) ntok = p.n_tok[grow];

@@ -55,6 +55,7 @@ struct TailArgs {
   ProjArgs pa;         // R / inst / n_tok / beta_q / outputs / workspace (ws_cnt, ws_sum, ws_arrive)
   uint64_t* tl;        // diagnostics: [ctas][16] %globaltimer phase stamps, or nullptr
   const int32_t* M_dev;  // device-side row count (refresh mode), or nullptr (then M)
+  int skip_le;           // refresh mode: leave when M_dev <= skip_le (the one-launch small path ran them)
   int mn_swap;           // grid (n2 tiles, m tiles, splits): real m-tiles launch first (refresh mode)
   int plan;            // the projection's last finisher then runs Alg. 1 (one rank: pl reads this
                        // rank's own record), with the whole CTA, in the freed stage ring
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(192, 1)
   if (p.M_dev) {   // refresh mode: the row count was produced on the device by the previous kernels
     pdl_wait();
     Mrows = __ldcg(p.M_dev);
-    if (m_tile * BM >= Mrows) return;   // every CTA of this m-tile (and its cluster) leaves before setup
+    if (m_tile * BM >= Mrows || Mrows <= p.skip_le) return;   // every CTA of this m-tile (and its cluster) leaves
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);

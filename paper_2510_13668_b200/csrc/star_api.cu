@@ -280,7 +280,8 @@ static bool small_path_available() {
 }
 
 static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, int32_t max_ctx, float* y_hat,
-                                int32_t* n_hat, const ProjArgs* proj, cudaStream_t st);
+                                int32_t* n_hat, const ProjArgs* proj, cudaStream_t st,
+                                const CUtensorMap* tmH = nullptr, const int32_t* M_dev = nullptr);
 
 // Whether a one-rank single-round plan runs in the fused tail's last CTA (STAR_PLAN_FUSE=1, read
 // once) instead of the cluster plan kernel launched after it (default).  Measured at TGT with a
@@ -885,6 +886,17 @@ static star_status refresh_impl(star_predictor* p, const void* h, int64_t ld_h, 
     return cuda_fail(e, "refresh_select launch");
   if ((e = launch_refresh_gather(R, h, ld_h * 2, p->d * 2, p->r_idx, p->r_M, p->r_h, st)) != cudaSuccess)
     return cuda_fail(e, "refresh_gather launch");
+  // the compacted rows: up to 512 in the one-launch small-batch kernel (which leaves when the
+  // device-side count is larger); beyond that, or without it, the 2-launch path
+  int skip_le = 0;
+  if (p->small_ok) {
+    if ((e = launch_small(p, R, n_tok ? p->r_ntok : nullptr, max_ctx_len, nullptr, p->r_nhat, nullptr, st, &p->tmA_r,
+                          p->r_M)) != cudaSuccess)
+      return cuda_fail(e, "refresh small-batch launch");
+    skip_le = 512;
+  }
+  if (R <= skip_le) goto scatter;
+  {
   // layer 1 on the compacted rows: 1-CTA tiles + cluster split-K sized for the expected row count
   // ~R/k (the grid covers R rows; tiles beyond the device-side count leave before any setup)
   const int m_tiles = (R + 127) / 128;
@@ -892,6 +904,7 @@ static star_status refresh_impl(star_predictor* p, const void* h, int64_t ld_h, 
   GemmArgs g{};
   g.M = R;
   g.M_dev = p->r_M;
+  g.skip_le = skip_le;
   g.max_ctx = max_ctx_len;
   g.head_ws = p->head_ws;
   g.N = p->m1;
@@ -917,6 +930,7 @@ static star_status refresh_impl(star_predictor* p, const void* h, int64_t ld_h, 
   TailArgs t{};
   t.M = R;
   t.M_dev = p->r_M;
+  t.skip_le = skip_le;
   t.mn_swap = 1;
   t.num_kb = num_kb2;
   t.splits = ts;
@@ -937,6 +951,8 @@ static star_status refresh_impl(star_predictor* p, const void* h, int64_t ld_h, 
   t.project = 0;
   if ((e = launch_tail(p->tmA2, p->tmB2, p->tmB3, t, m_tiles, st)) != cudaSuccess)
     return cuda_fail(e, "refresh tail launch");
+  }
+scatter:
   if (proj && R <= 8192 && refresh_scatter_project_smem(proj->n_inst, proj->H) <= (size_t)200 * 1024) {
     // aging scatter fused with the projection of the resulting N_hat (one CTA)
     if ((e = launch_refresh_scatter_project(*proj, p->r_pos, p->r_nhat, gen, g_last, nhat_last, p->r_M, n_refreshed,
@@ -1176,8 +1192,10 @@ star_status kv_migrate(const star_kv_pool* src, const int32_t* src_table, const 
 
 namespace star {
 static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, int32_t max_ctx, float* y_hat,
-                                int32_t* n_hat, const ProjArgs* proj, cudaStream_t st) {
+                                int32_t* n_hat, const ProjArgs* proj, cudaStream_t st, const CUtensorMap* tmH,
+                                const int32_t* M_dev) {
   SmallArgs a{};
+  a.M_dev = M_dev;
   a.M = R;
   a.kb1 = p->d / 64;
   a.b1 = p->b1;
@@ -1197,7 +1215,7 @@ static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, 
   a.tl = p->tl;   // diagnostics (star_predictor_timeline): [CTAs][32] phase stamps
   if (p->tl) p->tl_ctas = 2 * 16 * ((R + 127) / 128);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2, 16, (R + 127) / 128);
+  cfg.gridDim = dim3(2, 16, (R < 512 ? R + 127 : 512 + 127) / 128);
   cfg.blockDim = dim3(192, 1, 1);
   cfg.dynamicSmemBytes = SmallSmem::BYTES;
   cfg.stream = st;
@@ -1210,6 +1228,7 @@ static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, 
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, lenpred_small_kernel, p->tmA1, p->tmB1p, p->tmA2, p->tmW2s, p->tmA3, p->tmB3, a);
+  return cudaLaunchKernelEx(&cfg, lenpred_small_kernel, tmH ? *tmH : p->tmA1, p->tmB1p, p->tmA2, p->tmW2s, p->tmA3,
+                            p->tmB3, a);
 }
 }  // namespace star
