@@ -22,11 +22,10 @@
 //       blocks stream in first (independent), the Z1 blocks after z1_cnt[m][r] = 16 (acquire);
 //       tcgen05 N=32; the same DSMEM reduction (8 KB, owned 16 columns) -> + b2, ReLU, bf16 ->
 //       Z2, bump z2_cnt[m].
-//   L3  (clusters n == 0: one per m-tile) Z3 = W3 Z2 over the K half r after z2_cnt[m] = 32;
-//       DSMEM reduction (owned 32 columns), + b3, ReLU, the partial w4 dot of the owned columns
-//       -> CTA 0 of the cluster (DSMEM), which sums the two partial dots in rank order, + b4,
-//       quantizes (readings A8-A10) and adds the rows to the projection histogram; the last
-//       m-tile to finish finalises L/W/peak/growth/count and re-arms every counter.
+//   L3  (CTA 0 of cluster (m, 0): one per m-tile) Z3 = W3 Z2 over the full K = 512 after
+//       z2_cnt[m] = 32 (no split: no exchange, no cluster barrier), + b3, ReLU, the w4 dot in
+//       column order, + b4, the quantizer (readings A8-A10) and the rows' projection histogram;
+//       the last m-tile to finish finalises L/W/peak/growth/count and re-arms every counter.
 // Roles (192 threads, as in umma_gemm_kernel): warp 0 TMA producer, warp 1 MMA issuer (one
 // elected lane), warps 2-5 epilogue (TMEM lane quarter = warp % 4).
 #pragma once
@@ -66,9 +65,7 @@ struct SmallSmem {
   static constexpr uint32_t L1_RECV = 32u * 1024u;        // 32 KB (after the cluster barrier)
   static constexpr uint32_t SEND23 = 0;                   // L2 / L3 send (A slots are idle then)
   static constexpr uint32_t R2 = 192u * 1024u;            // layer-2 receive 8 KB (dedicated)
-  static constexpr uint32_t R3 = 200u * 1024u;            // layer-3 receive 16 KB (dedicated)
-  static constexpr uint32_t DOT = 216u * 1024u;           // [2][128] fp32 partial dots (CTA 0)
-  static constexpr uint32_t BAR = DOT + 1024u;
+  static constexpr uint32_t BAR = 200u * 1024u;
   static constexpr uint32_t BYTES = 1024u + BAR + 256u;
   static constexpr uint32_t HIST = 0;                     // finalize: histogram staging (ring idle), <= 96 KB
 };
@@ -160,8 +157,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* acc3 = acc2 + 1;
   uint64_t* r1bar = acc3 + 1;
   uint64_t* r2bar = r1bar + 1;
-  uint64_t* r3bar = r2bar + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(r3bar + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(r2bar + 1);
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -175,7 +171,7 @@ __global__ void __launch_bounds__(192, 1)
     m_tiles = (M + 127) / 128;
     if (m >= m_tiles) return;               // both CTAs of the cluster (same m) leave before setup
   }
-  const bool l3 = n == 0;   // this cluster also runs layer 3 + head for m-tile m
+  const bool l3 = n == 0 && rank == 0;   // this CTA also runs layer 3 + head for m-tile m
   int* z1_cnt = p.cnt;       // [4][2]: Z1 column halves published
   int* z2_cnt = p.cnt + 8;   // [4]
   int* done = p.cnt + 12;
@@ -205,11 +201,9 @@ __global__ void __launch_bounds__(192, 1)
     mbar_init(acc3, 1);
     mbar_init(r1bar, 1);
     mbar_init(r2bar, 1);
-    mbar_init(r3bar, 1);
     // the partner's bulk copies complete bytes on these: armed before it can send
     mbar_arrive_expect_tx(r1bar, 32768u);
     mbar_arrive_expect_tx(r2bar, 8192u);
-    if (l3) mbar_arrive_expect_tx(r3bar, 16384u);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<256>(tmem_slot);
@@ -306,18 +300,23 @@ __global__ void __launch_bounds__(192, 1)
         }
         tma_load_2d(smem + 16384 * s, &tmZ1, &full[s], rank * 1024 + i * 64, m * 128, pol_a);
       }
-      if (l3) {   // layer 3: W3 blocks, then the Z2 blocks after all 32 layer-2 CTAs of m-tile m
-        for (int i = 0; i < 4; ++i) {
+      if (l3) {   // layer 3 (full K = 512): W3 blocks, then the Z2 blocks after all 32 layer-2 CTAs of m-tile m
+        for (int i = 0; i < NS; ++i) {
           const int it = it3 + i, s = it % NS;
           mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&full[s], 16384u + 8192u);
-          tma_load_2d(smem + S::B0 + 16384 * s, &tmW3, &full[s], rank * 256 + i * 64, 0, pol_b);
+          tma_load_2d(smem + S::B0 + 16384 * s, &tmW3, &full[s], i * 64, 0, pol_b);
         }
         spin_wait_geq(z2_cnt + m, 32);
         fence_proxy_async_global();
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 8; ++i) {
           const int it = it3 + i, s = it % NS;
-          tma_load_2d(smem + 16384 * s, &tmZ2, &full[s], rank * 256 + i * 64, m * 128, pol_a);
+          if (i >= NS) {
+            mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
+            mbar_arrive_expect_tx(&full[s], 16384u + 8192u);
+            tma_load_2d(smem + S::B0 + 16384 * s, &tmW3, &full[s], i * 64, 0, pol_b);
+          }
+          tma_load_2d(smem + 16384 * s, &tmZ2, &full[s], i * 64, m * 128, pol_a);
         }
       }
     }
@@ -337,7 +336,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       umma_commit(acc2);
       if (l3) {
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 8; ++i) {
           const int it = it3 + i, s = it % NS;
           mbar_wait(&full[s], (uint32_t)(it / NS) & 1u);
           tc_fence_after();
@@ -422,43 +421,23 @@ __global__ void __launch_bounds__(192, 1)
     }
   }
 
-  if (l3) {
-    if (warp >= 2) {
-      // ---- layer 3: reduce the owned 32 Z3 columns, + b3, ReLU, partial w4 dot ----
-      mbar_wait(acc3, 0);
-      tc_fence_after();
-      if (te == 0) SMALL_TS(9);
-      tmem_to_block(trow, 160 + 32 * partner, 32, reinterpret_cast<float*>(smem + S::SEND23), row);
-      fence_proxy_async_smem();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (te == 0) {
-        bulk_s2cluster(mapa_shared(smem_u32(smem + S::R3), (uint32_t)partner), smem + S::SEND23, 16384u,
-                       mapa_shared(smem_u32(r3bar), (uint32_t)partner));
-        bulk_commit();
-      }
-      mbar_wait(r3bar, 0);
-      if (te == 0) SMALL_TS(16);
-      float dot = 0.0f;
+  if (l3 && warp >= 2) {
+    // ---- layer 3 (this CTA holds the whole 128 x 64 Z3 tile): + b3, ReLU, w4 dot, + b4 ----
+    mbar_wait(acc3, 0);
+    tc_fence_after();
+    if (te == 0) SMALL_TS(9);
+    float y = 0.0f;
+#pragma unroll 1
+    for (int c = 0; c < 64; c += 16) {
+      uint32_t v[16];
+      tmem_ld_32x32b_x16(trow + 160u + (uint32_t)c, v);
+      tmem_ld_wait();
 #pragma unroll
-      for (int c = 0; c < 32; c += 16) {
-        float f[16];
-        reduce16(trow, 160 + 32 * rank + c, reinterpret_cast<const float*>(smem + S::R3), c, rank, row, f);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int col = 32 * rank + c + j;
-          dot = fmaf(__ldg(p.w4 + col), fmaxf(f[j] + (p.b3 ? __ldg(p.b3 + col) : 0.0f), 0.0f), dot);
-        }
-      }
-      // partial dot -> CTA 0's DOT[rank][row] (distributed shared memory)
-      const uint32_t da = mapa_shared(smem_u32(smem + S::DOT + 4u * (uint32_t)(rank * 128 + row)), 0u);
-      asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(da), "f"(dot) : "memory");
-      if (te == 0) bulk_wait_read_all();
+      for (int j = 0; j < 16; ++j)
+        y = fmaf(__ldg(p.w4 + c + j), fmaxf(__uint_as_float(v[j]) + (p.b3 ? __ldg(p.b3 + c + j) : 0.0f), 0.0f), y);
     }
-    cluster_sync_all();   // both partial dots are in CTA 0
-    if (rank == 0 && warp >= 2) {
-      const float* D = reinterpret_cast<const float*>(smem + S::DOT);
-      float y = D[row] + D[128 + row];   // rank order (deterministic)
-      y += p.b4 ? __ldg(p.b4) : 0.0f;
+    y += p.b4 ? __ldg(p.b4) : 0.0f;
+    {
       const bool owner = grow < M;
       int32_t nh = 0, ntok = 0, inst = 0;
       if (owner) {

@@ -346,29 +346,42 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
 
   for (int round = 0; round < a.max_moves; ++round) {
     // ---- Phase 1: InstanceClassification, changed instances only ----
-    // W pass: one warp per instance, W_i = sum_{t>=1} beta_t L_i[t] and T_exec(i); the prefix
-    // sums P0/P1 that Phases 2-3 need are built below only when some instance is overloaded.
+    // One warp per changed instance builds the prefix sums Phases 2-3 need, P0_i[T] = sum_{t<=T}
+    // beta_t L_i[t] and P1_i[T] = sum_{t<=T} t beta_t L_i[t] (warp scans), and takes
+    // W_i = sum_{t>=1} beta_t L_i[t] = P0_i[H] - beta_0 L_i[0] from them, plus T_exec(i).
     for (int i = warp; i < n; i += nwarps) {
       __syncwarp();
       const int d = s.wdirty[i];
       __syncwarp();   // every lane has read the flag before lane 0 clears it
       if (!d) continue;
       const int64_t* Li = s.Ls + (int64_t)i * H1;
-      if (d == 2) {   // W_i given: T_exec(i) only
-        if (lane == 0) {
-          s.texec[i] = (i128)a.a_ps + (i128)a.b_ps * Li[0];
-          s.wdirty[i] = 0;
-        }
-        continue;
-      }
-      i128 wpart = 0;
-      for (int t = 1 + lane; t < H1; t += 32) wpart += mul_u32((i128)Li[t], s.beta[t]);
+      i128 c0 = 0, c1 = 0;
+      for (int base = 0; base < H1; base += 32) {
+        const int t = base + lane;
+        const i128 x = t < H1 ? mul_u32((i128)Li[t], s.beta[t]) : (i128)0;
+        i128 x0 = x, x1 = mul_u32(x, (uint32_t)t);
 #pragma unroll
-      for (int m = 16; m >= 1; m >>= 1) wpart += shfl_xor_i128(wpart, m);
-      if (lane == 0) {
-        s.Wv[i] = cur_only ? (i128)s.beta[0] * Li[0] : wpart;
+        for (int off = 1; off < 32; off <<= 1) {
+          const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off);
+          if (lane >= off) {
+            x0 += y0;
+            x1 += y1;
+          }
+        }
+        x0 += c0;
+        x1 += c1;
+        if (t < H1) {
+          s.P0[(int64_t)i * H1 + t] = x0;
+          s.P1[(int64_t)i * H1 + t] = x1;
+        }
+        c0 = shfl_idx_i128(x0, 31);
+        c1 = shfl_idx_i128(x1, 31);
+      }
+      if (lane == 0) {   // c0 = P0_i[H] (lanes past H add zeros)
+        if (d != 2) s.Wv[i] = cur_only ? (i128)s.beta[0] * Li[0] : c0 - (i128)s.beta[0] * Li[0];
         s.texec[i] = (i128)a.a_ps + (i128)a.b_ps * Li[0];
         s.wdirty[i] = 0;
+        s.pdirty[i] = 0;
       }
     }
     __syncthreads();
