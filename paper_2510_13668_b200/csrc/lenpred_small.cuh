@@ -423,6 +423,12 @@ __global__ void __launch_bounds__(192, 1)
 
   if (l3 && warp >= 2) {
     // ---- layer 3 (this CTA holds the whole 128 x 64 Z3 tile): + b3, ReLU, w4 dot, + b4 ----
+    const bool owner = grow < M;
+    int32_t ntok = 0, inst = 0;   // the row's N(r) and instance, fetched while layer 3 runs
+    if (owner) {
+      if (p.n_tok) ntok = p.n_tok[grow];
+      if (p.project) inst = p.pa.inst[grow];
+    }
     mbar_wait(acc3, 0);
     tc_fence_after();
     if (te == 0) SMALL_TS(9);
@@ -438,11 +444,8 @@ __global__ void __launch_bounds__(192, 1)
     }
     y += p.b4 ? __ldg(p.b4) : 0.0f;
     {
-      const bool owner = grow < M;
-      int32_t nh = 0, ntok = 0, inst = 0;
+      int32_t nh = 0;
       if (owner) {
-        if (p.n_tok) ntok = p.n_tok[grow];
-        if (p.project) inst = p.pa.inst[grow];
         int32_t cap = p.max_ctx - ntok;
         cap = cap < 0 ? 0 : cap;
         nh = __float2int_rn(fminf(fmaxf(y, 0.0f), (float)cap));   // quantize_nhat (readings A8-A10)

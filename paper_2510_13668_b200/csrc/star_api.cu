@@ -682,7 +682,11 @@ static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, 
       p->tl_l1_ctas = ((m_tiles + 1) & ~1) * (p->m1 / 256) * pair_splits;
     }
     // unsplit pairs over N = 2048: 9 non-uniform column tiles when they still fit one wave
-    const bool nu = pair && pair_splits == 1 && p->m1 == 2048 && ((m_tiles + 1) / 2) * 9 * 2 <= g_num_sms;
+    // (also over several waves: 9 tiles of <= 240 columns win whenever they need no more waves
+    // than 8 tiles of 256, e.g. M = 4096: 2 waves of 144 CTAs instead of 148 + 108)
+    const int slots = (g_num_sms / 2) * 2, npairs = (m_tiles + 1) / 2;
+    const int w8 = (npairs * 16 + slots - 1) / slots, w9 = (npairs * 18 + slots - 1) / slots;
+    const bool nu = pair && pair_splits == 1 && p->m1 == 2048 && w9 * 240 < w8 * 256;
     if (nu) p->tl_l1_ctas = ((m_tiles + 1) & ~1) * 9;
     if (!pair) {   // diagnostics timeline of the 1-CTA layer-1 kernel (rows: m x n x split CTAs)
       g.tl = p->tl_l1;
