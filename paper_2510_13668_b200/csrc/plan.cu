@@ -61,8 +61,7 @@ template <int kCl>
 __global__ void __launch_bounds__(kPlanThreads, 1) plan_cluster_kernel(const PlanArgs a) {
   extern __shared__ __align__(16) uint8_t smraw[];
   __shared__ Cand warp_best[kPlanThreads / 32];
-  __shared__ Cand cl_best[2 + kCl];
-  __shared__ uint64_t cl_bar;
+  __shared__ Cand cl_best[2];
   __shared__ int shv[8];
   const bool lead = cluster_ctarank() == 0;
   if (lead && threadIdx.x == 0) g_plan_tl[0] = globaltimer_ns();
@@ -71,8 +70,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_cluster_kernel(const Pla
     g_plan_tl[1] = globaltimer_ns();
     g_plan_tl[33] = clock64();
   }
-  plan_cta_fast<false, kCl>(a, smraw, (int)threadIdx.x, (int)blockDim.x, warp_best, shv, g_plan_tl, cl_best,
-                            &cl_bar);
+  plan_cta_fast<false, kCl>(a, smraw, (int)threadIdx.x, (int)blockDim.x, warp_best, shv, g_plan_tl, cl_best);
 }
 
 // Cluster size of the staged plan: STAR_PLAN_CLUSTER (1, 2, 4 or 8; read once) for A/B

@@ -128,25 +128,14 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // over the CTAs (4-slot groups interleaved by CTA rank, so the requests of an overloaded instance
 // spread over every SM); each round's CTA winners meet in distributed shared memory and every
 // CTA takes the same argmax (a total order), applies m* to its own copy of the loads and goes on.
-// Only CTA 0 writes the move list.  cl_best: [2 + kCl] shared Cands (round-parity double buffer,
-// then the last round's slots); cl_bar: a shared mbarrier.  The LAST round (the only one when
-// max_moves = 1) needs no barrier: every other CTA pushes its winner into CTA 0's slot with
-// st.async (completion on CTA 0's mbarrier) and is done; CTA 0 takes the argmax and writes m*.
+// Only CTA 0 writes the move list.  cl_best: [2] shared Cands (round-parity double buffer).
+// (Measured and rejected: pushing the last round's CTA winners to CTA 0 with st.async +
+// mbarrier instead of the cluster barrier -- the plan went 11.0 -> 15.4 us.)
 template <bool kFused = false, int kCl = 1>
 __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw, const int tid, const int nthreads,
-                                              Cand* warp_best, int* shv, uint64_t* tl, Cand* cl_best = nullptr,
-                                              uint64_t* cl_bar = nullptr) {
+                                              Cand* warp_best, int* shv, uint64_t* tl, Cand* cl_best = nullptr) {
   const int crank = kCl > 1 ? (int)cluster_ctarank() : 0;
   if (kCl > 1 && crank != 0) tl = nullptr;
-  bool pushed = false;   // the last round's winners went to CTA 0 (no exit barrier needed)
-  if constexpr (kCl > 1) {
-    if (crank == 0 && tid == 0) {
-      mbar_init(cl_bar, 1);
-      fence_barrier_init();
-      mbar_arrive_expect_tx(cl_bar, 32u * (kCl - 1));
-    }
-    cluster_sync_all();   // CTA 0's slot barrier is armed before any CTA can push
-  }
 #define PLAN_TS(k)                                           \
   do {                                                       \
     if (tl && tid == 0) {                                    \
@@ -612,32 +601,9 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     if (warp == 0) {
       if (lane < nwarps) c = warp_best[lane];
       c = warp_argmax_g(c);   // every lane holds the CTA's winner
-      if (kCl > 1 && lane == 0 && !last) cl_best[round & 1] = c;
+      if (kCl > 1 && lane == 0) cl_best[round & 1] = c;
     }
-    if (kCl > 1 && last) {
-      // last round: winners -> CTA 0 (st.async, 2 x 16 bytes, completion on its mbarrier)
-      pushed = true;
-      if (warp == 0 && lane == 0 && crank != 0) {
-        const uint32_t dst = mapa_shared(smem_u32(cl_best + 2 + crank), 0u);
-        const uint32_t bar = mapa_shared(smem_u32(cl_bar), 0u);
-        const unsigned __int128 us = (unsigned __int128)c.score;
-        const uint64_t lo = (uint64_t)us, hi = (uint64_t)(us >> 64);
-        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst),
-                     "r"((uint32_t)lo), "r"((uint32_t)(lo >> 32)), "r"((uint32_t)hi), "r"((uint32_t)(hi >> 32)), "r"(bar)
-                     : "memory");
-        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst + 16u),
-                     "r"((uint32_t)c.id), "r"((uint32_t)c.dst), "r"((uint32_t)c.g), "r"(0u), "r"(bar)
-                     : "memory");
-      }
-      if (crank != 0) break;   // CTA-uniform: this CTA is done
-      if (warp == 0) {
-        mbar_wait(cl_bar, 0);
-        Cand o = c;
-        if (lane >= 1 && lane < kCl) o = cl_best[2 + lane];
-        else if (lane >= kCl) { o.score = 0; o.id = 0; o.dst = 0; o.g = -1; }
-        c = warp_argmax_g(o);
-      }
-    } else if constexpr (kCl > 1) {
+    if constexpr (kCl > 1) {
       // cluster argmax: every CTA published its winner; meet (all threads), then warp 0 of every
       // CTA reads all kCl winners from distributed shared memory and takes the same argmax
       cluster_sync_all();
@@ -704,11 +670,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
   }
   PLAN_TS(7);
   if (tid == 0 && crank == 0) *a.n_moves = s_nmoves;
-  // no CTA leaves while a peer may still read its cl_best (the barrier rounds); after a pushed
-  // last round nobody reads a peer any more
-  if constexpr (kCl > 1) {
-    if (!pushed) cluster_sync_all();
-  }
+  if constexpr (kCl > 1) cluster_sync_all();   // no CTA leaves while a peer may still read its cl_best
 #undef PLAN_TS
 }
 
