@@ -299,7 +299,9 @@ star_status lenpred_forward_project_plan(star_predictor* p, const void* h, int64
 /* Diagnostics: %globaltimer stamps (ns) of the most recent single-CTA plan launch: [0] entry,
  * [1] launched, [12] static inputs staged, [13] after griddepcontrol.wait, [2] inputs staged,
  * [3] W pass, [4] classification, [9] candidates compacted, [5] candidate argmax, [6] move
- * applied, [7] end (per-round stamps hold the last round); [32 + k] the same as clock64.
+ * applied, [7] end (per-round stamps hold the last round); [32 + k] the same as clock64;
+ * [64 + 8 r + j] per CTA r of the cluster plan: j = 0 entry, 1 after griddepcontrol.wait,
+ * 2/4 before and 3/5 after the round's cluster barrier (round parity).  host64 holds 128 values.
  * Synchronises the device. */
 star_status star_plan_timeline(uint64_t* host64);
 

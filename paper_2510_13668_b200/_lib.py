@@ -481,7 +481,7 @@ def dispatch_requests(policy: int, L: torch.Tensor, beta_q: torch.Tensor, n_tok:
 
 def plan_timeline():
     """Diagnostics: phase stamps (ns) of the most recent single-CTA plan (star_plan_timeline)."""
-    buf = np.zeros(64, dtype=np.uint64)
+    buf = np.zeros(128, dtype=np.uint64)
     _check(lib().star_plan_timeline(buf.ctypes.data_as(P)), "star_plan_timeline")
     return buf
 

@@ -29,9 +29,12 @@ constexpr int kPlanThreads = 512;
 
 // diagnostics: %globaltimer stamps of the most recent single-CTA plan (star_plan_timeline)
 __device__ uint64_t g_plan_tl[64];
+__device__ uint64_t g_plan_cl_tl[64];   // per-CTA stamps of the cluster plan: [rank][entry, pdl, pre-sync, post-sync, ...]
 
 cudaError_t plan_timeline(uint64_t* host64) {
-  return cudaMemcpyFromSymbol(host64, g_plan_tl, sizeof(uint64_t) * 64);
+  cudaError_t e = cudaMemcpyFromSymbol(host64, g_plan_tl, sizeof(uint64_t) * 64);
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(host64 + 64, g_plan_cl_tl, sizeof(uint64_t) * 64);
+  return e;
 }
 
 
@@ -64,13 +67,16 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_cluster_kernel(const Pla
   __shared__ Cand cl_best[2];
   __shared__ int shv[8];
   const bool lead = cluster_ctarank() == 0;
+  if (threadIdx.x == 0) g_plan_cl_tl[cluster_ctarank() * 8] = globaltimer_ns();
+  PlanArgs ac = a;
   if (lead && threadIdx.x == 0) g_plan_tl[0] = globaltimer_ns();
   pdl_launch_dependents();
   if (lead && threadIdx.x == 0) {
     g_plan_tl[1] = globaltimer_ns();
     g_plan_tl[33] = clock64();
   }
-  plan_cta_fast<false, kCl>(a, smraw, (int)threadIdx.x, (int)blockDim.x, warp_best, shv, g_plan_tl, cl_best);
+  ac.cl_tl = g_plan_cl_tl;
+  plan_cta_fast<false, kCl>(ac, smraw, (int)threadIdx.x, (int)blockDim.x, warp_best, shv, g_plan_tl, cl_best);
 }
 
 // Cluster size of the staged plan: STAR_PLAN_CLUSTER (1, 2, 4 or 8; read once) for A/B

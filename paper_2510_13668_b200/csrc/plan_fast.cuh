@@ -58,26 +58,30 @@ inline size_t plan_fast_smem_layout(int n, int H, int world, int r_cap) {
 }
 
 // Cand order extended by the slot index, so the winner does not depend on enumeration order.
+// Branch-free (one predicate from comparisons, no early returns): used between shuffle steps, where
+// a divergent select would send the next shuffle down the slow (BRA.DIV) path.
 __device__ __forceinline__ bool cand_better_g(const Cand& x, const Cand& y) {
-  if (x.g < 0) return false;
-  if (y.g < 0) return true;
-  if (x.score != y.score) return x.score > y.score;
-  if (x.id != y.id) return x.id < y.id;
-  if (x.dst != y.dst) return x.dst < y.dst;
-  return x.g < y.g;
+  const bool s_gt = x.score > y.score, s_eq = x.score == y.score;
+  const bool tie = (x.id < y.id) | ((x.id == y.id) & ((x.dst < y.dst) | ((x.dst == y.dst) & (x.g < y.g))));
+  return (x.g >= 0) & ((y.g < 0) | s_gt | (s_eq & tie));
 }
 
 __device__ __forceinline__ Cand warp_argmax_g(Cand c) {
+  __syncwarp();   // reconverge first: shuffles of a diverged warp take the slow path
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
-    Cand o;
     const uint64_t lo = __shfl_xor_sync(0xFFFFFFFFu, (uint64_t)c.score, off);
     const uint64_t hi = __shfl_xor_sync(0xFFFFFFFFu, (uint64_t)(c.score >> 64), off);
+    Cand o;
     o.score = (i128)(((unsigned __int128)hi << 64) | lo);
     o.id = __shfl_xor_sync(0xFFFFFFFFu, c.id, off);
     o.dst = __shfl_xor_sync(0xFFFFFFFFu, c.dst, off);
     o.g = __shfl_xor_sync(0xFFFFFFFFu, c.g, off);
-    if (cand_better_g(o, c)) c = o;
+    const bool b = cand_better_g(o, c);   // selects, not a branch
+    c.score = b ? o.score : c.score;
+    c.id = b ? o.id : c.id;
+    c.dst = b ? o.dst : c.dst;
+    c.g = b ? o.g : c.g;
   }
   return c;
 }
@@ -330,6 +334,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
   if (tid == 0) s_nmoves = 0;
   PLAN_TS(12);
   pdl_wait();   // N_hat and L are written by the predecessor (predictor tail / projection / all-gather)
+  if (kCl > 1 && a.cl_tl && tid == 0) a.cl_tl[crank * 8 + 1] = globaltimer_ns();
   PLAN_TS(13);
   if (a.bulk) {
     if (!kFused && tid == issuer) issue_table(false, false, true);
@@ -364,6 +369,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
         i128 x0 = x, x1 = mul_u32(x, (uint32_t)t);
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
+          __syncwarp();   // the add below diverges: reconverge before the next shuffle
           const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off);
           if (lane >= off) {
             x0 += y0;
@@ -449,6 +455,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
         i128 x0 = bt, x1 = mul_u32(bt, (uint32_t)u), x2 = mul_u32(x1, (uint32_t)u);
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
+          __syncwarp();   // the add below diverges: reconverge before the next shuffle
           const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off), y2 = shfl_up_i128(x2, off);
           if (lane >= off) {
             x0 += y0;
@@ -482,6 +489,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
         i128 x0 = x, x1 = mul_u32(x, (uint32_t)t);
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
+          __syncwarp();   // the add below diverges: reconverge before the next shuffle
           const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off);
           if (lane >= off) {
             x0 += y0;
@@ -538,6 +546,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
       int x = cntl;   // inclusive warp scan of the per-lane counts
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
+        __syncwarp();
         const int y = __shfl_up_sync(0xFFFFFFFFu, x, off);
         if (lane >= off) x += y;
       }
@@ -606,7 +615,9 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     if constexpr (kCl > 1) {
       // cluster argmax: every CTA published its winner; meet (all threads), then warp 0 of every
       // CTA reads all kCl winners from distributed shared memory and takes the same argmax
+      if (a.cl_tl && tid == 0) a.cl_tl[crank * 8 + 2 + 2 * (round & 1)] = globaltimer_ns();
       cluster_sync_all();
+      if (a.cl_tl && tid == 0) a.cl_tl[crank * 8 + 3 + 2 * (round & 1)] = globaltimer_ns();
       if (warp == 0) {
         Cand o;
         o.score = 0; o.id = 0; o.dst = 0; o.g = -1;
