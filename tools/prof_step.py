@@ -23,7 +23,8 @@ import paper_2510_13668_b200 as star  # noqa: E402
 from paper_2510_13668_b200.step import RecordLayout, Step  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--mode", default="n1", choices=["n1", "rank", "kv", "proj"])
+ap.add_argument("--mode", default="n1", choices=["n1", "rank", "kv", "proj", "refresh"])
+ap.add_argument("--config", default="TGT")
 ap.add_argument("--steps", type=int, default=3)
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
@@ -58,6 +59,25 @@ if args.mode in ("n1", "rank"):
         st.run(h)
     torch.cuda.synchronize()
     print("moves", st.result())
+elif args.mode == "refresh":   # the bench's cadence-k step (k = 20, ~1/20 of the rows due)
+    c, snap, params_h, idx, pw, h_np = bench.make_workload(args.config, 1, 0, 0)
+    W = [torch.from_numpy(x).to(torch.bfloat16).to(dev) for x in (pw.W1, pw.W2, pw.W3)]
+    pred = star.Predictor(*W, torch.from_numpy(pw.w4).to(dev), max_rows=len(idx))
+    params = star.PlanParams.from_host(params_h, device=dev)
+    h = bench.longtail_hidden(star, pred, h_np, snap, idx, torch.bfloat16, dev)
+    R, k = len(idx), 20
+    st = Step(pred, params, c["n_inst"], r_cap=R, device=dev, refresh_k=k)
+    st.load_requests(*(torch.from_numpy(np.ascontiguousarray(a[idx])) for a in (snap.req_id, snap.inst, snap.n_tok)))
+    gen = (snap.n_tok[idx] - np.minimum(snap.n_tok[idx] - 1, 36)).astype(np.int32) + 100
+    g_last = (gen - (np.arange(R) % k) - 1).astype(np.int32)
+    st.set_generation(torch.from_numpy(gen), torch.from_numpy(g_last),
+                      torch.from_numpy(np.maximum(snap.true_rem[idx], 1).astype(np.int32)))
+    for i in range(args.steps + 1):
+        st.set_generation(torch.from_numpy(gen + i))
+        flush.fill_(1.0)
+        st.run(h)
+    torch.cuda.synchronize()
+    print("refreshed", int(st.n_refreshed.item()), "moves", st.result())
 elif args.mode == "kv":
     r = bench.kv_migration_timing(star, dev, reps=1)
     print({k: r[k] for k in ("pack", "unpack", "migrate")})
