@@ -48,12 +48,19 @@ struct SmallArgs {
   int32_t* n_hat;        // [M] or nullptr
   __nv_bfloat16* Z1;     // [>= M][2048]
   __nv_bfloat16* Z2;     // [>= M][512]
-  int* cnt;              // z1_cnt [4][2] | z2_cnt [4] | done [1]   (zero between launches)
+  int* cnt;              // per 512-row chunk c: [c*16 + 0..7] z1_cnt [4][2], [c*16 + 8..11] z2_cnt [4];
+                         // [SmallSmem::DONE] layer-3 completions (all zero between launches)
   int project;
   ProjArgs pa;
   uint64_t* tl;          // diagnostics: [ctas][32] %globaltimer phase stamps (slot 15 = SM id), or nullptr
-  const int32_t* M_dev;  // refresh mode: the row count comes from the device (<= 512 runs here,
-                         // more rows leave the whole grid to the 2-launch path), or nullptr (then M)
+  const int32_t* M_dev;  // refresh mode: the row count comes from the device, or nullptr (then M)
+  // refresh mode (cadence k): row p of the batch is request slot r_idx[p]; its N_hat, g_last = gen
+  // and N_hat_last are scattered there (the aged slots were handled by the select kernel)
+  const int32_t* r_idx;
+  const int32_t* r_gen;
+  int32_t* r_glast;
+  int32_t* r_nhat_last;
+  int32_t* r_nhat;
 };
 
 struct SmallSmem {
@@ -68,6 +75,7 @@ struct SmallSmem {
   static constexpr uint32_t BAR = 200u * 1024u;
   static constexpr uint32_t BYTES = 1024u + BAR + 256u;
   static constexpr uint32_t HIST = 0;                     // finalize: histogram staging (ring idle), <= 96 KB
+  static constexpr int DONE = 16 * 64;                    // index of the completion counter in cnt (<= 64 chunks)
 };
 static_assert(SmallSmem::BYTES <= 227u * 1024u, "small predictor smem");
 
@@ -138,6 +146,37 @@ __device__ __forceinline__ void relu_bf16_16(const float (&f)[16], const float* 
   }
 }
 
+// The projection's last step (by the last m-tile to finish, or by CTA 0 when a refresh step has no
+// due row): L/W/peak/growth/count from the global histogram (one warp per instance), then the
+// histogram is re-zeroed.  The histogram comes into shared memory with L2 loads (other SMs'
+// atomics) when it fits the ring's A slots.  Epilogue warps 2..5 (te = thread - 64).
+__device__ __forceinline__ void small_finalize(const SmallArgs& p, uint8_t* smem, int te, int warp) {
+  using S = SmallSmem;
+  const int nb = p.pa.n_inst * (p.pa.H + 2);
+  uint32_t* sbeta = reinterpret_cast<uint32_t*>(smem + S::R2);   // consumed by now
+  for (int t = te; t <= p.pa.H; t += 128) sbeta[t] = p.pa.beta_q[t];
+  const uint32_t* hc = p.pa.ws_cnt;
+  const unsigned long long* hs = p.pa.ws_sum;
+  if ((uint32_t)nb * 12u <= 96u * 1024u) {
+    unsigned long long* ss = reinterpret_cast<unsigned long long*>(smem + S::HIST);
+    uint32_t* sc = reinterpret_cast<uint32_t*>(ss + nb);
+    for (int k = te; k < nb; k += 128) {
+      ss[k] = __ldcg(p.pa.ws_sum + k);
+      sc[k] = __ldcg(p.pa.ws_cnt + k);
+    }
+    hc = sc;
+    hs = ss;
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  proj_finalize<false>(p.pa, hc, hs, sbeta, warp - 2, 4);
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  for (int k = te; k < nb; k += 128) {
+    p.pa.ws_cnt[k] = 0;
+    p.pa.ws_sum[k] = 0;
+  }
+  if (te == 0) *p.pa.ws_arrive = 0;
+}
+
 __global__ void __launch_bounds__(192, 1)
     lenpred_small_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW1,
                          const __grid_constant__ CUtensorMap tmZ1, const __grid_constant__ CUtensorMap tmW2,
@@ -163,18 +202,23 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = blockIdx.x, n = blockIdx.y, m = blockIdx.z;
   const int partner = rank ^ 1;
-  int M = p.M, m_tiles = gridDim.z;
-  if (p.M_dev) {   // refresh mode: the count was produced on the device by the previous kernels
+  const int te = threadIdx.x - 64;     // epilogue thread 0..127
+  int M = p.M;
+  if (p.M_dev) {   // refresh mode: the count was produced on the device by the previous kernel
     pdl_wait();
     M = __ldcg(p.M_dev);
-    if (M > 128 * (int)gridDim.z) return;   // too many rows: the 2-launch path runs them
-    m_tiles = (M + 127) / 128;
-    if (m >= m_tiles) return;               // both CTAs of the cluster (same m) leave before setup
   }
-  const bool l3 = n == 0 && rank == 0;   // this CTA also runs layer 3 + head for m-tile m
-  int* z1_cnt = p.cnt;       // [4][2]: Z1 column halves published
-  int* z2_cnt = p.cnt + 8;   // [4]
-  int* done = p.cnt + 12;
+  // rows are processed in chunks of 512 (4 m-tiles): one chunk unless a refresh step has more
+  // due rows; chunk c's m-tile m covers rows [512 c + 128 m, +128)
+  const int nchunks = (M + 511) / 512;
+  const int total_mt = (M + 127) / 128;     // m-tiles over all chunks (= layer-3 completions)
+  if (M == 0) {   // refresh step with no due row: the projection of the aged rows is still due
+    if (p.project && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && warp >= 2)
+      small_finalize(p, smem, te, warp);
+    return;
+  }
+  if (m * 128 >= M) return;   // this m-tile is empty in every chunk (both CTAs of the cluster)
+  const bool l3 = n == 0 && rank == 0;   // this CTA also runs layer 3 + head for its m-tile
   if (threadIdx.x == 0) {
     SMALL_TS(0);
     if (p.tl) {
@@ -201,14 +245,16 @@ __global__ void __launch_bounds__(192, 1)
     mbar_init(acc3, 1);
     mbar_init(r1bar, 1);
     mbar_init(r2bar, 1);
-    // the partner's bulk copies complete bytes on these: armed before it can send
+    // the partner's bulk copies complete bytes on these: armed for the first chunk before the
+    // barrier below; every later chunk's arm happens right after the previous chunk's data was
+    // consumed (still before that chunk's cluster barrier, after which the partner pushes)
     mbar_arrive_expect_tx(r1bar, 32768u);
     mbar_arrive_expect_tx(r2bar, 8192u);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<256>(tmem_slot);
   tc_fence_before();
-  cluster_sync_all();   // both CTAs armed their receive barriers
+  cluster_sync_all();   // barriers of both CTAs initialised and armed
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) SMALL_TS(1);
@@ -217,233 +263,250 @@ __global__ void __launch_bounds__(192, 1)
   const int kh = p.kb1 / 2;            // layer-1 K blocks of this split
   const int q = warp & 3;
   const int row = q * 32 + lane;       // row of the tile (epilogue warps)
-  const int grow = m * 128 + row;
   const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-  const int te = threadIdx.x - 64;     // epilogue thread 0..127
   // TMEM columns: L1 [0, 128), L2 [128, 160), L3 [160, 224)
-  const int it2 = kh, it3 = kh + 16;   // ring iteration numbers (stage = it % NS, phase = (it / NS) & 1)
+  const int per_chunk = kh + 16 + (l3 ? 8 : 0);   // ring iterations of one chunk (stage = it % NS)
+  int act = 0;                                     // chunks this CTA has processed (barrier parity)
 
-  // ============================ phase A: layer-1 mainloop ============================
-  if (warp == 0) {
-    if (elect_one()) {   // TMA producer
-      const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
-      const int pre = kh < NS ? kh : NS;   // W1 blocks before griddepcontrol.wait (PDL overlap)
-      for (int i = 0; i < pre; ++i) {
-        mbar_arrive_expect_tx(&full[i], 32768u);
-        tma_load_2d(smem + S::B0 + 16384 * i, &tmW1, &full[i], (rank * kh + i) * 64, n * 128, pol_b);
-      }
-      for (int i = 0; i < 16; ++i) tma_prefetch_2d(&tmW2, rank * 1024 + i * 64, n * 32);   // into L2 early
-      pdl_wait();
-      SMALL_TS(2);
-      for (int i = 0; i < kh; ++i) {
-        const int s = i % NS;
-        if (i >= pre) {
-          mbar_wait(&empty[s], ((uint32_t)(i / NS) & 1u) ^ 1u);
+  for (int chunk = 0; chunk < nchunks; ++chunk) {
+    const int row0 = chunk * 512 + m * 128;   // first row of this CTA's m-tile in this chunk
+    if (row0 >= M) break;                     // CTA-uniform (and cluster-uniform: same m)
+    const int grow = row0 + row;
+    const uint32_t par = (uint32_t)act & 1u;
+    const int it1 = act * per_chunk, it2 = it1 + kh, it3 = it2 + 16;
+    int* z1_cnt = p.cnt + chunk * 16;        // [4][2]: Z1 column halves published
+    int* z2_cnt = p.cnt + chunk * 16 + 8;    // [4]
+
+    // ============================ phase A: layer-1 mainloop ============================
+    if (warp == 0) {
+      if (elect_one()) {   // TMA producer
+        const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+        const int pre = kh < NS ? kh : NS;   // W1 blocks before griddepcontrol.wait (PDL overlap)
+        for (int i = 0; i < pre; ++i) {
+          const int it = it1 + i, s = it % NS;
+          mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&full[s], 32768u);
           tma_load_2d(smem + S::B0 + 16384 * s, &tmW1, &full[s], (rank * kh + i) * 64, n * 128, pol_b);
         }
-        tma_load_2d(smem + 16384 * s, &tmH, &full[s], (rank * kh + i) * 64, m * 128, pol_a);
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    if (elect_one()) {   // MMA issuer
-      for (int i = 0; i < kh; ++i) {
-        const int s = i % NS;
-        mbar_wait(&full[s], (uint32_t)(i / NS) & 1u);
-        tc_fence_after();
-        const uint64_t ad = umma_desc_sw128(smem_u32(smem + 16384 * s));
-        const uint64_t bd = umma_desc_sw128(smem_u32(smem + S::B0 + 16384 * s));
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          umma_ss<false>(tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), ID1, (i | k) != 0 ? 1u : 0u);
-        umma_commit(&empty[s]);
-      }
-      umma_commit(acc1);
-    }
-    __syncwarp();
-  } else {
-    // epilogue: stage the 64 columns the partner owns (lane-contiguous 32 KB block, free ring)
-    pdl_wait();
-    mbar_wait(acc1, 0);
-    tc_fence_after();
-    if (te == 0) SMALL_TS(3);
-    tmem_to_block(trow, 64 * partner, 64, reinterpret_cast<float*>(smem + S::L1_SEND), row);
-    fence_proxy_async_smem();   // generic smem writes -> the bulk copy (async proxy)
-  }
-  // the partner's ring is free (its layer-1 MMAs completed) and its send block is staged
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-
-  // ============================ phase B: layer-1 reduce, layer 2, layer 3 ============================
-  if (warp == 0) {
-    asm volatile("bar.sync 2, 160;" ::: "memory");   // the epilogue released the ring
-    if (elect_one()) {
-      const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
-      // layer 2: W2 blocks first (independent), the Z1 blocks once their half is published
-      for (int i = 0; i < NS; ++i) {
-        const int it = it2 + i, s = it % NS;
-        mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
-        mbar_arrive_expect_tx(&full[s], 16384u + 4096u);
-        tma_load_2d(smem + S::B0 + 16384 * s, &tmW2, &full[s], rank * 1024 + i * 64, n * 32, pol_b);
-      }
-      spin_wait_geq(z1_cnt + m * 2 + rank, 16);
-      fence_proxy_async_global();
-      SMALL_TS(5);
-      for (int i = 0; i < 16; ++i) {
-        const int it = it2 + i, s = it % NS;
-        if (i >= NS) {
-          mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
-          mbar_arrive_expect_tx(&full[s], 16384u + 4096u);
-          tma_load_2d(smem + S::B0 + 16384 * s, &tmW2, &full[s], rank * 1024 + i * 64, n * 32, pol_b);
+        if (act == 0) {
+          for (int i = 0; i < 16; ++i) tma_prefetch_2d(&tmW2, rank * 1024 + i * 64, n * 32);   // into L2 early
+          pdl_wait();
+          SMALL_TS(2);
         }
-        tma_load_2d(smem + 16384 * s, &tmZ1, &full[s], rank * 1024 + i * 64, m * 128, pol_a);
-      }
-      if (l3) {   // layer 3 (full K = 512): W3 blocks, then the Z2 blocks after all 32 layer-2 CTAs of m-tile m
-        for (int i = 0; i < NS; ++i) {
-          const int it = it3 + i, s = it % NS;
-          mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
-          mbar_arrive_expect_tx(&full[s], 16384u + 8192u);
-          tma_load_2d(smem + S::B0 + 16384 * s, &tmW3, &full[s], i * 64, 0, pol_b);
-        }
-        spin_wait_geq(z2_cnt + m, 32);
-        fence_proxy_async_global();
-        for (int i = 0; i < 8; ++i) {
-          const int it = it3 + i, s = it % NS;
-          if (i >= NS) {
+        for (int i = 0; i < kh; ++i) {
+          const int it = it1 + i, s = it % NS;
+          if (i >= pre) {
             mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
-            mbar_arrive_expect_tx(&full[s], 16384u + 8192u);
-            tma_load_2d(smem + S::B0 + 16384 * s, &tmW3, &full[s], i * 64, 0, pol_b);
+            mbar_arrive_expect_tx(&full[s], 32768u);
+            tma_load_2d(smem + S::B0 + 16384 * s, &tmW1, &full[s], (rank * kh + i) * 64, n * 128, pol_b);
           }
-          tma_load_2d(smem + 16384 * s, &tmZ2, &full[s], i * 64, m * 128, pol_a);
+          tma_load_2d(smem + 16384 * s, &tmH, &full[s], (rank * kh + i) * 64, row0, pol_a);
         }
       }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    if (elect_one()) {
-      for (int i = 0; i < 16; ++i) {
-        const int it = it2 + i, s = it % NS;
-        mbar_wait(&full[s], (uint32_t)(it / NS) & 1u);
-        tc_fence_after();
-        const uint64_t ad = umma_desc_sw128(smem_u32(smem + 16384 * s));
-        const uint64_t bd = umma_desc_sw128(smem_u32(smem + S::B0 + 16384 * s));
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          umma_ss<false>(tmem + 128, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), ID2, (i | k) != 0 ? 1u : 0u);
-        umma_commit(&empty[s]);
-      }
-      umma_commit(acc2);
-      if (l3) {
-        for (int i = 0; i < 8; ++i) {
-          const int it = it3 + i, s = it % NS;
+      __syncwarp();
+    } else if (warp == 1) {
+      if (elect_one()) {   // MMA issuer
+        for (int i = 0; i < kh; ++i) {
+          const int it = it1 + i, s = it % NS;
           mbar_wait(&full[s], (uint32_t)(it / NS) & 1u);
           tc_fence_after();
           const uint64_t ad = umma_desc_sw128(smem_u32(smem + 16384 * s));
           const uint64_t bd = umma_desc_sw128(smem_u32(smem + S::B0 + 16384 * s));
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_ss<false>(tmem + 160, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), ID3, (i | k) != 0 ? 1u : 0u);
+            umma_ss<false>(tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), ID1, (i | k) != 0 ? 1u : 0u);
           umma_commit(&empty[s]);
         }
-        umma_commit(acc3);
+        umma_commit(acc1);
       }
+      __syncwarp();
+    } else {
+      // epilogue: stage the 64 columns the partner owns (lane-contiguous 32 KB block, free ring)
+      if (act == 0) pdl_wait();
+      mbar_wait(acc1, par);
+      tc_fence_after();
+      if (te == 0) SMALL_TS(3);
+      tmem_to_block(trow, 64 * partner, 64, reinterpret_cast<float*>(smem + S::L1_SEND), row);
+      fence_proxy_async_smem();   // generic smem writes -> the bulk copy (async proxy)
     }
-    __syncwarp();
-  } else {
-    // ---- layer-1 split-K: push the staged block into the partner, reduce the owned 64 columns ----
-    if (te == 0) {
-      SMALL_TS(4);
-      bulk_s2cluster(mapa_shared(smem_u32(smem + S::L1_RECV), (uint32_t)partner), smem + S::L1_SEND, 32768u,
-                     mapa_shared(smem_u32(r1bar), (uint32_t)partner));
-      bulk_commit();
-    }
-    mbar_wait(r1bar, 0);
-    if (te == 0) SMALL_TS(12);
-    const float* recv = reinterpret_cast<const float*>(smem + S::L1_RECV);
-    uint32_t w[4][8];
-#pragma unroll
-    for (int c = 0; c < 64; c += 16) {
-      float f[16];
-      reduce16(trow, 64 * rank + c, recv, c, rank, row, f);
-      relu_bf16_16(f, p.b1, n * 128 + 64 * rank + c, w[c / 16]);
-    }
-    if (grow < M) {   // the row's 64 owned columns: 128 contiguous bytes
-      uint4* d = reinterpret_cast<uint4*>(p.Z1 + (int64_t)grow * 2048 + n * 128 + 64 * rank);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        d[2 * c] = make_uint4(w[c][0], w[c][1], w[c][2], w[c][3]);
-        d[2 * c + 1] = make_uint4(w[c][4], w[c][5], w[c][6], w[c][7]);
-      }
-    }
-    if (te == 0) SMALL_TS(13);
-    if (te == 0) bulk_wait_read_all();   // the send block was read: the ring may be reused
-    fence_proxy_async_global();          // Z1 (generic stores) -> the layer-2 TMA loads (async proxy)
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (te == 0) {
-      red_release_add(z1_cnt + m * 2 + n / 8, 1);
-      SMALL_TS(6);
-    }
-    asm volatile("bar.sync 2, 160;" ::: "memory");   // the producer may refill the ring
-
-    // ---- layer 2: reduce the owned 16 columns of the 128 x 32 tile ----
-    mbar_wait(acc2, 0);
+    // the partner's ring is free (its layer-1 MMAs completed) and its send block is staged
+    tc_fence_before();
+    cluster_sync_all();
     tc_fence_after();
-    if (te == 0) SMALL_TS(7);
-    tmem_to_block(trow, 128 + 16 * partner, 16, reinterpret_cast<float*>(smem + S::SEND23), row);
-    fence_proxy_async_smem();
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (te == 0) {
-      bulk_s2cluster(mapa_shared(smem_u32(smem + S::R2), (uint32_t)partner), smem + S::SEND23, 8192u,
-                     mapa_shared(smem_u32(r2bar), (uint32_t)partner));
-      bulk_commit();
-    }
-    mbar_wait(r2bar, 0);
-    if (te == 0) SMALL_TS(14);
-    {
-      float f[16];
-      uint32_t w2[8];
-      reduce16(trow, 128 + 16 * rank, reinterpret_cast<const float*>(smem + S::R2), 0, rank, row, f);
-      relu_bf16_16(f, p.b2, n * 32 + 16 * rank, w2);
-      if (grow < M) {
-        uint4* d = reinterpret_cast<uint4*>(p.Z2 + (int64_t)grow * 512 + n * 32 + 16 * rank);
-        d[0] = make_uint4(w2[0], w2[1], w2[2], w2[3]);
-        d[1] = make_uint4(w2[4], w2[5], w2[6], w2[7]);
+
+    // ============================ phase B: layer-1 reduce, layer 2, layer 3 ============================
+    if (warp == 0) {
+      asm volatile("bar.sync 2, 160;" ::: "memory");   // the epilogue released the ring
+      if (elect_one()) {
+        const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+        // layer 2: W2 blocks first (independent), the Z1 blocks once their half is published
+        for (int i = 0; i < NS; ++i) {
+          const int it = it2 + i, s = it % NS;
+          mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&full[s], 16384u + 4096u);
+          tma_load_2d(smem + S::B0 + 16384 * s, &tmW2, &full[s], rank * 1024 + i * 64, n * 32, pol_b);
+        }
+        spin_wait_geq(z1_cnt + m * 2 + rank, 16);
+        fence_proxy_async_global();
+        SMALL_TS(5);
+        for (int i = 0; i < 16; ++i) {
+          const int it = it2 + i, s = it % NS;
+          if (i >= NS) {
+            mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
+            mbar_arrive_expect_tx(&full[s], 16384u + 4096u);
+            tma_load_2d(smem + S::B0 + 16384 * s, &tmW2, &full[s], rank * 1024 + i * 64, n * 32, pol_b);
+          }
+          tma_load_2d(smem + 16384 * s, &tmZ1, &full[s], rank * 1024 + i * 64, row0, pol_a);
+        }
+        if (l3) {   // layer 3 (full K = 512): W3 blocks, then the Z2 blocks after all 32 layer-2 CTAs of the m-tile
+          for (int i = 0; i < NS; ++i) {
+            const int it = it3 + i, s = it % NS;
+            mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
+            mbar_arrive_expect_tx(&full[s], 16384u + 8192u);
+            tma_load_2d(smem + S::B0 + 16384 * s, &tmW3, &full[s], i * 64, 0, pol_b);
+          }
+          spin_wait_geq(z2_cnt + m, 32);
+          fence_proxy_async_global();
+          for (int i = 0; i < 8; ++i) {
+            const int it = it3 + i, s = it % NS;
+            if (i >= NS) {
+              mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
+              mbar_arrive_expect_tx(&full[s], 16384u + 8192u);
+              tma_load_2d(smem + S::B0 + 16384 * s, &tmW3, &full[s], i * 64, 0, pol_b);
+            }
+            tma_load_2d(smem + 16384 * s, &tmZ2, &full[s], i * 64, row0, pol_a);
+          }
+        }
+      }
+      __syncwarp();
+    } else if (warp == 1) {
+      if (elect_one()) {
+        for (int i = 0; i < 16; ++i) {
+          const int it = it2 + i, s = it % NS;
+          mbar_wait(&full[s], (uint32_t)(it / NS) & 1u);
+          tc_fence_after();
+          const uint64_t ad = umma_desc_sw128(smem_u32(smem + 16384 * s));
+          const uint64_t bd = umma_desc_sw128(smem_u32(smem + S::B0 + 16384 * s));
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_ss<false>(tmem + 128, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), ID2, (i | k) != 0 ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(acc2);
+        if (l3) {
+          for (int i = 0; i < 8; ++i) {
+            const int it = it3 + i, s = it % NS;
+            mbar_wait(&full[s], (uint32_t)(it / NS) & 1u);
+            tc_fence_after();
+            const uint64_t ad = umma_desc_sw128(smem_u32(smem + 16384 * s));
+            const uint64_t bd = umma_desc_sw128(smem_u32(smem + S::B0 + 16384 * s));
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma_ss<false>(tmem + 160, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), ID3, (i | k) != 0 ? 1u : 0u);
+            umma_commit(&empty[s]);
+          }
+          umma_commit(acc3);
+        }
+      }
+      __syncwarp();
+    } else {
+      // ---- layer-1 split-K: push the staged block into the partner, reduce the owned 64 columns ----
+      if (te == 0) {
+        SMALL_TS(4);
+        bulk_s2cluster(mapa_shared(smem_u32(smem + S::L1_RECV), (uint32_t)partner), smem + S::L1_SEND, 32768u,
+                       mapa_shared(smem_u32(r1bar), (uint32_t)partner));
+        bulk_commit();
+      }
+      mbar_wait(r1bar, par);
+      if (te == 0) SMALL_TS(12);
+      const bool more = chunk + 1 < nchunks && row0 + 512 < M;   // this CTA runs another chunk
+      const float* recv = reinterpret_cast<const float*>(smem + S::L1_RECV);
+      uint32_t w[4][8];
+#pragma unroll
+      for (int c = 0; c < 64; c += 16) {
+        float f[16];
+        reduce16(trow, 64 * rank + c, recv, c, rank, row, f);
+        relu_bf16_16(f, p.b1, n * 128 + 64 * rank + c, w[c / 16]);
+      }
+      if (grow < M) {   // the row's 64 owned columns: 128 contiguous bytes
+        uint4* d = reinterpret_cast<uint4*>(p.Z1 + (int64_t)grow * 2048 + n * 128 + 64 * rank);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          d[2 * c] = make_uint4(w[c][0], w[c][1], w[c][2], w[c][3]);
+          d[2 * c + 1] = make_uint4(w[c][4], w[c][5], w[c][6], w[c][7]);
+        }
+      }
+      if (te == 0) SMALL_TS(13);
+      asm volatile("bar.sync 1, 128;" ::: "memory");   // every thread has read the received block
+      if (te == 0 && more) mbar_arrive_expect_tx(r1bar, 32768u);   // armed for the next chunk
+      if (te == 0) bulk_wait_read_all();   // the send block was read: the ring may be reused
+      fence_proxy_async_global();          // Z1 (generic stores) -> the layer-2 TMA loads (async proxy)
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (te == 0) {
+        red_release_add(z1_cnt + m * 2 + n / 8, 1);
+        SMALL_TS(6);
+      }
+      asm volatile("bar.sync 2, 160;" ::: "memory");   // the producer may refill the ring
+
+      // ---- layer 2: reduce the owned 16 columns of the 128 x 32 tile ----
+      mbar_wait(acc2, par);
+      tc_fence_after();
+      if (te == 0) SMALL_TS(7);
+      tmem_to_block(trow, 128 + 16 * partner, 16, reinterpret_cast<float*>(smem + S::SEND23), row);
+      fence_proxy_async_smem();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (te == 0) {
+        bulk_s2cluster(mapa_shared(smem_u32(smem + S::R2), (uint32_t)partner), smem + S::SEND23, 8192u,
+                       mapa_shared(smem_u32(r2bar), (uint32_t)partner));
+        bulk_commit();
+      }
+      mbar_wait(r2bar, par);
+      if (te == 0) SMALL_TS(14);
+      {
+        float f[16];
+        uint32_t w2[8];
+        reduce16(trow, 128 + 16 * rank, reinterpret_cast<const float*>(smem + S::R2), 0, rank, row, f);
+        asm volatile("bar.sync 1, 128;" ::: "memory");   // every thread has read the received block
+        if (te == 0 && more) mbar_arrive_expect_tx(r2bar, 8192u);   // armed for the next chunk
+        relu_bf16_16(f, p.b2, n * 32 + 16 * rank, w2);
+        if (grow < M) {
+          uint4* d = reinterpret_cast<uint4*>(p.Z2 + (int64_t)grow * 512 + n * 32 + 16 * rank);
+          d[0] = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+          d[1] = make_uint4(w2[4], w2[5], w2[6], w2[7]);
+        }
+      }
+      if (te == 0) bulk_wait_read_all();
+      fence_proxy_async_global();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (te == 0) {
+        red_release_add(z2_cnt + m, 1);
+        SMALL_TS(8);
       }
     }
-    if (te == 0) bulk_wait_read_all();
-    fence_proxy_async_global();
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (te == 0) {
-      red_release_add(z2_cnt + m, 1);
-      SMALL_TS(8);
-    }
-  }
 
-  if (l3 && warp >= 2) {
-    // ---- layer 3 (this CTA holds the whole 128 x 64 Z3 tile): + b3, ReLU, w4 dot, + b4 ----
-    const bool owner = grow < M;
-    int32_t ntok = 0, inst = 0;   // the row's N(r) and instance, fetched while layer 3 runs
-    if (owner) {
-      if (p.n_tok) ntok = p.n_tok[grow];
-      if (p.project) inst = p.pa.inst[grow];
-    }
-    mbar_wait(acc3, 0);
-    tc_fence_after();
-    if (te == 0) SMALL_TS(9);
-    float y = 0.0f;
+    if (l3 && warp >= 2) {
+      // ---- layer 3 (this CTA holds the whole 128 x 64 Z3 tile): + b3, ReLU, w4 dot, + b4 ----
+      const bool owner = grow < M;
+      int32_t ntok = 0, inst = 0, r = grow;   // the row's N(r), instance and (refresh) slot, fetched
+      if (owner) {                            // while layer 3 runs
+        if (p.r_idx) r = p.r_idx[grow];
+        if (p.n_tok) ntok = p.n_tok[grow];
+        if (p.project) inst = p.pa.inst[r];
+      }
+      mbar_wait(acc3, par);
+      tc_fence_after();
+      if (te == 0) SMALL_TS(9);
+      float y = 0.0f;
 #pragma unroll 1
-    for (int c = 0; c < 64; c += 16) {
-      uint32_t v[16];
-      tmem_ld_32x32b_x16(trow + 160u + (uint32_t)c, v);
-      tmem_ld_wait();
+      for (int c = 0; c < 64; c += 16) {
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(trow + 160u + (uint32_t)c, v);
+        tmem_ld_wait();
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        y = fmaf(__ldg(p.w4 + c + j), fmaxf(__uint_as_float(v[j]) + (p.b3 ? __ldg(p.b3 + c + j) : 0.0f), 0.0f), y);
-    }
-    y += p.b4 ? __ldg(p.b4) : 0.0f;
-    {
+        for (int j = 0; j < 16; ++j)
+          y = fmaf(__ldg(p.w4 + c + j), fmaxf(__uint_as_float(v[j]) + (p.b3 ? __ldg(p.b3 + c + j) : 0.0f), 0.0f), y);
+      }
+      y += p.b4 ? __ldg(p.b4) : 0.0f;
       int32_t nh = 0;
       if (owner) {
         int32_t cap = p.max_ctx - ntok;
@@ -451,6 +514,11 @@ __global__ void __launch_bounds__(192, 1)
         nh = __float2int_rn(fminf(fmaxf(y, 0.0f), (float)cap));   // quantize_nhat (readings A8-A10)
         if (p.y_hat) p.y_hat[grow] = y;
         if (p.n_hat) p.n_hat[grow] = nh;
+        if (p.r_idx) {   // refresh: scatter into the request's slot and restart its cadence (reading A27)
+          p.r_nhat[r] = nh;
+          p.r_glast[r] = p.r_gen[r];
+          p.r_nhat_last[r] = nh;
+        }
       }
       if (p.project) {
         uint32_t errbits = 0;
@@ -461,43 +529,19 @@ __global__ void __launch_bounds__(192, 1)
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (te == 0) {
         SMALL_TS(10);
-        *s_last = (atomicAdd(done, 1) == m_tiles - 1) ? 1 : 0;
+        *s_last = (atomicAdd(p.cnt + S::DONE, 1) == total_mt - 1) ? 1 : 0;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (*s_last) {
         fence_acq_rel_gpu();
-        if (p.project) {
-          // finalize from the global histogram (one warp per instance), re-zero it; the
-          // histogram comes into shared memory with L2 loads (other SMs' atomics) when it fits
-          const int nb = p.pa.n_inst * (p.pa.H + 2);
-          uint32_t* sbeta = reinterpret_cast<uint32_t*>(smem + S::R2);   // consumed
-          for (int t = te; t <= p.pa.H; t += 128) sbeta[t] = p.pa.beta_q[t];
-          const uint32_t* hc = p.pa.ws_cnt;
-          const unsigned long long* hs = p.pa.ws_sum;
-          if ((uint32_t)nb * 12u <= 96u * 1024u) {   // the ring's A slots (idle)
-            unsigned long long* ss = reinterpret_cast<unsigned long long*>(smem + S::HIST);
-            uint32_t* sc = reinterpret_cast<uint32_t*>(ss + nb);
-            for (int k = te; k < nb; k += 128) {
-              ss[k] = __ldcg(p.pa.ws_sum + k);
-              sc[k] = __ldcg(p.pa.ws_cnt + k);
-            }
-            hc = sc;
-            hs = ss;
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          proj_finalize<false>(p.pa, hc, hs, sbeta, warp - 2, 4);
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          for (int k = te; k < nb; k += 128) {
-            p.pa.ws_cnt[k] = 0;
-            p.pa.ws_sum[k] = 0;
-          }
-          if (te == 0) *p.pa.ws_arrive = 0;
-        }
+        if (p.project) small_finalize(p, smem, te, warp);
         // every counter of this launch has been consumed: re-arm them for the next one
-        for (int k = te; k < 13; k += 128) p.cnt[k] = 0;
+        for (int k = te; k < nchunks * 16; k += 128) p.cnt[k] = 0;
+        if (te == 0) p.cnt[S::DONE] = 0;
         if (te == 0) SMALL_TS(11);
       }
     }
+    ++act;
   }
   tc_fence_before();
   __syncthreads();

@@ -162,6 +162,116 @@ __global__ void __launch_bounds__(kScatProjThreads) refresh_scatter_project_kern
   proj_finalize(a, scnt, ssum, sbeta, threadIdx.x >> 5, blockDim.x >> 5);
 }
 
+// Multi-CTA select for the one-launch predictor (refresh_select_gather_age_kernel): grid
+// ceil(R / 1024) CTAs, all resident (<= SMs, checked on the host).  Per CTA: the due flags of its
+// 1024 rows and their block scan; the CTA counts meet in global memory (arrival counter) so every
+// CTA knows its base -- the compaction keeps row order, as the single-CTA select does; the CTA
+// then writes idx / N(r) of its due rows and copies their hidden states into the compacted
+// buffer (one warp per row, 16-byte vectors).  Rows that are NOT due age in place (reading A27)
+// and, with the projection fused, go into its histogram here -- they do not depend on the
+// predictor -- while the predictor adds the due rows and finalises.
+struct SelArgs {
+  int R;
+  const int32_t* gen;
+  const int32_t* g_last;
+  const int32_t* nhat_last;
+  int32_t k;
+  const int32_t* n_tok;
+  const uint8_t* h;
+  int64_t ld_bytes;
+  int row_bytes;
+  int32_t* idx;          // [R] compacted position -> row
+  int32_t* ntok_c;       // [R] N(r) of the compacted rows
+  uint8_t* hc;           // [R][row_bytes] compacted hidden states
+  int32_t* n_hat;        // [R] aged N_hat of the rows that are not due
+  int32_t* M_out;        // device row count
+  int32_t* n_refreshed;  // nullable
+  int* blk;              // [grid] CTA counts | [grid] arrival | [grid + 1] done  (zero between launches)
+  int project;
+  ProjArgs pa;
+};
+
+__global__ void __launch_bounds__(kSelThreads) refresh_select_gather_age_kernel(const SelArgs a) {
+  __shared__ int wsum[kSelThreads / 32];
+  __shared__ int s_base, s_cnt;
+  __shared__ int s_rows[kSelThreads];
+  pdl_wait();
+  pdl_launch_dependents();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x, b = blockIdx.x;
+  const int r = b * kSelThreads + tid;
+  bool f = false;
+  int gl = 0, g = 0;
+  if (r < a.R) {
+    gl = a.g_last[r];
+    g = a.gen[r];
+    f = gl < 0 || g - gl >= a.k;   // should_refresh
+  }
+  const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
+  if (lane == 0) wsum[warp] = __popc(m);
+  __syncthreads();
+  if (warp == 0) {   // exclusive scan of the 32 warp counts
+    const int v = wsum[lane];
+    int x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      __syncwarp();
+      const int y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+      if (lane >= off) x += y;
+    }
+    wsum[lane] = x - v;
+    if (lane == 31) s_cnt = x;
+  }
+  __syncthreads();
+  const int lp = wsum[warp] + __popc(m & ((1u << lane) - 1u));   // position among this CTA's due rows
+  if (tid == 0) {   // publish this CTA's count
+    a.blk[b] = s_cnt;
+    fence_acq_rel_gpu();
+    atomicAdd(a.blk + G, 1);
+  }
+  // rows that are not due age in place and (fused projection) enter the histogram now
+  int nh = 0;
+  if (r < a.R && !f) {
+    const int aged = a.nhat_last[r] - (g - gl);   // reading A27
+    nh = aged > 0 ? aged : 0;
+    a.n_hat[r] = nh;
+  }
+  if (a.project) {
+    uint32_t errbits = 0;
+    const bool valid = r < a.R && !f;
+    proj_accumulate(a.pa, valid, valid ? a.pa.inst[r] : 0, valid ? a.n_tok[r] : 0, nh, a.pa.ws_cnt, a.pa.ws_sum,
+                    errbits);
+    if (errbits && a.pa.err) atomicOr(a.pa.err, (int)errbits);
+  }
+  if (f) s_rows[lp] = r;
+  if (tid == 0) {   // every CTA's count is in: this CTA's base is the sum of the lower CTAs' counts
+    spin_wait_geq(a.blk + G, G);
+    int base = 0;
+    for (int j = 0; j < b; ++j) base += __ldcg(a.blk + j);
+    s_base = base;
+    if (b == G - 1) {
+      *a.M_out = base + s_cnt;
+      if (a.n_refreshed) *a.n_refreshed = base + s_cnt;
+    }
+    if (atomicAdd(a.blk + G + 1, 1) == G - 1) {   // the last reader re-arms the counters
+      a.blk[G] = 0;
+      a.blk[G + 1] = 0;
+    }
+  }
+  __syncthreads();
+  const int base = s_base, cnt = s_cnt;
+  if (f) {
+    a.idx[base + lp] = r;
+    a.ntok_c[base + lp] = a.n_tok ? a.n_tok[r] : 0;
+  }
+  const int nvec = a.row_bytes / 16;
+  for (int j = warp; j < cnt; j += kSelThreads / 32) {   // gather: one warp per due row
+    const int4* src = reinterpret_cast<const int4*>(a.h + (int64_t)s_rows[j] * a.ld_bytes);
+    int4* dst = reinterpret_cast<int4*>(a.hc + (int64_t)(base + j) * a.row_bytes);
+    for (int v = lane; v < nvec; v += 32) dst[v] = __ldg(src + v);
+  }
+}
+
 static cudaLaunchConfig_t pdl_cfg(dim3 grid, dim3 block, cudaStream_t st, cudaLaunchAttribute* at) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
@@ -218,5 +328,35 @@ cudaError_t launch_refresh_scatter_project(const ProjArgs& a, const int32_t* pos
   return cudaLaunchKernelEx(&cfg, refresh_scatter_project_kernel, a, pos, nhat_c, gen, g_last, nhat_last, M_dev,
                             n_refreshed);
 }
+
+cudaError_t launch_refresh_select_fused(int R, const int32_t* gen, const int32_t* g_last, const int32_t* nhat_last,
+                                        int32_t k, const int32_t* n_tok, const void* h, int64_t ld_bytes, int row_bytes,
+                                        int32_t* idx, int32_t* ntok_c, void* hc, int32_t* n_hat, int32_t* M_out,
+                                        int32_t* n_refreshed, int* blk, const ProjArgs* proj, cudaStream_t st) {
+  SelArgs a{};
+  a.R = R;
+  a.gen = gen;
+  a.g_last = g_last;
+  a.nhat_last = nhat_last;
+  a.k = k;
+  a.n_tok = n_tok;
+  a.h = static_cast<const uint8_t*>(h);
+  a.ld_bytes = ld_bytes;
+  a.row_bytes = row_bytes;
+  a.idx = idx;
+  a.ntok_c = ntok_c;
+  a.hc = static_cast<uint8_t*>(hc);
+  a.n_hat = n_hat;
+  a.M_out = M_out;
+  a.n_refreshed = n_refreshed;
+  a.blk = blk;
+  a.project = proj ? 1 : 0;
+  if (proj) a.pa = *proj;
+  cudaLaunchAttribute at[1];
+  cudaLaunchConfig_t cfg = pdl_cfg(dim3((R + kSelThreads - 1) / kSelThreads), dim3(kSelThreads), st, at);
+  return cudaLaunchKernelEx(&cfg, refresh_select_gather_age_kernel, a);
+}
+
+int refresh_select_fused_max_rows() { return kSelThreads * g_num_sms; }
 
 }  // namespace star

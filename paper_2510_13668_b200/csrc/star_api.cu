@@ -279,9 +279,17 @@ static bool small_path_available() {
   return ncl >= 64;
 }
 
+struct SmallRefresh {   // refresh mode: the compacted batch and the slots it scatters into
+  const int32_t* M_dev;
+  const int32_t* idx;
+  const int32_t* gen;
+  int32_t* g_last;
+  int32_t* nhat_last;
+  int32_t* n_hat;
+};
 static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, int32_t max_ctx, float* y_hat,
                                 int32_t* n_hat, const ProjArgs* proj, cudaStream_t st,
-                                const CUtensorMap* tmH = nullptr, const int32_t* M_dev = nullptr);
+                                const CUtensorMap* tmH = nullptr, const SmallRefresh* rf = nullptr);
 
 // Whether a one-rank single-round plan runs in the fused tail's last CTA (STAR_PLAN_FUSE=1, read
 // once) instead of the cluster plan kernel launched after it (default).  Measured at TGT with a
@@ -371,6 +379,7 @@ struct star_predictor {
   // one-launch predictor for <= 512 rows (lenpred_small.cuh)
   CUtensorMap tmW2s;          // W2 with 32-row boxes
   int* small_cnt = nullptr;   // its phase counters (zero between launches)
+  int* r_blk = nullptr;       // refresh: the multi-CTA select's counts and counters (zero between launches)
   bool small_ok = false;      // shape supported and 32 clusters of 4 co-resident
   uint64_t* tl_small = nullptr;
   const void* last_h = nullptr;
@@ -402,6 +411,7 @@ static void free_pred(star_predictor* p) {
   cudaFree(p->tl);
   cudaFree(p->tl_l1);
   cudaFree(p->small_cnt);
+  cudaFree(p->r_blk);
   cudaFree(p->tl_small);
   cudaFree(p->r_idx);
   cudaFree(p->r_pos);
@@ -520,8 +530,11 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
     }
     p->small_ok = small_path_available();
     if (p->small_ok) {
-      if (cudaMalloc(reinterpret_cast<void**>(&p->small_cnt), 64 * sizeof(int)) != cudaSuccess ||
-          cudaMemset(p->small_cnt, 0, 64 * sizeof(int)) != cudaSuccess) {
+      const size_t ncnt = (size_t)SmallSmem::DONE + 16, nblk = 2 * (size_t)g_num_sms + 16;
+      if (cudaMalloc(reinterpret_cast<void**>(&p->small_cnt), ncnt * sizeof(int)) != cudaSuccess ||
+          cudaMemset(p->small_cnt, 0, ncnt * sizeof(int)) != cudaSuccess ||
+          cudaMalloc(reinterpret_cast<void**>(&p->r_blk), nblk * sizeof(int)) != cudaSuccess ||
+          cudaMemset(p->r_blk, 0, nblk * sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         free_pred(p);
         return fail(STAR_ENOMEM, "device allocation failed");
@@ -886,21 +899,25 @@ static star_status refresh_impl(star_predictor* p, const void* h, int64_t ld_h, 
     return fail(STAR_EINVAL, "h rows must be 16-byte aligned");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
   cudaError_t e;
+  if (p->small_ok && R <= refresh_select_fused_max_rows() && R <= 64 * 512) {
+    // one-launch path: the multi-CTA select compacts + gathers the due rows, ages the others (and
+    // projects them); the small-batch predictor runs the due rows in 512-row chunks, scatters their
+    // N_hat into their slots, adds them to the projection and finalises it
+    if ((e = launch_refresh_select_fused(R, gen, g_last, nhat_last, k, n_tok, h, ld_h * 2, p->d * 2, p->r_idx,
+                                         p->r_ntok, p->r_h, n_hat, p->r_M, n_refreshed, p->r_blk, proj, st)) !=
+        cudaSuccess)
+      return cuda_fail(e, "refresh select launch");
+    SmallRefresh rf{p->r_M, p->r_idx, gen, g_last, nhat_last, n_hat};
+    if ((e = launch_small(p, R, n_tok ? p->r_ntok : nullptr, max_ctx_len, nullptr, nullptr, proj, st, &p->tmA_r,
+                          &rf)) != cudaSuccess)
+      return cuda_fail(e, "refresh small-batch launch");
+    return STAR_OK;
+  }
   if ((e = launch_refresh_select(R, gen, g_last, k, n_tok, p->r_idx, p->r_ntok, p->r_pos, p->r_M, st)) != cudaSuccess)
     return cuda_fail(e, "refresh_select launch");
   if ((e = launch_refresh_gather(R, h, ld_h * 2, p->d * 2, p->r_idx, p->r_M, p->r_h, st)) != cudaSuccess)
     return cuda_fail(e, "refresh_gather launch");
-  // the compacted rows: up to 512 in the one-launch small-batch kernel (which leaves when the
-  // device-side count is larger); beyond that, or without it, the 2-launch path
-  int skip_le = 0;
-  if (p->small_ok) {
-    if ((e = launch_small(p, R, n_tok ? p->r_ntok : nullptr, max_ctx_len, nullptr, p->r_nhat, nullptr, st, &p->tmA_r,
-                          p->r_M)) != cudaSuccess)
-      return cuda_fail(e, "refresh small-batch launch");
-    skip_le = 512;
-  }
-  if (R <= skip_le) goto scatter;
-  {
+  const int skip_le = 0;   // (the 2-launch kernels run every row here)
   // layer 1 on the compacted rows: 1-CTA tiles + cluster split-K sized for the expected row count
   // ~R/k (the grid covers R rows; tiles beyond the device-side count leave before any setup)
   const int m_tiles = (R + 127) / 128;
@@ -955,8 +972,6 @@ static star_status refresh_impl(star_predictor* p, const void* h, int64_t ld_h, 
   t.project = 0;
   if ((e = launch_tail(p->tmA2, p->tmB2, p->tmB3, t, m_tiles, st)) != cudaSuccess)
     return cuda_fail(e, "refresh tail launch");
-  }
-scatter:
   if (proj && R <= 8192 && refresh_scatter_project_smem(proj->n_inst, proj->H) <= (size_t)200 * 1024) {
     // aging scatter fused with the projection of the resulting N_hat (one CTA)
     if ((e = launch_refresh_scatter_project(*proj, p->r_pos, p->r_nhat, gen, g_last, nhat_last, p->r_M, n_refreshed,
@@ -1197,9 +1212,16 @@ star_status kv_migrate(const star_kv_pool* src, const int32_t* src_table, const 
 namespace star {
 static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, int32_t max_ctx, float* y_hat,
                                 int32_t* n_hat, const ProjArgs* proj, cudaStream_t st, const CUtensorMap* tmH,
-                                const int32_t* M_dev) {
+                                const SmallRefresh* rf) {
   SmallArgs a{};
-  a.M_dev = M_dev;
+  if (rf) {
+    a.M_dev = rf->M_dev;
+    a.r_idx = rf->idx;
+    a.r_gen = rf->gen;
+    a.r_glast = rf->g_last;
+    a.r_nhat_last = rf->nhat_last;
+    a.r_nhat = rf->n_hat;
+  }
   a.M = R;
   a.kb1 = p->d / 64;
   a.b1 = p->b1;

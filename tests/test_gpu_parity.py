@@ -500,7 +500,7 @@ def test_refresh_step_parity(star, oracle_mod, R, k, seed):
 
 
 @pytest.mark.parametrize("R,k,seed,n", [(2048, 20, 0, 8), (777, 7, 1, 3), (64, 1, 2, 1), (5000, 20, 3, 64),
-                                        (6000, 20, 4, 8)])
+                                        (6000, 20, 4, 8), (512, 20, 5, 1), (4096, 20, 6, 8)])
 def test_refresh_project_fused_equals_separate(star, oracle_mod, R, k, seed, n):
     """lenpred_forward_refresh_project (aging scatter fused with the projection, one CTA) ==
     lenpred_forward_refresh + project_instance_load, bit for bit (N_hat, cadence state, L, W, peak,
@@ -515,8 +515,10 @@ def test_refresh_project_fused_equals_separate(star, oracle_mod, R, k, seed, n):
     h = _dev(datagen.make_hidden(seed, R, c["d"], "bf16", scale=scale), torch.bfloat16)
     gen = g.integers(0, 5000, R).astype(np.int32)
     g_last = np.where(g.random(R) < 0.1, -1, gen - g.integers(0, 2 * k + 1, R)).astype(np.int32)
-    if R >= 6000:   # first step of a batch: no prediction yet, every row due (the grid runs every m-tile)
+    if R >= 6000:   # first step of a batch: no prediction yet, every row due (12 chunks of 512 rows)
         g_last[:] = -1
+    if seed == 5:   # no row due this step: only the aged rows, the projection must still be finalised
+        g_last[:] = gen
     nhat_last = g.integers(0, 30000, R).astype(np.int32)
     W, _ = _weights_dev(pw)
     pred = star.Predictor(*W, max_rows=R)
