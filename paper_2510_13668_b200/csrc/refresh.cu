@@ -191,13 +191,24 @@ struct SelArgs {
   ProjArgs pa;
 };
 
+constexpr int kSelHistBins = 2560;   // shared histogram of the aged rows (n_inst * (H + 2) <= this)
+
 __global__ void __launch_bounds__(kSelThreads) refresh_select_gather_age_kernel(const SelArgs a) {
   __shared__ int wsum[kSelThreads / 32];
   __shared__ int s_base, s_cnt;
   __shared__ int s_rows[kSelThreads];
+  __shared__ unsigned long long s_sum[kSelHistBins];
+  __shared__ uint32_t s_hc[kSelHistBins];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nb = a.project ? a.pa.n_inst * (a.pa.H + 2) : 0;
+  const bool shist = nb <= kSelHistBins;   // else the aged rows go straight to the global histogram
+  if (shist)
+    for (int j = tid; j < nb; j += kSelThreads) {
+      s_sum[j] = 0;
+      s_hc[j] = 0;
+    }
   pdl_wait();
   pdl_launch_dependents();
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x, b = blockIdx.x;
   const int r = b * kSelThreads + tid;
   bool f = false;
@@ -237,11 +248,26 @@ __global__ void __launch_bounds__(kSelThreads) refresh_select_gather_age_kernel(
     a.n_hat[r] = nh;
   }
   if (a.project) {
+    // the long-tailed batch puts most rows of an instance in one bin (N_hat > H): aggregate per
+    // warp (match_any) into a shared histogram, then one global add per non-empty bin per CTA
     uint32_t errbits = 0;
     const bool valid = r < a.R && !f;
-    proj_accumulate(a.pa, valid, valid ? a.pa.inst[r] : 0, valid ? a.n_tok[r] : 0, nh, a.pa.ws_cnt, a.pa.ws_sum,
-                    errbits);
+    const int32_t ins = valid ? a.pa.inst[r] : 0, nt = valid ? a.n_tok[r] : 0;
+    if (shist)
+      proj_accumulate<true>(a.pa, valid, ins, nt, nh, s_hc, s_sum, errbits);
+    else
+      proj_accumulate(a.pa, valid, ins, nt, nh, a.pa.ws_cnt, a.pa.ws_sum, errbits);
     if (errbits && a.pa.err) atomicOr(a.pa.err, (int)errbits);
+    if (shist) {
+      __syncthreads();
+      for (int j = tid; j < nb; j += kSelThreads) {
+        const uint32_t c = s_hc[j];
+        if (c) {
+          atomicAdd(a.pa.ws_cnt + j, c);
+          atomicAdd(a.pa.ws_sum + j, s_sum[j]);
+        }
+      }
+    }
   }
   if (f) s_rows[lp] = r;
   if (tid == 0) {   // every CTA's count is in: this CTA's base is the sum of the lower CTAs' counts
