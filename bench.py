@@ -693,7 +693,9 @@ def run_star(args):
 
     # ---- roofline: the layer-1 tcgen05 GEMM (dominant kernel), timed live inside the step ----
     peaks = load_peaks()
-    flops_l1 = 2.0 * R * c["d"] * 2048
+    small_path = R <= 512 and pred.path(R) == 1
+    # the timed launch: layer 1 alone (2 R d m1), or the whole one-launch predictor (2 R (d m1 + m1 m2 + m2 m3 + m3))
+    flops_l1 = 2.0 * R * (c["d"] * 2048 + (2048 * 512 + 512 * 64 + 64 if small_path else 0))
     achieved = flops_l1 / (l1_avg_ms / 1e3) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -702,16 +704,28 @@ def run_star(args):
             traffic = json.load(f).get(f"{args.config}/w{world}/layer1")
     m_tiles = (R + 127) // 128
     pair = c["dtype"] == "bf16" and (m_tiles == 2 or (m_tiles + 1) // 2 * 2 * 8 >= 148 * 5 // 8)
-    roofline = {"kernel": ("umma_pair_gemm_kernel<256> (tcgen05 cta_group::2 + TMA)" if pair else
-                           "umma_gemm_kernel (tcgen05 + TMA, cluster split-K)") + " = predictor layer 1",
-                "bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
-                "algorithmic_flop_per_launch": flops_l1, "flop_per_request": 2.0 * c["d"] * 2048,
+    # the contraction's own dtype: bf16 at its measured peak; fp32 runs as 3xTF32 (three tcgen05 kind::tf32
+    # MMAs per product) against the TF32 peak = measured bf16 x 0.5 (the nominal dense TF32 : BF16 ratio)
+    f32 = c["dtype"] == "f32"
+    peak = peaks["bf16_tflops"] * (0.5 if f32 else 1.0)
+    small = small_path
+    kname = ("lenpred_small_kernel (one launch: layers 1-3, head, projection; events around the whole launch)"
+             if small else ("umma_pair_gemm_kernel<256> (tcgen05 cta_group::2 + TMA)" if pair else
+                            "umma_gemm_kernel (tcgen05 + TMA, cluster split-K)") + " = predictor layer 1")
+    roofline = {"kernel": kname,
+                "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "algorithmic_flop_per_launch": flops_l1, "flop_per_request": flops_l1 / max(R, 1),
                 "avg_launch_us": l1_avg_ms * 1e3, "share_of_step": l1_avg_ms / step_l1_avg_ms,
                 "timing": "CUDA events recorded on the step's stream around the layer-1 launch inside the "
                           "captured step, over a second timed loop of the same K steps (the event pair "
                           "itself costs a few us, so the headline step time is taken without it)",
-                "peak_source": peaks["source"] + " bf16_tflops (burst figure: the kernel runs inside a ~60 us step)"}
+                "peak_source": peaks["source"] + " bf16_tflops (burst figure: the kernel runs inside a ~60 us step)"
+                               + (" x 0.5 = TF32 (3xTF32: the tensor pipe does 3 MMAs per algorithmic product, so "
+                                  "frac_3xtf32 = achieved / (peak / 3) is the fraction of what 3xTF32 can reach)"
+                                  if f32 else "")}
+    if f32:
+        roofline["frac_3xtf32"] = achieved / (peak / 3.0)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "us_per_step": ms_per_step * 1e3,

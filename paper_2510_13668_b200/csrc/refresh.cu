@@ -290,11 +290,30 @@ __global__ void __launch_bounds__(kSelThreads) refresh_select_gather_age_kernel(
     a.idx[base + lp] = r;
     a.ntok_c[base + lp] = a.n_tok ? a.n_tok[r] : 0;
   }
+  // gather the due rows' hidden states: a flat (row, 16-byte vector) index space over all 1024
+  // threads, 8 independent loads in flight per thread before their stores (the rows come cold
+  // from HBM; a dependent load -> store chain per vector made this the slowest part of the kernel)
   const int nvec = a.row_bytes / 16;
-  for (int j = warp; j < cnt; j += kSelThreads / 32) {   // gather: one warp per due row
-    const int4* src = reinterpret_cast<const int4*>(a.h + (int64_t)s_rows[j] * a.ld_bytes);
-    int4* dst = reinterpret_cast<int4*>(a.hc + (int64_t)(base + j) * a.row_bytes);
-    for (int v = lane; v < nvec; v += 32) dst[v] = __ldg(src + v);
+  const int total = cnt * nvec;
+  constexpr int kU = 8;
+  for (int b0 = 0; b0 < total; b0 += kU * kSelThreads) {
+    int4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = b0 + u * kSelThreads + tid;
+      if (e < total) {
+        const int j = e / nvec, c = e - j * nvec;
+        v[u] = ld_stream_int4(reinterpret_cast<const int4*>(a.h + (int64_t)s_rows[j] * a.ld_bytes) + c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = b0 + u * kSelThreads + tid;
+      if (e < total) {
+        const int j = e / nvec, c = e - j * nvec;
+        reinterpret_cast<int4*>(a.hc + (int64_t)(base + j) * a.row_bytes)[c] = v[u];
+      }
+    }
   }
 }
 
