@@ -701,7 +701,8 @@ def run_star(args):
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(f"{args.config}/w{world}/layer1")
+            traffic = json.load(f).get(f"{args.config}/w{world}/" + ("small" if R <= 512 and pred.path(R) == 1
+                                                                       else "layer1"))
     m_tiles = (R + 127) // 128
     pair = c["dtype"] == "bf16" and (m_tiles == 2 or (m_tiles + 1) // 2 * 2 * 8 >= 148 * 5 // 8)
     # the contraction's own dtype: bf16 at its measured peak; fp32 runs as 3xTF32 (three tcgen05 kind::tf32

@@ -204,20 +204,8 @@ __global__ void __launch_bounds__(192, 1)
   const int partner = rank ^ 1;
   const int te = threadIdx.x - 64;     // epilogue thread 0..127
   int M = p.M;
-  if (p.M_dev) {   // refresh mode: the count was produced on the device by the previous kernel
-    pdl_wait();
-    M = __ldcg(p.M_dev);
-  }
-  // rows are processed in chunks of 512 (4 m-tiles): one chunk unless a refresh step has more
-  // due rows; chunk c's m-tile m covers rows [512 c + 128 m, +128)
-  const int nchunks = (M + 511) / 512;
-  const int total_mt = (M + 127) / 128;     // m-tiles over all chunks (= layer-3 completions)
-  if (M == 0) {   // refresh step with no due row: the projection of the aged rows is still due
-    if (p.project && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && warp >= 2)
-      small_finalize(p, smem, te, warp);
-    return;
-  }
-  if (m * 128 >= M) return;   // this m-tile is empty in every chunk (both CTAs of the cluster)
+  const bool dev_rows = p.M_dev != nullptr;   // refresh mode: the row count comes from the predecessor
+  if (!dev_rows && m * 128 >= M) return;      // (the host sizes the grid to M)
   const bool l3 = n == 0 && rank == 0;   // this CTA also runs layer 3 + head for its m-tile
   if (threadIdx.x == 0) {
     SMALL_TS(0);
@@ -261,6 +249,53 @@ __global__ void __launch_bounds__(192, 1)
   pdl_launch_dependents();
 
   const int kh = p.kb1 / 2;            // layer-1 K blocks of this split
+  const int pre = kh < NS ? kh : NS;   // layer-1 W1 blocks issued before griddepcontrol.wait (PDL overlap)
+  int pre_done = 0;
+  if (dev_rows) {
+    // the weight blocks of the first stages do not depend on the predecessor: out before its end
+    if (warp == 0) {
+      if (elect_one()) {
+        const uint64_t pol_b = policy_evict_last();
+        for (int i = 0; i < pre; ++i) {
+          mbar_arrive_expect_tx(&full[i], 32768u);
+          tma_load_2d(smem + S::B0 + 16384 * i, &tmW1, &full[i], (rank * kh + i) * 64, n * 128, pol_b);
+        }
+        for (int i = 0; i < 16; ++i) tma_prefetch_2d(&tmW2, rank * 1024 + i * 64, n * 32);
+      }
+      __syncwarp();
+    }
+    pre_done = pre;
+    pdl_wait();
+    M = __ldcg(p.M_dev);
+    if (m * 128 >= M) {
+      // this m-tile is empty in every chunk (both CTAs of the cluster): complete the issued stages
+      // (their h boxes are zero-filled or unused rows) and leave; with no due row at all, CTA 0
+      // still finalises the projection of the aged rows
+      if (warp == 0) {
+        if (elect_one()) {
+          for (int i = 0; i < pre; ++i) {
+            tma_load_2d(smem + 16384 * i, &tmH, &full[i], (rank * kh + i) * 64, m * 128, policy_evict_first());
+            mbar_wait(&full[i], 0);
+          }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      if (M == 0 && p.project && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && warp >= 2)
+        small_finalize(p, smem, te, warp);
+      tc_fence_before();
+      __syncthreads();
+      if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<256>(tmem);
+      }
+      return;
+    }
+  }
+  // rows are processed in chunks of 512 (4 m-tiles): one chunk unless a refresh step has more
+  // due rows; chunk c's m-tile m covers rows [512 c + 128 m, +128)
+  const int nchunks = (M + 511) / 512;
+  const int total_mt = (M + 127) / 128;     // m-tiles over all chunks (= layer-3 completions)
   const int q = warp & 3;
   const int row = q * 32 + lane;       // row of the tile (epilogue warps)
   const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
@@ -281,14 +316,13 @@ __global__ void __launch_bounds__(192, 1)
     if (warp == 0) {
       if (elect_one()) {   // TMA producer
         const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
-        const int pre = kh < NS ? kh : NS;   // W1 blocks before griddepcontrol.wait (PDL overlap)
-        for (int i = 0; i < pre; ++i) {
+        for (int i = (act == 0 ? pre_done : 0); i < pre; ++i) {   // W1 blocks before griddepcontrol.wait
           const int it = it1 + i, s = it % NS;
           mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&full[s], 32768u);
           tma_load_2d(smem + S::B0 + 16384 * s, &tmW1, &full[s], (rank * kh + i) * 64, n * 128, pol_b);
         }
-        if (act == 0) {
+        if (act == 0 && !pre_done) {
           for (int i = 0; i < 16; ++i) tma_prefetch_2d(&tmW2, rank * 1024 + i * 64, n * 32);   // into L2 early
           pdl_wait();
           SMALL_TS(2);
