@@ -16,6 +16,7 @@
 #include "lenpred_kernels.cuh"
 #include "lenpred_small.cuh"
 #include "lenpred_tail.cuh"
+#include "lenpred_tail2.cuh"
 #include "plan_core.cuh"
 #include "star_internal.h"
 
@@ -291,6 +292,16 @@ static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, 
                                 int32_t* n_hat, const ProjArgs* proj, cudaStream_t st,
                                 const CUtensorMap* tmH = nullptr, const SmallRefresh* rf = nullptr);
 
+// The large-batch tail: clusters of 4 per m-tile (lenpred_tail2.cuh); STAR_TAIL2=0 selects the
+// round-1 split-K tail (A/B measurements).
+static bool tail2_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("STAR_TAIL2");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 // Whether a one-rank single-round plan runs in the fused tail's last CTA (STAR_PLAN_FUSE=1, read
 // once) instead of the cluster plan kernel launched after it (default).  Measured at TGT with a
 // move (Alg. 1 past Phase 1): 117.3 us fused (192 threads score the candidates) vs 99.4 us with
@@ -378,6 +389,8 @@ struct star_predictor {
   CUtensorMap tmB1p;          // W1 with 128-row boxes (CTA-pair kernel: each CTA loads half of B)
   // one-launch predictor for <= 512 rows (lenpred_small.cuh)
   CUtensorMap tmW2s;          // W2 with 32-row boxes
+  CUtensorMap tmW2t;          // W2 with 128-row boxes (tail2)
+  int* tail2_done = nullptr;  // tail2: m-tiles finished (zero between launches)
   int* small_cnt = nullptr;   // its phase counters (zero between launches)
   int* r_blk = nullptr;       // refresh: the multi-CTA select's counts and counters (zero between launches)
   bool small_ok = false;      // shape supported and 32 clusters of 4 co-resident
@@ -412,6 +425,7 @@ static void free_pred(star_predictor* p) {
   cudaFree(p->tl_l1);
   cudaFree(p->small_cnt);
   cudaFree(p->r_blk);
+  cudaFree(p->tail2_done);
   cudaFree(p->tl_small);
   cudaFree(p->r_idx);
   cudaFree(p->r_pos);
@@ -524,11 +538,19 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
     return st;
   }
   if (!f32 && m1 == 2048 && m2 == 512 && d % 256 == 0) {
-    if ((st = make_tmap(&p->tmW2s, W2, false, (uint64_t)m1, m2, (uint64_t)m1 * 2, 32)) != STAR_OK) {
+    if ((st = make_tmap(&p->tmW2s, W2, false, (uint64_t)m1, m2, (uint64_t)m1 * 2, 32)) != STAR_OK ||
+        (st = make_tmap(&p->tmW2t, W2, false, (uint64_t)m1, m2, (uint64_t)m1 * 2, 128)) != STAR_OK) {
       free_pred(p);
       return st;
     }
     p->small_ok = small_path_available();
+    if (cudaMalloc(reinterpret_cast<void**>(&p->tail2_done), 16) != cudaSuccess ||
+        cudaMemset(p->tail2_done, 0, 16) != cudaSuccess) {
+      cudaGetLastError();
+      free_pred(p);
+      return fail(STAR_ENOMEM, "device allocation failed");
+    }
+    func_attr((const void*)tail2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tail2Smem::BYTES);
     if (p->small_ok) {
       const size_t ncnt = (size_t)SmallSmem::DONE + 16, nblk = 2 * (size_t)g_num_sms + 16;
       if (cudaMalloc(reinterpret_cast<void**>(&p->small_cnt), ncnt * sizeof(int)) != cudaSuccess ||
@@ -711,6 +733,43 @@ static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, 
     if (e != cudaSuccess) return cuda_fail(e, "layer-1 GEMM launch");
     if (p->ev1) record_timing_event(p->ev1, st);
     g.tl = nullptr;
+  }
+  // ---- fused tail, large batches: one cluster of 4 per m-tile, no split-K (lenpred_tail2.cuh) ----
+  if (!f32 && p->tail2_done && p->m2 == 512 && p->m3 == 64 && m_tiles >= 5 && tail2_enabled() &&
+      !(proj && plan && plan->world == 1 && plan->max_moves <= 1 && plan_fuse_enabled())) {
+    Tail2Args t{};
+    t.M = R;
+    t.num_kb = p->m1 / 64;
+    t.b2 = p->b2;
+    t.b3 = p->b3;
+    t.w4 = p->w4;
+    t.b4 = p->b4;
+    t.n_tok = n_tok;
+    t.max_ctx = max_ctx_len;
+    t.y_hat = y_hat;
+    t.n_hat = n_hat;
+    t.done = p->tail2_done;
+    t.project = proj ? 1 : 0;
+    if (proj) t.pa = *proj;
+    t.tl = p->tl;
+    if (p->tl) p->tl_ctas = 4 * m_tiles;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(4, m_tiles, 1);
+    cfg.blockDim = dim3(192, 1, 1);
+    cfg.dynamicSmemBytes = Tail2Smem::BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 4;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tail2_kernel, p->tmA2, p->tmW2t, p->tmB3, t);
+    if (e != cudaSuccess) return cuda_fail(e, "tail2 launch");
+    return STAR_OK;
   }
   // ---- fused tail: layer 2 -> layer 3 -> head -> quantizer [-> projection] ----
   const int n2 = p->m2 / 256;
