@@ -171,9 +171,19 @@ __global__ void __launch_bounds__(192, 1)
       umma_commit(acc3);
     }
     __syncwarp();
-  } else {
-    // ---- layer-2 epilogue: relu(Z2 + b2) -> bf16 -> the swizzled layer-3 A operand in smem ----
+  }
+  // CTA 0's epilogue threads own the rows' outputs: fetch N(r) and the instance now, off the
+  // critical path (after griddepcontrol.wait: the predecessor may have written them)
+  int32_t ntok = 0, inst = 0;
+  if (warp >= 2) {
     pdl_wait();   // the outputs below may still be read by the previous kernel
+    if (rank == 0 && grow < p.M) {
+      if (p.n_tok) ntok = p.n_tok[grow];
+      if (p.project) inst = p.pa.inst[grow];
+    }
+  }
+  if (warp >= 2) {
+    // ---- layer-2 epilogue: relu(Z2 + b2) -> bf16 -> the swizzled layer-3 A operand in smem ----
     mbar_wait(acc2, 0);
     tc_fence_after();
     if (te == 0) TAIL2_TS(3);
@@ -260,10 +270,8 @@ __global__ void __launch_bounds__(192, 1)
     float y = ((D[row] + D[128 + row]) + D[256 + row]) + D[384 + row];   // rank order
     y += p.b4 ? __ldg(p.b4) : 0.0f;
     const bool owner = grow < p.M;
-    int32_t nh = 0, ntok = 0, inst = 0;
+    int32_t nh = 0;
     if (owner) {
-      if (p.n_tok) ntok = p.n_tok[grow];
-      if (p.project) inst = p.pa.inst[grow];
       int32_t cap = p.max_ctx - ntok;
       cap = cap < 0 ? 0 : cap;
       nh = __float2int_rn(fminf(fmaxf(y, 0.0f), (float)cap));   // quantize_nhat (readings A8-A10)
