@@ -681,6 +681,146 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// Persistent form of the 9-column-tile pair GEMM for layer 1 over two tiles per CTA pair (e.g.
+// M = 4096: 16 row pairs x 9 column tiles = 144 pair tiles on 72 pairs): the grid is one wave;
+// pair P computes tiles P and P + npairs (tile t = row pair t / 9, column tile t % 9), the second
+// tile's mainloop into the other half of a 512-column TMEM allocation while the epilogue stores
+// the first (the epilogue no longer idles the tensor core, and there is no second-wave launch).
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    umma_pair_nu2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const GemmArgs p, int ntiles) {
+  using S = PairSmem<BN>;
+  constexpr int BK = 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S::STAGES * S::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S::STAGES * S::B_BYTES);
+  uint64_t* empty = full + S::STAGES;
+  uint64_t* accum = empty + S::STAGES;   // [2]: one per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();       // 0 = leader (issues the MMAs), 1 = peer
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int nmine = (pair + npairs < ntiles) ? 2 : 1;
+  const int nkb = p.num_kb;
+  auto tile_geom = [&](int j, int& m_row0, int& n0, int& nw) {
+    const int t = pair + j * npairs;
+    const int mp = t / 9, nt = t % 9;
+    m_row0 = mp * 256 + (int)rank * 128;
+    nw = nt < 7 ? 224 : 240;
+    n0 = nt * 224 + (nt > 7 ? (nt - 7) * 16 : 0);
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < S::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&accum[0], 1);
+    mbar_init(&accum[1], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync_relaxed();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (elect_one()) {   // TMA producer (both CTAs): the two tiles back to back through one ring
+      const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+      const uint32_t full0 = mapa_shared(smem_u32(&full[0]), 0);
+      const int pre = nkb < S::STAGES ? nkb : S::STAGES;
+      int m_row0, n0, nw;
+      tile_geom(0, m_row0, n0, nw);
+      for (int i = 0; i < pre; ++i) {   // weights before griddepcontrol.wait
+        if (rank == 0) mbar_arrive_expect_tx(&full[i], 2 * S::STAGE_BYTES);
+        tma_load_2d_pair(sB + i * S::B_BYTES, &tmB, full0 + (uint32_t)(i * 8), i * BK, n0 + (int)rank * (nw / 2), pol_b);
+      }
+      pdl_wait();
+      for (int j = 0; j < nmine; ++j) {
+        tile_geom(j, m_row0, n0, nw);
+        const int b_row = n0 + (int)rank * (nw / 2);
+        for (int i = 0; i < nkb; ++i) {
+          const int it = j * nkb + i, s = it % S::STAGES;
+          const uint32_t ph = (uint32_t)(it / S::STAGES) & 1u;
+          if (it >= pre) {
+            mbar_wait(&empty[s], ph ^ 1u);
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * S::STAGE_BYTES);
+            tma_load_2d_pair(sB + s * S::B_BYTES, &tmB, full0 + (uint32_t)(s * 8), i * BK, b_row, pol_b);
+          }
+          tma_load_2d_pair(sA + s * S::A_BYTES, &tmA, full0 + (uint32_t)(s * 8), i * BK, m_row0, pol_a);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (rank == 0 && elect_one()) {   // MMA issuer (leader): tile j into TMEM columns [256 j, +nw)
+      for (int j = 0; j < nmine; ++j) {
+        int m_row0, n0, nw;
+        tile_geom(j, m_row0, n0, nw);
+        const uint32_t idesc = umma_idesc(false, 256, (uint32_t)nw);
+        for (int i = 0; i < nkb; ++i) {
+          const int it = j * nkb + i, s = it % S::STAGES;
+          mbar_wait(&full[s], (uint32_t)(it / S::STAGES) & 1u);
+          tc_fence_after();
+          const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * S::A_BYTES));
+          const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * S::B_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_pair(tmem + 256u * j, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (i | k) != 0 ? 1u : 0u);
+          umma_commit_pair(&empty[s], (uint16_t)3);
+        }
+        umma_commit_pair(&accum[j], (uint16_t)3);
+      }
+    }
+    __syncwarp();
+  } else {
+    // epilogue (both CTAs): own 128 lanes of each tile; tile 0's stores overlap tile 1's mainloop
+    const int q = warp & 3;
+    const uint32_t trow0 = tmem + ((uint32_t)(q * 32) << 16);
+    pdl_wait();   // Z1 may still be read by the previous kernel
+    float head_acc = 0.0f;
+    for (int j = 0; j < nmine; ++j) {
+      int m_row0, n0, nw;
+      tile_geom(j, m_row0, n0, nw);
+      const int row = m_row0 + q * 32 + lane;
+      const uint32_t trow = trow0 + 256u * j;
+      mbar_wait(&accum[j], 0);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < nw; c += 32) {
+        uint32_t v[16], u[16];
+        tmem_ld_32x32b_x16(trow + (uint32_t)c, v);
+        if (c + 16 < nw) tmem_ld_32x32b_x16(trow + (uint32_t)(c + 16), u);
+        tmem_ld_wait();
+        float f[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) f[jj] = __uint_as_float(v[jj]);
+        epilogue16<false>(p, row, n0 + c, f, head_acc, nullptr, 0);
+        if (c + 16 < nw) {
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) f[jj] = __uint_as_float(u[jj]);
+          epilogue16<false>(p, row, n0 + c + 16, f, head_acc, nullptr, 0);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_relaxed();   // the pair's MMAs and TMEM reads are done before the pair frees TMEM
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem);
+  }
+}
+
 // 3xTF32 operand preparation: x [R][K] fp32 (row stride ld) -> out [R][3K]
 //   pattern A: [hi | hi | lo]   (activations)     pattern B: [hi | lo | hi] (weights)
 // so that A'.B'^T = hi.hi + hi.lo + lo.hi (the lo.lo term, ~2^-22 relative, is dropped).

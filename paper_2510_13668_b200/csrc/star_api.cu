@@ -200,6 +200,39 @@ static cudaError_t launch_pair_gemm(const CUtensorMap& a, const CUtensorMap& b, 
                       : cudaLaunchKernelEx(&cfg, umma_pair_gemm_kernel<256, false>, a, b, c, p);
 }
 
+// Persistent 9-column-tile pairs, two tiles per pair (umma_pair_nu2_kernel): one wave of
+// 2 * ceil(tiles / 2) CTAs.  STAR_L1_PERSIST=0 keeps the two-wave grid (A/B measurements).
+static bool l1_persist_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("STAR_L1_PERSIST");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+static cudaError_t launch_pair_nu2(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int m_tiles,
+                                   cudaStream_t st) {
+  cudaError_t e = func_attr((const void*)umma_pair_nu2_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)PairSmem<256>::BYTES);
+  if (e != cudaSuccess) return e;
+  const int ntiles = ((m_tiles + 1) / 2) * 9;
+  const int npairs = (ntiles + 1) / 2;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * npairs, 1, 1);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = PairSmem<256>::BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, umma_pair_nu2_kernel<256>, a, b, p, ntiles);
+}
+
 // Timing events must be real event-record nodes inside a captured graph (External flag);
 // outside capture a plain record.  Errors are cleared so they cannot leak into a launch check.
 static void record_timing_event(cudaEvent_t ev, cudaStream_t st) {
@@ -728,7 +761,11 @@ static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, 
       p->tl_l1_ctas = m_tiles * (p->m1 / p->bn1) * g.splits;
     }
     if (p->ev0) record_timing_event(p->ev0, st);
-    cudaError_t e = pair ? launch_pair_gemm(p->tmA1, p->tmB1p, tmC1, g, m_tiles, st, nu)
+    // two 9-tile waves fit one wave of pairs with two tiles each
+    const int nu_tiles = ((m_tiles + 1) / 2) * 9;
+    const bool nu2 = nu && nu_tiles * 2 > slots && (nu_tiles + 1) / 2 * 2 <= slots && l1_persist_enabled();
+    cudaError_t e = nu2 ? launch_pair_nu2(p->tmA1, p->tmB1p, g, m_tiles, st)
+                  : pair ? launch_pair_gemm(p->tmA1, p->tmB1p, tmC1, g, m_tiles, st, nu)
                          : launch_gemm(p->bn1, f32, p->tmA1, p->tmB1, tmC1, g, m_tiles, st);
     if (e != cudaSuccess) return cuda_fail(e, "layer-1 GEMM launch");
     if (p->ev1) record_timing_event(p->ev1, st);
