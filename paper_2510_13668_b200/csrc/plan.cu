@@ -67,7 +67,11 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_cluster_kernel(const Pla
   __shared__ Cand cl_best[2];
   __shared__ int shv[8];
   const bool lead = cluster_ctarank() == 0;
-  if (threadIdx.x == 0) g_plan_cl_tl[cluster_ctarank() * 8] = globaltimer_ns();
+  if (threadIdx.x == 0) {
+    g_plan_cl_tl[cluster_ctarank() * 8] = globaltimer_ns();
+    g_plan_cl_tl[cluster_ctarank() * 8 + 6] = 0;   // max evaluation cycles (atomicMax below)
+  }
+  __syncthreads();
   PlanArgs ac = a;
   if (lead && threadIdx.x == 0) g_plan_tl[0] = globaltimer_ns();
   pdl_launch_dependents();

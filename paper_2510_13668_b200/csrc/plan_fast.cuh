@@ -572,6 +572,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     // one (candidate, target) pair per thread: the scoring is a dependent chain of int128 steps,
     // so spreading the pairs (not the candidates) over the threads shortens each thread's chain
     const int npairs = ncand * nU;
+    const long long ev_t0 = (a.cl_tl && round == 0) ? clock64() : 0;
     for (int pi = tid; pi < npairs; pi += nthreads) {
       const int c = pi / nU, qq = pi - c * nU;
       const int g = s.cidx[c];
@@ -595,6 +596,11 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
       cd.dst = u;
       cd.g = g;
       if (cand_better_g(cd, best)) best = cd;
+    }
+    if (a.cl_tl && round == 0) {   // diagnostics: slowest thread's evaluation cycles, pairs, candidates
+      const unsigned long long dt = (unsigned long long)(clock64() - ev_t0);
+      atomicMax(reinterpret_cast<unsigned long long*>(a.cl_tl + crank * 8 + 6), dt);
+      if (tid == 0) a.cl_tl[crank * 8 + 7] = ((uint64_t)ncand << 32) | (uint64_t)(uint32_t)nU;
     }
     PLAN_TS(10);
     __syncwarp();

@@ -39,3 +39,7 @@ t0 = cl[:, 0].min()
 print("per-CTA (us from the earliest entry): entry, pdl_wait, pre-sync, post-sync (round-parity 0)")
 for r in range(8):
     print(r, [round((cl[r, j] - t0) / 1e3, 2) if cl[r, j] else None for j in (0, 1, 2, 3)])
+print("per-CTA slowest-thread evaluation (cycles), candidates, targets:")
+for r in range(8):
+    v = int(cl[r, 7])
+    print(r, int(cl[r, 6]), v >> 32, v & 0xFFFFFFFF)
