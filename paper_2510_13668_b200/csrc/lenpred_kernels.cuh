@@ -748,11 +748,6 @@ __global__ void __launch_bounds__(192, 1)
       for (int j = 0; j < nmine; ++j) {
         tile_geom(j, m_row0, n0, nw);
         const int b_row = n0 + (int)rank * (nw / 2);
-        // L2 prefetch, one per operand block: the tile's A rows by the pair of column tile 0, its
-        // B rows by the pair of the wave's first row pair (as the non-persistent kernel's prefetch 2)
-        const int t = pair + j * npairs;
-        const bool pf_a = p.prefetch != 1 && (t % 9) == 0;
-        const bool pf_b = p.prefetch != 1 && (t / 9) == (j * npairs) / 9;
         for (int i = 0; i < nkb; ++i) {
           const int it = j * nkb + i, s = it % S::STAGES;
           const uint32_t ph = (uint32_t)(it / S::STAGES) & 1u;
@@ -762,10 +757,6 @@ __global__ void __launch_bounds__(192, 1)
             tma_load_2d_pair(sB + s * S::B_BYTES, &tmB, full0 + (uint32_t)(s * 8), i * BK, b_row, pol_b);
           }
           tma_load_2d_pair(sA + s * S::A_BYTES, &tmA, full0 + (uint32_t)(s * 8), i * BK, m_row0, pol_a);
-          if (i + kPrefetchKB < nkb) {
-            if (pf_a) tma_prefetch_2d(&tmA, (i + kPrefetchKB) * BK, m_row0);
-            if (pf_b) tma_prefetch_2d(&tmB, (i + kPrefetchKB) * BK, b_row);
-          }
         }
       }
     }

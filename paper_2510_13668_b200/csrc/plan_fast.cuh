@@ -619,7 +619,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
     if (warp == 0) {
       if (lane < nwarps) c = warp_best[lane];
       c = warp_argmax_g(c);   // every lane holds the CTA's winner
-      if (kCl > 1 && !kGlob && lane == 0) cl_best[round & 1] = c;
+      if (kCl > 1 && lane == 0) cl_best[round & 1] = c;
     }
     if constexpr (kCl > 1 && kGlob) {
       // global argmax: publish this CTA's winner (release), wait for all kCl, read them (L2)

@@ -745,7 +745,7 @@ static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, 
       g.l1_cnt = p->l1_cnt;
       // L2 prefetch by one CTA per tile row / column: cold L2 (the in-step case) 30.8 us vs 33.0 us
       // when every consumer prefetches, warm 24.8 vs 24.3 us (M = 2048, tools/gemm_bench.cu)
-      g.prefetch = getenv("STAR_L1_PREFETCH") && atoi(getenv("STAR_L1_PREFETCH")) == 0 ? 1 : 2;
+      g.prefetch = 2;
       g.tl = p->tl_l1;
       p->tl_l1_ctas = ((m_tiles + 1) & ~1) * (p->m1 / 256) * pair_splits;
     }
