@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_cluster_kernel(const Pla
 
 // The same plan on kCl CTAs that are not a cluster (global-memory argmax): no GPC placement
 // constraint, so the grid starts on free SMs while the predecessor still runs (PDL).
-__device__ __align__(16) uint8_t g_plan_gx[8 * 2 * 32 + 16];
+__device__ uint8_t g_plan_gx[8 * 2 * 32 + 16];
 template <int kCl>
 __global__ void __launch_bounds__(kPlanThreads, 1) plan_multi_kernel(const PlanArgs a) {
   extern __shared__ __align__(16) uint8_t smraw[];
