@@ -83,35 +83,6 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_cluster_kernel(const Pla
   plan_cta_fast<false, kCl>(ac, smraw, (int)threadIdx.x, (int)blockDim.x, warp_best, shv, g_plan_tl, cl_best);
 }
 
-// The same plan on kCl CTAs that are not a cluster (global-memory argmax): no GPC placement
-// constraint, so the grid starts on free SMs while the predecessor still runs (PDL).
-__device__ uint8_t g_plan_gx[8 * 2 * 32 + 16];
-template <int kCl>
-__global__ void __launch_bounds__(kPlanThreads, 1) plan_multi_kernel(const PlanArgs a) {
-  extern __shared__ __align__(16) uint8_t smraw[];
-  __shared__ Cand warp_best[kPlanThreads / 32];
-  __shared__ int shv[8];
-  const bool lead = blockIdx.x == 0;
-  if (lead && threadIdx.x == 0) g_plan_tl[0] = globaltimer_ns();
-  pdl_launch_dependents();
-  if (lead && threadIdx.x == 0) {
-    g_plan_tl[1] = globaltimer_ns();
-    g_plan_tl[33] = clock64();
-  }
-  PlanArgs ac = a;
-  ac.gx = g_plan_gx;
-  plan_cta_fast<false, kCl, true>(ac, smraw, (int)threadIdx.x, (int)blockDim.x, warp_best, shv, g_plan_tl);
-}
-
-// STAR_PLAN_GLOBAL=0: the cluster form instead of the global-argmax form (A/B measurements).
-static bool plan_global_enabled() {
-  static int v = [] {
-    const char* e = getenv("STAR_PLAN_GLOBAL");
-    return e ? atoi(e) : 1;
-  }();
-  return v != 0;
-}
-
 // Cluster size of the staged plan: STAR_PLAN_CLUSTER (1, 2, 4 or 8; read once) for A/B
 // measurements, default 8.
 static int plan_cluster_size() {
@@ -171,9 +142,7 @@ cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg,
   const size_t smem = staged ? plan_fast_smem_layout(a.n, a.H, a.world, a.r_cap)
                              : plan_smem_layout(a.n, a.H, a.world, a.r_cap, false);
   const int ncl = staged ? plan_cluster_size() : 1;
-  const bool glob = staged && ncl == 8 && plan_global_enabled();
   auto kern = !staged ? plan_kernel<false>
-            : glob ? plan_multi_kernel<8>
             : ncl == 8 ? plan_cluster_kernel<8> : ncl == 4 ? plan_cluster_kernel<4>
             : ncl == 2 ? plan_cluster_kernel<2> : plan_kernel<true>;
   if (smem > 48 * 1024) {
@@ -195,7 +164,7 @@ cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg,
   at[1].val.clusterDim.y = 1;
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = (ncl > 1 && !glob) ? 2 : 1;
+  cfg.numAttrs = ncl > 1 ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 

@@ -34,7 +34,6 @@ struct PlanArgs {
   int bulk;                 // every segment array 16-byte aligned: the table may be bulk-copied
   const int64_t* W0;        // nullable: W_i of the input L (round 0), e.g. the projection's own
   uint64_t* cl_tl;          // diagnostics: per-CTA %globaltimer stamps of the cluster plan [8][8], or nullptr
-  uint8_t* gx;              // multi-CTA plan without a cluster: [2][kCl] Cands + 3 counters (zero between launches)
 };
 
 template <typename T>

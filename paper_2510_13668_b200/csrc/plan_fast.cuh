@@ -135,13 +135,10 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // Only CTA 0 writes the move list.  cl_best: [2] shared Cands (round-parity double buffer).
 // (Measured and rejected: pushing the last round's CTA winners to CTA 0 with st.async +
 // mbarrier instead of the cluster barrier -- the plan went 11.0 -> 15.4 us.)
-// kGlob: the kCl CTAs are NOT a cluster (so the grid can start on any free SMs while the
-// predecessor still runs, programmatic dependent launch): the round's CTA winners meet in global
-// memory (a.gx: [2][kCl] Cands + counters; every CTA resident, the wait traps after ~2 s).
-template <bool kFused = false, int kCl = 1, bool kGlob = false>
+template <bool kFused = false, int kCl = 1>
 __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw, const int tid, const int nthreads,
                                               Cand* warp_best, int* shv, uint64_t* tl, Cand* cl_best = nullptr) {
-  const int crank = kCl > 1 ? (kGlob ? (int)blockIdx.x : (int)cluster_ctarank()) : 0;
+  const int crank = kCl > 1 ? (int)cluster_ctarank() : 0;
   if (kCl > 1 && crank != 0) tl = nullptr;
 #define PLAN_TS(k)                                           \
   do {                                                       \
@@ -621,31 +618,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
       c = warp_argmax_g(c);   // every lane holds the CTA's winner
       if (kCl > 1 && lane == 0) cl_best[round & 1] = c;
     }
-    if constexpr (kCl > 1 && kGlob) {
-      // global argmax: publish this CTA's winner (release), wait for all kCl, read them (L2)
-      Cand* gc = reinterpret_cast<Cand*>(a.gx) + (round & 1) * kCl;
-      int* gcnt = reinterpret_cast<int*>(a.gx + 2 * kCl * sizeof(Cand));
-      if (warp == 0) {
-        if (lane == 0) {
-          gc[crank] = c;
-          fence_acq_rel_gpu();
-          atomicAdd(gcnt + (round & 1), 1);
-          spin_wait_geq(gcnt + (round & 1), kCl * (round / 2 + 1));   // cumulative per parity slot
-        }
-        __syncwarp();
-        Cand o;
-        o.score = 0; o.id = 0; o.dst = 0; o.g = -1;
-        if (lane < kCl) {
-          const uint64_t* src = reinterpret_cast<const uint64_t*>(gc + lane);
-          const uint64_t lo = __ldcg(src), hi = __ldcg(src + 1), ig = __ldcg(src + 2), gg = __ldcg(src + 3);
-          o.score = (i128)(((unsigned __int128)hi << 64) | lo);
-          o.id = (int32_t)(uint32_t)ig;
-          o.dst = (int32_t)(uint32_t)(ig >> 32);
-          o.g = (int32_t)(uint32_t)gg;
-        }
-        c = warp_argmax_g(o);
-      }
-    } else if constexpr (kCl > 1) {
+    if constexpr (kCl > 1) {
       // cluster argmax: every CTA published its winner; meet (all threads), then warp 0 of every
       // CTA reads all kCl winners from distributed shared memory and takes the same argmax
       if (a.cl_tl && tid == 0) a.cl_tl[crank * 8 + 2 + 2 * (round & 1)] = globaltimer_ns();
@@ -714,19 +687,7 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
   }
   PLAN_TS(7);
   if (tid == 0 && crank == 0) *a.n_moves = s_nmoves;
-  if constexpr (kCl > 1 && kGlob) {
-    // the last CTA out re-arms the exchange counters for the next launch (nobody waits on them now)
-    if (tid == 0) {
-      int* gcnt = reinterpret_cast<int*>(a.gx + 2 * kCl * sizeof(Cand));
-      if (atomicAdd(gcnt + 2, 1) == kCl - 1) {
-        gcnt[0] = 0;
-        gcnt[1] = 0;
-        gcnt[2] = 0;
-      }
-    }
-  } else if constexpr (kCl > 1) {
-    cluster_sync_all();   // no CTA leaves while a peer may still read its cl_best
-  }
+  if constexpr (kCl > 1) cluster_sync_all();   // no CTA leaves while a peer may still read its cl_best
 #undef PLAN_TS
 }
 
