@@ -193,24 +193,28 @@ struct SelArgs {
 
 constexpr int kSelHistBins = 2560;   // shared histogram of the aged rows (n_inst * (H + 2) <= this)
 
-__global__ void __launch_bounds__(kSelThreads) refresh_select_gather_age_kernel(const SelArgs a) {
-  __shared__ int wsum[kSelThreads / 32];
+// 256 rows per CTA (the gather of the due rows' hidden states spreads over R / 256 SMs: with 1024
+// rows per CTA, two CTAs gathered the C2 step's ~100 rows and the kernel took ~21 us)
+constexpr int kSel2Threads = 256;
+
+__global__ void __launch_bounds__(kSel2Threads) refresh_select_gather_age_kernel(const SelArgs a) {
+  __shared__ int wsum[kSel2Threads / 32];
   __shared__ int s_base, s_cnt;
-  __shared__ int s_rows[kSelThreads];
+  __shared__ int s_rows[kSel2Threads];
   __shared__ unsigned long long s_sum[kSelHistBins];
   __shared__ uint32_t s_hc[kSelHistBins];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nb = a.project ? a.pa.n_inst * (a.pa.H + 2) : 0;
   const bool shist = nb <= kSelHistBins;   // else the aged rows go straight to the global histogram
   if (shist)
-    for (int j = tid; j < nb; j += kSelThreads) {
+    for (int j = tid; j < nb; j += kSel2Threads) {
       s_sum[j] = 0;
       s_hc[j] = 0;
     }
   pdl_wait();
   pdl_launch_dependents();
   const int G = gridDim.x, b = blockIdx.x;
-  const int r = b * kSelThreads + tid;
+  const int r = b * kSel2Threads + tid;
   bool f = false;
   int gl = 0, g = 0;
   if (r < a.R) {
@@ -221,8 +225,8 @@ __global__ void __launch_bounds__(kSelThreads) refresh_select_gather_age_kernel(
   const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
   if (lane == 0) wsum[warp] = __popc(m);
   __syncthreads();
-  if (warp == 0) {   // exclusive scan of the 32 warp counts
-    const int v = wsum[lane];
+  if (warp == 0) {   // exclusive scan of the 8 warp counts
+    const int v = lane < kSel2Threads / 32 ? wsum[lane] : 0;
     int x = v;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -230,7 +234,7 @@ __global__ void __launch_bounds__(kSelThreads) refresh_select_gather_age_kernel(
       const int y = __shfl_up_sync(0xFFFFFFFFu, x, off);
       if (lane >= off) x += y;
     }
-    wsum[lane] = x - v;
+    if (lane < kSel2Threads / 32) wsum[lane] = x - v;
     if (lane == 31) s_cnt = x;
   }
   __syncthreads();
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(kSelThreads) refresh_select_gather_age_kernel(
     if (errbits && a.pa.err) atomicOr(a.pa.err, (int)errbits);
     if (shist) {
       __syncthreads();
-      for (int j = tid; j < nb; j += kSelThreads) {
+      for (int j = tid; j < nb; j += kSel2Threads) {
         const uint32_t c = s_hc[j];
         if (c) {
           atomicAdd(a.pa.ws_cnt + j, c);
@@ -296,11 +300,11 @@ __global__ void __launch_bounds__(kSelThreads) refresh_select_gather_age_kernel(
   const int nvec = a.row_bytes / 16;
   const int total = cnt * nvec;
   constexpr int kU = 8;
-  for (int b0 = 0; b0 < total; b0 += kU * kSelThreads) {
+  for (int b0 = 0; b0 < total; b0 += kU * kSel2Threads) {
     int4 v[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int e = b0 + u * kSelThreads + tid;
+      const int e = b0 + u * kSel2Threads + tid;
       if (e < total) {
         const int j = e / nvec, c = e - j * nvec;
         v[u] = ld_stream_int4(reinterpret_cast<const int4*>(a.h + (int64_t)s_rows[j] * a.ld_bytes) + c);
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(kSelThreads) refresh_select_gather_age_kernel(
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int e = b0 + u * kSelThreads + tid;
+      const int e = b0 + u * kSel2Threads + tid;
       if (e < total) {
         const int j = e / nvec, c = e - j * nvec;
         reinterpret_cast<int4*>(a.hc + (int64_t)(base + j) * a.row_bytes)[c] = v[u];
@@ -398,10 +402,10 @@ cudaError_t launch_refresh_select_fused(int R, const int32_t* gen, const int32_t
   a.project = proj ? 1 : 0;
   if (proj) a.pa = *proj;
   cudaLaunchAttribute at[1];
-  cudaLaunchConfig_t cfg = pdl_cfg(dim3((R + kSelThreads - 1) / kSelThreads), dim3(kSelThreads), st, at);
+  cudaLaunchConfig_t cfg = pdl_cfg(dim3((R + kSel2Threads - 1) / kSel2Threads), dim3(kSel2Threads), st, at);
   return cudaLaunchKernelEx(&cfg, refresh_select_gather_age_kernel, a);
 }
 
-int refresh_select_fused_max_rows() { return kSelThreads * g_num_sms; }
+int refresh_select_fused_max_rows() { return kSel2Threads * g_num_sms; }
 
 }  // namespace star
