@@ -93,7 +93,6 @@ __device__ __forceinline__ void bulk_s2cluster(uint32_t dst_cluster, const void*
       "r"(smem_u32(src_cta)), "r"(bytes), "r"(mbar_cluster)
       : "memory");
 }
-__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

@@ -189,15 +189,24 @@ struct SelArgs {
   int* blk;              // [grid] CTA counts | [grid] arrival | [grid + 1] done  (zero between launches)
   int project;
   ProjArgs pa;
+  uint64_t* tl;          // diagnostics: rows [400 + CTA][32] of the predictor's timeline buffer, or nullptr
 };
 
-constexpr int kSelHistBins = 2560;   // shared histogram of the aged rows (n_inst * (H + 2) <= this)
+constexpr int kSelHistBins = 2560;
+#define SEL_TS(k)                                                                 \
+  do {                                                                            \
+    if (a.tl && threadIdx.x == 0) a.tl[(400 + blockIdx.x) * 32 + (k)] = globaltimer_ns(); \
+  } while (0)   // shared histogram of the aged rows (n_inst * (H + 2) <= this)
 
 // 256 rows per CTA (the gather of the due rows' hidden states spreads over R / 256 SMs: with 1024
 // rows per CTA, two CTAs gathered the C2 step's ~100 rows and the kernel took ~21 us)
 constexpr int kSel2Threads = 256;
 
+constexpr uint32_t kSelStageBytes = 160u * 1024u;   // gather staging: the CTA's due rows, chunked
+
 __global__ void __launch_bounds__(kSel2Threads) refresh_select_gather_age_kernel(const SelArgs a) {
+  extern __shared__ __align__(128) uint8_t stage[];   // kSelStageBytes
+  __shared__ uint64_t gbar;
   __shared__ int wsum[kSel2Threads / 32];
   __shared__ int s_base, s_cnt;
   __shared__ int s_rows[kSel2Threads];
@@ -211,8 +220,10 @@ __global__ void __launch_bounds__(kSel2Threads) refresh_select_gather_age_kernel
       s_sum[j] = 0;
       s_hc[j] = 0;
     }
+  SEL_TS(0);
   pdl_wait();
   pdl_launch_dependents();
+  SEL_TS(1);
   const int G = gridDim.x, b = blockIdx.x;
   const int r = b * kSel2Threads + tid;
   bool f = false;
@@ -239,6 +250,24 @@ __global__ void __launch_bounds__(kSel2Threads) refresh_select_gather_age_kernel
   }
   __syncthreads();
   const int lp = wsum[warp] + __popc(m & ((1u << lane) - 1u));   // position among this CTA's due rows
+  if (f) s_rows[lp] = r;
+  __syncthreads();
+  // gather, part 1: the due rows' hidden states start streaming into shared memory now (bulk
+  // copies, all in flight at once) -- their compacted position is known only after the CTA counts
+  // meet below, but the loads do not need it
+  const int cnt0 = s_cnt;
+  const int rows_per_chunk = (int)(kSelStageBytes / (uint32_t)a.row_bytes);
+  if (tid == 0) {
+    mbar_init(&gbar, 1);
+    fence_barrier_init();
+    const int n = cnt0 < rows_per_chunk ? cnt0 : rows_per_chunk;
+    if (n > 0) {
+      mbar_arrive_expect_tx(&gbar, (uint32_t)(n * a.row_bytes));
+      for (int j = 0; j < n; ++j)
+        bulk_g2s(stage + (size_t)j * a.row_bytes, a.h + (int64_t)s_rows[j] * a.ld_bytes, (uint32_t)a.row_bytes, &gbar);
+    }
+  }
+  SEL_TS(2);
   if (tid == 0) {   // publish this CTA's count
     a.blk[b] = s_cnt;
     fence_acq_rel_gpu();
@@ -273,7 +302,7 @@ __global__ void __launch_bounds__(kSel2Threads) refresh_select_gather_age_kernel
       }
     }
   }
-  if (f) s_rows[lp] = r;
+  SEL_TS(3);
   if (tid == 0) {   // every CTA's count is in: this CTA's base is the sum of the lower CTAs' counts
     spin_wait_geq(a.blk + G, G);
     int base = 0;
@@ -289,36 +318,36 @@ __global__ void __launch_bounds__(kSel2Threads) refresh_select_gather_age_kernel
     }
   }
   __syncthreads();
+  SEL_TS(4);
   const int base = s_base, cnt = s_cnt;
   if (f) {
     a.idx[base + lp] = r;
     a.ntok_c[base + lp] = a.n_tok ? a.n_tok[r] : 0;
   }
-  // gather the due rows' hidden states: a flat (row, 16-byte vector) index space over all 1024
-  // threads, 8 independent loads in flight per thread before their stores (the rows come cold
-  // from HBM; a dependent load -> store chain per vector made this the slowest part of the kernel)
-  const int nvec = a.row_bytes / 16;
-  const int total = cnt * nvec;
-  constexpr int kU = 8;
-  for (int b0 = 0; b0 < total; b0 += kU * kSel2Threads) {
-    int4 v[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int e = b0 + u * kSel2Threads + tid;
-      if (e < total) {
-        const int j = e / nvec, c = e - j * nvec;
-        v[u] = ld_stream_int4(reinterpret_cast<const int4*>(a.h + (int64_t)s_rows[j] * a.ld_bytes) + c);
+  // gather, part 2: each chunk of staged rows goes out to its compacted position (bulk stores);
+  // the next chunk (more due rows than shared memory holds) streams in after the stores read it
+  if (tid == 0) {
+    uint32_t ph = 0;
+    for (int j0 = 0; j0 < cnt; j0 += rows_per_chunk) {
+      const int n = cnt - j0 < rows_per_chunk ? cnt - j0 : rows_per_chunk;
+      mbar_wait(&gbar, ph);
+      ph ^= 1u;
+      for (int j = 0; j < n; ++j)
+        bulk_s2g(a.hc + (int64_t)(base + j0 + j) * a.row_bytes, stage + (size_t)j * a.row_bytes, (uint32_t)a.row_bytes);
+      bulk_commit();
+      const int j1 = j0 + rows_per_chunk;
+      if (j1 < cnt) {
+        bulk_wait_read_all();   // the staging buffer was read by the stores
+        const int n1 = cnt - j1 < rows_per_chunk ? cnt - j1 : rows_per_chunk;
+        mbar_arrive_expect_tx(&gbar, (uint32_t)(n1 * a.row_bytes));
+        for (int j = 0; j < n1; ++j)
+          bulk_g2s(stage + (size_t)j * a.row_bytes, a.h + (int64_t)s_rows[j1 + j] * a.ld_bytes, (uint32_t)a.row_bytes,
+                   &gbar);
       }
     }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int e = b0 + u * kSel2Threads + tid;
-      if (e < total) {
-        const int j = e / nvec, c = e - j * nvec;
-        reinterpret_cast<int4*>(a.hc + (int64_t)(base + j) * a.row_bytes)[c] = v[u];
-      }
-    }
+    bulk_wait_all();   // the compacted rows are in global memory before the grid completes
   }
+  SEL_TS(5);
 }
 
 static cudaLaunchConfig_t pdl_cfg(dim3 grid, dim3 block, cudaStream_t st, cudaLaunchAttribute* at) {
@@ -381,8 +410,10 @@ cudaError_t launch_refresh_scatter_project(const ProjArgs& a, const int32_t* pos
 cudaError_t launch_refresh_select_fused(int R, const int32_t* gen, const int32_t* g_last, const int32_t* nhat_last,
                                         int32_t k, const int32_t* n_tok, const void* h, int64_t ld_bytes, int row_bytes,
                                         int32_t* idx, int32_t* ntok_c, void* hc, int32_t* n_hat, int32_t* M_out,
-                                        int32_t* n_refreshed, int* blk, const ProjArgs* proj, cudaStream_t st) {
+                                        int32_t* n_refreshed, int* blk, const ProjArgs* proj, cudaStream_t st,
+                                        uint64_t* tl) {
   SelArgs a{};
+  a.tl = tl;
   a.R = R;
   a.gen = gen;
   a.g_last = g_last;
@@ -402,7 +433,13 @@ cudaError_t launch_refresh_select_fused(int R, const int32_t* gen, const int32_t
   a.project = proj ? 1 : 0;
   if (proj) a.pa = *proj;
   cudaLaunchAttribute at[1];
+  if ((row_bytes & 15) || (ld_bytes & 15) || (reinterpret_cast<uintptr_t>(h) & 15) || (uint32_t)row_bytes > kSelStageBytes)
+    return cudaErrorInvalidValue;
+  cudaError_t e = func_attr((const void*)refresh_select_gather_age_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kSelStageBytes);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = pdl_cfg(dim3((R + kSel2Threads - 1) / kSel2Threads), dim3(kSel2Threads), st, at);
+  cfg.dynamicSmemBytes = kSelStageBytes;
   return cudaLaunchKernelEx(&cfg, refresh_select_gather_age_kernel, a);
 }
 

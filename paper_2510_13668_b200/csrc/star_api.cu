@@ -1000,7 +1000,7 @@ static star_status refresh_impl(star_predictor* p, const void* h, int64_t ld_h, 
     // projects them); the small-batch predictor runs the due rows in 512-row chunks, scatters their
     // N_hat into their slots, adds them to the projection and finalises it
     if ((e = launch_refresh_select_fused(R, gen, g_last, nhat_last, k, n_tok, h, ld_h * 2, p->d * 2, p->r_idx,
-                                         p->r_ntok, p->r_h, n_hat, p->r_M, n_refreshed, p->r_blk, proj, st)) !=
+                                         p->r_ntok, p->r_h, n_hat, p->r_M, n_refreshed, p->r_blk, proj, st, p->tl)) !=
         cudaSuccess)
       return cuda_fail(e, "refresh select launch");
     SmallRefresh rf{p->r_M, p->r_idx, gen, g_last, nhat_last, n_hat};

@@ -57,7 +57,8 @@ struct ProjArgs;
 cudaError_t launch_refresh_select_fused(int R, const int32_t* gen, const int32_t* g_last, const int32_t* nhat_last,
                                         int32_t k, const int32_t* n_tok, const void* h, int64_t ld_bytes, int row_bytes,
                                         int32_t* idx, int32_t* ntok_c, void* hc, int32_t* n_hat, int32_t* M_out,
-                                        int32_t* n_refreshed, int* blk, const ProjArgs* proj, cudaStream_t st);
+                                        int32_t* n_refreshed, int* blk, const ProjArgs* proj, cudaStream_t st,
+                                        uint64_t* tl = nullptr);
 int refresh_select_fused_max_rows();
 size_t refresh_scatter_project_smem(int n_inst, int H);
 cudaError_t launch_refresh_scatter_project(const ProjArgs& a, const int32_t* pos, const int32_t* nhat_c,
