@@ -227,10 +227,13 @@ __global__ void __launch_bounds__(kSel2Threads) refresh_select_gather_age_kernel
   const int G = gridDim.x, b = blockIdx.x;
   const int r = b * kSel2Threads + tid;
   bool f = false;
-  int gl = 0, g = 0;
-  if (r < a.R) {
+  int gl = 0, g = 0, nl = 0, ins = 0, nt = 0;
+  if (r < a.R) {   // every per-row input in one round of loads
     gl = a.g_last[r];
     g = a.gen[r];
+    nl = a.nhat_last[r];
+    if (a.project) ins = a.pa.inst[r];
+    if (a.n_tok) nt = a.n_tok[r];
     f = gl < 0 || g - gl >= a.k;   // should_refresh
   }
   const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
@@ -257,7 +260,10 @@ __global__ void __launch_bounds__(kSel2Threads) refresh_select_gather_age_kernel
   // meet below, but the loads do not need it
   const int cnt0 = s_cnt;
   const int rows_per_chunk = (int)(kSelStageBytes / (uint32_t)a.row_bytes);
-  if (tid == 0) {
+  if (tid == 0) {   // publish this CTA's count first (the other CTAs wait for it)
+    a.blk[b] = cnt0;
+    fence_acq_rel_gpu();
+    atomicAdd(a.blk + G, 1);
     mbar_init(&gbar, 1);
     fence_barrier_init();
     const int n = cnt0 < rows_per_chunk ? cnt0 : rows_per_chunk;
@@ -268,15 +274,10 @@ __global__ void __launch_bounds__(kSel2Threads) refresh_select_gather_age_kernel
     }
   }
   SEL_TS(2);
-  if (tid == 0) {   // publish this CTA's count
-    a.blk[b] = s_cnt;
-    fence_acq_rel_gpu();
-    atomicAdd(a.blk + G, 1);
-  }
   // rows that are not due age in place and (fused projection) enter the histogram now
   int nh = 0;
   if (r < a.R && !f) {
-    const int aged = a.nhat_last[r] - (g - gl);   // reading A27
+    const int aged = nl - (g - gl);   // reading A27
     nh = aged > 0 ? aged : 0;
     a.n_hat[r] = nh;
   }
@@ -285,7 +286,6 @@ __global__ void __launch_bounds__(kSel2Threads) refresh_select_gather_age_kernel
     // warp (match_any) into a shared histogram, then one global add per non-empty bin per CTA
     uint32_t errbits = 0;
     const bool valid = r < a.R && !f;
-    const int32_t ins = valid ? a.pa.inst[r] : 0, nt = valid ? a.n_tok[r] : 0;
     if (shist)
       proj_accumulate<true>(a.pa, valid, ins, nt, nh, s_hc, s_sum, errbits);
     else
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kSel2Threads) refresh_select_gather_age_kernel
   const int base = s_base, cnt = s_cnt;
   if (f) {
     a.idx[base + lp] = r;
-    a.ntok_c[base + lp] = a.n_tok ? a.n_tok[r] : 0;
+    a.ntok_c[base + lp] = nt;
   }
   // gather, part 2: each chunk of staged rows goes out to its compacted position (bulk stores);
   // the next chunk (more due rows than shared memory holds) streams in after the stores read it
