@@ -35,8 +35,10 @@
 namespace star {
 
 struct SmallArgs {
-  int M;                 // rows (<= 512)
+  int M;                 // rows (<= 512 per chunk)
   int kb1;               // layer-1 K blocks (d / 64), even
+  int n1;                // layer-1 tile width: 128 (3-4 m-tiles), 64 (2), 32 (1): always 2048 / n1 column
+                         // tiles x m-tiles x 2 K halves = 128 CTAs
   const float* b1;       // [2048] or nullptr
   const float* b2;       // [512] or nullptr
   const float* b3;       // [64] or nullptr
@@ -75,7 +77,7 @@ struct SmallSmem {
   static constexpr uint32_t BAR = 200u * 1024u;
   static constexpr uint32_t BYTES = 1024u + BAR + 256u;
   static constexpr uint32_t HIST = 0;                     // finalize: histogram staging (ring idle), <= 96 KB
-  static constexpr int DONE = 16 * 64;                    // index of the completion counter in cnt (<= 64 chunks)
+  static constexpr int DONE = 16 * 256;                   // index of the completion counter in cnt (<= 256 chunks)
 };
 static_assert(SmallSmem::BYTES <= 227u * 1024u, "small predictor smem");
 
@@ -183,7 +185,6 @@ __global__ void __launch_bounds__(192, 1)
                          const SmallArgs p) {
   using S = SmallSmem;
   constexpr int NS = S::STAGES;
-  constexpr uint32_t ID1 = umma_idesc(false, 128, 128);
   constexpr uint32_t ID2 = umma_idesc(false, 128, 32);
   constexpr uint32_t ID3 = umma_idesc(false, 128, 64);
   extern __shared__ uint8_t smem_raw[];
@@ -205,6 +206,7 @@ __global__ void __launch_bounds__(192, 1)
   int M = p.M;
   const bool dev_rows = p.M_dev != nullptr;   // refresh mode: the row count comes from the predecessor
   if (!dev_rows && m * 128 >= M) return;      // (the host sizes the grid to M)
+  const bool l2 = n < 16;                // layer 2 has 16 column tiles (32 wide) per m-tile
   const bool l3 = n == 0 && rank == 0;   // this CTA also runs layer 3 + head for its m-tile
   if (threadIdx.x == 0) {
     SMALL_TS(0);
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(192, 1)
     // the partner's bulk copies complete bytes on these: armed for the first chunk before the
     // barrier below; every later chunk's arm happens right after the previous chunk's data was
     // consumed (still before that chunk's cluster barrier, after which the partner pushes)
-    mbar_arrive_expect_tx(r1bar, 32768u);
+    mbar_arrive_expect_tx(r1bar, (uint32_t)p.n1 * 256u);   // the partner's n1/2 columns x 128 rows x 4 B
     mbar_arrive_expect_tx(r2bar, 8192u);
     fence_barrier_init();
   }
@@ -248,6 +250,9 @@ __global__ void __launch_bounds__(192, 1)
   pdl_launch_dependents();
 
   const int kh = p.kb1 / 2;            // layer-1 K blocks of this split
+  const int N1 = p.n1, half1 = N1 / 2;  // layer-1 tile width; each CTA of the pair owns half of it
+  const uint32_t l1_stage = 16384u + (uint32_t)N1 * 128u, l1_xchg = (uint32_t)half1 * 512u;
+  const uint32_t ID1 = umma_idesc(false, 128, (uint32_t)N1);
   const int pre = kh < NS ? kh : NS;   // layer-1 W1 blocks issued before griddepcontrol.wait (PDL overlap)
   int pre_done = 0;
   if (dev_rows) {
@@ -256,10 +261,11 @@ __global__ void __launch_bounds__(192, 1)
       if (elect_one()) {
         const uint64_t pol_b = policy_evict_last();
         for (int i = 0; i < pre; ++i) {
-          mbar_arrive_expect_tx(&full[i], 32768u);
-          tma_load_2d(smem + S::B0 + 16384 * i, &tmW1, &full[i], (rank * kh + i) * 64, n * 128, pol_b);
+          mbar_arrive_expect_tx(&full[i], l1_stage);
+          tma_load_2d(smem + S::B0 + 16384 * i, &tmW1, &full[i], (rank * kh + i) * 64, n * N1, pol_b);
         }
-        for (int i = 0; i < 16; ++i) tma_prefetch_2d(&tmW2, rank * 1024 + i * 64, n * 32);
+        if (n < 16)
+          for (int i = 0; i < 16; ++i) tma_prefetch_2d(&tmW2, rank * 1024 + i * 64, n * 32);
       }
       __syncwarp();
     }
@@ -293,21 +299,23 @@ __global__ void __launch_bounds__(192, 1)
   }
   // rows are processed in chunks of 512 (4 m-tiles): one chunk unless a refresh step has more
   // due rows; chunk c's m-tile m covers rows [512 c + 128 m, +128)
-  const int nchunks = (M + 511) / 512;
+  const int chunk_rows = 128 * (int)gridDim.z;   // rows per chunk: the grid's m-tiles
+  const int nchunks = (M + chunk_rows - 1) / chunk_rows;
   const int total_mt = (M + 127) / 128;     // m-tiles over all chunks (= layer-3 completions)
   const int q = warp & 3;
   const int row = q * 32 + lane;       // row of the tile (epilogue warps)
   const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
   // TMEM columns: L1 [0, 128), L2 [128, 160), L3 [160, 224)
-  const int per_chunk = kh + 16 + (l3 ? 8 : 0);   // ring iterations of one chunk (stage = it % NS)
+  const int per_chunk = kh + (l2 ? 16 : 0) + (l3 ? 8 : 0);   // ring iterations of one chunk (stage = it % NS)
   int act = 0;                                     // chunks this CTA has processed (barrier parity)
 
   for (int chunk = 0; chunk < nchunks; ++chunk) {
-    const int row0 = chunk * 512 + m * 128;   // first row of this CTA's m-tile in this chunk
+    const int row0 = chunk * chunk_rows + m * 128;   // first row of this CTA's m-tile in this chunk
     if (row0 >= M) break;                     // CTA-uniform (and cluster-uniform: same m)
     const int grow = row0 + row;
+    const bool more = chunk + 1 < nchunks && row0 + chunk_rows < M;   // this CTA runs another chunk
     const uint32_t par = (uint32_t)act & 1u;
-    const int it1 = act * per_chunk, it2 = it1 + kh, it3 = it2 + 16;
+    const int it1 = act * per_chunk, it2 = it1 + kh, it3 = it2 + (l2 ? 16 : 0);
     int* z1_cnt = p.cnt + chunk * 16;        // [4][2]: Z1 column halves published
     int* z2_cnt = p.cnt + chunk * 16 + 8;    // [4]
 
@@ -318,11 +326,12 @@ __global__ void __launch_bounds__(192, 1)
         for (int i = (act == 0 ? pre_done : 0); i < pre; ++i) {   // W1 blocks before griddepcontrol.wait
           const int it = it1 + i, s = it % NS;
           mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
-          mbar_arrive_expect_tx(&full[s], 32768u);
-          tma_load_2d(smem + S::B0 + 16384 * s, &tmW1, &full[s], (rank * kh + i) * 64, n * 128, pol_b);
+          mbar_arrive_expect_tx(&full[s], l1_stage);
+          tma_load_2d(smem + S::B0 + 16384 * s, &tmW1, &full[s], (rank * kh + i) * 64, n * N1, pol_b);
         }
         if (act == 0 && !pre_done) {
-          for (int i = 0; i < 16; ++i) tma_prefetch_2d(&tmW2, rank * 1024 + i * 64, n * 32);   // into L2 early
+          if (l2)
+            for (int i = 0; i < 16; ++i) tma_prefetch_2d(&tmW2, rank * 1024 + i * 64, n * 32);   // into L2 early
           pdl_wait();
           SMALL_TS(2);
         }
@@ -330,8 +339,8 @@ __global__ void __launch_bounds__(192, 1)
           const int it = it1 + i, s = it % NS;
           if (i >= pre) {
             mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
-            mbar_arrive_expect_tx(&full[s], 32768u);
-            tma_load_2d(smem + S::B0 + 16384 * s, &tmW1, &full[s], (rank * kh + i) * 64, n * 128, pol_b);
+            mbar_arrive_expect_tx(&full[s], l1_stage);
+            tma_load_2d(smem + S::B0 + 16384 * s, &tmW1, &full[s], (rank * kh + i) * 64, n * N1, pol_b);
           }
           tma_load_2d(smem + 16384 * s, &tmH, &full[s], (rank * kh + i) * 64, row0, pol_a);
         }
@@ -359,7 +368,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(acc1, par);
       tc_fence_after();
       if (te == 0) SMALL_TS(3);
-      tmem_to_block(trow, 64 * partner, 64, reinterpret_cast<float*>(smem + S::L1_SEND), row);
+      tmem_to_block(trow, half1 * partner, half1, reinterpret_cast<float*>(smem + S::L1_SEND), row);
       fence_proxy_async_smem();   // generic smem writes -> the bulk copy (async proxy)
     }
     // the partner's ring is free (its layer-1 MMAs completed) and its send block is staged
@@ -370,7 +379,7 @@ __global__ void __launch_bounds__(192, 1)
     // ============================ phase B: layer-1 reduce, layer 2, layer 3 ============================
     if (warp == 0) {
       asm volatile("bar.sync 2, 160;" ::: "memory");   // the epilogue released the ring
-      if (elect_one()) {
+      if (l2 && elect_one()) {
         const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
         // layer 2: W2 blocks first (independent), the Z1 blocks once their half is published
         for (int i = 0; i < NS; ++i) {
@@ -379,7 +388,7 @@ __global__ void __launch_bounds__(192, 1)
           mbar_arrive_expect_tx(&full[s], 16384u + 4096u);
           tma_load_2d(smem + S::B0 + 16384 * s, &tmW2, &full[s], rank * 1024 + i * 64, n * 32, pol_b);
         }
-        spin_wait_geq(z1_cnt + m * 2 + rank, 16);
+        spin_wait_geq(z1_cnt + m * 2 + rank, 2048 / N1);   // every n-tile pair of this K half
         fence_proxy_async_global();
         SMALL_TS(5);
         for (int i = 0; i < 16; ++i) {
@@ -413,7 +422,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       __syncwarp();
     } else if (warp == 1) {
-      if (elect_one()) {
+      if (l2 && elect_one()) {   // (l3 implies l2)
         for (int i = 0; i < 16; ++i) {
           const int it = it2 + i, s = it % NS;
           mbar_wait(&full[s], (uint32_t)(it / NS) & 1u);
@@ -446,41 +455,38 @@ __global__ void __launch_bounds__(192, 1)
       // ---- layer-1 split-K: push the staged block into the partner, reduce the owned 64 columns ----
       if (te == 0) {
         SMALL_TS(4);
-        bulk_s2cluster(mapa_shared(smem_u32(smem + S::L1_RECV), (uint32_t)partner), smem + S::L1_SEND, 32768u,
+        bulk_s2cluster(mapa_shared(smem_u32(smem + S::L1_RECV), (uint32_t)partner), smem + S::L1_SEND, l1_xchg,
                        mapa_shared(smem_u32(r1bar), (uint32_t)partner));
         bulk_commit();
       }
       mbar_wait(r1bar, par);
       if (te == 0) SMALL_TS(12);
-      const bool more = chunk + 1 < nchunks && row0 + 512 < M;   // this CTA runs another chunk
       const float* recv = reinterpret_cast<const float*>(smem + S::L1_RECV);
-      uint32_t w[4][8];
-#pragma unroll
-      for (int c = 0; c < 64; c += 16) {
+#pragma unroll 1
+      for (int c = 0; c < half1; c += 16) {   // the row's owned columns, 16 (32 bytes) at a time
         float f[16];
-        reduce16(trow, 64 * rank + c, recv, c, rank, row, f);
-        relu_bf16_16(f, p.b1, n * 128 + 64 * rank + c, w[c / 16]);
-      }
-      if (grow < M) {   // the row's 64 owned columns: 128 contiguous bytes
-        uint4* d = reinterpret_cast<uint4*>(p.Z1 + (int64_t)grow * 2048 + n * 128 + 64 * rank);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          d[2 * c] = make_uint4(w[c][0], w[c][1], w[c][2], w[c][3]);
-          d[2 * c + 1] = make_uint4(w[c][4], w[c][5], w[c][6], w[c][7]);
+        uint32_t w[8];
+        reduce16(trow, half1 * rank + c, recv, c, rank, row, f);
+        relu_bf16_16(f, p.b1, n * N1 + half1 * rank + c, w);
+        if (grow < M) {
+          uint4* d = reinterpret_cast<uint4*>(p.Z1 + (int64_t)grow * 2048 + n * N1 + half1 * rank + c);
+          d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          d[1] = make_uint4(w[4], w[5], w[6], w[7]);
         }
       }
       if (te == 0) SMALL_TS(13);
       asm volatile("bar.sync 1, 128;" ::: "memory");   // every thread has read the received block
-      if (te == 0 && more) mbar_arrive_expect_tx(r1bar, 32768u);   // armed for the next chunk
+      if (te == 0 && more) mbar_arrive_expect_tx(r1bar, l1_xchg);   // armed for the next chunk
       if (te == 0) bulk_wait_read_all();   // the send block was read: the ring may be reused
       fence_proxy_async_global();          // Z1 (generic stores) -> the layer-2 TMA loads (async proxy)
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (te == 0) {
-        red_release_add(z1_cnt + m * 2 + n / 8, 1);
+        red_release_add(z1_cnt + m * 2 + (n * N1) / 1024, 1);
         SMALL_TS(6);
       }
       asm volatile("bar.sync 2, 160;" ::: "memory");   // the producer may refill the ring
-
+    }
+    if (l2 && warp >= 2) {
       // ---- layer 2: reduce the owned 16 columns of the 128 x 32 tile ----
       mbar_wait(acc2, par);
       tc_fence_after();

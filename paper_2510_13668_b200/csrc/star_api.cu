@@ -314,6 +314,7 @@ static bool small_path_available() {
 }
 
 struct SmallRefresh {   // refresh mode: the compacted batch and the slots it scatters into
+  int rows_expected;      // sizes the grid (the count itself is on the device)
   const int32_t* M_dev;
   const int32_t* idx;
   const int32_t* gen;
@@ -423,6 +424,7 @@ struct star_predictor {
   // one-launch predictor for <= 512 rows (lenpred_small.cuh)
   CUtensorMap tmW2s;          // W2 with 32-row boxes
   CUtensorMap tmW2t;          // W2 with 128-row boxes (tail2)
+  CUtensorMap tmW1n[2];       // W1 with 32- / 64-row boxes (the small-batch kernel's narrow layer-1 tiles)
   int* tail2_done = nullptr;  // tail2: m-tiles finished (zero between launches)
   int* small_cnt = nullptr;   // its phase counters (zero between launches)
   int* r_blk = nullptr;       // refresh: the multi-CTA select's counts and counters (zero between launches)
@@ -572,7 +574,9 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
   }
   if (!f32 && m1 == 2048 && m2 == 512 && d % 256 == 0) {
     if ((st = make_tmap(&p->tmW2s, W2, false, (uint64_t)m1, m2, (uint64_t)m1 * 2, 32)) != STAR_OK ||
-        (st = make_tmap(&p->tmW2t, W2, false, (uint64_t)m1, m2, (uint64_t)m1 * 2, 128)) != STAR_OK) {
+        (st = make_tmap(&p->tmW2t, W2, false, (uint64_t)m1, m2, (uint64_t)m1 * 2, 128)) != STAR_OK ||
+        (st = make_tmap(&p->tmW1n[0], W1, false, (uint64_t)d, m1, (uint64_t)d * 2, 32)) != STAR_OK ||
+        (st = make_tmap(&p->tmW1n[1], W1, false, (uint64_t)d, m1, (uint64_t)d * 2, 64)) != STAR_OK) {
       free_pred(p);
       return st;
     }
@@ -1003,7 +1007,7 @@ static star_status refresh_impl(star_predictor* p, const void* h, int64_t ld_h, 
                                          p->r_ntok, p->r_h, n_hat, p->r_M, n_refreshed, p->r_blk, proj, st, p->tl)) !=
         cudaSuccess)
       return cuda_fail(e, "refresh select launch");
-    SmallRefresh rf{p->r_M, p->r_idx, gen, g_last, nhat_last, n_hat};
+    SmallRefresh rf{(R + k - 1) / k, p->r_M, p->r_idx, gen, g_last, nhat_last, n_hat};
     if ((e = launch_small(p, R, n_tok ? p->r_ntok : nullptr, max_ctx_len, nullptr, nullptr, proj, st, &p->tmA_r,
                           &rf)) != cudaSuccess)
       return cuda_fail(e, "refresh small-batch launch");
@@ -1335,9 +1339,16 @@ static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, 
   a.project = proj ? 1 : 0;
   if (proj) a.pa = *proj;
   a.tl = p->tl;   // diagnostics (star_predictor_timeline): [CTAs][32] phase stamps
-  if (p->tl) p->tl_ctas = 2 * 16 * ((R + 127) / 128);
+  if (p->tl) p->tl_ctas = 128;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2, 16, (R < 512 ? R + 127 : 512 + 127) / 128);
+  // 128 CTAs whatever the row count: 1 m-tile -> 32-column layer-1 tiles (64 per m-tile), 2 -> 64,
+  // 3-4 -> 128 (refresh: sized for the expected due rows; more rows run in further chunks)
+  const int rows = rf ? (rf->rows_expected < R ? rf->rows_expected : R) : R;
+  int mt = (rows + 127) / 128;
+  mt = mt < 1 ? 1 : (mt > 4 ? 4 : mt);
+  const int n1 = mt == 1 ? 32 : (mt == 2 ? 64 : 128);
+  a.n1 = n1;
+  cfg.gridDim = dim3(2, 2048 / n1, mt);
   cfg.blockDim = dim3(192, 1, 1);
   cfg.dynamicSmemBytes = SmallSmem::BYTES;
   cfg.stream = st;
@@ -1350,7 +1361,8 @@ static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, 
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, lenpred_small_kernel, tmH ? *tmH : p->tmA1, p->tmB1p, p->tmA2, p->tmW2s, p->tmA3,
+  const CUtensorMap& tmW1 = n1 == 32 ? p->tmW1n[0] : (n1 == 64 ? p->tmW1n[1] : p->tmB1p);
+  return cudaLaunchKernelEx(&cfg, lenpred_small_kernel, tmH ? *tmH : p->tmA1, tmW1, p->tmA2, p->tmW2s, p->tmA3,
                             p->tmB3, a);
 }
 }  // namespace star
