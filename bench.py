@@ -617,7 +617,7 @@ def run_star(args):
             es[3].synchronize()
             acc += [es[k].elapsed_time(es[k + 1]) * 1e3 / nrep for k in range(3)]
         stage = {"predict+project": round(acc[0], 2), "allgather": round(acc[1], 2), "plan": round(acc[2], 2),
-                 "layer1_gemm": round(l1_avg_ms * 1e3, 2),
+                 ("predictor_launch" if pred.path(R) else "layer1_gemm"): round(l1_avg_ms * 1e3, 2),
                  "note": "event nodes between stages (each costs a few us and blocks PDL overlap); "
                          "the sum exceeds us_per_step"}
 
@@ -693,7 +693,8 @@ def run_star(args):
 
     # ---- roofline: the layer-1 tcgen05 GEMM (dominant kernel), timed live inside the step ----
     peaks = load_peaks()
-    small_path = R <= 512 and pred.path(R) == 1
+    path = pred.path(R) if R >= 1 else 0
+    small_path = path in (1, 2)   # one-launch predictor (bf16 <= 512 rows / fp32 <= 128 rows)
     # the timed launch: layer 1 alone (2 R d m1), or the whole one-launch predictor (2 R (d m1 + m1 m2 + m2 m3 + m3))
     flops_l1 = 2.0 * R * (c["d"] * 2048 + (2048 * 512 + 512 * 64 + 64 if small_path else 0))
     achieved = flops_l1 / (l1_avg_ms / 1e3) / 1e12
@@ -701,8 +702,7 @@ def run_star(args):
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(f"{args.config}/w{world}/" + ("small" if R <= 512 and pred.path(R) == 1
-                                                                       else "layer1"))
+            traffic = json.load(f).get(f"{args.config}/w{world}/" + ("small" if small_path else "layer1"))
     m_tiles = (R + 127) // 128
     pair = c["dtype"] == "bf16" and (m_tiles == 2 or (m_tiles + 1) // 2 * 2 * 8 >= 148 * 5 // 8)
     # the contraction's own dtype: bf16 at its measured peak; fp32 runs as 3xTF32 (three tcgen05 kind::tf32
@@ -710,7 +710,9 @@ def run_star(args):
     f32 = c["dtype"] == "f32"
     peak = peaks["bf16_tflops"] * (0.5 if f32 else 1.0)
     small = small_path
-    kname = ("lenpred_small_kernel (one launch: layers 1-3, head, projection; events around the whole launch)"
+    kname = ("lenpred_f32_kernel (one launch: 3xTF32 layers 1-3 with the A operand split into TMEM, head, "
+             "quantizer, projection; events around the whole launch)" if path == 2 else
+             "lenpred_small_kernel (one launch: layers 1-3, head, projection; events around the whole launch)"
              if small else ("umma_pair_gemm_kernel<256> (tcgen05 cta_group::2 + TMA)" if pair else
                             "umma_gemm_kernel (tcgen05 + TMA, cluster split-K)") + " = predictor layer 1")
     roofline = {"kernel": kname,

@@ -188,7 +188,8 @@ class Predictor:
         return float(ms.value)
 
     def path(self, R: int) -> int:
-        """1 if a forward of R rows runs the one-launch small-batch kernel, else 0 (star.h)."""
+        """1 if a forward of R rows runs the one-launch small-batch (bf16) kernel, 2 the one-launch fp32
+        kernel, else 0 (star.h)."""
         v = C.c_int()
         _check(lib().star_predictor_path(self.handle, int(R), C.byref(v)), "star_predictor_path")
         return int(v.value)

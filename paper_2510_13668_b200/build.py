@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(HERE, "libstar.so")
 SOURCES = ["star_api.cu", "project.cu", "plan.cu", "plan_large.cu", "dispatch.cu", "refresh.cu", "migrate.cu"]
-HEADERS = ["ptx.cuh", "lenpred_kernels.cuh", "lenpred_tail.cuh", "lenpred_small.cuh", "lenpred_tail2.cuh", "project_core.cuh", "plan_core.cuh", "plan_fast.cuh", "star_internal.h"]
+HEADERS = ["ptx.cuh", "lenpred_kernels.cuh", "lenpred_tail.cuh", "lenpred_small.cuh", "lenpred_f32.cuh", "lenpred_tail2.cuh", "project_core.cuh", "plan_core.cuh", "plan_fast.cuh", "star_internal.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

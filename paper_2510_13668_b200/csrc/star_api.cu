@@ -13,6 +13,7 @@
 #include <string>
 #include <tuple>
 
+#include "lenpred_f32.cuh"
 #include "lenpred_kernels.cuh"
 #include "lenpred_small.cuh"
 #include "lenpred_tail.cuh"
@@ -313,6 +314,25 @@ static bool small_path_available() {
   return ncl >= 64;
 }
 
+// The one-launch fp32 predictor (lenpred_f32.cuh, <= 128 rows) needs its 128 CTAs (~161 KB of
+// shared memory, 512 TMEM columns each) resident at once.  STAR_F32_SMALL=0 disables it (A/B measurements).
+static bool f32_small_available() {
+  const char* e = getenv("STAR_F32_SMALL");
+  if (e && atoi(e) == 0) return false;
+  if (func_attr((const void*)lenpred_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                (int)F32Smem::BYTES) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lenpred_f32_kernel, 192, F32Smem::BYTES) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return per_sm >= 1 && per_sm * g_num_sms >= 128;
+}
+
 struct SmallRefresh {   // refresh mode: the compacted batch and the slots it scatters into
   int rows_expected;      // sizes the grid (the count itself is on the device)
   const int32_t* M_dev;
@@ -325,6 +345,8 @@ struct SmallRefresh {   // refresh mode: the compacted batch and the slots it sc
 static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, int32_t max_ctx, float* y_hat,
                                 int32_t* n_hat, const ProjArgs* proj, cudaStream_t st,
                                 const CUtensorMap* tmH = nullptr, const SmallRefresh* rf = nullptr);
+static cudaError_t launch_f32_small(star_predictor* p, int R, const int32_t* n_tok, int32_t max_ctx, float* y_hat,
+                                    int32_t* n_hat, const ProjArgs* proj, cudaStream_t st);
 
 // The large-batch tail: clusters of 4 per m-tile (lenpred_tail2.cuh); STAR_TAIL2=0 selects the
 // round-1 split-K tail (A/B measurements).
@@ -430,6 +452,14 @@ struct star_predictor {
   int* r_blk = nullptr;       // refresh: the multi-CTA select's counts and counters (zero between launches)
   bool small_ok = false;      // shape supported and 32 clusters of 4 co-resident
   uint64_t* tl_small = nullptr;
+  // one-launch fp32 predictor for <= 128 rows (lenpred_f32.cuh): raw fp32 operand maps
+  CUtensorMap tmHf, tmW1f, tmW2f, tmW3f, tmZ1f, tmZ2f;
+  int* f32_cnt = nullptr;     // its arrival counters (zero between launches)
+  float *W1p = nullptr, *W2p = nullptr, *W3p = nullptr;   // its weights as [hi; lo] tf32 planes
+  bool f32_ok = false;
+  const void* last_hf = nullptr;
+  int64_t last_ldf = 0;
+  int last_Rf = -1;
   const void* last_h = nullptr;
   int64_t last_ld = 0;
   int last_R = -1;
@@ -459,6 +489,10 @@ static void free_pred(star_predictor* p) {
   cudaFree(p->tl);
   cudaFree(p->tl_l1);
   cudaFree(p->small_cnt);
+  cudaFree(p->f32_cnt);
+  cudaFree(p->W1p);
+  cudaFree(p->W2p);
+  cudaFree(p->W3p);
   cudaFree(p->r_blk);
   cudaFree(p->tail2_done);
   cudaFree(p->tl_small);
@@ -572,6 +606,38 @@ star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, i
     free_pred(p);
     return st;
   }
+  if (f32 && m1 == 2048 && m2 == 512 && d % 128 == 0 && p->ws_floats >= (size_t)F32_WS_FLOATS) {
+    const size_t n1 = (size_t)m1 * d, n2 = (size_t)m2 * m1, n3 = (size_t)m3 * m2;
+    if (cudaMalloc(reinterpret_cast<void**>(&p->W1p), 2 * n1 * 4) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void**>(&p->W2p), 2 * n2 * 4) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void**>(&p->W3p), 2 * n3 * 4) != cudaSuccess) {
+      cudaGetLastError();
+      free_pred(p);
+      return fail(STAR_ENOMEM, "device allocation failed");
+    }
+    tf32_planes_kernel<<<1024, 256, 0, stream>>>(static_cast<const float*>(W1), (int64_t)n1, p->W1p);
+    tf32_planes_kernel<<<512, 256, 0, stream>>>(static_cast<const float*>(W2), (int64_t)n2, p->W2p);
+    tf32_planes_kernel<<<64, 256, 0, stream>>>(static_cast<const float*>(W3), (int64_t)n3, p->W3p);
+    if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess) {
+      free_pred(p);
+      return cuda_fail(e, "tf32_planes_kernel");
+    }
+    if ((st = make_tmap(&p->tmW1f, p->W1p, true, (uint64_t)d, 2 * m1, (uint64_t)d * 4, 64)) != STAR_OK ||
+        (st = make_tmap(&p->tmW2f, p->W2p, true, (uint64_t)m1, 2 * m2, (uint64_t)m1 * 4, 32)) != STAR_OK ||
+        (st = make_tmap(&p->tmW3f, p->W3p, true, (uint64_t)m2, 2 * m3, (uint64_t)m2 * 4, 64)) != STAR_OK ||
+        (st = make_tmap(&p->tmZ1f, p->Z1, true, (uint64_t)m1, max_rows, (uint64_t)m1 * 4, 128)) != STAR_OK ||
+        (st = make_tmap(&p->tmZ2f, p->Z2, true, (uint64_t)m2, max_rows, (uint64_t)m2 * 4, 128)) != STAR_OK) {
+      free_pred(p);
+      return st;
+    }
+    p->f32_ok = f32_small_available();
+    if (p->f32_ok && (cudaMalloc(reinterpret_cast<void**>(&p->f32_cnt), F32Cnt::N * sizeof(int)) != cudaSuccess ||
+                      cudaMemset(p->f32_cnt, 0, F32Cnt::N * sizeof(int)) != cudaSuccess)) {
+      cudaGetLastError();
+      free_pred(p);
+      return fail(STAR_ENOMEM, "device allocation failed");
+    }
+  }
   if (!f32 && m1 == 2048 && m2 == 512 && d % 256 == 0) {
     if ((st = make_tmap(&p->tmW2s, W2, false, (uint64_t)m1, m2, (uint64_t)m1 * 2, 32)) != STAR_OK ||
         (st = make_tmap(&p->tmW2t, W2, false, (uint64_t)m1, m2, (uint64_t)m1 * 2, 128)) != STAR_OK ||
@@ -663,7 +729,7 @@ star_status star_predictor_timeline(star_predictor* p, int enable, uint64_t* hos
 
 star_status star_predictor_path(star_predictor* p, int R, int* path) {
   if (!p || !path) return fail(STAR_EINVAL, "predictor / path is NULL");
-  *path = (!p->f32 && p->small_ok && R >= 1 && R <= 512) ? 1 : 0;
+  *path = (!p->f32 && p->small_ok && R >= 1 && R <= 512) ? 1 : ((p->f32 && p->f32_ok && R >= 1 && R <= 128) ? 2 : 0);
   return STAR_OK;
 }
 
@@ -689,6 +755,21 @@ static star_status forward_impl(star_predictor* p, const void* h, int64_t ld_h, 
   const bool f32 = p->f32;
   const int kx = f32 ? 3 : 1;
   const int m_tiles = (R + 127) / 128;
+  if (f32 && p->f32_ok && R >= 1 && R <= 128 &&
+      (!proj || (size_t)proj->n_inst * (proj->H + 2) * 12 + (size_t)(proj->H + 1) * 4 <= F32Smem::HIST_MAX)) {
+    // one launch: Eq. 2 in 3xTF32 + quantizer (+ projection)
+    if (h != p->last_hf || ld_h != p->last_ldf || R != p->last_Rf) {
+      if ((s = make_tmap(&p->tmHf, h, true, p->d, R, (uint64_t)ld_h * 4, 128)) != STAR_OK) return s;
+      p->last_hf = h;
+      p->last_ldf = ld_h;
+      p->last_Rf = R;
+    }
+    if (p->ev0) record_timing_event(p->ev0, st);
+    cudaError_t e = launch_f32_small(p, R, n_tok, max_ctx_len, y_hat, n_hat, proj, st);
+    if (e != cudaSuccess) return cuda_fail(e, "lenpred_f32_kernel launch");
+    if (p->ev1) record_timing_event(p->ev1, st);
+    return STAR_OK;
+  }
   if (f32) {
     const int64_t total = (int64_t)R * p->d;
     int blocks = (int)((total + 255) / 256);
@@ -1364,5 +1445,43 @@ static cudaError_t launch_small(star_predictor* p, int R, const int32_t* n_tok, 
   const CUtensorMap& tmW1 = n1 == 32 ? p->tmW1n[0] : (n1 == 64 ? p->tmW1n[1] : p->tmB1p);
   return cudaLaunchKernelEx(&cfg, lenpred_small_kernel, tmH ? *tmH : p->tmA1, tmW1, p->tmA2, p->tmW2s, p->tmA3,
                             p->tmB3, a);
+}
+
+static cudaError_t launch_f32_small(star_predictor* p, int R, const int32_t* n_tok, int32_t max_ctx, float* y_hat,
+                                    int32_t* n_hat, const ProjArgs* proj, cudaStream_t st) {
+  F32Args a{};
+  a.M = R;
+  a.kb1 = p->d / 32;
+  a.b1 = p->b1;
+  a.b2 = p->b2;
+  a.b3 = p->b3;
+  a.w4 = p->w4;
+  a.b4 = p->b4;
+  a.n_tok = n_tok;
+  a.max_ctx = max_ctx;
+  a.y_hat = y_hat;
+  a.n_hat = n_hat;
+  a.Z1 = static_cast<float*>(p->Z1);
+  a.Z2 = static_cast<float*>(p->Z2);
+  a.P1 = p->ws;
+  a.P2 = a.P1 + 4 * 32 * 16 * 512;
+  a.P3 = a.P2 + 8 * 16 * 8 * 512;
+  a.yp = a.P3 + 4 * 16 * 512;
+  a.cnt = p->f32_cnt;
+  a.project = proj ? 1 : 0;
+  if (proj) a.pa = *proj;
+  a.tl = p->tl;   // diagnostics (star_predictor_timeline): [128][32] phase stamps
+  if (p->tl) p->tl_ctas = 128;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(128, 1, 1);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = F32Smem::BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, lenpred_f32_kernel, p->tmHf, p->tmW1f, p->tmZ1f, p->tmW2f, p->tmZ2f, p->tmW3f, a);
 }
 }  // namespace star

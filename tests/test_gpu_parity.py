@@ -724,3 +724,81 @@ def test_small_path_forward_project(star, oracle_mod, d, R, biases, n, ld_pad):
         assert np.array_equal(v, rp[k]), k
     assert err.item() == 0 and int(ws.sum().item()) == 0
     pred.close()
+
+
+# ============================================================================ one-launch fp32 predictor
+@pytest.mark.parametrize("d,R,biases,n,ld_pad,max_rows", [(896, 128, False, 2, 0, 128), (896, 64, True, 1, 0, 600),
+                                                          (128, 1, True, 1, 8, 1), (4096, 128, False, 8, 0, 256),
+                                                          (1024, 77, True, 3, 32, 77), (2048, 100, False, 200, 0, 128),
+                                                          (512, 5, False, 2, 0, 5)])
+def test_f32_small_path_forward_project(star, oracle_mod, d, R, biases, n, ld_pad, max_rows):
+    """The one-launch fp32 predictor (<= 128 rows: 3xTF32 layers 1-3 with the operands split in
+    shared memory, head, quantizer and the projection in one kernel; BASELINE configs[0] shape
+    first): every row within the fp32 tolerance of the fp64 oracle, N_hat == the oracle quantizer
+    of its y_hat, L/W/peak/growth/count == the oracle projection of that N_hat bit for bit;
+    repeated launches (counters re-armed) bit-identical, also with a row stride > d and
+    max_rows < 128 (TMA zero-fills the rows past the map)."""
+    pw = datagen.make_predictor_weights(d + R + 7, d, "f32", biases=biases)
+    snap = datagen.make_snapshot(R + n + 7, n, (R + n - 1) // n)
+    n_tok, inst = snap.n_tok[:R].copy(), snap.inst[:R].astype(np.int32)
+    scale = np.maximum(snap.true_rem[:R], 1).astype(np.float32) / 60.0
+    h = datagen.make_hidden(d + R + 7, R, d, "f32", scale=scale)
+    hpad = np.zeros((R, d + ld_pad), np.float32)
+    hpad[:, :d] = h
+    hd = _dev(hpad)[:, :d]
+    W, b = _weights_dev(pw, biases)
+    pred = star.Predictor(*W, *b, max_rows=max_rows)
+    assert pred.path(R) == 2
+    beta = datagen.beta_schedule_q16(50)
+    bq = _dev(beta.astype(np.int32))
+    ws = torch.zeros(star.project_workspace_bytes(n, 50), dtype=torch.uint8, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    runs = []
+    for _ in range(3):
+        y, nh, out = star.lenpred_forward_project(pred, hd, _dev(n_tok), _dev(inst), n, 50, bq, ws, err_flag=err)
+        torch.cuda.synchronize()
+        runs.append([y.cpu().numpy(), nh[:R].cpu().numpy()] +
+                    [getattr(out, k).cpu().numpy() for k in ("L", "W", "peak", "growth", "count")])
+    for r in runs[1:]:
+        for a_, b_ in zip(runs[0], r):
+            assert np.array_equal(a_, b_)
+    y, nh = runs[0][0], runs[0][1]
+    ref = oracle_mod.lenpred_weights(h, pw)
+    assert _rel_err(y, ref) <= TOL["f32"]
+    assert np.array_equal(nh, oracle_mod.quantize(y, n_tok))
+    rp = oracle_mod.project(inst, n_tok, nh, n, 50, beta)
+    for k, v in zip(("L", "W", "peak", "growth", "count"), runs[0][2:]):
+        assert np.array_equal(v, rp[k]), k
+    assert err.item() == 0
+    # the plain forward (no projection, no n_tok) through the same kernel
+    y2, nh2 = star.lenpred_forward(pred, hd)
+    torch.cuda.synchronize()
+    assert np.array_equal(y2.cpu().numpy(), y)
+    assert np.array_equal(nh2.cpu().numpy(), oracle_mod.quantize(y, None))
+    pred.close()
+
+
+def test_f32_small_path_many_instances_falls_back(star, oracle_mod):
+    """A projection histogram too large for the kernel's shared memory (600 instances x 52 bins)
+    runs the multi-launch fp32 path: same tolerance, projection bit-exact."""
+    d, R, n = 896, 128, 600
+    pw = datagen.make_predictor_weights(11, d, "f32")
+    snap = datagen.make_snapshot(12, n, 1)
+    idx = np.arange(R)
+    n_tok, inst = snap.n_tok[idx].copy(), snap.inst[idx].astype(np.int32)
+    h = datagen.make_hidden(13, R, d, "f32")
+    W, b = _weights_dev(pw)
+    pred = star.Predictor(*W, *b, max_rows=R)
+    beta = datagen.beta_schedule_q16(50)
+    ws = torch.zeros(star.project_workspace_bytes(n, 50), dtype=torch.uint8, device="cuda")
+    y, nh, out = star.lenpred_forward_project(pred, _dev(h), _dev(n_tok), _dev(inst), n, 50,
+                                              _dev(beta.astype(np.int32)), ws)
+    torch.cuda.synchronize()
+    y = y.cpu().numpy()
+    assert _rel_err(y, oracle_mod.lenpred_weights(h, pw)) <= TOL["f32"]
+    nh = nh[:R].cpu().numpy()
+    assert np.array_equal(nh, oracle_mod.quantize(y, n_tok))
+    rp = oracle_mod.project(inst, n_tok, nh, n, 50, beta)
+    for k in ("L", "W", "peak", "growth", "count"):
+        assert np.array_equal(getattr(out, k).cpu().numpy(), rp[k]), k
+    pred.close()
