@@ -21,14 +21,15 @@
 //       (deterministic), + b1, ReLU -> Z1 (fp32, L2-resident) and bumps z1_cnt[j1 / 4].
 //   L2  CTA c: Z2 columns [32 j2, +32) (j2 = c % 16) over Z1 columns [256 s2, +256) (s2 = c / 16:
 //       L1 n-tiles 4 s2 .. 4 s2 + 3, z1_cnt[s2] = 16), N=32; the W2 blocks are in flight before
-//       the wait.  Same partial / reduce: 8 splits, CTA (j2, s2) owns 4 columns -> Z2, z2_cnt[j2 / 4].
-//   L3  CTAs 0..3: Z3 (64 columns) over Z2 columns [128 s3, +128) (z2_cnt[s3] = 32), N=64 ->
-//       partial; CTA s3 adds columns [16 s3, +16) in split order, + b3, ReLU, the w4 dot over its
-//       16 columns (column order) -> y partial; the last of the four adds the y partials in order
-//       0..3, + b4, the quantizer (readings A8-A10), the rows' projection histogram in shared
+//       the wait.  Same partial / reduce: 8 splits, CTA (j2, s2) owns 4 columns -> Z2, z2_cnt[j2 / 2].
+//   L3  CTAs 0..7: Z3 (64 columns) over Z2 columns [64 s3, +64) (z2_cnt[s3] = 16), N=64 ->
+//       partial; CTA s3 adds columns [8 s3, +8) in split order, + b3, ReLU, the w4 dot over its
+//       8 columns (column order) -> y partial; the last of the eight adds the y partials in order
+//       0..7, + b4, the quantizer (readings A8-A10), the rows' projection histogram in shared
 //       memory, the finalize (L/W/peak/growth/count), and re-arms every counter.
-// Roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer (one elected lane), warps 2-5
-// operand splitting during the mainloops and the epilogues (TMEM lane quarter = warp % 4).
+// Roles (320 threads): warp 0 TMA producer, warp 1 MMA issuer (one elected lane), warps 2-9 the
+// operand split (warps 2-5 columns 0-15 of each block, 6-9 columns 16-31; TMEM lane quarter =
+// warp % 4), warps 2-5 the epilogues.
 #pragma once
 #include "lenpred_kernels.cuh"
 #include "project_core.cuh"
@@ -51,8 +52,8 @@ struct F32Args {
   float* Z2;             // [>= M][512]
   float* P1;             // [4][32][16][128][4] layer-1 partials
   float* P2;             // [8][16][8][128][4]
-  float* P3;             // [4][16][128][4]
-  float* yp;             // [4][128]
+  float* P3;             // [8][16][128][4]
+  float* yp;             // [8][128]
   int* cnt;              // F32Cnt counters (all zero between launches)
   int project;           // fused projection (histogram in shared memory)
   ProjArgs pa;
@@ -60,10 +61,10 @@ struct F32Args {
 };
 
 // scratch floats: P1 + P2 + P3 + y partials
-constexpr int F32_WS_FLOATS = 4 * 32 * 16 * 512 + 8 * 16 * 8 * 512 + 4 * 16 * 512 + 4 * 128;
+constexpr int F32_WS_FLOATS = 4 * 32 * 16 * 512 + 8 * 16 * 8 * 512 + 8 * 16 * 512 + 8 * 128;
 
 struct F32Cnt {
-  static constexpr int P1 = 0, Z1 = 32, P2 = 40, Z2 = 56, P3 = 60, Y = 61, N = 64;
+  static constexpr int P1 = 0, Z1 = 32, P2 = 40, Z2 = 56, P3 = 64, Y = 65, N = 72;
 };
 
 struct F32Smem {
@@ -119,6 +120,14 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
       "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // D[tmem] (+)= A[tmem] . B[smem]^T, kind::tf32 (A: M rows in TMEM lanes, one element per column).
@@ -132,12 +141,13 @@ __device__ __forceinline__ void umma_ts_tf32(uint32_t d_tmem, uint32_t a_tmem, u
       : "memory");
 }
 
-// One phase's operand split, epilogue threads (row = TMEM lane): for every landed stage, read
-// this row's 32 fp32 of the A block (SW128: 16-byte chunk c of row r sits at c ^ (r & 7)), split
-// into hi = rna_tf32(x) and lo = x - hi, write both into the stage's TMEM A slot, signal the MMA
-// warp.  `it0` = ring iterations before this phase (stage = it % NS), nkb K blocks of 32.
+// One phase's operand split, 8 warps (row = TMEM lane, `half` = which 16 of the block's 32
+// columns): for every landed stage, read this row's 16 fp32 of the A block (SW128: 16-byte chunk
+// c of row r sits at c ^ (r & 7)), split into hi = rna_tf32(x) and lo = x - hi, write both into
+// the stage's TMEM A slot, signal the MMA warp.  `it0` = ring iterations before this phase
+// (stage = it % NS), nkb K blocks of 32.
 __device__ __forceinline__ void f32_convert(const uint8_t* smem, uint64_t* full, uint64_t* conv, int it0, int nkb,
-                                            int row, uint32_t trow, int lane, long long* dbg) {
+                                            int row, int half, uint32_t trow, int lane, long long* dbg) {
   using S = F32Smem;
   for (int i = 0; i < nkb; ++i) {
     const int it = it0 + i, s = it % S::STAGES;
@@ -145,12 +155,12 @@ __device__ __forceinline__ void f32_convert(const uint8_t* smem, uint64_t* full,
     mbar_wait(&full[s], (uint32_t)(it / S::STAGES) & 1u);
     const long long t1 = clock64();
     const uint8_t* rp = smem + S::STAGE * s + S::A_RAW + row * 128;
-    float4 x[8];
+    float4 x[4];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) x[c] = *reinterpret_cast<const float4*>(rp + ((c ^ (row & 7)) << 4));
-    uint32_t hi[32], lo[32];
+    for (int c = 0; c < 4; ++c) x[c] = *reinterpret_cast<const float4*>(rp + (((4 * half + c) ^ (row & 7)) << 4));
+    uint32_t hi[16], lo[16];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < 4; ++c) {
       const float v[4] = {x[c].x, x[c].y, x[c].z, x[c].w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -159,9 +169,9 @@ __device__ __forceinline__ void f32_convert(const uint8_t* smem, uint64_t* full,
         lo[4 * c + e] = __float_as_uint(v[e] - h);
       }
     }
-    const uint32_t ta = trow + F32Tmem::A0 + 64u * (uint32_t)s;
-    tmem_st_32x32b_x32(ta, hi);
-    tmem_st_32x32b_x32(ta + 32u, lo);
+    const uint32_t ta = trow + F32Tmem::A0 + 64u * (uint32_t)s + 16u * (uint32_t)half;
+    tmem_st_32x32b_x16(ta, hi);
+    tmem_st_32x32b_x16(ta + 32u, lo);
     tmem_st_wait();
     tc_fence_before();
     __syncwarp();
@@ -213,7 +223,7 @@ __device__ __forceinline__ void f32_store_partial(uint32_t trow, int c0, int ng,
   }
 }
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     lenpred_f32_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW1,
                        const __grid_constant__ CUtensorMap tmZ1, const __grid_constant__ CUtensorMap tmW2,
                        const __grid_constant__ CUtensorMap tmZ2, const __grid_constant__ CUtensorMap tmW3,
@@ -235,7 +245,7 @@ __global__ void __launch_bounds__(192, 1)
   const int c = blockIdx.x;
   const int j1 = c & 31, s1 = c >> 5;   // layer 1: n-tile (64 columns), K quarter
   const int j2 = c & 15, s2 = c >> 4;   // layer 2: n-tile (32 columns), K eighth
-  const bool l3 = c < 4;                // layer 3: K quarter s3 = c
+  const bool l3 = c < 8;                // layer 3: K eighth s3 = c
   const int te = threadIdx.x - 64;
   const int M = p.M;
   if (threadIdx.x == 0) F32_TS(0);
@@ -250,7 +260,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 4);
+      mbar_init(&conv[s], 8);
       mbar_init(&empty[s], 1);
     }
     mbar_init(acc, 1);
@@ -264,8 +274,8 @@ __global__ void __launch_bounds__(192, 1)
   pdl_launch_dependents();
 
   const int kq = p.kb1 / 4;                   // layer-1 K blocks of this quarter
-  const int n1_it = kq, n2_it = 8, n3_it = 4;  // ring iterations per phase
-  const int q = warp & 3, row = q * 32 + lane;
+  const int n1_it = kq, n2_it = 8, n3_it = 2;  // ring iterations per phase
+  const int q = warp & 3, row = q * 32 + lane, half = warp >= 6 ? 1 : 0;
   const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
   int* cnt = p.cnt;
   long long dc[6] = {0, 0, 0, 0, 0, 0};   // diagnostics, converter te = 0: cycles waiting for / splitting stages
@@ -291,9 +301,9 @@ __global__ void __launch_bounds__(192, 1)
         tma_prefetch_2d(&tmW2, (s2 * 8 + i) * 32, 512 + j2 * 32);
       }
       if (l3)
-        for (int i = 0; i < 4; ++i) {
-          tma_prefetch_2d(&tmW3, (c * 4 + i) * 32, 0);
-          tma_prefetch_2d(&tmW3, (c * 4 + i) * 32, 64);
+        for (int i = 0; i < 2; ++i) {
+          tma_prefetch_2d(&tmW3, (c * 2 + i) * 32, 0);
+          tma_prefetch_2d(&tmW3, (c * 2 + i) * 32, 64);
         }
       pdl_wait();
       F32_TS(1);
@@ -327,19 +337,19 @@ __global__ void __launch_bounds__(192, 1)
         }
         tma_load_2d(smem + S::STAGE * s + S::A_RAW, &tmZ1, &full[s], (s2 * 8 + i) * 32, 0, pol_a);
       }
-      if (l3) {   // layer 3: W3 blocks, then the Z2 blocks after their 4 n-tiles
+      if (l3) {   // layer 3: W3 blocks, then the Z2 blocks after their 2 n-tiles
         const int it3 = n1_it + n2_it;
         for (int i = 0; i < n3_it; ++i) {
           const int it = it3 + i, s = it % NS;
           mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&full[s], 16384u + 2u * 8192u);
-          load_b(&tmW3, s, (c * 4 + i) * 32, 0, 64, 8192u);
+          load_b(&tmW3, s, (c * 2 + i) * 32, 0, 64, 8192u);
         }
-        spin_wait_geq(cnt + C::Z2 + c, 32);
+        spin_wait_geq(cnt + C::Z2 + c, 16);
         fence_proxy_async_global();
         for (int i = 0; i < n3_it; ++i) {
           const int it = it3 + i, s = it % NS;
-          tma_load_2d(smem + S::STAGE * s + S::A_RAW, &tmZ2, &full[s], (c * 4 + i) * 32, 0, pol_a);
+          tma_load_2d(smem + S::STAGE * s + S::A_RAW, &tmZ2, &full[s], (c * 2 + i) * 32, 0, pol_a);
         }
       }
     }
@@ -360,11 +370,16 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
     __syncwarp();
+  } else if (warp >= 6) {
+    // ---------------- operand split, columns 16..31 of every block (no epilogue work)
+    f32_convert(smem, full, conv, 0, n1_it, row, 1, trow, lane, nullptr);
+    f32_convert(smem, full, conv, n1_it, n2_it, row, 1, trow, lane, nullptr);
+    if (l3) f32_convert(smem, full, conv, n1_it + n2_it, n3_it, row, 1, trow, lane, nullptr);
   } else {
-    // ---------------- operand split + epilogues (128 threads, row = TMEM lane)
+    // ---------------- operand split (columns 0..15) + epilogues (128 threads, row = TMEM lane)
     pdl_wait();
     // ===== layer 1
-    f32_convert(smem, full, conv, 0, n1_it, row, trow, lane, te == 0 ? dc : nullptr);
+    f32_convert(smem, full, conv, 0, n1_it, row, 0, trow, lane, te == 0 ? dc : nullptr);
     mbar_wait(acc, 0);
     tc_fence_after();
     if (te == 0) F32_TS(2);
@@ -413,7 +428,7 @@ __global__ void __launch_bounds__(192, 1)
       F32_TS(4);
     }
     // ===== layer 2
-    f32_convert(smem, full, conv, n1_it, n2_it, row, trow, lane, te == 0 ? dc + 2 : nullptr);
+    f32_convert(smem, full, conv, n1_it, n2_it, row, 0, trow, lane, te == 0 ? dc + 2 : nullptr);
     mbar_wait(acc, 1);
     tc_fence_after();
     if (te == 0) F32_TS(6);
@@ -453,10 +468,10 @@ __global__ void __launch_bounds__(192, 1)
     fence_proxy_async_global();
     asm volatile("bar.sync 1, 128;" ::: "memory");
     if (te == 0) {
-      red_release_add_f(cnt + C::Z2 + (j2 >> 2), 1);
+      red_release_add_f(cnt + C::Z2 + (j2 >> 1), 1);
       F32_TS(8);
     }
-    // ===== layer 3 + head (CTAs 0..3)
+    // ===== layer 3 + head (CTAs 0..7)
     if (l3) {
       const bool owner = row < M;
       int32_t ntok = 0, inst = 0;   // fetched while layer 3 runs
@@ -464,13 +479,13 @@ __global__ void __launch_bounds__(192, 1)
         if (p.n_tok) ntok = p.n_tok[row];
         if (p.project) inst = p.pa.inst[row];
       }
-      float w4s[16], b3s[16];
+      float w4s[8], b3s[8];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        w4s[j] = __ldg(p.w4 + c * 16 + j);
-        b3s[j] = p.b3 ? __ldg(p.b3 + c * 16 + j) : 0.0f;
+      for (int j = 0; j < 8; ++j) {
+        w4s[j] = __ldg(p.w4 + c * 8 + j);
+        b3s[j] = p.b3 ? __ldg(p.b3 + c * 8 + j) : 0.0f;
       }
-      f32_convert(smem, full, conv, n1_it + n2_it, n3_it, row, trow, lane, te == 0 ? dc + 4 : nullptr);
+      f32_convert(smem, full, conv, n1_it + n2_it, n3_it, row, 0, trow, lane, te == 0 ? dc + 4 : nullptr);
       mbar_wait(acc, 0);
       tc_fence_after();
       if (te == 0) F32_TS(9);
@@ -478,22 +493,22 @@ __global__ void __launch_bounds__(192, 1)
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (te == 0) {
         red_release_add_f(cnt + C::P3, 1);
-        spin_wait_geq(cnt + C::P3, 4);
+        spin_wait_geq(cnt + C::P3, 8);
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       float y = 0.0f;
       {
-        float4 x[4][4];
+        float4 x[8][2];
 #pragma unroll
-        for (int s = 0; s < 4; ++s)
+        for (int s = 0; s < 8; ++s)
 #pragma unroll
-          for (int g = 0; g < 4; ++g)
-            x[s][g] = __ldcg(reinterpret_cast<const float4*>(p.P3 + ((size_t)s * 16 + c * 4 + g) * 512) + row);
+          for (int g = 0; g < 2; ++g)
+            x[s][g] = __ldcg(reinterpret_cast<const float4*>(p.P3 + ((size_t)s * 16 + c * 2 + g) * 512) + row);
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
+        for (int g = 0; g < 2; ++g) {
           float4 f = x[0][g];
 #pragma unroll
-          for (int s = 1; s < 4; ++s) {
+          for (int s = 1; s < 8; ++s) {
             f.x += x[s][g].x;
             f.y += x[s][g].y;
             f.z += x[s][g].z;
@@ -509,14 +524,14 @@ __global__ void __launch_bounds__(192, 1)
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (te == 0) {
         F32_TS(10);
-        *s_last = atom_add_acq_rel(cnt + C::Y, 1) == 3 ? 1 : 0;
+        *s_last = atom_add_acq_rel(cnt + C::Y, 1) == 7 ? 1 : 0;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (*s_last) {
         fence_acq_rel_gpu();
         float yy = __ldcg(p.yp + row);
 #pragma unroll
-        for (int s = 1; s < 4; ++s) yy += __ldcg(p.yp + s * 128 + row);
+        for (int s = 1; s < 8; ++s) yy += __ldcg(p.yp + s * 128 + row);
         yy += p.b4 ? __ldg(p.b4) : 0.0f;
         int32_t nh = 0;
         if (owner) {

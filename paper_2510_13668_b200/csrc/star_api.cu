@@ -325,7 +325,7 @@ static bool f32_small_available() {
     return false;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lenpred_f32_kernel, 192, F32Smem::BYTES) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lenpred_f32_kernel, 320, F32Smem::BYTES) !=
       cudaSuccess) {
     cudaGetLastError();
     return false;
@@ -1466,7 +1466,7 @@ static cudaError_t launch_f32_small(star_predictor* p, int R, const int32_t* n_t
   a.P1 = p->ws;
   a.P2 = a.P1 + 4 * 32 * 16 * 512;
   a.P3 = a.P2 + 8 * 16 * 8 * 512;
-  a.yp = a.P3 + 4 * 16 * 512;
+  a.yp = a.P3 + 8 * 16 * 512;
   a.cnt = p->f32_cnt;
   a.project = proj ? 1 : 0;
   if (proj) a.pa = *proj;
@@ -1474,7 +1474,7 @@ static cudaError_t launch_f32_small(star_predictor* p, int R, const int32_t* n_t
   if (p->tl) p->tl_ctas = 128;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(128, 1, 1);
-  cfg.blockDim = dim3(192, 1, 1);
+  cfg.blockDim = dim3(320, 1, 1);
   cfg.dynamicSmemBytes = F32Smem::BYTES;
   cfg.stream = st;
   cudaLaunchAttribute at[1];

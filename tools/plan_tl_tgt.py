@@ -33,3 +33,7 @@ for k in order:
     if c:
         print(f"  clk {lbl[k]:14s} {(c - tl[33]) / 1965.0:7.2f} us" + ("" if prev is None else f"  (+{(c - prev) / 1965.0:.2f})"))
         prev = c
+print("per-CTA: eval cycles of the slowest thread (round 0), candidates, targets")
+for r_ in range(8):
+    v7 = int(tl[64 + 8 * r_ + 7])
+    print(f"  cta {r_}: eval {int(tl[64 + 8 * r_ + 6]):6d} cyc  ncand {v7 >> 32}  nU {v7 & 0xffffffff}")
