@@ -401,7 +401,7 @@ def tgt_rank_timing(star, Step, dev, flush, seed=0, reps=200, world=8, cfg="TGT"
     if not stages:
         pred.close()
         return {"requests_per_instance": c["r_per_inst"], "us_per_step_p50": round(float(np.median(ts)), 2),
-                "us_per_step_min": round(float(np.min(ts)), 2), "launches_per_step": launches, "moves": n_moves,
+                "us_per_step_mean": round(float(np.mean(ts)), 2), "us_per_step_min": round(float(np.min(ts)), 2), "launches_per_step": launches, "moves": n_moves,
                 "rank_requests_per_s": round(c["r_per_inst"] / (float(np.median(ts)) * 1e-6), 1)}
     # stage split (event nodes between the stages: each costs ~2 us and blocks the PDL overlap, so
     # the stages sum to more than the step)
@@ -427,7 +427,10 @@ def tgt_rank_timing(star, Step, dev, flush, seed=0, reps=200, world=8, cfg="TGT"
     return {"workload": "TGT, one rank of W=8: 1 instance x 512 requests, d=4096 bf16; Alg. 1 over the 8 gathered "
                         "records (4096 requests)",
             "us_per_step_p50": round(float(np.median(ts)), 2), "us_per_step_p99": round(float(np.percentile(ts, 99)), 2),
+            "us_per_step_mean": round(float(np.mean(ts)), 2),
             "us_per_step_min": round(float(np.min(ts)), 2), "us_per_step_p10": round(float(np.percentile(ts, 10)), 2),
+            "timer_note": "per-step event pairs: on this B200 the elapsed times come in ~2.05 us steps, so the p50 "
+                          "moves in whole steps; the mean over the samples resolves finer",
             "target_us": 50.0, "launches_per_step": launches, "moves": n_moves,
             "exchange_budget_us": round(50.0 - float(np.median(ts)), 2),
             "exchange_estimate_us": "5-15 (SURVEY.md 8(d): NCCL all-gather of 8 x %d B over NVLink; unmeasured here, "

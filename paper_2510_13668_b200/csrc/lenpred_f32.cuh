@@ -73,8 +73,10 @@ struct F32Smem {
   static constexpr uint32_t STAGE = 32u * 1024u;
   static constexpr uint32_t A_RAW = 0, B_HI = 16384u, B_LO = 24576u;
   static constexpr uint32_t BAR = STAGES * STAGE;
-  static constexpr uint32_t BYTES = 1024u + BAR + 256u;
+  static constexpr uint32_t BYTES = 1024u + BAR + 256u + 2048u;
   static constexpr uint32_t HIST_MAX = BAR - 4096u;   // finalize: histogram + beta (ring idle)
+  static constexpr uint32_t CBETA = BAR + 256u;        // beta [<= 512], prefetched by the layer-3 CTAs
+  static constexpr int CBETA_MAX = 512;
 };
 // TMEM columns (512 allocated): accumulators L1 [0, 64), L2 [64, 96), L3 [128, 192); the A operand
 // of ring stage s at [192 + 64 s, +32) (hi) and [+32, +64) (lo).
@@ -479,6 +481,8 @@ __global__ void __launch_bounds__(320, 1)
         if (p.n_tok) ntok = p.n_tok[row];
         if (p.project) inst = p.pa.inst[row];
       }
+      if (p.project && p.pa.H + 1 <= S::CBETA_MAX)   // the finalize's beta, while layer 3 runs
+        for (int t = te; t <= p.pa.H; t += 128) reinterpret_cast<uint32_t*>(smem + S::CBETA)[t] = p.pa.beta_q[t];
       float w4s[8], b3s[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -546,12 +550,15 @@ __global__ void __launch_bounds__(320, 1)
           const int nb = p.pa.n_inst * (p.pa.H + 2);
           unsigned long long* ss = reinterpret_cast<unsigned long long*>(smem);
           uint32_t* sc = reinterpret_cast<uint32_t*>(ss + nb);
-          uint32_t* sbeta = sc + nb;
+          uint32_t* sbeta = reinterpret_cast<uint32_t*>(smem + S::CBETA);   // prefetched
           for (int k = te; k < nb; k += 128) {
             ss[k] = 0ull;
             sc[k] = 0u;
           }
-          for (int t = te; t <= p.pa.H; t += 128) sbeta[t] = p.pa.beta_q[t];
+          if (p.pa.H + 1 > S::CBETA_MAX) {
+            sbeta = sc + nb;
+            for (int t = te; t <= p.pa.H; t += 128) sbeta[t] = p.pa.beta_q[t];
+          }
           asm volatile("bar.sync 1, 128;" ::: "memory");
           uint32_t errbits = 0;
           proj_accumulate<true>(p.pa, owner, inst, ntok, nh, sc, ss, errbits);

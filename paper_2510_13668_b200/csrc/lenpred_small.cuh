@@ -75,7 +75,10 @@ struct SmallSmem {
   static constexpr uint32_t SEND23 = 0;                   // L2 / L3 send (A slots are idle then)
   static constexpr uint32_t R2 = 192u * 1024u;            // layer-2 receive 8 KB (dedicated)
   static constexpr uint32_t BAR = 200u * 1024u;
-  static constexpr uint32_t BYTES = 1024u + BAR + 256u;
+  // layer-3 CTAs: w4 [64], b3 [64], beta [<= 512] prefetched while layer 1 runs
+  static constexpr uint32_t CW4 = BAR + 256u, CB3 = CW4 + 256u, CBETA = CB3 + 256u;
+  static constexpr int CBETA_MAX = 512;
+  static constexpr uint32_t BYTES = 1024u + CBETA + 4u * CBETA_MAX;
   static constexpr uint32_t HIST = 0;                     // finalize: histogram staging (ring idle), <= 96 KB
   static constexpr int DONE = 16 * 256;                   // index of the completion counter in cnt (<= 256 chunks)
 };
@@ -151,11 +154,14 @@ __device__ __forceinline__ void relu_bf16_16(const float (&f)[16], const float* 
 // due row): L/W/peak/growth/count from the global histogram (one warp per instance), then the
 // histogram is re-zeroed.  The histogram comes into shared memory with L2 loads (other SMs'
 // atomics) when it fits the ring's A slots.  Epilogue warps 2..5 (te = thread - 64).
-__device__ __forceinline__ void small_finalize(const SmallArgs& p, uint8_t* smem, int te, int warp) {
+__device__ __forceinline__ void small_finalize(const SmallArgs& p, uint8_t* smem, int te, int warp, bool beta_ready) {
   using S = SmallSmem;
   const int nb = p.pa.n_inst * (p.pa.H + 2);
-  uint32_t* sbeta = reinterpret_cast<uint32_t*>(smem + S::R2);   // consumed by now
-  for (int t = te; t <= p.pa.H; t += 128) sbeta[t] = p.pa.beta_q[t];
+  uint32_t* sbeta = reinterpret_cast<uint32_t*>(smem + S::CBETA);   // prefetched (H + 1 <= CBETA_MAX)
+  if (!beta_ready || p.pa.H + 1 > S::CBETA_MAX) {
+    sbeta = reinterpret_cast<uint32_t*>(smem + S::R2);   // consumed by now
+    for (int t = te; t <= p.pa.H; t += 128) sbeta[t] = p.pa.beta_q[t];
+  }
   const uint32_t* hc = p.pa.ws_cnt;
   const unsigned long long* hs = p.pa.ws_sum;
   if ((uint32_t)nb * 12u <= 96u * 1024u) {
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       __syncthreads();
       if (M == 0 && p.project && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && warp >= 2)
-        small_finalize(p, smem, te, warp);
+        small_finalize(p, smem, te, warp, false);
       tc_fence_before();
       __syncthreads();
       if (warp == 1) {
@@ -364,7 +370,20 @@ __global__ void __launch_bounds__(192, 1)
       __syncwarp();
     } else {
       // epilogue: stage the 64 columns the partner owns (lane-contiguous 32 KB block, free ring)
-      if (act == 0) pdl_wait();
+      if (act == 0) {
+        if (l3) {   // constants of the head and the finalize, fetched while layer 1 runs
+          float* cw4 = reinterpret_cast<float*>(smem + S::CW4);
+          float* cb3 = reinterpret_cast<float*>(smem + S::CB3);
+          if (te < 64) {
+            cw4[te] = p.w4[te];
+            cb3[te] = p.b3 ? p.b3[te] : 0.0f;
+          }
+          if (p.project && p.pa.H + 1 <= S::CBETA_MAX)
+            for (int t = te; t <= p.pa.H; t += 128)
+              reinterpret_cast<uint32_t*>(smem + S::CBETA)[t] = p.pa.beta_q[t];
+        }
+        pdl_wait();
+      }
       mbar_wait(acc1, par);
       tc_fence_after();
       if (te == 0) SMALL_TS(3);
@@ -536,14 +555,15 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       if (te == 0) SMALL_TS(9);
       float y = 0.0f;
+      const float* cw4 = reinterpret_cast<const float*>(smem + S::CW4);
+      const float* cb3 = reinterpret_cast<const float*>(smem + S::CB3);
 #pragma unroll 1
       for (int c = 0; c < 64; c += 16) {
         uint32_t v[16];
         tmem_ld_32x32b_x16(trow + 160u + (uint32_t)c, v);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          y = fmaf(__ldg(p.w4 + c + j), fmaxf(__uint_as_float(v[j]) + (p.b3 ? __ldg(p.b3 + c + j) : 0.0f), 0.0f), y);
+        for (int j = 0; j < 16; ++j) y = fmaf(cw4[c + j], fmaxf(__uint_as_float(v[j]) + cb3[c + j], 0.0f), y);
       }
       y += p.b4 ? __ldg(p.b4) : 0.0f;
       int32_t nh = 0;
@@ -573,7 +593,7 @@ __global__ void __launch_bounds__(192, 1)
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (*s_last) {
         fence_acq_rel_gpu();
-        if (p.project) small_finalize(p, smem, te, warp);
+        if (p.project) small_finalize(p, smem, te, warp, true);
         // every counter of this launch has been consumed: re-arm them for the next one
         for (int k = te; k < nchunks * 16; k += 128) p.cnt[k] = 0;
         if (te == 0) p.cnt[S::DONE] = 0;

@@ -52,7 +52,10 @@ struct Tail2Smem {
   static constexpr uint32_t DOT = 208u * 1024u;      // [4][128] partial dots (CTA 0)
   static constexpr uint32_t BAR = DOT + 2048u;
   static constexpr uint32_t HIST = 96u * 1024u;      // finalize: histogram staging (ring idle), <= 96 KB
-  static constexpr uint32_t BYTES = 1024u + BAR + 256u;
+  // constants fetched while layer 2 runs: this rank's w4 / b3 slices, beta [<= 512] (rank 0)
+  static constexpr uint32_t CW4 = BAR + 256u, CB3 = CW4 + 64u, CBETA = CB3 + 64u;
+  static constexpr int CBETA_MAX = 512;
+  static constexpr uint32_t BYTES = 1024u + CBETA + 4u * CBETA_MAX;
 };
 static_assert(Tail2Smem::BYTES <= 227u * 1024u, "tail2 smem");
 
@@ -176,6 +179,12 @@ __global__ void __launch_bounds__(192, 1)
   // critical path (after griddepcontrol.wait: the predecessor may have written them)
   int32_t ntok = 0, inst = 0;
   if (warp >= 2) {
+    if (te < 16) {   // the head's constants (static: before griddepcontrol.wait)
+      reinterpret_cast<float*>(smem + S::CW4)[te] = p.w4[16 * rank + te];
+      reinterpret_cast<float*>(smem + S::CB3)[te] = p.b3 ? p.b3[16 * rank + te] : 0.0f;
+    }
+    if (rank == 0 && p.project && p.pa.H + 1 <= S::CBETA_MAX)
+      for (int t = te; t <= p.pa.H; t += 128) reinterpret_cast<uint32_t*>(smem + S::CBETA)[t] = p.pa.beta_q[t];
     pdl_wait();   // the outputs below may still be read by the previous kernel
     if (rank == 0 && grow < p.M) {
       if (p.n_tok) ntok = p.n_tok[grow];
@@ -255,11 +264,10 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
+    const float* cw4 = reinterpret_cast<const float*>(smem + S::CW4);
+    const float* cb3 = reinterpret_cast<const float*>(smem + S::CB3);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int col = 16 * rank + j;
-      dot = fmaf(__ldg(p.w4 + col), fmaxf(f[j] + (p.b3 ? __ldg(p.b3 + col) : 0.0f), 0.0f), dot);
-    }
+    for (int j = 0; j < 16; ++j) dot = fmaf(cw4[j], fmaxf(f[j] + cb3[j], 0.0f), dot);
     const uint32_t da = mapa_shared(smem_u32(smem + S::DOT + 4u * (uint32_t)(rank * 128 + row)), 0u);
     asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(da), "f"(dot) : "memory");
     if (te == 0) bulk_wait_read_all();
@@ -293,8 +301,11 @@ __global__ void __launch_bounds__(192, 1)
         fence_acq_rel_gpu();
         // the ring, RECV and DOT are idle: reuse the small-batch kernel's finalize on this layout
         const int nb = p.pa.n_inst * (p.pa.H + 2);
-        uint32_t* sbeta = reinterpret_cast<uint32_t*>(smem + S::W3);   // W3 consumed by the layer-3 MMA
-        for (int t = te; t <= p.pa.H; t += 128) sbeta[t] = p.pa.beta_q[t];
+        uint32_t* sbeta = reinterpret_cast<uint32_t*>(smem + S::CBETA);   // prefetched
+        if (p.pa.H + 1 > S::CBETA_MAX) {
+          sbeta = reinterpret_cast<uint32_t*>(smem + S::W3);   // W3 consumed by the layer-3 MMA
+          for (int t = te; t <= p.pa.H; t += 128) sbeta[t] = p.pa.beta_q[t];
+        }
         const uint32_t* hc = p.pa.ws_cnt;
         const unsigned long long* hs = p.pa.ws_sum;
         if ((uint32_t)nb * 12u <= 96u * 1024u) {

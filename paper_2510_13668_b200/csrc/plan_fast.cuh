@@ -214,7 +214,9 @@ __device__ __forceinline__ void plan_cta_fast(const PlanArgs& a, uint8_t* smraw,
       fence_barrier_init();
       mbar_arrive_expect_tx(s.bar, (uint32_t)a.world * (4 * fl32 + (a.pinned ? fl8 : 0)));
     }
-    if (nhat_part) fence_proxy_async_global();   // N_hat written through the generic proxy
+    // N_hat written through the generic proxy by THIS kernel (fused form) needs the proxy fence;
+    // after griddepcontrol.wait the predecessor grid's completion has published it
+    if (nhat_part && kFused) fence_proxy_async_global();
     for (int k = 0; k < a.world; ++k)
       for (int arr = 0; arr < 5; ++arr) {
         if (arr == 4 && !a.pinned) continue;
