@@ -2,8 +2,8 @@
 
     python tools/prof_step.py [--mode n1|rank|kv|proj] [--steps 3]
 
-n1    the bench's N = 1 step (TGT: 8 x 512 requests on one GPU, d = 4096 bf16): layer-1 GEMM,
-      fused tail (+ projection), cluster plan
+n1    the bench's N = 1 step of --config (TGT: 8 x 512 requests on one GPU, d = 4096 bf16: layer-1
+      GEMM, fused tail (+ projection), cluster plan; C1: the one-launch fp32 predictor, cluster plan)
 rank  one rank of the W = 8 TGT job: the one-launch small-batch predictor over 512 rows, then
       the cluster plan over the 8 gathered records (4096 requests)
 kv    one KV-migration pack / unpack / migrate (NEXT-4) of a 13.7K-token request
@@ -36,9 +36,10 @@ if args.mode in ("n1", "rank"):
     steps, hs = [], []
     buf = pred = params = None
     for k in range(world):
-        c, snap, params_h, idx, pw, h_np = bench.make_workload("TGT", world, k, 0)
+        c, snap, params_h, idx, pw, h_np = bench.make_workload(args.config, world, k, 0)
+        tdt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
         if pred is None:
-            W = [torch.from_numpy(x).to(torch.bfloat16).to(dev) for x in (pw.W1, pw.W2, pw.W3)]
+            W = [torch.from_numpy(x).to(tdt).to(dev) for x in (pw.W1, pw.W2, pw.W3)]
             pred = star.Predictor(*W, torch.from_numpy(pw.w4).to(dev), max_rows=len(idx))
             params = star.PlanParams.from_host(params_h, device=dev)
             if world > 1:
@@ -48,7 +49,7 @@ if args.mode in ("n1", "rank"):
         st.load_requests(*(torch.from_numpy(np.ascontiguousarray(a[idx])) for a in (snap.req_id, snap.inst,
                                                                                      snap.n_tok)),
                          pinned=torch.from_numpy(np.ascontiguousarray(snap.pinned[idx])))
-        h = bench.longtail_hidden(star, pred, h_np, snap, idx, torch.bfloat16, dev)
+        h = bench.longtail_hidden(star, pred, h_np, snap, idx, tdt, dev)
         st.run(h)
         steps.append(st)
         hs.append(h)
