@@ -713,10 +713,21 @@ def run_star(args):
     f32 = c["dtype"] == "f32"
     peak = peaks["bf16_tflops"] * (0.5 if f32 else 1.0)
     small = small_path
+    # which layer-1 kernel the library picks (mirrors forward_impl in star_api.cu): 9 non-uniform
+    # column tiles when they need no more waves than 8, and the persistent two-tile form when
+    # those tiles would take two waves but two tiles per pair fit one
+    npairs, slots = (m_tiles + 1) // 2, (148 // 2) * 2
+    w8, w9 = -(-npairs * 16 // slots), -(-npairs * 18 // slots)
+    nu = pair and w9 * 240 < w8 * 256
+    nu2 = nu and npairs * 9 * 2 > slots and (npairs * 9 + 1) // 2 * 2 <= slots and \
+        os.environ.get("STAR_L1_PERSIST", "1") != "0"
     kname = ("lenpred_f32_kernel (one launch: 3xTF32 layers 1-3 with the A operand split into TMEM, head, "
              "quantizer, projection; events around the whole launch)" if path == 2 else
              "lenpred_small_kernel (one launch: layers 1-3, head, projection; events around the whole launch)"
-             if small else ("umma_pair_gemm_kernel<256> (tcgen05 cta_group::2 + TMA)" if pair else
+             if small else ("umma_pair_nu2_kernel<256> (persistent tcgen05 cta_group::2 pairs + TMA, two "
+                            "9-column tiles per pair, one wave)" if nu2 else
+                            "umma_pair_gemm_kernel<256> (tcgen05 cta_group::2 + TMA" +
+                            (", 9 column tiles)" if nu else ")") if pair else
                             "umma_gemm_kernel (tcgen05 + TMA, cluster split-K)") + " = predictor layer 1")
     roofline = {"kernel": kname,
                 "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
