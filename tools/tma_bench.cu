@@ -127,10 +127,10 @@ int main() {
     run<4, 256>(ta, tb, grid, 64, a_rows, b_rows, 1, flush, flush_bytes);
     run<6, 128>(ta, tb128, grid, 64, a_rows, b_rows, 1, flush, flush_bytes);
   }
-  // no flush: warm L2
-  for (int grid : {128}) {
-    run<4, 256>(ta, tb, grid, 64, a_rows, b_rows, 2, flush, 0);
+  // no flush: warm L2 (share 1: every CTA streams the same blocks, the most L2 reuse possible)
+  for (int grid : {32, 64, 128, 148}) {
     run<6, 128>(ta, tb128, grid, 64, a_rows, b_rows, 2, flush, 0);
+    run<6, 128>(ta, tb128, grid, 64, a_rows, b_rows, 1, flush, 0);
   }
   return 0;
 }
