@@ -429,8 +429,6 @@ def tgt_rank_timing(star, Step, dev, flush, seed=0, reps=200, world=8, cfg="TGT"
             "us_per_step_p50": round(float(np.median(ts)), 2), "us_per_step_p99": round(float(np.percentile(ts, 99)), 2),
             "us_per_step_mean": round(float(np.mean(ts)), 2),
             "us_per_step_min": round(float(np.min(ts)), 2), "us_per_step_p10": round(float(np.percentile(ts, 10)), 2),
-            "timer_note": "per-step event pairs: on this B200 the elapsed times come in ~2.05 us steps, so the p50 "
-                          "moves in whole steps; the mean over the samples resolves finer",
             "target_us": 50.0, "launches_per_step": launches, "moves": n_moves,
             "exchange_budget_us": round(50.0 - float(np.median(ts)), 2),
             "exchange_estimate_us": "5-15 (SURVEY.md 8(d): NCCL all-gather of 8 x %d B over NVLink; unmeasured here, "
@@ -995,7 +993,8 @@ def refresh_step_timing(star, Step, pred, params, c, snap, idx, h_dev, dev, flus
             ts.append(e0.elapsed_time(e1) * 1e3)
             nref.append(int(st.n_refreshed.item()))
     t = float(np.median(ts))
-    return {"k": k, "us_per_step": round(t, 2), "requests_per_s": R / (t * 1e-6),
+    return {"k": k, "us_per_step": round(t, 2), "us_per_step_mean": round(float(np.mean(ts)), 2),
+            "requests_per_s": R / (t * 1e-6),
             "rows_repredicted_per_step": float(np.mean(nref)), "launches_per_step": launches,
             "note": "paper's deployment mode (k = 20, PAPER.md:463-469): due rows re-predicted, the rest "
                     "aged; projection + plan over all requests every step"}

@@ -198,9 +198,9 @@ constexpr int kSelHistBins = 2560;
     if (a.tl && threadIdx.x == 0) a.tl[(400 + blockIdx.x) * 32 + (k)] = globaltimer_ns(); \
   } while (0)   // shared histogram of the aged rows (n_inst * (H + 2) <= this)
 
-// 256 rows per CTA (the gather of the due rows' hidden states spreads over R / 256 SMs: with 1024
+// 128 rows per CTA (the gather of the due rows' hidden states spreads over R / 128 SMs: with 1024
 // rows per CTA, two CTAs gathered the C2 step's ~100 rows and the kernel took ~21 us)
-constexpr int kSel2Threads = 256;
+constexpr int kSel2Threads = 128;
 
 constexpr uint32_t kSelStageBytes = 160u * 1024u;   // gather staging: the CTA's due rows, chunked
 

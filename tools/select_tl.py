@@ -27,7 +27,7 @@ for i in range(4):
     st.run(h)
 torch.cuda.synchronize()
 tl = pred.timeline(fetch=True, raw=True).astype(np.int64)
-G = (R + 255) // 256
+G = (R + 127) // 128
 sel = tl[400:400 + G, :6]
 t0 = sel[:, 0].min()
 print(f"{cfg}: R={R} select CTAs={G}; stamps (us from the earliest entry): entry, after pdl_wait, flags+scan, aged+projected, counts met, gathered")
