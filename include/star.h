@@ -74,8 +74,11 @@ const char* star_version(void);
  * of 256 (bf16) / 128 (f32), m3 == 64.
  * Precision: STAR_BF16 -> bf16 operands on tcgen05 kind::f16, fp32 accumulation in TMEM,
  * Z1/Z2 rounded to bf16; STAR_F32 -> fp32 operands via 3xTF32 (hi/lo split,
- * hi*hi + hi*lo + lo*hi, tcgen05 kind::tf32), fp32 accumulation.  Layer 4 and the biases are
- * fp32 on the CUDA cores.
+ * hi*hi + hi*lo + lo*hi, tcgen05 kind::tf32), fp32 accumulation, Z1/Z2 kept in fp32 (the
+ * one-launch fp32 kernel for R <= 128 splits the activations into tensor memory and the
+ * MMAs read A from there; its split-K sums run in a different order than the multi-launch
+ * path's, so the two agree within the fp32 tolerance, not bit for bit).  Layer 4 and the
+ * biases are fp32 on the CUDA cores.
  * ===================================================================================== */
 typedef struct star_predictor star_predictor;  /* opaque: TMA descriptors, scratch Z1/Z2 */
 
@@ -84,7 +87,8 @@ typedef struct star_predictor star_predictor;  /* opaque: TMA descriptors, scrat
  *   K-major, the UMMA B operand as-is);  w4 [m3] fp32;  b1 [m1], b2 [m2], b3 [m3], b4 [1] fp32
  *   or NULL (NULL reproduces Eq. 2 literally, reading A1).
  * max_rows bounds R of later forward calls.  For STAR_F32 the weights are split into tf32
- * hi/lo copies here (library-owned).  This is the only call that allocates device memory;
+ * hi/lo copies here (library-owned: the multi-launch path's [hi|lo|hi] rows and, for m1 = 2048,
+ * m2 = 512, d % 128 == 0, the one-launch kernel's hi / lo planes).  This is the only call that allocates device memory;
  * it synchronises `stream` before returning. */
 star_status star_predictor_create(star_predictor** out, int d, int m1, int m2, int m3, star_dtype dt,
                                   const void* W1, const void* W2, const void* W3, const float* w4,
@@ -173,8 +177,11 @@ star_status star_predictor_timeline(star_predictor* p, int enable, uint64_t* hos
 star_status star_predictor_layer1_ms(star_predictor* p, float* ms);
 /* Which kernels a forward of R rows runs: *path = 1 for the one-launch small-batch predictor
  * (bf16, m1 = 2048, m2 = 512, d % 256 == 0, 1 <= R <= 512, and its 128 CTAs co-resident on this
- * device; the layer-1 timing events then bracket that whole launch), 0 for the layer-1 GEMM +
- * fused tail (bf16) or the 3 GEMMs (fp32). */
+ * device; the layer-1 timing events then bracket that whole launch), 2 for the one-launch fp32
+ * predictor (fp32, m1 = 2048, m2 = 512, d % 128 == 0, 1 <= R <= 128, 128 CTAs co-resident; with a
+ * fused projection only while n_inst * (H + 2) * 12 + (H + 1) * 4 bytes fit its shared memory,
+ * ~156 KB, else the multi-launch path runs), 0 for the layer-1 GEMM + fused tail (bf16) or the
+ * 3 GEMMs (fp32). */
 star_status star_predictor_path(star_predictor* p, int R, int* path);
 
 /* =====================================================================================
