@@ -83,15 +83,21 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_cluster_kernel(const Pla
   plan_cta_fast<false, kCl>(ac, smraw, (int)threadIdx.x, (int)blockDim.x, warp_best, shv, g_plan_tl, cl_best);
 }
 
-// Cluster size of the staged plan: STAR_PLAN_CLUSTER (1, 2, 4 or 8; read once) for A/B
-// measurements, default 8.
-static int plan_cluster_size() {
+// Cluster size of the staged plan by request slots: 8 CTAs split the compaction and the pair
+// scoring of a 4096-slot table best, but a cluster of 8 rarely finds a free GPC while the
+// predictor holds 128 SMs, so for small tables a smaller cluster that launches early (its static
+// staging under the predictor, PDL) wins (same-box A/B: C1, 128 slots: 36.0 us with 2 CTAs vs
+// 36.9 us with 8; one rank at 256 requests (2048 gathered slots): 43.0 vs 44.3 us with 4; TGT,
+// 4096 slots: 80.2 us with 8 vs 80.7 with 4).  STAR_PLAN_CLUSTER (1, 2, 4 or 8; read once)
+// overrides it for A/B measurements.
+static int plan_cluster_size(int slots) {
   static int v = [] {
     const char* e = getenv("STAR_PLAN_CLUSTER");
-    const int x = e ? atoi(e) : 8;
-    return (x == 1 || x == 2 || x == 4 || x == 8) ? x : 8;
+    const int x = e ? atoi(e) : 0;
+    return (x == 1 || x == 2 || x == 4 || x == 8) ? x : 0;
   }();
-  return v;
+  if (v) return v;
+  return slots <= 256 ? 2 : (slots <= 2048 ? 4 : 8);
 }
 
 // Minimum dynamic shared memory (request table read from global memory).
@@ -141,7 +147,7 @@ cudaError_t launch_plan(const star_plan_params* p, const star_plan_segments* sg,
   const bool staged = plan_fast_smem_layout(a.n, a.H, a.world, a.r_cap) <= lim;
   const size_t smem = staged ? plan_fast_smem_layout(a.n, a.H, a.world, a.r_cap)
                              : plan_smem_layout(a.n, a.H, a.world, a.r_cap, false);
-  const int ncl = staged ? plan_cluster_size() : 1;
+  const int ncl = staged ? plan_cluster_size(a.world * plan_fast_pitch(a.r_cap)) : 1;
   auto kern = !staged ? plan_kernel<false>
             : ncl == 8 ? plan_cluster_kernel<8> : ncl == 4 ? plan_cluster_kernel<4>
             : ncl == 2 ? plan_cluster_kernel<2> : plan_kernel<true>;
