@@ -31,6 +31,14 @@
  *    cleared by the library) and the offending element is ignored.
  *  - Only sm_100a (B200) is supported; every call fails with STAR_ENOTSUP elsewhere.  There
  *    is no CPU fallback.
+ *  - A predictor (and a projection / plan workspace) holds scratch and arrival counters that
+ *    one call uses at a time: calls on the same predictor must be ordered (one stream, or
+ *    streams joined by events); distinct predictors are independent.
+ *  - The one-launch kernels (small-batch bf16, fp32, refresh select, multi-CTA plans) hand
+ *    phases off between CTAs through device counters and assume their grid is co-resident
+ *    (checked with the occupancy API when the predictor is created); if other work holds the
+ *    SMs (MPS partitions, green contexts) a wait traps after ~2 s (STAR_ECUDA on the next
+ *    synchronisation) instead of hanging the device.
  */
 #ifndef STAR_H_
 #define STAR_H_
