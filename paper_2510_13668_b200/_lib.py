@@ -195,14 +195,25 @@ class Predictor:
         return int(v.value)
 
 
+def _h_ld(h: torch.Tensor, pred: "Predictor") -> int:
+    """Row stride (elements) of the hidden-state matrix: rows contiguous, unit column stride.  An
+    empty batch (R = 0) carries no data, whatever strides torch gave the empty view."""
+    if h.dim() != 2:
+        raise StarError("h must be 2-D")
+    if h.shape[0] == 0:
+        return pred.d
+    if h.stride(1) != 1:
+        raise StarError("h must be 2-D with unit column stride")
+    return h.stride(0)
+
+
 def lenpred_forward(pred: Predictor, h: torch.Tensor, n_tok: Optional[torch.Tensor] = None,
                     max_ctx_len: int = L_CTX, y_hat: Optional[torch.Tensor] = None,
                     n_hat: Optional[torch.Tensor] = None, want_y: bool = True, want_n: bool = True,
                     stream=None):
     """Eq. 2 forward on the rows of h ([R, ld_h >= d], dtype of the predictor)."""
     R = h.shape[0]
-    if h.dim() != 2 or h.stride(1) != 1:
-        raise StarError("h must be 2-D with unit column stride")
+    ld_h = _h_ld(h, pred)
     exp = torch.bfloat16 if pred.dt == STAR_BF16 else torch.float32
     if h.dtype != exp or not h.is_cuda:
         raise StarError(f"h must be a CUDA {exp} tensor")
@@ -213,7 +224,7 @@ def lenpred_forward(pred: Predictor, h: torch.Tensor, n_tok: Optional[torch.Tens
         n_hat = torch.empty(R, dtype=torch.int32, device=dev)
     if n_tok is not None:
         _req(n_tok, torch.int32, "n_tok")
-    _check(lib().lenpred_forward(pred.handle, _ptr(h), h.stride(0), R, _ptr(n_tok), max_ctx_len,
+    _check(lib().lenpred_forward(pred.handle, _ptr(h), ld_h, R, _ptr(n_tok), max_ctx_len,
                                  _ptr(y_hat), _ptr(n_hat), _stream(stream)), "lenpred_forward")
     return y_hat, n_hat
 
@@ -225,8 +236,7 @@ def lenpred_forward_project(pred: Predictor, h: torch.Tensor, n_tok: torch.Tenso
                             err_flag: Optional[torch.Tensor] = None, want_y: bool = True, stream=None):
     """Eq. 2 forward fused with the projection of its N_hat (star.h lenpred_forward_project)."""
     R = h.shape[0]
-    if h.dim() != 2 or h.stride(1) != 1:
-        raise StarError("h must be 2-D with unit column stride")
+    ld_h = _h_ld(h, pred)
     exp = torch.bfloat16 if pred.dt == STAR_BF16 else torch.float32
     if h.dtype != exp or not h.is_cuda:
         raise StarError(f"h must be a CUDA {exp} tensor")
@@ -239,7 +249,7 @@ def lenpred_forward_project(pred: Predictor, h: torch.Tensor, n_tok: torch.Tenso
         n_hat = torch.empty(max(R, 1), dtype=torch.int32, device=dev)
     if out is None:
         out = ProjectOut(n_inst, H, dev)
-    _check(lib().lenpred_forward_project(pred.handle, _ptr(h), h.stride(0), R, _ptr(n_tok), max_ctx_len,
+    _check(lib().lenpred_forward_project(pred.handle, _ptr(h), ld_h, R, _ptr(n_tok), max_ctx_len,
                                          _ptr(y_hat), _ptr(n_hat), n_inst, inst_base, H, _ptr(inst), _ptr(beta_q),
                                          _ptr(out.L), _ptr(out.W), _ptr(out.peak), _ptr(out.growth),
                                          _ptr(out.count), _ptr(workspace), _ptr(err_flag), _stream(stream)),
@@ -255,14 +265,13 @@ def lenpred_forward_project_plan(pred: Predictor, h: torch.Tensor, n_tok: torch.
                                  err_flag: Optional[torch.Tensor] = None, stream=None):
     """One-rank step: forward + projection + Alg. 1 (star.h lenpred_forward_project_plan)."""
     R = h.shape[0]
-    if h.dim() != 2 or h.stride(1) != 1:
-        raise StarError("h must be 2-D with unit column stride")
+    ld_h = _h_ld(h, pred)
     exp = torch.bfloat16 if pred.dt == STAR_BF16 else torch.float32
     if h.dtype != exp or not h.is_cuda:
         raise StarError(f"h must be a CUDA {exp} tensor")
     for n_, t in (("n_tok", n_tok), ("inst", inst), ("beta_q", beta_q), ("n_hat", n_hat)):
         _req(t, torch.int32, n_)
-    _check(lib().lenpred_forward_project_plan(pred.handle, _ptr(h), h.stride(0), R, _ptr(n_tok), max_ctx_len,
+    _check(lib().lenpred_forward_project_plan(pred.handle, _ptr(h), ld_h, R, _ptr(n_tok), max_ctx_len,
                                               _ptr(y_hat), _ptr(n_hat), n_inst, H, _ptr(inst), _ptr(beta_q),
                                               _ptr(out.L), _ptr(out.W), _ptr(out.peak), _ptr(out.growth),
                                               _ptr(out.count), _ptr(workspace), C.byref(params.c), C.byref(seg),
@@ -277,13 +286,14 @@ def lenpred_forward_refresh(pred: Predictor, h: torch.Tensor, n_tok: torch.Tenso
                             stream=None):
     """Prediction cadence k (star.h lenpred_forward_refresh); g_last / nhat_last are updated in place."""
     R = h.shape[0]
-    if h.dim() != 2 or h.stride(1) != 1 or h.dtype != torch.bfloat16 or not h.is_cuda:
+    ld_h = _h_ld(h, pred)
+    if h.dtype != torch.bfloat16 or not h.is_cuda:
         raise StarError("h must be a 2-D CUDA bf16 tensor with unit column stride")
     for n_, t in (("n_tok", n_tok), ("gen", gen), ("g_last", g_last), ("nhat_last", nhat_last)):
         _req(t, torch.int32, n_)
     if n_hat is None:
         n_hat = torch.empty(max(R, 1), dtype=torch.int32, device=h.device)
-    _check(lib().lenpred_forward_refresh(pred.handle, _ptr(h), h.stride(0), R, _ptr(n_tok), max_ctx_len, _ptr(gen),
+    _check(lib().lenpred_forward_refresh(pred.handle, _ptr(h), ld_h, R, _ptr(n_tok), max_ctx_len, _ptr(gen),
                                          _ptr(g_last), _ptr(nhat_last), int(k), _ptr(n_hat), _ptr(n_refreshed),
                                          _stream(stream)), "lenpred_forward_refresh")
     return n_hat[:R]
@@ -298,7 +308,8 @@ def lenpred_forward_refresh_project(pred: Predictor, h: torch.Tensor, n_tok: tor
                                     R: Optional[int] = None, stream=None):
     """Cadence-k step of one worker (star.h lenpred_forward_refresh_project): refresh + projection."""
     R = h.shape[0] if R is None else R
-    if h.dim() != 2 or h.stride(1) != 1 or h.dtype != torch.bfloat16 or not h.is_cuda:
+    ld_h = _h_ld(h, pred)
+    if h.dtype != torch.bfloat16 or not h.is_cuda:
         raise StarError("h must be a 2-D CUDA bf16 tensor with unit column stride")
     for n_, t in (("n_tok", n_tok), ("gen", gen), ("g_last", g_last), ("nhat_last", nhat_last), ("inst", inst),
                   ("beta_q", beta_q)):
@@ -308,7 +319,7 @@ def lenpred_forward_refresh_project(pred: Predictor, h: torch.Tensor, n_tok: tor
     if out is None:
         out = ProjectOut(n_inst, H, h.device)
     _check(lib().lenpred_forward_refresh_project(
-        pred.handle, _ptr(h), h.stride(0), R, _ptr(n_tok), max_ctx_len, _ptr(gen), _ptr(g_last), _ptr(nhat_last),
+        pred.handle, _ptr(h), ld_h, R, _ptr(n_tok), max_ctx_len, _ptr(gen), _ptr(g_last), _ptr(nhat_last),
         int(k), _ptr(n_hat), _ptr(n_refreshed), n_inst, inst_base, H, _ptr(inst), _ptr(beta_q), _ptr(out.L),
         _ptr(out.W), _ptr(out.peak), _ptr(out.growth), _ptr(out.count), _ptr(workspace), _ptr(err_flag),
         _stream(stream)), "lenpred_forward_refresh_project")

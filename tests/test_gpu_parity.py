@@ -681,6 +681,53 @@ def test_step_gathered_ranks_plan_equals_oracle(star, oracle_mod, cfg, world, r_
     pred.close()
 
 
+def test_step_gathered_with_an_empty_rank(star, oracle_mod):
+    """A decode instance block with no running requests (rank 3 of 4: instances 6 and 7 empty):
+    its rank runs the step on R = 0 and must still publish a valid record (zero loads, count 0)
+    over whatever the gathered buffer held before; every rank's plan == the oracle's."""
+    from paper_2510_13668_b200.step import RecordLayout, Step, split_snapshot_by_rank
+    n, world, r_per, d = 8, 4, 96, 1024
+    snap0 = datagen.make_snapshot(5, n, r_per, skewed=True, pinned_frac=0.05)
+    keep = snap0.inst < 6
+    pw = datagen.make_predictor_weights(5, d, "bf16")
+    W, b = _weights_dev(pw, False)
+    params_h = datagen.make_plan_params(snap0, H=50, max_moves=2)
+    params = star.PlanParams.from_host(params_h)
+    idxs = [i[keep[i]] for i in (split_snapshot_by_rank(snap0.inst, n, world, k) for k in range(world))]
+    assert len(idxs[3]) == 0
+    r_cap = max(len(i) for i in idxs)
+    pred = star.Predictor(*W, *b, max_rows=r_cap)
+    buf = torch.full((world * RecordLayout(n // world, 50, r_cap).nbytes,), 0xAB, dtype=torch.uint8, device="cuda")
+    steps = []
+    for k, idx in enumerate(idxs):
+        h = datagen.make_hidden(500 + k, len(idx), d, "bf16")
+        st = Step(pred, params, n, r_cap=r_cap, rank=k, world=world, gathered=buf)
+        st.load_requests(*(torch.from_numpy(np.ascontiguousarray(a[idx])) for a in (snap0.req_id, snap0.inst,
+                                                                                      snap0.n_tok)),
+                         pinned=torch.from_numpy(np.ascontiguousarray(snap0.pinned[idx])))
+        st.run(_dev(h, torch.bfloat16))
+        steps.append(st)
+    torch.cuda.synchronize()
+    order = np.concatenate(idxs)
+    nh = np.concatenate([st.v["n_hat"][:len(i)].cpu().numpy() for st, i in zip(steps, idxs)])
+    ids, inst, n_tok, pin = (a[order] for a in (snap0.req_id, snap0.inst, snap0.n_tok, snap0.pinned))
+    ref_p = oracle_mod.project(inst, n_tok, nh, n, 50, params_h.beta_q)
+    assert not ref_p["L"][6:].any()
+    for k, st in enumerate(steps):
+        assert np.array_equal(st.v["L"].cpu().numpy(), ref_p["L"][2 * k:2 * k + 2])
+    assert steps[-1].err.item() == 0   # the last rank planned with every record in place
+    ref = oracle_mod.plan(params_h, ref_p["L"], ids, inst, n_tok, nh, pin)
+    assert steps[-1].result() == ref
+    # (the earlier ranks planned while later records still held the 0xAB fill: re-plan on the final buffer)
+    for st in steps:
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        moves, nm = star.plan_reschedule_segmented(params, st.seg, err_flag=err)
+        torch.cuda.synchronize()
+        assert err.item() == 0
+        assert star.decode_moves(moves, nm) == ref
+    pred.close()
+
+
 # ============================================================================ one-launch small-batch predictor
 @pytest.mark.parametrize("d,R,biases,n,ld_pad", [(4096, 512, True, 1, 0), (4096, 384, False, 3, 64), (4096, 129, False, 8, 0),
                                                  (5120, 511, True, 2, 0), (1024, 64, False, 1, 0), (4096, 1, True, 1, 8),
