@@ -728,6 +728,43 @@ def test_step_gathered_with_an_empty_rank(star, oracle_mod):
     pred.close()
 
 
+@pytest.mark.parametrize("case", ["world1_empty", "refresh_empty", "no_moves_allowed", "one_instance", "fp32_world1"])
+def test_step_edge_cases(star, oracle_mod, case):
+    """Degenerate steps through the public Step API, each against the oracle: no running request
+    on a one-rank step (zero loads, no move) and in the cadence-k mode; max_moves = 0 on an
+    overloaded snapshot (no move, loads exact); a single instance (no target, no move); an fp32
+    one-rank step (the one-launch fp32 predictor, then the plan)."""
+    from paper_2510_13668_b200.step import Step
+    n, r_per, d, dt = 4, 64, 1024, "bf16"
+    if case == "one_instance":
+        n = 1
+    if case == "fp32_world1":
+        n, r_per, d, dt = 2, 64, 896, "f32"
+    snap = datagen.make_snapshot(9, n, r_per, skewed=n > 1)
+    params_h = datagen.make_plan_params(snap, H=50, max_moves=0 if case == "no_moves_allowed" else 2)
+    params = star.PlanParams.from_host(params_h)
+    pw = datagen.make_predictor_weights(9, d, dt)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    W, b = _weights_dev(pw, False)
+    pred = star.Predictor(*W, *b, max_rows=snap.R)
+    idx = np.arange(0 if case.endswith("empty") else snap.R)
+    st = Step(pred, params, n, r_cap=snap.R, refresh_k=20 if case == "refresh_empty" else None)
+    st.load_requests(*(torch.from_numpy(np.ascontiguousarray(a[idx])) for a in (snap.req_id, snap.inst, snap.n_tok)))
+    scale = np.maximum(snap.true_rem[idx], 1).astype(np.float32) / 60.0
+    h = datagen.make_hidden(90, len(idx), d, dt, scale=scale if len(idx) else None)
+    st.run(_dev(h, tdt) if len(idx) else torch.empty((0, d), dtype=tdt, device="cuda"))
+    torch.cuda.synchronize()
+    assert st.err.item() == 0
+    nh = st.v["n_hat"][:len(idx)].cpu().numpy()
+    ref_p = oracle_mod.project(snap.inst[idx].astype(np.int32), snap.n_tok[idx], nh, n, 50, params_h.beta_q)
+    assert np.array_equal(st.v["L"].cpu().numpy(), ref_p["L"])
+    ref = oracle_mod.plan(params_h, ref_p["L"], snap.req_id[idx], snap.inst[idx], snap.n_tok[idx], nh, None)
+    assert st.result() == ref
+    if case in ("world1_empty", "refresh_empty", "no_moves_allowed", "one_instance"):
+        assert ref == []
+    pred.close()
+
+
 # ============================================================================ one-launch small-batch predictor
 @pytest.mark.parametrize("d,R,biases,n,ld_pad", [(4096, 512, True, 1, 0), (4096, 384, False, 3, 64), (4096, 129, False, 8, 0),
                                                  (5120, 511, True, 2, 0), (1024, 64, False, 1, 0), (4096, 1, True, 1, 8),
