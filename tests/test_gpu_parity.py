@@ -264,7 +264,11 @@ def _predict(star, pw, h, biases=False, n_tok=None, max_rows=None):
                                               (896, "bf16", 640, False),
                                               # layer 1 as 9 non-uniform column tiles (6-8 row pairs):
                                               # odd m-tile count (phantom rows) and a ragged last tile
-                                              (4096, "bf16", 1300, True), (4096, "bf16", 1537, False)])
+                                              (4096, "bf16", 1300, True), (4096, "bf16", 1537, False),
+                                              # hidden sizes that are multiples of 8 only (the last K block
+                                              # is partly out of bounds: TMA zero fill)
+                                              (72, "bf16", 50, True), (520, "bf16", 700, False),
+                                              (200, "f32", 33, False), (104, "f32", 128, True)])
 def test_predictor_parity(star, oracle_mod, d, dtype, R, biases):
     pw = datagen.make_predictor_weights(d, d, dtype, biases=biases)
     h = datagen.make_hidden(d + 1, R, d, dtype)
