@@ -470,15 +470,19 @@ def _nhat_close(got, ref_y, n_tok, tol):
     return np.all(np.abs(got.astype(np.float64) - ref) <= np.maximum(1.0, tol * np.abs(ref)) + 1.0)
 
 
-@pytest.mark.parametrize("R,k,seed", [(2048, 20, 0), (2047, 20, 1), (300, 7, 2), (4096, 20, 3), (64, 1, 4)])
-def test_refresh_step_parity(star, oracle_mod, R, k, seed):
-    c = datagen.CONFIGS["C2"]
+@pytest.mark.parametrize("R,k,seed,d", [(2048, 20, 0, 4096), (2047, 20, 1, 4096), (300, 7, 2, 4096), (4096, 20, 3, 4096),
+                                        (64, 1, 4, 4096),
+                                        # more due rows than one 512-row chunk of the one-launch predictor
+                                        (2048, 2, 5, 4096), (1000, 1, 6, 1024),
+                                        # d % 256 != 0: the multi-launch refresh path
+                                        (300, 5, 7, 896)])
+def test_refresh_step_parity(star, oracle_mod, R, k, seed, d):
     g = datagen.rng(seed)
     snap = datagen.make_snapshot(seed, 8, (R + 7) // 8)
     n_tok = snap.n_tok[:R].copy()
-    pw = datagen.make_predictor_weights(seed, c["d"], "bf16")
+    pw = datagen.make_predictor_weights(seed, d, "bf16")
     scale = np.exp(g.normal(0.0, 1.5, R)).astype(np.float32)
-    h = datagen.make_hidden(seed, R, c["d"], "bf16", scale=scale)
+    h = datagen.make_hidden(seed, R, d, "bf16", scale=scale)
     gen = g.integers(0, 5000, R).astype(np.int32)
     g_last = np.where(g.random(R) < 0.1, -1, gen - g.integers(0, 2 * k + 1, R)).astype(np.int32)
     nhat_last = g.integers(0, 30000, R).astype(np.int32)
