@@ -140,6 +140,7 @@ class Step:
         self.proj_out.count = self.v["icount"]
         self.R = 0
         self.graph = None
+        self._graph_R = -1
         # prediction cadence (NEXT-1): re-predict a request every refresh_k generated tokens, age
         # its prediction in between; None = predict every request every step
         self.refresh_k = refresh_k
@@ -234,9 +235,17 @@ class Step:
         with torch.cuda.graph(g):
             self.run(h)
         self.graph = g
+        self._graph_R = self.R   # the request count (and h's address) are baked into the graph
         return g
 
     def replay(self):
+        """One launch of the captured step.  The request arrays and h may change in place; the
+        request COUNT may not (it is baked into the kernels' grids): recapture after a
+        load_requests() that changed it."""
+        if self.graph is None:
+            raise RuntimeError("Step.replay() before Step.capture()")
+        if self.R != self._graph_R:
+            raise RuntimeError(f"request count changed since capture ({self._graph_R} -> {self.R}): capture again")
         self.graph.replay()
         return self.moves, self.n_moves
 

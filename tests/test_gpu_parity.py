@@ -773,6 +773,40 @@ def test_step_edge_cases(star, oracle_mod, case):
     pred.close()
 
 
+def test_step_capture_replay_guards(star, oracle_mod):
+    """Step.capture / replay (the public one-launch-per-step API): a replay after new request data
+    of the same count equals a fresh run; a changed request count refuses to replay stale grids."""
+    from paper_2510_13668_b200.step import Step
+    n, r_per, d = 4, 64, 1024
+    snap = datagen.make_snapshot(11, n, r_per, skewed=True)
+    params_h = datagen.make_plan_params(snap, H=50, max_moves=2)
+    params = star.PlanParams.from_host(params_h)
+    pw = datagen.make_predictor_weights(11, d, "bf16")
+    W, b = _weights_dev(pw, False)
+    pred = star.Predictor(*W, *b, max_rows=snap.R)
+    st = Step(pred, params, n, r_cap=snap.R)
+    with pytest.raises(RuntimeError):
+        st.replay()
+    st.load_requests(*(torch.from_numpy(a) for a in (snap.req_id, snap.inst, snap.n_tok)))
+    h = _dev(datagen.make_hidden(110, snap.R, d, "bf16",
+                                 scale=np.maximum(snap.true_rem, 1).astype(np.float32) / 60.0), torch.bfloat16)
+    st.capture(h)
+    # new hidden states and token counts, same count: replay == the oracle on the new inputs
+    h2 = datagen.make_hidden(111, snap.R, d, "bf16", scale=np.maximum(snap.true_rem, 1).astype(np.float32) / 50.0)
+    h.copy_(_dev(h2, torch.bfloat16))
+    st.load_requests(*(torch.from_numpy(a) for a in (snap.req_id, snap.inst, snap.n_tok + 3)))
+    st.replay()
+    torch.cuda.synchronize()
+    nh = st.v["n_hat"][:snap.R].cpu().numpy()
+    ref_p = oracle_mod.project(snap.inst, snap.n_tok + 3, nh, n, 50, params_h.beta_q)
+    assert np.array_equal(st.v["L"].cpu().numpy(), ref_p["L"])
+    assert st.result() == oracle_mod.plan(params_h, ref_p["L"], snap.req_id, snap.inst, snap.n_tok + 3, nh, None)
+    st.load_requests(*(torch.from_numpy(a[:-1]) for a in (snap.req_id, snap.inst, snap.n_tok)))
+    with pytest.raises(RuntimeError):
+        st.replay()
+    pred.close()
+
+
 # ============================================================================ one-launch small-batch predictor
 @pytest.mark.parametrize("d,R,biases,n,ld_pad", [(4096, 512, True, 1, 0), (4096, 384, False, 3, 64), (4096, 129, False, 8, 0),
                                                  (5120, 511, True, 2, 0), (1024, 64, False, 1, 0), (4096, 1, True, 1, 8),
