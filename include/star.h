@@ -378,7 +378,9 @@ star_status dispatch_requests(int policy, int n_inst, int H, const uint32_t* bet
  * block_bytes, equal n_layers and block_bytes for kv_migrate.  A block id outside [0, n_blocks)
  * sets STAR_ERRF_BLOCK in *err_flag and that (layer, block) copy is skipped.  Asynchronous on
  * `stream`, no allocation, graph capturable; n = 0 enqueues nothing.  Overlap with decode by
- * issuing on a separate (low-priority) stream.
+ * issuing on a separate (low-priority) stream.  The copies of one call run concurrently: a block
+ * must not be both read and written by the same call (src and dst may be the same pool when the
+ * two tables are disjoint; a destination block listed twice gets either copy).
  * ===================================================================================== */
 #define STAR_ERRF_BLOCK 4  /* KV block id outside the pool */
 
