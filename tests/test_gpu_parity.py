@@ -807,6 +807,50 @@ def test_step_capture_replay_guards(star, oracle_mod):
     pred.close()
 
 
+def test_two_predictors_concurrent_streams(star, oracle_mod):
+    """Two predictors on two streams at once (bf16 one-launch at 512 rows, fp32 one-launch at
+    128 rows, each fused with its projection, then a plan each): the results equal the same calls
+    run one after the other -- no state is shared between predictors."""
+    beta = datagen.beta_schedule_q16(50)
+    bq = _dev(beta.astype(np.int32))
+    cases = []
+    for seed, d, dt, R, n in ((21, 4096, "bf16", 512, 4), (22, 896, "f32", 128, 2)):
+        pw = datagen.make_predictor_weights(seed, d, dt)
+        snap = datagen.make_snapshot(seed, n, R // n, skewed=True)
+        tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+        W, b = _weights_dev(pw, False)
+        pred = star.Predictor(*W, *b, max_rows=R)
+        h = _dev(datagen.make_hidden(seed, R, d, dt, scale=np.maximum(snap.true_rem, 1).astype(np.float32) / 60.0),
+                 tdt)
+        params_h = datagen.make_plan_params(snap, H=50, max_moves=2)
+        cases.append((pred, h, snap, n, star.PlanParams.from_host(params_h), params_h))
+
+    def run(stream_of):
+        outs = []
+        for k, (pred, h, snap, n, pp, _) in enumerate(cases):
+            st = stream_of(k)
+            with torch.cuda.stream(st):
+                ws = torch.zeros(star.project_workspace_bytes(n, 50), dtype=torch.uint8, device="cuda")
+                y, nh, out = star.lenpred_forward_project(pred, h, _dev(snap.n_tok), _dev(snap.inst), n, 50, bq, ws)
+                moves, nm = star.plan_reschedule(pp, out.L, _dev(snap.req_id), _dev(snap.inst), _dev(snap.n_tok), nh)
+                outs.append((y, nh, out.L, moves, nm))
+        torch.cuda.synchronize()
+        return [(y.cpu().numpy(), nh.cpu().numpy(), L.cpu().numpy(), star.decode_moves(m, c)) for y, nh, L, m, c in outs]
+
+    seq = run(lambda k: torch.cuda.current_stream())
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for _ in range(3):
+        par = run(lambda k: streams[k])
+        for a, b_ in zip(seq, par):
+            assert np.array_equal(a[0], b_[0]) and np.array_equal(a[1], b_[1]) and np.array_equal(a[2], b_[2])
+            assert a[3] == b_[3]
+    for (pred, h, snap, n, pp, params_h), (y, nh, L, moves) in zip(cases, seq):
+        ref_p = oracle_mod.project(snap.inst, snap.n_tok, nh, n, 50, beta)
+        assert np.array_equal(L, ref_p["L"])
+        assert moves == oracle_mod.plan(params_h, ref_p["L"], snap.req_id, snap.inst, snap.n_tok, nh, None)
+        pred.close()
+
+
 # ============================================================================ one-launch small-batch predictor
 @pytest.mark.parametrize("d,R,biases,n,ld_pad", [(4096, 512, True, 1, 0), (4096, 384, False, 3, 64), (4096, 129, False, 8, 0),
                                                  (5120, 511, True, 2, 0), (1024, 64, False, 1, 0), (4096, 1, True, 1, 8),
