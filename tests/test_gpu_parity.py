@@ -281,6 +281,22 @@ def test_predictor_parity(star, oracle_mod, d, dtype, R, biases):
     assert np.array_equal(nh, oracle_mod.quantize(y, n_tok))
 
 
+@pytest.mark.parametrize("d,dtype,m1,m2,R", [(512, "bf16", 1024, 256, 300), (1024, "bf16", 768, 512, 700),
+                                             (256, "f32", 512, 256, 100), (384, "f32", 384, 128, 200)])
+def test_predictor_parity_other_widths(star, oracle_mod, d, dtype, m1, m2, R):
+    """Eq. 2 with hidden widths other than the paper's 2048 / 512 (star.h: m1, m2 multiples of 256
+    for bf16, 128 for fp32; m3 = 64): the general kernels, against the fp64 oracle."""
+    pw = datagen.make_predictor_weights(d + m1, d, dtype, m1=m1, m2=m2)
+    h = datagen.make_hidden(d + 3, R, d, dtype)
+    n_tok = datagen.make_snapshot(d, 1, R).n_tok
+    pred, y, nh = _predict(star, pw, h, False, n_tok)
+    assert pred.path(R) == 0
+    err = _rel_err(y, oracle_mod.lenpred_weights(h, pw))
+    assert err <= TOL[dtype], f"max rel err {err:.3e}"
+    assert np.array_equal(nh, oracle_mod.quantize(y, n_tok))
+    pred.close()
+
+
 @pytest.mark.parametrize("cfg,R", [("C2", 2048), ("C3", 4096), ("C4", 4096), ("TGT", 4096), ("TGT", 512),
                                    ("C2", 256)])
 def test_predictor_full_size_all_rows(star, oracle_mod, cfg, R):
