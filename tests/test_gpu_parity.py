@@ -789,6 +789,46 @@ def test_step_edge_cases(star, oracle_mod, case):
     pred.close()
 
 
+@pytest.mark.parametrize("H,world", [(0, 1), (256, 1), (256, 4), (1, 4)])
+def test_step_horizon_extremes(star, oracle_mod, H, world):
+    """Projection horizons at the ends of the supported range (H = 0: current loads only; H = 256)
+    through the Step API, one rank and the gathered 4-rank form: loads and plan == oracle."""
+    from paper_2510_13668_b200.step import RecordLayout, Step, split_snapshot_by_rank
+    n, r_per, d = 8, 64, 1024
+    snap = datagen.make_snapshot(13 + H, n, r_per, skewed=True)
+    params_h = datagen.make_plan_params(snap, H=H, max_moves=3)
+    params = star.PlanParams.from_host(params_h)
+    pw = datagen.make_predictor_weights(13, d, "bf16")
+    W, b = _weights_dev(pw, False)
+    idxs = [split_snapshot_by_rank(snap.inst, n, world, k) for k in range(world)]
+    r_cap = max(len(i) for i in idxs)
+    pred = star.Predictor(*W, *b, max_rows=r_cap)
+    buf = (torch.zeros(world * RecordLayout(n // world, H, r_cap).nbytes, dtype=torch.uint8, device="cuda")
+           if world > 1 else None)
+    steps = []
+    for k, idx in enumerate(idxs):
+        st = Step(pred, params, n, r_cap=r_cap, rank=k, world=world, gathered=buf)
+        st.load_requests(*(torch.from_numpy(np.ascontiguousarray(a[idx])) for a in (snap.req_id, snap.inst,
+                                                                                      snap.n_tok)))
+        h = datagen.make_hidden(130 + k, len(idx), d, "bf16",
+                                scale=np.maximum(snap.true_rem[idx], 1).astype(np.float32) / 60.0)
+        st.run(_dev(h, torch.bfloat16))
+        steps.append(st)
+    torch.cuda.synchronize()
+    order = np.concatenate(idxs)
+    nh = np.concatenate([st.v["n_hat"][:len(i)].cpu().numpy() for st, i in zip(steps, idxs)])
+    ids, inst, n_tok = (a[order] for a in (snap.req_id, snap.inst, snap.n_tok))
+    ref_p = oracle_mod.project(inst, n_tok, nh, n, H, params_h.beta_q)
+    for k, st in enumerate(steps):
+        loc = slice(k * (n // world), (k + 1) * (n // world))
+        assert np.array_equal(st.v["L"].cpu().numpy(), ref_p["L"][loc])
+        assert np.array_equal(st.v["W"].cpu().numpy(), ref_p["W"][loc])
+    ref = oracle_mod.plan(params_h, ref_p["L"], ids, inst, n_tok, nh, None)
+    assert steps[-1].result() == ref
+    assert steps[-1].err.item() == 0
+    pred.close()
+
+
 def test_step_capture_replay_guards(star, oracle_mod):
     """Step.capture / replay (the public one-launch-per-step API): a replay after new request data
     of the same count equals a fresh run; a changed request count refuses to replay stale grids."""
