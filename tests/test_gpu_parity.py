@@ -829,6 +829,60 @@ def test_step_horizon_extremes(star, oracle_mod, H, world):
     pred.close()
 
 
+def test_step_refresh_gathered_ranks(star, oracle_mod):
+    """The cadence-k mode on every rank of a 4-rank job (gathered records on one GPU): each rank's
+    refreshed / aged N_hat and cadence state follow oracle.refresh_step (aged rows and state
+    exact, refreshed rows within the bf16 tolerance), its loads equal the oracle projection of its
+    own N_hat, and every rank's plan over the gathered records equals the oracle's."""
+    from paper_2510_13668_b200.step import RecordLayout, Step, split_snapshot_by_rank
+    n, world, r_per, d, k = 8, 4, 96, 1024, 5
+    snap = datagen.make_snapshot(17, n, r_per, skewed=True)
+    params_h = datagen.make_plan_params(snap, H=50, max_moves=2)
+    params = star.PlanParams.from_host(params_h)
+    pw = datagen.make_predictor_weights(17, d, "bf16")
+    W, b = _weights_dev(pw, False)
+    g = datagen.rng(17)
+    idxs = [split_snapshot_by_rank(snap.inst, n, world, q) for q in range(world)]
+    r_cap = max(len(i) for i in idxs)
+    pred = star.Predictor(*W, *b, max_rows=r_cap)
+    buf = torch.zeros(world * RecordLayout(n // world, 50, r_cap).nbytes, dtype=torch.uint8, device="cuda")
+    steps, states = [], []
+    for q, idx in enumerate(idxs):
+        R = len(idx)
+        h = datagen.make_hidden(170 + q, R, d, "bf16", scale=np.maximum(snap.true_rem[idx], 1).astype(np.float32) / 60.0)
+        gen = g.integers(10, 3000, R).astype(np.int32)
+        g_last = np.where(g.random(R) < 0.2, -1, gen - g.integers(0, 2 * k, R)).astype(np.int32)
+        nhat_last = g.integers(0, 5000, R).astype(np.int32)
+        st = Step(pred, params, n, r_cap=r_cap, rank=q, world=world, gathered=buf, refresh_k=k)
+        st.load_requests(*(torch.from_numpy(np.ascontiguousarray(a[idx])) for a in (snap.req_id, snap.inst,
+                                                                                      snap.n_tok)))
+        st.set_generation(torch.from_numpy(gen), torch.from_numpy(g_last), torch.from_numpy(nhat_last))
+        st.run(_dev(h, torch.bfloat16))
+        steps.append(st)
+        states.append((h, gen, g_last, nhat_last))
+    torch.cuda.synchronize()
+    nhs = []
+    for st, idx, (h, gen, g_last, nhat_last) in zip(steps, idxs, states):
+        R = len(idx)
+        nh_ref, gl_ref, nl_ref, due = oracle_mod.refresh_step(h, pw, snap.n_tok[idx], gen, g_last, nhat_last, k)
+        nh = st.v["n_hat"][:R].cpu().numpy()
+        assert np.array_equal(nh[~due], nh_ref[~due])
+        assert np.array_equal(st.g_last[:R].cpu().numpy(), gl_ref)
+        d_ = np.abs(nh[due].astype(np.float64) - nh_ref[due])
+        assert np.all(d_ <= np.maximum(1.0, 2e-2 * np.abs(nh_ref[due])) + 1.0)
+        assert int(st.n_refreshed.item()) == int(due.sum())
+        nhs.append(nh)
+    order = np.concatenate(idxs)
+    nh_all = np.concatenate(nhs)
+    ids, inst, n_tok = (a[order] for a in (snap.req_id, snap.inst, snap.n_tok))
+    ref_p = oracle_mod.project(inst, n_tok, nh_all, n, 50, params_h.beta_q)
+    for q, st in enumerate(steps):
+        assert np.array_equal(st.v["L"].cpu().numpy(), ref_p["L"][2 * q:2 * q + 2])
+    ref = oracle_mod.plan(params_h, ref_p["L"], ids, inst, n_tok, nh_all, None)
+    assert steps[-1].result() == ref and steps[-1].err.item() == 0
+    pred.close()
+
+
 def test_step_capture_replay_guards(star, oracle_mod):
     """Step.capture / replay (the public one-launch-per-step API): a replay after new request data
     of the same count equals a fresh run; a changed request count refuses to replay stale grids."""
