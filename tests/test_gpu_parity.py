@@ -883,6 +883,53 @@ def test_step_refresh_gathered_ranks(star, oracle_mod):
     pred.close()
 
 
+def test_step_refresh_over_many_steps(star, oracle_mod):
+    """The cadence state evolving over 12 decode steps (every request generates one token per step,
+    the hidden states change every step): each step's N_hat, g_last and N_hat_last follow
+    oracle.refresh_step from the previous step's oracle state (aged rows exact; refreshed rows
+    within the bf16 tolerance, the oracle then continues from the GPU's own N_hat so the
+    comparison does not drift), loads and plan == oracle."""
+    from paper_2510_13668_b200.step import Step
+    n, r_per, d, k = 4, 64, 1024, 4
+    snap = datagen.make_snapshot(19, n, r_per, skewed=True)
+    R = snap.R
+    params_h = datagen.make_plan_params(snap, H=50, max_moves=1)
+    params = star.PlanParams.from_host(params_h)
+    pw = datagen.make_predictor_weights(19, d, "bf16")
+    W, b = _weights_dev(pw, False)
+    pred = star.Predictor(*W, *b, max_rows=R)
+    st = Step(pred, params, n, r_cap=R, refresh_k=k)
+    n_tok = snap.n_tok.copy()
+    gen = np.zeros(R, np.int32)
+    g_last = np.full(R, -1, np.int32)
+    nhat_last = np.zeros(R, np.int32)
+    st.load_requests(*(torch.from_numpy(a) for a in (snap.req_id, snap.inst, n_tok)))
+    st.set_generation(torch.from_numpy(gen), torch.from_numpy(g_last), torch.from_numpy(nhat_last))
+    for step in range(12):
+        h = datagen.make_hidden(1900 + step, R, d, "bf16", scale=np.maximum(snap.true_rem, 1).astype(np.float32) / 60.0)
+        st.v["n_tok"][:R].copy_(torch.from_numpy(n_tok))
+        st.set_generation(torch.from_numpy(gen))
+        st.run(_dev(h, torch.bfloat16))
+        torch.cuda.synchronize()
+        nh_ref, gl_ref, nl_ref, due = oracle_mod.refresh_step(h, pw, n_tok, gen, g_last, nhat_last, k)
+        nh = st.v["n_hat"][:R].cpu().numpy()
+        assert np.array_equal(nh[~due], nh_ref[~due]), step
+        assert np.array_equal(st.g_last[:R].cpu().numpy(), gl_ref), step
+        d_ = np.abs(nh[due].astype(np.float64) - nh_ref[due])
+        assert np.all(d_ <= np.maximum(1.0, 2e-2 * np.abs(nh_ref[due])) + 1.0), step
+        nl = st.nhat_last[:R].cpu().numpy()
+        assert np.array_equal(nl[~due], nl_ref[~due]) and np.array_equal(nl[due], nh[due]), step
+        ref_p = oracle_mod.project(snap.inst, n_tok, nh, n, 50, params_h.beta_q)
+        assert np.array_equal(st.v["L"].cpu().numpy(), ref_p["L"]), step
+        assert st.result() == oracle_mod.plan(params_h, ref_p["L"], snap.req_id, snap.inst, n_tok, nh, None), step
+        # next step: continue from the GPU's own state; every request generates one token
+        g_last, nhat_last = gl_ref, nl.copy()
+        gen = gen + 1
+        n_tok = n_tok + 1
+    assert st.err.item() == 0
+    pred.close()
+
+
 def test_step_capture_replay_guards(star, oracle_mod):
     """Step.capture / replay (the public one-launch-per-step API): a replay after new request data
     of the same count equals a fresh run; a changed request count refuses to replay stale grids."""
