@@ -41,8 +41,10 @@ CONFIG_ORDER = ["C1", "C2", "C3", "C4", "TGT"]
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
-    ap.add_argument("--warmup", type=int, default=20)
+    # defaults per arm (None = not given): the GPU arm 500 / 20; the reference arm (the CPU oracle,
+    # ~1.3 s per whole TGT step on 16 cores) 10 / 2, so that a bare run of either ends within minutes
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", choices=["star", "reference"], default="star")
     ap.add_argument("--config", default="TGT", choices=CONFIG_ORDER)
     ap.add_argument("--seed", type=int, default=0)
@@ -54,7 +56,12 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU budget of the cpu_baseline sample")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no clocks/e2e/cpu legs")
     ap.add_argument("--json-out", default=None)
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 10 if args.impl == "reference" else 500
+    if args.warmup is None:
+        args.warmup = 2 if args.impl == "reference" else 20
+    return args
 
 
 def dist_env():
