@@ -1129,3 +1129,16 @@ def test_f32_small_path_many_instances_falls_back(star, oracle_mod):
     for k in ("L", "W", "peak", "growth", "count"):
         assert np.array_equal(getattr(out, k).cpu().numpy(), rp[k]), k
     pred.close()
+
+
+def test_example_decode_loop(star):
+    """examples/decode_loop.py (the serving-loop example of the README) runs end to end through the
+    public API, in both prediction modes."""
+    import importlib.util
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples", "decode_loop.py")
+    spec = importlib.util.spec_from_file_location("decode_loop", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.main(["--steps", "6", "--requests", "32", "--d", "1024"]) >= 0
+    assert mod.main(["--steps", "6", "--requests", "32", "--d", "1024", "--k", "4"]) >= 0
