@@ -1142,3 +1142,4 @@ def test_example_decode_loop(star):
     spec.loader.exec_module(mod)
     assert mod.main(["--steps", "6", "--requests", "32", "--d", "1024"]) >= 0
     assert mod.main(["--steps", "6", "--requests", "32", "--d", "1024", "--k", "4"]) >= 0
+    assert mod.main(["--steps", "12", "--requests", "32", "--d", "1024", "--kv"]) >= 0
