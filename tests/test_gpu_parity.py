@@ -1143,3 +1143,55 @@ def test_example_decode_loop(star):
     assert mod.main(["--steps", "6", "--requests", "32", "--d", "1024"]) >= 0
     assert mod.main(["--steps", "6", "--requests", "32", "--d", "1024", "--k", "4"]) >= 0
     assert mod.main(["--steps", "12", "--requests", "32", "--d", "1024", "--kv"]) >= 0
+
+
+_FALLBACK_SCRIPT = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import datagen, oracle
+import paper_2510_13668_b200 as star
+from paper_2510_13668_b200.step import Step
+out = []
+for dt, d, R, n in (("bf16", 1024, 384, 4), ("f32", 896, 128, 2)):
+    pw = datagen.make_predictor_weights(31, d, dt)
+    snap = datagen.make_snapshot(31, n, R // n, skewed=True)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    W = [torch.from_numpy(w).to(tdt).cuda() for w in (pw.W1, pw.W2, pw.W3)]
+    pred = star.Predictor(*W, torch.from_numpy(pw.w4).cuda(), max_rows=R)
+    assert pred.path(R) == 0, "the one-launch forms are switched off"
+    params_h = datagen.make_plan_params(snap, H=50, max_moves=2)
+    st = Step(pred, star.PlanParams.from_host(params_h), n, r_cap=R)
+    st.load_requests(*(torch.from_numpy(a) for a in (snap.req_id, snap.inst, snap.n_tok)))
+    h = datagen.make_hidden(31, R, d, dt, scale=np.maximum(snap.true_rem, 1).astype(np.float32) / 60.0)
+    st.run(torch.from_numpy(h).to(tdt).cuda())
+    torch.cuda.synchronize()
+    nh = st.v["n_hat"][:R].cpu().numpy()
+    y, _ = star.lenpred_forward(pred, torch.from_numpy(h).to(tdt).cuda())
+    torch.cuda.synchronize()
+    ref = oracle.lenpred_weights(h, pw)
+    err = float(np.max(np.abs(y.cpu().numpy() - ref) / np.maximum(np.abs(ref), 1.0)))
+    assert err <= (2e-2 if dt == "bf16" else 1e-3), err
+    rp = oracle.project(snap.inst, snap.n_tok, nh, n, 50, params_h.beta_q)
+    assert np.array_equal(st.v["L"].cpu().numpy(), rp["L"])
+    assert st.result() == oracle.plan(params_h, rp["L"], snap.req_id, snap.inst, snap.n_tok, nh, None)
+    out.append(err)
+print("fallback ok", out)
+'''
+
+
+@pytest.mark.parametrize("env", [{"STAR_SMALL": "0", "STAR_F32_SMALL": "0"},
+                                 {"STAR_TAIL2": "0", "STAR_SMALL": "0", "STAR_F32_SMALL": "0"},
+                                 {"STAR_PLAN_FUSE": "1", "STAR_SMALL": "0", "STAR_F32_SMALL": "0"}])
+def test_fallback_paths_subprocess(star, env):
+    """The paths a device takes when the one-launch forms are unavailable (their co-residency
+    check fails, e.g. on an MPS partition) or switched off, in a fresh process: the multi-launch
+    predictor (round-1 fused tail, 3xTF32 GEMMs), the fused plan in the tail's last CTA; Step ==
+    oracle (loads, plan), predictor within tolerance."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _FALLBACK_SCRIPT, root], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "fallback ok" in r.stdout
