@@ -86,26 +86,6 @@ __device__ __forceinline__ Cand warp_argmax_g(Cand c) {
   return c;
 }
 
-// a * b (mod 2^128) for a 32-bit unsigned b: four 32x32->64 multiply-adds over the limbs of a
-// (the generic __int128 product costs ~4x as many IMADs and dominated the candidate scoring).
-__device__ __forceinline__ i128 mul_u32(i128 a, uint32_t b) {
-  const unsigned __int128 ua = (unsigned __int128)a;
-  const uint64_t lo = (uint64_t)ua, hi = (uint64_t)(ua >> 64);
-  const uint64_t p0 = (uint64_t)(uint32_t)lo * b;
-  const uint64_t p1 = (lo >> 32) * b + (p0 >> 32);
-  const uint64_t p2 = (uint64_t)(uint32_t)hi * b + (p1 >> 32);
-  const uint64_t p3 = (hi >> 32) * b + (p2 >> 32);
-  const uint64_t rlo = (p0 & 0xFFFFFFFFull) | (p1 << 32);
-  const uint64_t rhi = (p2 & 0xFFFFFFFFull) | (p3 << 32);
-  return (i128)(((unsigned __int128)rhi << 64) | rlo);
-}
-// a * b (mod 2^128) for a 32-bit signed b
-__device__ __forceinline__ i128 mul_i32(i128 a, int32_t b) {
-  const uint32_t m = b < 0 ? (uint32_t)(-(int64_t)b) : (uint32_t)b;
-  const i128 r = mul_u32(a, m);
-  return b < 0 ? -r : r;
-}
-
 template <class T>
 __device__ __forceinline__ T* carve(uint8_t*& p, size_t count) {
   // align by pointer arithmetic (an integer round trip would lose the shared address space and

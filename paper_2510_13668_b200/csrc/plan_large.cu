@@ -2,16 +2,21 @@
 // tens of thousands of running requests; the paper's budget is <= 300 ms at 256 instances,
 // PAPER.md:460).  Same exact-integer semantics and candidate order as plan.cu (the GPU parity
 // tests compare both against the CPU oracle); the state lives in a global workspace instead of
-// one CTA's shared memory and every round is two launches:
-//   plan_prep_kernel   per-instance W_i and the beta-weighted prefix sums P0_i / P1_i (one warp
-//                      per instance; round 0 also copies the gathered loads and clears the
-//                      moved bitmap; later rounds rebuild only the two instances the last move
-//                      touched)
-//   plan_scan_kernel   every CTA classifies (Phase 1) from the global W, scores its slice of the
-//                      requests against every target in U (Phase 2/3, best_target), reduces to a
-//                      CTA candidate; the last CTA to arrive picks m* in the total order
-//                      (gain desc, req_id asc, dst asc), applies it to the loads, records the
-//                      move and marks the round's dirty instances (or sets the stop flag).
+// one CTA's shared memory; round 0 is two launches, every later round one:
+//   plan_prep_kernel   (round 0) per-instance W_i and the beta-weighted prefix sums P0_i / P1_i
+//                      (one warp per instance), the B0/B1/B2 prefix sums of beta, the gathered
+//                      loads copied, the moved bitmap cleared
+//   plan_scan_kernel   every CTA classifies (Phase 1) from the global W (a thread per instance),
+//                      reads a strided share of the slots (a thread per slot, one round trip for
+//                      the request fields), compacts its candidates in shared memory, and scores
+//                      its (candidate, target in U) pairs spread over all threads (Phase 2/3,
+//                      loads batched four deep), folding the results into per-thread bests that
+//                      are reduced once to a CTA candidate; the last CTA to arrive picks m* in the
+//                      total order (gain desc, req_id asc, dst asc), applies it to the loads,
+//                      rebuilds the two touched instances' W and prefix sums and records the move
+//                      (or sets the stop flag).
+// The scan is L2-latency bound (a few hundred candidates x a few hundred targets of exact int128
+// arithmetic): every step is laid out to keep dependent global round trips few.
 // Kernel boundaries are the grid-wide synchronisation; every kernel exits immediately once the
 // stop flag is set, so the host can enqueue max_moves rounds without reading anything back.
 #include <cstdint>
@@ -32,6 +37,7 @@ struct LargeWS {
   i128* P0;           // [n][H+1]
   i128* P1;           // [n][H+1]
   i128* Wv;           // [n]
+  i128* Bt;           // [3][H+1] B0/B1/B2 prefix sums of beta (prep, round 0)
   uint32_t* moved;    // [ceil(slots/32)]
   Cand* cta_best;     // [kMaxScanCtas]
   uint32_t* ctr;      // arrival counter
@@ -49,6 +55,7 @@ static LargeWS carve(void* ws, int n, int H, int64_t slots, size_t* total) {
   w.P0 = reinterpret_cast<i128*>(p + o); o = align16(o + 16 * (size_t)n * H1);
   w.P1 = reinterpret_cast<i128*>(p + o); o = align16(o + 16 * (size_t)n * H1);
   w.Wv = reinterpret_cast<i128*>(p + o); o = align16(o + 16 * (size_t)n);
+  w.Bt = reinterpret_cast<i128*>(p + o); o = align16(o + 16 * 3 * H1);
   w.moved = reinterpret_cast<uint32_t*>(p + o); o = align16(o + 4 * (size_t)((slots + 31) / 32));
   w.cta_best = reinterpret_cast<Cand*>(p + o); o = align16(o + sizeof(Cand) * kMaxScanCtas);
   w.ctr = reinterpret_cast<uint32_t*>(p + o); o = align16(o + 16);
@@ -64,9 +71,9 @@ __device__ void large_prefix_row(const PlanArgs& a, const LargeWS& w, int i, boo
   i128 wpart = 0, c0 = 0, c1 = 0;
   for (int base = 0; base < H1; base += 32) {
     const int t = base + lane;
-    const i128 x = t < H1 ? (i128)a.beta_q[t] * Li[t] : (i128)0;
+    const i128 x = t < H1 ? mul_u32((i128)Li[t], a.beta_q[t]) : (i128)0;
     if (t >= 1) wpart += x;
-    i128 x0 = x, x1 = x * t;
+    i128 x0 = x, x1 = mul_u32(x, (uint32_t)t);
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off);
@@ -104,6 +111,34 @@ __global__ void __launch_bounds__(kPrepThreads) plan_prep_kernel(const PlanArgs 
       *w.ctr = 0;
       *a.n_moves = 0;
     }
+    if (blockIdx.x == gridDim.x - 1 && (threadIdx.x >> 5) == (blockDim.x >> 5) - 1) {   // B0/B1/B2 (warp scan)
+      i128 c0 = 0, c1 = 0, c2 = 0;
+      for (int base = 0; base < H1; base += 32) {
+        const int u = base + lane;
+        const i128 bt = u < H1 ? (i128)a.beta_q[u] : (i128)0;
+        i128 x0 = bt, x1 = mul_u32(bt, (uint32_t)u), x2 = mul_u32(x1, (uint32_t)u);
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off), y2 = shfl_up_i128(x2, off);
+          if (lane >= off) {
+            x0 += y0;
+            x1 += y1;
+            x2 += y2;
+          }
+        }
+        x0 += c0;
+        x1 += c1;
+        x2 += c2;
+        if (u < H1) {
+          w.Bt[u] = x0;
+          w.Bt[H1 + u] = x1;
+          w.Bt[2 * H1 + u] = x2;
+        }
+        c0 = shfl_idx_i128(x0, 31);
+        c1 = shfl_idx_i128(x1, 31);
+        c2 = shfl_idx_i128(x2, 31);
+      }
+    }
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < (slots + 31) / 32;
          k += (int64_t)gridDim.x * blockDim.x)
       w.moved[k] = 0u;
@@ -113,14 +148,104 @@ __global__ void __launch_bounds__(kPrepThreads) plan_prep_kernel(const PlanArgs 
       __syncwarp();
       large_prefix_row(a, w, i, cur_only);
     }
-  } else {
-    if (w.state[0]) return;
-    if (gw < 2) large_prefix_row(a, w, w.state[2 + gw], cur_only);   // the two rows the last move touched
+  }
+}
+
+// Branch-free candidate order (gain desc, req_id asc, dst asc): used between shuffle steps, where a
+// divergent select would send the next shuffle down the slow (BRA.DIV) path.
+__device__ __forceinline__ bool lg_better(const Cand& x, const Cand& y) {
+  const bool tie = (x.id < y.id) | ((x.id == y.id) & (x.dst < y.dst));
+  return (x.g >= 0) & ((y.g < 0) | (x.score > y.score) | ((x.score == y.score) & tie));
+}
+__device__ __forceinline__ void lg_take(Cand& c, const Cand& o) {
+  const bool b = lg_better(o, c);
+  c.score = b ? o.score : c.score;
+  c.id = b ? o.id : c.id;
+  c.dst = b ? o.dst : c.dst;
+  c.g = b ? o.g : c.g;
+}
+__device__ __forceinline__ Cand lg_warp_argmax(Cand c) {
+  __syncwarp();   // reconverge first
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    Cand o;
+    const uint64_t lo = __shfl_xor_sync(0xFFFFFFFFu, (uint64_t)c.score, off);
+    const uint64_t hi = __shfl_xor_sync(0xFFFFFFFFu, (uint64_t)(c.score >> 64), off);
+    o.score = (i128)(((unsigned __int128)hi << 64) | lo);
+    o.id = __shfl_xor_sync(0xFFFFFFFFu, c.id, off);
+    o.dst = __shfl_xor_sync(0xFFFFFFFFu, c.dst, off);
+    o.g = __shfl_xor_sync(0xFFFFFFFFu, c.g, off);
+    lg_take(c, o);
+  }
+  return c;
+}
+
+// Per-candidate terms of the score (closed-form gain 2n * score; same arithmetic
+// as plan.cu's best_target with the int128 products taken by 32-bit limbs: N, N_hat are int32):
+//   score(u) = N (P0_src[T] - P0_u[T]) + (P1_src[T] - P1_u[T]) - (N^2 B0[T] + 2N B1[T] + B2[T]).
+struct LgCands {
+  int src[kScanThreads], rid[kScanThreads], g[kScanThreads], N[kScanThreads], nh[kScanThreads], T[kScanThreads];
+  int64_t need[kScanThreads];                       // C_mem demand (reading A18)
+  i128 self[kScanThreads], p0[kScanThreads], p1[kScanThreads], mig[kScanThreads];
+};
+
+// Phase 2/3 over the CTA's (candidate, target) pairs, spread over all threads (the scoring is a
+// dependent chain of int128 steps, so spreading the pairs, not the candidates, shortens the
+// slowest thread); four pairs per thread and step with every load issued before any score is
+// formed.  kSm: the per-target terms a + b L_u[0] and the C_mem slack are staged in shared memory
+// (else formed here from global memory: tables too large to stage).
+template <bool kSm>
+__device__ __forceinline__ void lg_score_pairs(const PlanArgs& a, bool strict, bool cur_only, const LgCands& cs,
+                                               int nc, const int* ulist, const i128* utex, const int64_t* uslack,
+                                               int nU, const LargeWS& w, int H1, Cand& best) {
+  constexpr int kU = 4;
+  const int npairs = nc * nU, bd = blockDim.x;
+  for (int pi0 = threadIdx.x; pi0 < npairs; pi0 += kU * bd) {
+    int ci[kU], u[kU];
+    i128 p0[kU], p1[kU], tex[kU];
+    int64_t slack[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int pi = pi0 + k * bd;
+      const bool v = pi < npairs;
+      const int c = v ? pi / nU : 0, q = v ? pi - c * nU : 0;
+      ci[k] = c;
+      u[k] = v ? ulist[q] : -1;
+      const int uu = v ? u[k] : 0;   // loads of row 0 stand in for absent pairs
+      const int64_t o = (int64_t)uu * H1 + cs.T[c];
+      p0[k] = w.P0[o];
+      p1[k] = w.P1[o];
+      if (kSm) {
+        tex[k] = utex[q];
+        slack[k] = uslack[q];
+      } else {
+        const int64_t L0 = w.Ls[(int64_t)uu * H1];
+        tex[k] = (i128)a.a_ps + (i128)a.b_ps * L0;
+        slack[k] = 0;
+        if (a.c_mem) {
+          const i128 sl = (i128)a.c_mem[uu] - L0 - (strict ? 0 : (a.reserved ? a.reserved[uu] : 0));
+          slack[k] = sl > (i128)INT64_MAX ? INT64_MAX : (sl < (i128)INT64_MIN ? INT64_MIN : (int64_t)sl);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int c = ci[k];
+      bool ok = u[k] >= 0;
+      if (!cur_only) ok &= mul_i32(tex[k], cs.nh[c]) > cs.mig[c];   // (a): N_hat (a + b L_u[0]) > c0 + c1 N
+      if (a.c_mem) ok &= cs.need[c] <= slack[k];                    // (b): C_mem
+      Cand cd;
+      cd.score = mul_i32(cs.p0[c] - p0[k], cs.N[c]) + (cs.p1[c] - p1[k]) - cs.self[c];
+      cd.id = cs.rid[c];
+      cd.dst = u[k];
+      cd.g = (ok & (cd.score > 0)) ? cs.g[c] : -1;
+      lg_take(best, cd);
+    }
   }
 }
 
 __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs a, const LargeWS w,
-                                                                    int64_t slots, int round) {
+                                                                    int64_t slots, int round, int lu_smem) {
   extern __shared__ __align__(16) uint8_t smraw[];
   pdl_wait();
   pdl_launch_dependents();
@@ -128,15 +253,24 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
   const int n = a.n, H1 = a.H + 1;
   const bool strict = (a.flags & 1u) != 0;
   const bool cur_only = (a.flags & 2u) != 0;
-  i128* B = reinterpret_cast<i128*>(smraw);                      // [3][H+1]
-  int* ulist = reinterpret_cast<int*>(B + 3 * H1);               // [n]
-  int* seg_count = ulist + n;                                    // [world]
+  i128* B = reinterpret_cast<i128*>(smraw);                              // [3][H+1]
+  i128* utex = B + 3 * H1;                                               // [n] (lu_smem): a + b L_u[0] of ulist[q]
+  int64_t* uslack = reinterpret_cast<int64_t*>(utex + (lu_smem ? n : 0)); // [n] (lu_smem): C_mem slack of ulist[q]
+  int* ulist = reinterpret_cast<int*>(uslack + (lu_smem ? n : 0));        // [n]
+  int* seg_count = ulist + n;                                            // [world]
   uint8_t* inO = reinterpret_cast<uint8_t*>(seg_count + a.world);
   __shared__ Cand warp_best[kScanThreads / 32];
-  __shared__ int s_nU, s_anyO, s_last;
+  __shared__ i128 s_wpart[kScanThreads / 32];
+  __shared__ int s_nU, s_nc, s_last;
+  __shared__ LgCands cs;   // the CTA's candidates of the current slot chunk
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int bd = blockDim.x;
 
-  for (int k = tid; k < a.world; k += blockDim.x) {
+  if (tid == 0) {
+    s_nU = 0;
+    s_nc = 0;
+  }
+  for (int k = tid; k < a.world; k += bd) {
     int c = a.r_cap;
     if (a.r_count) {
       c = *seg_ptr(a.r_count, k, a.seg_stride);
@@ -147,95 +281,112 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
     }
     seg_count[k] = c;
   }
+  // Phase 1 from the global W: every thread sums / classifies its instances
+  i128 w_own = 0;
+  int64_t l_own = 0;
+  if (tid < n) {
+    w_own = w.Wv[tid];
+    l_own = w.Ls[(int64_t)tid * H1];
+  }
+  i128 wpart = w_own;
+  for (int i = tid + bd; i < n; i += bd) wpart += w.Wv[i];
   __syncwarp();   // reconverge first: shuffles of a diverged warp take a slow path
-  if (warp == nwarps - 1) {   // B0/B1/B2 prefix (warp scan)
-    i128 c0 = 0, c1 = 0, c2 = 0;
-    for (int base = 0; base < H1; base += 32) {
-      const int u = base + lane;
-      const i128 bt = u < H1 ? (i128)a.beta_q[u] : (i128)0;
-      i128 x0 = bt, x1 = bt * u, x2 = bt * u * u;
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const i128 y0 = shfl_up_i128(x0, off), y1 = shfl_up_i128(x1, off), y2 = shfl_up_i128(x2, off);
-        if (lane >= off) {
-          x0 += y0;
-          x1 += y1;
-          x2 += y2;
-        }
-      }
-      x0 += c0;
-      x1 += c1;
-      x2 += c2;
-      if (u < H1) {
-        B[u] = x0;
-        B[H1 + u] = x1;
-        B[2 * H1 + u] = x2;
-      }
-      c0 = shfl_idx_i128(x0, 31);
-      c1 = shfl_idx_i128(x1, 31);
-      c2 = shfl_idx_i128(x2, 31);
-    }
-  }
-  __syncwarp();
-  if (warp == 0) {   // Phase 1 from the global W
-    i128 wsum = 0;
-    for (int i = lane; i < n; i += 32) wsum += w.Wv[i];
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) wsum += shfl_xor_i128(wsum, m);
-    const i128 rhs = (i128)(a.theta_den + a.theta_num) * wsum;
-    bool anyO = false;
-    int nU = 0;
-    for (int base = 0; base < n; base += 32) {
-      const int i = base + lane;
-      bool o = false, u = false;
-      if (i < n) {
-        o = (i128)n * a.theta_den * w.Wv[i] > rhs;
-        u = !o && ((i128)n * a.theta_den * (i128)65536 * w.Ls[(int64_t)i * H1] < rhs);
-        inO[i] = o ? 1 : 0;
-      }
-      anyO |= __any_sync(0xFFFFFFFFu, o) != 0;
-      const uint32_t um = __ballot_sync(0xFFFFFFFFu, u);
-      if (u) ulist[nU + __popc(um & ((1u << lane) - 1u))] = i;
-      nU += __popc(um);
-    }
-    if (lane == 0) {
-      s_nU = nU;
-      s_anyO = anyO ? 1 : 0;
-    }
-  }
+  for (int m = 16; m >= 1; m >>= 1) wpart += shfl_xor_i128(wpart, m);
+  if (lane == 0) s_wpart[warp] = wpart;
+  for (int t = tid; t < 3 * H1; t += bd) B[t] = w.Bt[t];
   __syncthreads();
+  i128 wsum = 0;
+  for (int k = 0; k < nwarps; ++k) wsum += s_wpart[k];
+  const i128 rhs = mul_u32(wsum, (uint32_t)a.theta_den + (uint32_t)a.theta_num);   // den >= 1, num >= 0
+  bool any_o = false;
+  for (int i = tid; i < n; i += bd) {
+    const i128 Wi = i == tid ? w_own : w.Wv[i];
+    const int64_t L0 = i == tid ? l_own : w.Ls[(int64_t)i * H1];
+    const bool o = mul_u32(mul_u32(Wi, (uint32_t)n), (uint32_t)a.theta_den) > rhs;
+    const bool u = !o && (mul_u32(mul_u32(mul_u32((i128)L0, (uint32_t)n), (uint32_t)a.theta_den), 65536u) < rhs);
+    inO[i] = o ? 1 : 0;
+    any_o |= o;
+    if (u) {   // U in any order: the argmax is over a total order
+      const int q = atomicAdd(&s_nU, 1);
+      ulist[q] = i;
+      if (lu_smem) {
+        utex[q] = (i128)a.a_ps + (i128)a.b_ps * L0;
+        int64_t sk = 0;
+        if (a.c_mem) {
+          const i128 sl = (i128)a.c_mem[i] - L0 - (strict ? 0 : (a.reserved ? a.reserved[i] : 0));
+          sk = sl > (i128)INT64_MAX ? INT64_MAX : (sl < (i128)INT64_MIN ? INT64_MIN : (int64_t)sl);
+        }
+        uslack[q] = sk;
+      }
+    }
+  }
+  const int anyO = __syncthreads_or(any_o ? 1 : 0);
+  const int nU = s_nU;
 
   Cand best;
   best.score = 0;
   best.id = 0;
   best.dst = 0;
   best.g = -1;
-  if (s_anyO) {   // one request per warp at a time, lanes over the targets
-    const int nU = s_nU;
-    const int64_t gwarp = (int64_t)blockIdx.x * nwarps + warp, nwarp_all = (int64_t)gridDim.x * nwarps;
-    for (int64_t g = gwarp; g < slots; g += nwarp_all) {
-      const int k = (int)(g / a.r_cap), j = (int)(g % a.r_cap);
-      if (j >= seg_count[k]) continue;
-      if ((w.moved[g >> 5] >> (g & 31)) & 1u) continue;
-      const int32_t src = seg_ptr(a.inst, k, a.seg_stride)[j];
-      if (src < 0 || src >= n) {
-        if (a.err && lane == 0) atomicOr(a.err, 1);
-        continue;
+  if (anyO) {
+    // Thread t of CTA b reads slot b + grid * (t + bd * it) (an instance's contiguous slots land in
+    // different CTAs), the CTA's candidates are compacted in shared memory, and the warps take them
+    // round-robin: every warp scores about the same number of candidates.
+    const int64_t grid = gridDim.x;
+    for (int64_t it0 = (int64_t)blockIdx.x; it0 < slots; it0 += grid * bd) {
+      const int64_t g = it0 + grid * tid;
+      bool cand = false;
+      int32_t src = 0, rid = 0, N = 0, nh = 0;
+      if (g < slots) {
+        const int k = (int)(g / a.r_cap), j = (int)(g % a.r_cap);
+        if (j < seg_count[k]) {
+          const uint32_t mw = w.moved[g >> 5];
+          src = seg_ptr(a.inst, k, a.seg_stride)[j];
+          N = seg_ptr(a.n_tok, k, a.seg_stride)[j];
+          nh = seg_ptr(a.n_hat, k, a.seg_stride)[j];
+          rid = seg_ptr(a.req_id, k, a.seg_stride)[j];
+          const bool pin = a.pinned && seg_ptr(a.pinned, k, a.seg_stride)[j];
+          const bool moved = (mw >> (g & 31)) & 1u;
+          const bool bad = src < 0 || src >= n;
+          if (bad && !moved && a.err) atomicOr(a.err, 1);
+          cand = !bad && !moved && !pin && inO[src];
+        }
       }
-      if (!inO[src]) continue;
-      if (a.pinned && seg_ptr(a.pinned, k, a.seg_stride)[j]) continue;
-      const int64_t N = seg_ptr(a.n_tok, k, a.seg_stride)[j];
-      const int64_t nh = seg_ptr(a.n_hat, k, a.seg_stride)[j];
-      const int32_t rid = seg_ptr(a.req_id, k, a.seg_stride)[j];
-      const Cand c = best_target_warp(a, strict, cur_only, (int)g, src, N, nh, rid, ulist, nU, w.Ls, w.P0, w.P1, B,
-                                      H1);
-      if (cand_better(c, best)) best = c;
+      if (cand) {
+        const int q = atomicAdd(&s_nc, 1);
+        cs.src[q] = src;
+        cs.rid[q] = rid;
+        cs.g[q] = (int)g;
+        cs.N[q] = N;
+        cs.nh[q] = nh;
+      }
+      __syncthreads();
+      const int nc = s_nc;
+      if (tid < nc) {   // the candidate's own terms, once
+        const int c_src = cs.src[tid], c_N = cs.N[tid], c_nh = cs.nh[tid];
+        int T = c_nh - 1 < 0 ? 0 : (c_nh - 1 > a.H ? a.H : c_nh - 1);
+        if (cur_only) T = 0;
+        cs.T[tid] = T;
+        cs.p0[tid] = w.P0[(int64_t)c_src * H1 + T];
+        cs.p1[tid] = w.P1[(int64_t)c_src * H1 + T];
+        cs.self[tid] = mul_i32(mul_i32(B[T], c_N), c_N) + mul_i32(B[H1 + T], c_N) * 2 + B[2 * H1 + T];
+        cs.mig[tid] = (i128)a.c0_ps + mul_i32((i128)a.c1_ps, c_N);
+        cs.need[tid] = strict ? (cur_only ? 0 : (int64_t)c_nh) : (int64_t)c_N + (cur_only ? 0 : (int64_t)c_nh);
+      }
+      __syncthreads();
+      if (lu_smem)
+        lg_score_pairs<true>(a, strict, cur_only, cs, nc, ulist, utex, uslack, nU, w, H1, best);
+      else
+        lg_score_pairs<false>(a, strict, cur_only, cs, nc, ulist, nullptr, nullptr, nU, w, H1, best);
+      __syncthreads();
+      if (tid == 0) s_nc = 0;
+      __syncthreads();
     }
   }
-  best = warp_argmax(best);
+  best = lg_warp_argmax(best);
   if (lane == 0) warp_best[warp] = best;
   __syncthreads();
-  __syncwarp();
   if (warp == 0) {
     Cand c;
     if (lane < nwarps) {
@@ -243,7 +394,7 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
     } else {
       c.score = 0; c.id = 0; c.dst = 0; c.g = -1;
     }
-    c = warp_argmax(c);
+    c = lg_warp_argmax(c);
     if (lane == 0) {
       w.cta_best[blockIdx.x] = c;
       fence_acq_rel_gpu();
@@ -251,12 +402,12 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
     }
   }
   __syncthreads();
-  if (!s_last || warp != 0) return;
+  if (!s_last) return;
   // ---- last CTA: m* over the CTA candidates (a total order, so the reduction order is free) ----
   fence_acq_rel_gpu();
   Cand c;
   c.score = 0; c.id = 0; c.dst = 0; c.g = -1;
-  for (int b = lane; b < (int)gridDim.x; b += 32) {   // written by other CTAs before fence + arrival: L2 reads
+  for (int b = tid; b < (int)gridDim.x; b += bd) {   // written by other CTAs before fence + arrival: L2 reads
     const ulonglong2* src = reinterpret_cast<const ulonglong2*>(w.cta_best + b);
     const ulonglong2 v0 = __ldcg(src), v1 = __ldcg(src + 1);
     Cand o;
@@ -264,29 +415,42 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
     o.id = (int32_t)(uint32_t)v1.x;
     o.dst = (int32_t)(uint32_t)(v1.x >> 32);
     o.g = (int32_t)(uint32_t)v1.y;
-    if (cand_better(o, c)) c = o;
+    lg_take(c, o);
   }
-  c = warp_argmax(c);
-  if (c.g < 0 || !s_anyO) {
-    if (lane == 0) {
+  c = lg_warp_argmax(c);
+  if (lane == 0) warp_best[warp] = c;
+  const int m0 = w.state[1];   // read by every thread before warp 0 updates it (after the barrier)
+  __syncthreads();
+  if (warp >= 2) return;
+  if (lane < nwarps) {
+    c = warp_best[lane];
+  } else {
+    c.score = 0; c.id = 0; c.dst = 0; c.g = -1;
+  }
+  c = lg_warp_argmax(c);   // warps 0 and 1 hold the same m*
+  if (c.g < 0 || !anyO) {
+    if (warp == 0 && lane == 0) {
       w.state[0] = 1;   // no improving move: stop
       *w.ctr = 0;
     }
     return;
   }
-  // ExecuteMigration is out of the path: apply m* to the loads for the next round.
+  // ExecuteMigration is out of the path: apply m* to the loads for the next round and rebuild the
+  // two touched instances' W and prefix sums here (no per-round prep launch): warp 0 takes the
+  // source row, warp 1 the destination row.
   const int k = c.g / a.r_cap, j = c.g % a.r_cap;
   const int src = seg_ptr(a.inst, k, a.seg_stride)[j];
   const int64_t N = seg_ptr(a.n_tok, k, a.seg_stride)[j];
   const int64_t nh = seg_ptr(a.n_hat, k, a.seg_stride)[j];
+  const int row = warp == 0 ? src : c.dst;
   for (int t = lane; t < H1; t += 32) {
     const int64_t ct = (t == 0) ? N : (t < nh ? N + t : 0);
-    w.Ls[(int64_t)src * H1 + t] -= ct;
-    w.Ls[(int64_t)c.dst * H1 + t] += ct;
+    w.Ls[(int64_t)row * H1 + t] += warp == 0 ? -ct : ct;
   }
-  if (lane == 0) {
+  __syncwarp();
+  if (m0 + 1 < a.max_moves) large_prefix_row(a, w, row, cur_only);   // each lane re-reads what it wrote
+  if (warp == 0 && lane == 0) {
     w.moved[c.g >> 5] |= 1u << (c.g & 31);
-    const int m = w.state[1];
     const i128 gain = (i128)2 * n * c.score;
     star_move mv;
     mv.req_id = c.id;
@@ -295,12 +459,12 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
     mv.round = round;
     mv.gain_hi = (int64_t)(gain >> 64);
     mv.gain_lo = (uint64_t)gain;
-    a.moves[m] = mv;
-    w.state[1] = m + 1;
-    *a.n_moves = m + 1;
+    a.moves[m0] = mv;
+    w.state[1] = m0 + 1;
+    *a.n_moves = m0 + 1;
     w.state[2] = src;
     w.state[3] = c.dst;
-    if (m + 1 >= a.max_moves) w.state[0] = 1;
+    if (m0 + 1 >= a.max_moves) w.state[0] = 1;
     *w.ctr = 0;
   }
 }
@@ -334,7 +498,9 @@ cudaError_t launch_plan_large(const PlanArgs& a, void* workspace, cudaStream_t s
   int scan_grid = (int)((slots + (kScanThreads / 32) - 1) / (kScanThreads / 32));   // a warp per request
   scan_grid = scan_grid < 1 ? 1 : (scan_grid > 2 * g_num_sms ? 2 * g_num_sms : scan_grid);
   const size_t H1 = (size_t)a.H + 1;
-  const size_t smem = 16 * 3 * H1 + 4 * (size_t)a.n + 4 * (size_t)a.world + (size_t)a.n + 16;
+  const size_t smem0 = 16 * 3 * H1 + 4 * (size_t)a.n + 4 * (size_t)a.world + (size_t)a.n + 16;
+  const int lu_smem = smem0 + 24 * (size_t)a.n <= 160 * 1024 ? 1 : 0;   // U's per-target terms beside the list
+  const size_t smem = smem0 + (lu_smem ? 24 * (size_t)a.n : 0);
   if (smem > 48 * 1024) {
     e = func_attr((const void*)plan_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -346,12 +512,8 @@ cudaError_t launch_plan_large(const PlanArgs& a, void* workspace, cudaStream_t s
   cs.stream = stream;
   cs.attrs = at;
   cs.numAttrs = 1;
-  cudaLaunchConfig_t cp1 = cp;
-  cp1.gridDim = dim3(1, 1, 1);
-  for (int r = 0; r < a.max_moves; ++r) {
-    if (r > 0 && (e = cudaLaunchKernelEx(&cp1, plan_prep_kernel, a, w, 0, slots)) != cudaSuccess) return e;
-    if ((e = cudaLaunchKernelEx(&cs, plan_scan_kernel, a, w, slots, r)) != cudaSuccess) return e;
-  }
+  for (int r = 0; r < a.max_moves; ++r)   // round r's last CTA rebuilds the rows round r + 1 reads
+    if ((e = cudaLaunchKernelEx(&cs, plan_scan_kernel, a, w, slots, r, lu_smem)) != cudaSuccess) return e;
   return cudaSuccess;
 }
 
