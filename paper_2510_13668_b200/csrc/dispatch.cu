@@ -16,13 +16,15 @@
 // chosen instance's load row gets c_r and its prefix-sum row is rebuilt by one warp scan.
 #include <cstdint>
 #include <cuda_runtime.h>
+#include "plan_core.cuh"
 #include "ptx.cuh"
 #include "star_internal.h"
 
 namespace star {
 
-typedef __int128 i128;
 constexpr int kDispThreads = 512;
+constexpr int kSeqMaxInst = 1024;   // dispatch_seq_kernel: one instance per thread
+constexpr int kSeqMaxArr = 4096;    // arrivals staged in shared memory
 
 struct DispArgs {
   int policy, n, H, A;
@@ -172,6 +174,244 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispArgs a
   }
 }
 
+// Sequential placement without rebuilding prefix sums (n <= 1024 instances, A <= 4096 arrivals).
+// Placing arrival r' (N', N_hat') on instance i adds c_t (c_0 = N', c_t = (N'+t)[t < N_hat']) to
+// L_i, so with m = min(T, T') (T' = clamp(N_hat' - 1, 0, H)) its prefix sums grow by the closed forms
+//     dP0_i[T] = N' B0[m] + B1[m],   dP1_i[T] = N' B1[m] + B2[m]
+// (B0/B1/B2 = prefix sums of beta_t, t beta_t, t^2 beta_t): exactly the terms the rebuilt row would
+// hold.  Thread i owns instance i: the initial prefix row (written once, read back only by i, one
+// arrival ahead), its current L_i[0] and the arrivals placed on it (those with T' = H, the
+// long-tailed majority, as a sum of N' and a count: O(1) per arrival; the others as a list); the
+// only sequential step per arrival is the block argmin (one barrier: the warp results are
+// double-buffered).
+// The loads L are updated once at the end (order-free integer atomics).
+__device__ __forceinline__ bool dkey_better_bf(const DKey& x, const DKey& y) {   // branch-free dkey_less
+  return (x.i >= 0) & ((y.i < 0) | (x.score < y.score) | ((x.score == y.score) & (x.i < y.i)));
+}
+__device__ __forceinline__ DKey dkey_argmin_bf(DKey k, int width) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    if (m >= width) continue;   // uniform
+    const DKey o = dkey_shfl(k, m);
+    const bool b = dkey_better_bf(o, k);
+    k.score = b ? o.score : k.score;
+    k.i = b ? o.i : k.i;
+  }
+  return k;
+}
+
+template <int J>   // instances per thread (i = J * tid + j)
+__global__ void __launch_bounds__(kSeqMaxInst / J) dispatch_seq_kernel(const DispArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ i128 wsc[2][32];
+  __shared__ int widx[2][32];
+  const int H1 = a.H + 1, n = a.n, A = a.A;
+  i128* B = reinterpret_cast<i128*>(sm);   // [3][H+1]
+  int* sN = reinterpret_cast<int*>(B + 3 * H1);
+  int* sNh = sN + A;
+  int* sT = sNh + A;
+  int* snext = sT + A;
+  int* sB = snext + A;
+  uint32_t* sbeta = reinterpret_cast<uint32_t*>(sB + A);   // [H+1]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = (int)(blockDim.x >> 5);
+  pdl_wait();
+  for (int t = tid; t < H1; t += blockDim.x) sbeta[t] = a.beta_q[t];
+  for (int r = tid; r < A; r += blockDim.x) {
+    const int N = a.n_tok[r], nh = a.n_hat[r];
+    sN[r] = N;
+    sNh[r] = nh;
+    sT[r] = nh - 1 < 0 ? 0 : (nh - 1 > a.H ? a.H : nh - 1);
+  }
+  if (a.policy == 2 && warp == 0) {   // B0/B1/B2 (warp scan)
+    i128 c0 = 0, c1 = 0, c2 = 0;
+    for (int base = 0; base < H1; base += 32) {
+      const int u = base + lane;
+      const i128 bt = u < H1 ? (i128)a.beta_q[u] : (i128)0;
+      i128 x0 = bt, x1 = mul_u32(bt, (uint32_t)u), x2 = mul_u32(x1, (uint32_t)u);
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const i128 y0 = shfl_up_i128d(x0, off), y1 = shfl_up_i128d(x1, off), y2 = shfl_up_i128d(x2, off);
+        if (lane >= off) {
+          x0 += y0;
+          x1 += y1;
+          x2 += y2;
+        }
+      }
+      x0 += c0;
+      x1 += c1;
+      x2 += c2;
+      if (u < H1) {
+        B[u] = x0;
+        B[H1 + u] = x1;
+        B[2 * H1 + u] = x2;
+      }
+      c0 = shfl_idx_i128d(x0, 31);
+      c1 = shfl_idx_i128d(x1, 31);
+      c2 = shfl_idx_i128d(x2, 31);
+    }
+  }
+  // per owned instance: current L_i[0], C_mem, reserved, the arrivals placed on it (those with
+  // T' = H as a sum of N', a count and their prefix-sum growth at T = H; the others as a list)
+  int64_t L0[J], cm[J], rs[J], sumN_H[J];
+  int head[J], cnt_H[J];
+  i128 corrH0[J], corrH1[J], nx0[J], nx1[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int i = J * tid + j;
+    L0[j] = i < n ? a.L[(int64_t)i * H1] : 0;
+    cm[j] = (i < n && a.c_mem) ? a.c_mem[i] : 0;
+    rs[j] = (i < n && a.reserved) ? a.reserved[i] : 0;
+    sumN_H[j] = 0;
+    head[j] = -1;
+    cnt_H[j] = 0;
+    corrH0[j] = corrH1[j] = nx0[j] = nx1[j] = 0;
+  }
+  __syncthreads();   // beta, arrivals, B staged
+  if (a.policy == 2) {   // the initial prefix rows of the owned instances (read back only by this thread)
+    for (int j = 0; j < J; ++j) {
+      const int i = J * tid + j;
+      if (i >= n) break;
+      i128 c0 = 0, c1 = 0;
+      for (int t0 = 0; t0 < H1; t0 += 16) {   // sixteen loads in flight, then the running sums
+        int64_t v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = t0 + k < H1 ? a.L[(int64_t)i * H1 + t0 + k] : 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int t = t0 + k;
+          if (t < H1) {
+            const i128 x = mul_u32((i128)v[k], sbeta[t]);
+            c0 += x;
+            c1 += mul_u32(x, (uint32_t)t);
+            a.P0[(int64_t)i * H1 + t] = c0;
+            a.P1[(int64_t)i * H1 + t] = c1;
+          }
+        }
+      }
+    }
+    if (A > 0) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) {   // P0_i / P1_i at the next arrival's T, one arrival ahead
+        const int i = J * tid + j;
+        if (i < n) {
+          nx0[j] = a.P0[(int64_t)i * H1 + sT[0]];
+          nx1[j] = a.P1[(int64_t)i * H1 + sT[0]];
+        }
+      }
+    }
+  }
+  for (int r = 0; r < A; ++r) {
+    const int N = sN[r], T = sT[r];
+    int b;
+    if (a.policy == 0) {
+      b = (int)(((int64_t)a.counter + r) % n);
+    } else {
+      DKey k;
+      k.score = 0;
+      k.i = -1;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int i = J * tid + j;
+        i128 p0 = nx0[j], p1 = nx1[j];
+        if (a.policy == 2 && i < n && r + 1 < A) {
+          nx0[j] = a.P0[(int64_t)i * H1 + sT[r + 1]];
+          nx1[j] = a.P1[(int64_t)i * H1 + sT[r + 1]];
+        }
+        DKey kj;
+        kj.score = 0;
+        kj.i = -1;
+        if (i < n) {
+          if (a.policy == 1) {
+            kj.score = (i128)L0[j];
+            kj.i = i;
+          } else {
+            bool ok = true;
+            if (a.c_mem) ok = (i128)L0[j] + rs[j] + N + sNh[r] <= (i128)cm[j];
+            if (T == a.H) {   // uniform: T is the arrival's
+              p0 += corrH0[j];
+              p1 += corrH1[j];
+            } else {
+              p0 += B[T] * (i128)sumN_H[j] + mul_u32(B[H1 + T], (uint32_t)cnt_H[j]);
+              p1 += B[H1 + T] * (i128)sumN_H[j] + mul_u32(B[2 * H1 + T], (uint32_t)cnt_H[j]);
+            }
+            for (int q = head[j]; q >= 0; q = snext[q]) {   // placed on i with T' < H
+              const int m = T < sT[q] ? T : sT[q];
+              const int Nq = sN[q];
+              p0 += mul_i32(B[m], Nq) + B[H1 + m];
+              p1 += mul_i32(B[H1 + m], Nq) + B[2 * H1 + m];
+            }
+            kj.score = mul_i32(p0, N) + p1;
+            kj.i = ok ? i : -1;
+          }
+        }
+        const bool bt = dkey_better_bf(kj, k);
+        k.score = bt ? kj.score : k.score;
+        k.i = bt ? kj.i : k.i;
+      }
+      __syncwarp();
+      k = dkey_argmin_bf(k, 32);
+      if (nwarps > 1) {
+        if (lane == 0) {
+          wsc[r & 1][warp] = k.score;
+          widx[r & 1][warp] = k.i;
+        }
+        __syncthreads();
+        if (lane < nwarps) {
+          k.score = wsc[r & 1][lane];
+          k.i = widx[r & 1][lane];
+        } else {
+          k.score = 0;
+          k.i = -1;
+        }
+        k = dkey_argmin_bf(k, nwarps);
+      }
+      b = __shfl_sync(0xFFFFFFFFu, k.i, 0);
+    }
+    if (tid == 0) {
+      a.assign[r] = b;
+      sB[r] = b;
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      if (b >= 0 && b == J * tid + j) {   // the owner records the placement
+        L0[j] += N;
+        if (T == a.H) {
+          sumN_H[j] += N;
+          ++cnt_H[j];
+          corrH0[j] += mul_i32(B[a.H], N) + B[H1 + a.H];
+          corrH1[j] += mul_i32(B[H1 + a.H], N) + B[2 * H1 + a.H];
+        } else {
+          snext[r] = head[j];
+          head[j] = r;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int r = warp; r < A; r += nwarps) {   // L_b[t] += c_r[t] (reading A5), order-free
+    const int b = sB[r];
+    if (b < 0) continue;
+    const int64_t N = sN[r], nh = sNh[r];
+    for (int t = lane; t < H1; t += 32) {
+      const int64_t c = t == 0 ? N : (t < nh ? N + t : 0);
+      if (c) atomicAdd(reinterpret_cast<unsigned long long*>(a.L + (int64_t)b * H1 + t), (unsigned long long)c);
+    }
+  }
+}
+
+template <int J>
+static cudaError_t launch_seq(cudaLaunchConfig_t cfg, const DispArgs& a, size_t smem) {
+  if (smem > 48 * 1024) {
+    const cudaError_t e =
+        func_attr((const void*)dispatch_seq_kernel<J>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const int threads = (a.n + J - 1) / J;
+  cfg.blockDim = dim3((unsigned)((threads + 31) / 32 * 32), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  return cudaLaunchKernelEx(&cfg, dispatch_seq_kernel<J>, a);
+}
+
 size_t dispatch_workspace_bytes(int n, int H) { return (size_t)n * (size_t)(H + 1) * 32; }
 
 cudaError_t launch_dispatch(int policy, int n, int H, const uint32_t* beta_q, int64_t* L, const int64_t* c_mem,
@@ -201,6 +441,12 @@ cudaError_t launch_dispatch(int policy, int n, int H, const uint32_t* beta_q, in
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  if (n <= kSeqMaxInst && A <= kSeqMaxArr) {
+    const size_t smem = 16 * 3 * (size_t)(H + 1) + 5 * 4 * (size_t)A + 4 * (size_t)(H + 1);
+    // one instance per thread (measured at 256 instances: two or four per thread on fewer warps
+    // is 1.0x / 1.5x slower per arrival; the argmin chain, not the issue rate, bounds it)
+    return launch_seq<1>(cfg, a, smem);
+  }
   return cudaLaunchKernelEx(&cfg, dispatch_kernel, a);
 }
 

@@ -244,15 +244,49 @@ __device__ __forceinline__ void lg_score_pairs(const PlanArgs& a, bool strict, b
   }
 }
 
+// One request slot's fields (slot g < slots: every segment holds r_cap slots of storage, so the
+// loads are in bounds before the slot is checked against the segment's request count).
+struct LgSlot {
+  int32_t src, rid, N, nh;
+  uint32_t mw;   // the slot's word of the moved bitmap
+  int pin;
+};
+__device__ __forceinline__ void lg_load_slot(const PlanArgs& a, const LargeWS& w, int64_t g, int64_t slots,
+                                             LgSlot& f) {
+  f.src = f.rid = f.N = f.nh = 0;
+  f.mw = 0u;
+  f.pin = 0;
+  if (g < slots) {
+    const int k = (int)(g / a.r_cap), j = (int)(g % a.r_cap);
+    f.mw = w.moved[g >> 5];
+    f.src = seg_ptr(a.inst, k, a.seg_stride)[j];
+    f.N = seg_ptr(a.n_tok, k, a.seg_stride)[j];
+    f.nh = seg_ptr(a.n_hat, k, a.seg_stride)[j];
+    f.rid = seg_ptr(a.req_id, k, a.seg_stride)[j];
+    f.pin = a.pinned ? seg_ptr(a.pinned, k, a.seg_stride)[j] : 0;
+  }
+}
+
 __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs a, const LargeWS w,
                                                                     int64_t slots, int round, int lu_smem) {
   extern __shared__ __align__(16) uint8_t smraw[];
   pdl_wait();
   pdl_launch_dependents();
-  if (w.state[0]) return;
   const int n = a.n, H1 = a.H + 1;
   const bool strict = (a.flags & 1u) != 0;
   const bool cur_only = (a.flags & 2u) != 0;
+  const int64_t grid = gridDim.x;
+  // every independent load of the round is issued here, together (the kernel is a chain of global
+  // round trips): the stop flag, this thread's first slot, its instance's W and L[0], the B table
+  LgSlot f;
+  lg_load_slot(a, w, (int64_t)blockIdx.x + grid * threadIdx.x, slots, f);
+  i128 w_own = 0;
+  int64_t l_own = 0;
+  if ((int)threadIdx.x < n) {
+    w_own = w.Wv[threadIdx.x];
+    l_own = w.Ls[(int64_t)threadIdx.x * H1];
+  }
+  if (w.state[0]) return;
   i128* B = reinterpret_cast<i128*>(smraw);                              // [3][H+1]
   i128* utex = B + 3 * H1;                                               // [n] (lu_smem): a + b L_u[0] of ulist[q]
   int64_t* uslack = reinterpret_cast<int64_t*>(utex + (lu_smem ? n : 0)); // [n] (lu_smem): C_mem slack of ulist[q]
@@ -282,12 +316,6 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
     seg_count[k] = c;
   }
   // Phase 1 from the global W: every thread sums / classifies its instances
-  i128 w_own = 0;
-  int64_t l_own = 0;
-  if (tid < n) {
-    w_own = w.Wv[tid];
-    l_own = w.Ls[(int64_t)tid * H1];
-  }
   i128 wpart = w_own;
   for (int i = tid + bd; i < n; i += bd) wpart += w.Wv[i];
   __syncwarp();   // reconverge first: shuffles of a diverged warp take a slow path
@@ -333,33 +361,26 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
     // Thread t of CTA b reads slot b + grid * (t + bd * it) (an instance's contiguous slots land in
     // different CTAs), the CTA's candidates are compacted in shared memory, and the warps take them
     // round-robin: every warp scores about the same number of candidates.
-    const int64_t grid = gridDim.x;
     for (int64_t it0 = (int64_t)blockIdx.x; it0 < slots; it0 += grid * bd) {
       const int64_t g = it0 + grid * tid;
+      if (it0 != (int64_t)blockIdx.x) lg_load_slot(a, w, g, slots, f);   // the first chunk is in f already
       bool cand = false;
-      int32_t src = 0, rid = 0, N = 0, nh = 0;
       if (g < slots) {
         const int k = (int)(g / a.r_cap), j = (int)(g % a.r_cap);
         if (j < seg_count[k]) {
-          const uint32_t mw = w.moved[g >> 5];
-          src = seg_ptr(a.inst, k, a.seg_stride)[j];
-          N = seg_ptr(a.n_tok, k, a.seg_stride)[j];
-          nh = seg_ptr(a.n_hat, k, a.seg_stride)[j];
-          rid = seg_ptr(a.req_id, k, a.seg_stride)[j];
-          const bool pin = a.pinned && seg_ptr(a.pinned, k, a.seg_stride)[j];
-          const bool moved = (mw >> (g & 31)) & 1u;
-          const bool bad = src < 0 || src >= n;
+          const bool moved = (f.mw >> (g & 31)) & 1u;
+          const bool bad = f.src < 0 || f.src >= n;
           if (bad && !moved && a.err) atomicOr(a.err, 1);
-          cand = !bad && !moved && !pin && inO[src];
+          cand = !bad && !moved && !f.pin && inO[f.src];
         }
       }
       if (cand) {
         const int q = atomicAdd(&s_nc, 1);
-        cs.src[q] = src;
-        cs.rid[q] = rid;
+        cs.src[q] = f.src;
+        cs.rid[q] = f.rid;
         cs.g[q] = (int)g;
-        cs.N[q] = N;
-        cs.nh[q] = nh;
+        cs.N[q] = f.N;
+        cs.nh[q] = f.nh;
       }
       __syncthreads();
       const int nc = s_nc;

@@ -443,6 +443,29 @@ def test_dispatch_bitexact_cluster_scale(star, oracle_mod, n, A):
         assert np.array_equal(Ld.cpu().numpy(), ref_L), policy
 
 
+@pytest.mark.parametrize("n,A,H", [(1, 40, 50), (33, 300, 7), (1024, 48, 50), (1100, 24, 50), (40, 4100, 3)])
+def test_dispatch_bitexact_kernel_limits(star, oracle_mod, n, A, H):
+    """Both dispatch kernels and their boundary: the sequential one-instance-per-thread kernel
+    (n <= 1024, A <= 4096: closed-form prefix corrections instead of row rebuilds) and the
+    row-rebuilding kernel above either limit; every policy bit-exact vs the from-scratch oracle,
+    with C_mem and reserved KV."""
+    g = datagen.rng(n * 7 + A)
+    L = g.integers(0, 20000, (n, H + 1)).astype(np.int64)
+    beta = datagen.beta_schedule_q16(H)
+    n_tok = g.integers(1, 4000, A).astype(np.int32)
+    n_hat = np.minimum(g.pareto(1.2, A) * 40, 20000).astype(np.int32)
+    c_mem = (L[:, 0] + g.integers(0, 60000, n)).astype(np.int64)
+    reserved = g.integers(0, 300, n).astype(np.int64)
+    for policy in (0, 1, 2):
+        ref_a, ref_L = oracle_mod.dispatch(policy, L, beta, n_tok, n_hat, c_mem, reserved, counter=5)
+        Ld = _dev(L)
+        got = star.dispatch_requests(policy, Ld, _dev(beta.astype(np.int32)), _dev(n_tok), _dev(n_hat), _dev(c_mem),
+                                     _dev(reserved), counter=5)
+        torch.cuda.synchronize()
+        assert got.cpu().numpy().tolist() == ref_a.tolist(), policy
+        assert np.array_equal(Ld.cpu().numpy(), ref_L), policy
+
+
 # ============================================================================ cluster-scale plan (NEXT-3)
 def _plan_gpu_large(star, params_h, L, snap, n_hat):
     pp = star.PlanParams.from_host(params_h)
