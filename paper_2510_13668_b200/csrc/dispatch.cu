@@ -188,16 +188,30 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispArgs a
 __device__ __forceinline__ bool dkey_better_bf(const DKey& x, const DKey& y) {   // branch-free dkey_less
   return (x.i >= 0) & ((y.i < 0) | (x.score < y.score) | ((x.score == y.score) & (x.i < y.i)));
 }
-__device__ __forceinline__ DKey dkey_argmin_bf(DKey k, int width) {
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) {
-    if (m >= width) continue;   // uniform
-    const DKey o = dkey_shfl(k, m);
-    const bool b = dkey_better_bf(o, k);
-    k.score = b ? o.score : k.score;
-    k.i = b ? o.i : k.i;
-  }
-  return k;
+
+// Warp argmin of (score, i) by hardware reductions: the key as five order-preserving 32-bit words
+// (score with its sign bit flipped, then i; an empty key is all ones), minimised word by word
+// among the lanes still tied (redux.sync: one instruction per word instead of a shuffle tree).
+__device__ __forceinline__ DKey dkey_argmin_redux(const DKey& k) {
+  const bool v = k.i >= 0;
+  const unsigned __int128 us = v ? ((unsigned __int128)k.score ^ ((unsigned __int128)1 << 127)) : ~(unsigned __int128)0;
+  const uint32_t w3 = (uint32_t)(us >> 96), w2 = (uint32_t)(us >> 64), w1 = (uint32_t)(us >> 32), w0 = (uint32_t)us;
+  const uint32_t wi = v ? (uint32_t)k.i : 0xFFFFFFFFu;
+  const uint32_t m3 = __reduce_min_sync(0xFFFFFFFFu, w3);
+  bool eq = w3 == m3;
+  const uint32_t m2 = __reduce_min_sync(0xFFFFFFFFu, eq ? w2 : 0xFFFFFFFFu);
+  eq &= w2 == m2;
+  const uint32_t m1 = __reduce_min_sync(0xFFFFFFFFu, eq ? w1 : 0xFFFFFFFFu);
+  eq &= w1 == m1;
+  const uint32_t m0 = __reduce_min_sync(0xFFFFFFFFu, eq ? w0 : 0xFFFFFFFFu);
+  eq &= w0 == m0;
+  const uint32_t mi = __reduce_min_sync(0xFFFFFFFFu, eq ? wi : 0xFFFFFFFFu);
+  DKey r;
+  r.i = (int)mi;   // 0xFFFFFFFF -> -1: no feasible key in the warp
+  const unsigned __int128 um = ((unsigned __int128)m3 << 96) | ((unsigned __int128)m2 << 64) |
+                               ((unsigned __int128)m1 << 32) | (unsigned __int128)m0;
+  r.score = (i128)(um ^ ((unsigned __int128)1 << 127));
+  return r;
 }
 
 template <int J>   // instances per thread (i = J * tid + j)
@@ -349,7 +363,7 @@ __global__ void __launch_bounds__(kSeqMaxInst / J) dispatch_seq_kernel(const Dis
         k.i = bt ? kj.i : k.i;
       }
       __syncwarp();
-      k = dkey_argmin_bf(k, 32);
+      k = dkey_argmin_redux(k);
       if (nwarps > 1) {
         if (lane == 0) {
           wsc[r & 1][warp] = k.score;
@@ -363,9 +377,9 @@ __global__ void __launch_bounds__(kSeqMaxInst / J) dispatch_seq_kernel(const Dis
           k.score = 0;
           k.i = -1;
         }
-        k = dkey_argmin_bf(k, nwarps);
+        k = dkey_argmin_redux(k);
       }
-      b = __shfl_sync(0xFFFFFFFFu, k.i, 0);
+      b = k.i;   // every lane holds the winner
     }
     if (tid == 0) {
       a.assign[r] = b;

@@ -443,7 +443,8 @@ def test_dispatch_bitexact_cluster_scale(star, oracle_mod, n, A):
         assert np.array_equal(Ld.cpu().numpy(), ref_L), policy
 
 
-@pytest.mark.parametrize("n,A,H", [(1, 40, 50), (33, 300, 7), (1024, 48, 50), (1100, 24, 50), (40, 4100, 3)])
+@pytest.mark.parametrize("n,A,H", [(1, 40, 50), (33, 300, 7), (1024, 48, 50), (1100, 24, 50), (16, 4096, 50),
+                                   (40, 4100, 3)])
 def test_dispatch_bitexact_kernel_limits(star, oracle_mod, n, A, H):
     """Both dispatch kernels and their boundary: the sequential one-instance-per-thread kernel
     (n <= 1024, A <= 4096: closed-form prefix corrections instead of row rebuilds) and the
