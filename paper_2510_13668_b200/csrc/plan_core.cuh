@@ -97,6 +97,49 @@ __device__ __forceinline__ i128 mul_i32(i128 a, int32_t b) {
   return b < 0 ? -r : r;
 }
 
+// Warp argmax in the order (score desc, id asc, dst asc, g asc) -- plan_fast.cuh cand_better_g --
+// by hardware reductions: the key as seven order-preserving
+// 32-bit words (the score complemented, so its maximum is the minimum; id, dst, g with the sign bit
+// flipped; an empty candidate all ones), minimised word by word among the lanes still tied
+// (redux.sync: one instruction per word instead of a five-step shuffle tree).  Every lane returns
+// the winner.
+__device__ __forceinline__ Cand warp_argmax_g(const Cand& c) {
+  __syncwarp();   // reconverge first
+  const bool v = c.g >= 0;
+  const unsigned __int128 us = v ? ~((unsigned __int128)c.score ^ ((unsigned __int128)1 << 127)) : ~(unsigned __int128)0;
+  const uint32_t w[4] = {(uint32_t)(us >> 96), (uint32_t)(us >> 64), (uint32_t)(us >> 32), (uint32_t)us};
+  const uint32_t wid = v ? (uint32_t)c.id ^ 0x80000000u : 0xFFFFFFFFu;
+  const uint32_t wdst = v ? (uint32_t)c.dst ^ 0x80000000u : 0xFFFFFFFFu;
+  const uint32_t wg = v ? (uint32_t)c.g ^ 0x80000000u : 0xFFFFFFFFu;
+  uint32_t m[4];
+  bool eq = true;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    m[k] = __reduce_min_sync(0xFFFFFFFFu, eq ? w[k] : 0xFFFFFFFFu);
+    eq &= w[k] == m[k];
+  }
+  const uint32_t mid = __reduce_min_sync(0xFFFFFFFFu, eq ? wid : 0xFFFFFFFFu);
+  eq &= wid == mid;
+  const uint32_t mdst = __reduce_min_sync(0xFFFFFFFFu, eq ? wdst : 0xFFFFFFFFu);
+  eq &= wdst == mdst;
+  const uint32_t mg = __reduce_min_sync(0xFFFFFFFFu, eq ? wg : 0xFFFFFFFFu);
+  Cand r;
+  if (mg == 0xFFFFFFFFu) {   // no candidate in the warp (valid slots are < 2^31 - 1)
+    r.score = 0;
+    r.id = 0;
+    r.dst = 0;
+    r.g = -1;
+  } else {
+    const unsigned __int128 um = ((unsigned __int128)m[0] << 96) | ((unsigned __int128)m[1] << 64) |
+                                 ((unsigned __int128)m[2] << 32) | (unsigned __int128)m[3];
+    r.score = (i128)(~um ^ ((unsigned __int128)1 << 127));
+    r.id = (int32_t)(mid ^ 0x80000000u);
+    r.dst = (int32_t)(mdst ^ 0x80000000u);
+    r.g = (int32_t)(mg ^ 0x80000000u);
+  }
+  return r;
+}
+
 __device__ __forceinline__ i128 shfl_up_i128(i128 v, int off) {
   const unsigned long long lo = __shfl_up_sync(0xFFFFFFFFu, (unsigned long long)v, off);
   const long long hi = __shfl_up_sync(0xFFFFFFFFu, (long long)(v >> 64), off);

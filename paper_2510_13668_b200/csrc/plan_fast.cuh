@@ -66,47 +66,6 @@ __device__ __forceinline__ bool cand_better_g(const Cand& x, const Cand& y) {
   return (x.g >= 0) & ((y.g < 0) | s_gt | (s_eq & tie));
 }
 
-// Warp argmax in the cand_better_g order by hardware reductions: the key as seven order-preserving
-// 32-bit words (the score complemented, so its maximum is the minimum; id, dst, g with the sign bit
-// flipped; an empty candidate all ones), minimised word by word among the lanes still tied
-// (redux.sync: one instruction per word instead of a five-step shuffle tree).  Every lane returns
-// the winner.
-__device__ __forceinline__ Cand warp_argmax_g(const Cand& c) {
-  __syncwarp();   // reconverge first
-  const bool v = c.g >= 0;
-  const unsigned __int128 us = v ? ~((unsigned __int128)c.score ^ ((unsigned __int128)1 << 127)) : ~(unsigned __int128)0;
-  const uint32_t w[4] = {(uint32_t)(us >> 96), (uint32_t)(us >> 64), (uint32_t)(us >> 32), (uint32_t)us};
-  const uint32_t wid = v ? (uint32_t)c.id ^ 0x80000000u : 0xFFFFFFFFu;
-  const uint32_t wdst = v ? (uint32_t)c.dst ^ 0x80000000u : 0xFFFFFFFFu;
-  const uint32_t wg = v ? (uint32_t)c.g ^ 0x80000000u : 0xFFFFFFFFu;
-  uint32_t m[4];
-  bool eq = true;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    m[k] = __reduce_min_sync(0xFFFFFFFFu, eq ? w[k] : 0xFFFFFFFFu);
-    eq &= w[k] == m[k];
-  }
-  const uint32_t mid = __reduce_min_sync(0xFFFFFFFFu, eq ? wid : 0xFFFFFFFFu);
-  eq &= wid == mid;
-  const uint32_t mdst = __reduce_min_sync(0xFFFFFFFFu, eq ? wdst : 0xFFFFFFFFu);
-  eq &= wdst == mdst;
-  const uint32_t mg = __reduce_min_sync(0xFFFFFFFFu, eq ? wg : 0xFFFFFFFFu);
-  Cand r;
-  if (mg == 0xFFFFFFFFu) {   // no candidate in the warp (valid slots are < 2^31 - 1)
-    r.score = 0;
-    r.id = 0;
-    r.dst = 0;
-    r.g = -1;
-  } else {
-    const unsigned __int128 um = ((unsigned __int128)m[0] << 96) | ((unsigned __int128)m[1] << 64) |
-                                 ((unsigned __int128)m[2] << 32) | (unsigned __int128)m[3];
-    r.score = (i128)(~um ^ ((unsigned __int128)1 << 127));
-    r.id = (int32_t)(mid ^ 0x80000000u);
-    r.dst = (int32_t)(mdst ^ 0x80000000u);
-    r.g = (int32_t)(mg ^ 0x80000000u);
-  }
-  return r;
-}
 
 template <class T>
 __device__ __forceinline__ T* carve(uint8_t*& p, size_t count) {

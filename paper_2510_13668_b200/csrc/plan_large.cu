@@ -151,10 +151,10 @@ __global__ void __launch_bounds__(kPrepThreads) plan_prep_kernel(const PlanArgs 
   }
 }
 
-// Branch-free candidate order (gain desc, req_id asc, dst asc): used between shuffle steps, where a
-// divergent select would send the next shuffle down the slow (BRA.DIV) path.
+// Branch-free candidate order (gain desc, req_id asc, dst asc, then the slot: warp_argmax_g's order)
+// for the per-thread running best.
 __device__ __forceinline__ bool lg_better(const Cand& x, const Cand& y) {
-  const bool tie = (x.id < y.id) | ((x.id == y.id) & (x.dst < y.dst));
+  const bool tie = (x.id < y.id) | ((x.id == y.id) & ((x.dst < y.dst) | ((x.dst == y.dst) & (x.g < y.g))));
   return (x.g >= 0) & ((y.g < 0) | (x.score > y.score) | ((x.score == y.score) & tie));
 }
 __device__ __forceinline__ void lg_take(Cand& c, const Cand& o) {
@@ -163,21 +163,6 @@ __device__ __forceinline__ void lg_take(Cand& c, const Cand& o) {
   c.id = b ? o.id : c.id;
   c.dst = b ? o.dst : c.dst;
   c.g = b ? o.g : c.g;
-}
-__device__ __forceinline__ Cand lg_warp_argmax(Cand c) {
-  __syncwarp();   // reconverge first
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    Cand o;
-    const uint64_t lo = __shfl_xor_sync(0xFFFFFFFFu, (uint64_t)c.score, off);
-    const uint64_t hi = __shfl_xor_sync(0xFFFFFFFFu, (uint64_t)(c.score >> 64), off);
-    o.score = (i128)(((unsigned __int128)hi << 64) | lo);
-    o.id = __shfl_xor_sync(0xFFFFFFFFu, c.id, off);
-    o.dst = __shfl_xor_sync(0xFFFFFFFFu, c.dst, off);
-    o.g = __shfl_xor_sync(0xFFFFFFFFu, c.g, off);
-    lg_take(c, o);
-  }
-  return c;
 }
 
 // Per-candidate terms of the score (closed-form gain 2n * score; same arithmetic
@@ -405,7 +390,7 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
       __syncthreads();
     }
   }
-  best = lg_warp_argmax(best);
+  best = warp_argmax_g(best);
   if (lane == 0) warp_best[warp] = best;
   __syncthreads();
   if (warp == 0) {
@@ -415,7 +400,7 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
     } else {
       c.score = 0; c.id = 0; c.dst = 0; c.g = -1;
     }
-    c = lg_warp_argmax(c);
+    c = warp_argmax_g(c);
     if (lane == 0) {
       w.cta_best[blockIdx.x] = c;
       fence_acq_rel_gpu();
@@ -438,7 +423,7 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
     o.g = (int32_t)(uint32_t)v1.y;
     lg_take(c, o);
   }
-  c = lg_warp_argmax(c);
+  c = warp_argmax_g(c);
   if (lane == 0) warp_best[warp] = c;
   const int m0 = w.state[1];   // read by every thread before warp 0 updates it (after the barrier)
   __syncthreads();
@@ -448,7 +433,7 @@ __global__ void __launch_bounds__(kScanThreads) plan_scan_kernel(const PlanArgs 
   } else {
     c.score = 0; c.id = 0; c.dst = 0; c.g = -1;
   }
-  c = lg_warp_argmax(c);   // warps 0 and 1 hold the same m*
+  c = warp_argmax_g(c);   // warps 0 and 1 hold the same m*
   if (c.g < 0 || !anyO) {
     if (warp == 0 && lane == 0) {
       w.state[0] = 1;   // no improving move: stop
