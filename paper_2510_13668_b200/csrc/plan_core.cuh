@@ -66,37 +66,6 @@ __device__ __forceinline__ Cand shfl_cand(const Cand& c, int src_lane) {
   return o;
 }
 
-__device__ __forceinline__ Cand warp_argmax(Cand c) {
-  __syncwarp();   // reconverge first: shuffles of a diverged warp take a slow path
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    Cand o = shfl_cand(c, lane ^ off);
-    if (cand_better(o, c)) c = o;
-  }
-  return c;
-}
-
-// a * b (mod 2^128) for a 32-bit unsigned b: four 32x32->64 multiply-adds over the limbs of a
-// (the generic __int128 product costs ~4x as many IMADs and dominated the candidate scoring).
-__device__ __forceinline__ i128 mul_u32(i128 a, uint32_t b) {
-  const unsigned __int128 ua = (unsigned __int128)a;
-  const uint64_t lo = (uint64_t)ua, hi = (uint64_t)(ua >> 64);
-  const uint64_t p0 = (uint64_t)(uint32_t)lo * b;
-  const uint64_t p1 = (lo >> 32) * b + (p0 >> 32);
-  const uint64_t p2 = (uint64_t)(uint32_t)hi * b + (p1 >> 32);
-  const uint64_t p3 = (hi >> 32) * b + (p2 >> 32);
-  const uint64_t rlo = (p0 & 0xFFFFFFFFull) | (p1 << 32);
-  const uint64_t rhi = (p2 & 0xFFFFFFFFull) | (p3 << 32);
-  return (i128)(((unsigned __int128)rhi << 64) | rlo);
-}
-// a * b (mod 2^128) for a 32-bit signed b
-__device__ __forceinline__ i128 mul_i32(i128 a, int32_t b) {
-  const uint32_t m = b < 0 ? (uint32_t)(-(int64_t)b) : (uint32_t)b;
-  const i128 r = mul_u32(a, m);
-  return b < 0 ? -r : r;
-}
-
 // Warp argmax in the order (score desc, id asc, dst asc, g asc) -- plan_fast.cuh cand_better_g --
 // by hardware reductions: the key as seven order-preserving
 // 32-bit words (the score complemented, so its maximum is the minimum; id, dst, g with the sign bit
@@ -139,6 +108,28 @@ __device__ __forceinline__ Cand warp_argmax_g(const Cand& c) {
   }
   return r;
 }
+__device__ __forceinline__ Cand warp_argmax(const Cand& c) { return warp_argmax_g(c); }
+
+// a * b (mod 2^128) for a 32-bit unsigned b: four 32x32->64 multiply-adds over the limbs of a
+// (the generic __int128 product costs ~4x as many IMADs and dominated the candidate scoring).
+__device__ __forceinline__ i128 mul_u32(i128 a, uint32_t b) {
+  const unsigned __int128 ua = (unsigned __int128)a;
+  const uint64_t lo = (uint64_t)ua, hi = (uint64_t)(ua >> 64);
+  const uint64_t p0 = (uint64_t)(uint32_t)lo * b;
+  const uint64_t p1 = (lo >> 32) * b + (p0 >> 32);
+  const uint64_t p2 = (uint64_t)(uint32_t)hi * b + (p1 >> 32);
+  const uint64_t p3 = (hi >> 32) * b + (p2 >> 32);
+  const uint64_t rlo = (p0 & 0xFFFFFFFFull) | (p1 << 32);
+  const uint64_t rhi = (p2 & 0xFFFFFFFFull) | (p3 << 32);
+  return (i128)(((unsigned __int128)rhi << 64) | rlo);
+}
+// a * b (mod 2^128) for a 32-bit signed b
+__device__ __forceinline__ i128 mul_i32(i128 a, int32_t b) {
+  const uint32_t m = b < 0 ? (uint32_t)(-(int64_t)b) : (uint32_t)b;
+  const i128 r = mul_u32(a, m);
+  return b < 0 ? -r : r;
+}
+
 
 __device__ __forceinline__ i128 shfl_up_i128(i128 v, int off) {
   const unsigned long long lo = __shfl_up_sync(0xFFFFFFFFu, (unsigned long long)v, off);
@@ -199,51 +190,6 @@ __device__ __forceinline__ Cand best_target(const PlanArgs& a, bool strict, bool
     if (cand_better(c, best)) best = c;
   }
   return best;
-}
-
-// Warp-cooperative variant of best_target: the lanes split the target list (lane q, q+32, ...),
-// so the per-target loads are coalesced and a request with hundreds of targets costs
-// ceil(nU / 32) iterations instead of nU.  Every lane must call it with identical request
-// arguments; returns the best candidate of the warp in every lane (warp_argmax, total order).
-__device__ __forceinline__ Cand best_target_warp(const PlanArgs& a, bool strict, bool cur_only, int g, int src,
-                                                 int64_t N, int64_t nh, int32_t rid, const int* ulist, int nU,
-                                                 const int64_t* Ls, const i128* P0, const i128* P1, const i128* B,
-                                                 int H1) {
-  Cand best;
-  best.score = 0;
-  best.id = 0;
-  best.dst = 0;
-  best.g = -1;
-  int T = (int)(nh - 1 < 0 ? 0 : (nh - 1 > a.H ? a.H : nh - 1));
-  if (cur_only) T = 0;
-  const i128 self = (i128)N * N * B[T] + (i128)2 * N * B[H1 + T] + B[2 * H1 + T];
-  const i128 src_part = (i128)N * P0[(int64_t)src * H1 + T] + P1[(int64_t)src * H1 + T];
-  const i128 mig = (i128)a.c0_ps + (i128)a.c1_ps * N;
-  for (int q = (int)(threadIdx.x & 31); q < nU; q += 32) {
-    const int u = ulist[q];
-    const int64_t Lu0 = Ls[(int64_t)u * H1];
-    if (!cur_only) {
-      if (!((i128)nh * ((i128)a.a_ps + (i128)a.b_ps * Lu0) > mig)) continue;
-    }
-    if (a.c_mem) {
-      i128 need = Lu0;
-      if (strict) {
-        if (!cur_only) need += nh;
-      } else {
-        need += (a.reserved ? a.reserved[u] : 0) + N + (cur_only ? 0 : nh);
-      }
-      if (!(need <= (i128)a.c_mem[u])) continue;
-    }
-    const i128 score = src_part - ((i128)N * P0[(int64_t)u * H1 + T] + P1[(int64_t)u * H1 + T]) - self;
-    if (score <= 0) continue;
-    Cand c;
-    c.score = score;
-    c.id = rid;
-    c.dst = u;
-    c.g = g;
-    if (cand_better(c, best)) best = c;
-  }
-  return warp_argmax(best);
 }
 
 // Barriers for plan_cta: the whole CTA, or the 128 epilogue threads of the fused tail.
