@@ -20,6 +20,7 @@
 // Kernel boundaries are the grid-wide synchronisation; every kernel exits immediately once the
 // stop flag is set, so the host can enqueue max_moves rounds without reading anything back.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "plan_core.cuh"
 #include "ptx.cuh"
@@ -505,7 +506,11 @@ cudaError_t launch_plan_large(const PlanArgs& a, void* workspace, cudaStream_t s
   scan_grid = scan_grid < 1 ? 1 : (scan_grid > 2 * g_num_sms ? 2 * g_num_sms : scan_grid);
   const size_t H1 = (size_t)a.H + 1;
   const size_t smem0 = 16 * 3 * H1 + 4 * (size_t)a.n + 4 * (size_t)a.world + (size_t)a.n + 16;
-  const int lu_smem = smem0 + 24 * (size_t)a.n <= 160 * 1024 ? 1 : 0;   // U's per-target terms beside the list
+  static const bool force_global = [] {   // STAR_PLAN_LARGE_GLOBAL=1: per-target terms from global memory
+    const char* e = getenv("STAR_PLAN_LARGE_GLOBAL");   // (the > ~6500-instance form, testable at any size)
+    return e && e[0] == '1';
+  }();
+  const int lu_smem = !force_global && smem0 + 24 * (size_t)a.n <= 160 * 1024 ? 1 : 0;   // U's per-target terms
   const size_t smem = smem0 + (lu_smem ? 24 * (size_t)a.n : 0);
   if (smem > 48 * 1024) {
     e = func_attr((const void*)plan_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

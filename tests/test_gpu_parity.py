@@ -503,6 +503,43 @@ def test_plan_large_bitexact_cluster_scale(star, oracle_mod, n, r_per, moves, fl
         assert _plan_gpu(star, params, L, snap, n_hat) == ref
 
 
+_PLAN_GLOBAL_SCRIPT = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import datagen, oracle
+import paper_2510_13668_b200 as star
+for n, r_per, moves, flags in ((256, 8, 3, 0), (128, 16, 2, 1), (96, 24, 3, 2), (40, 30, 3, 0)):
+    snap = datagen.make_snapshot(n + r_per, n, r_per, pinned_frac=0.03)
+    n_hat = snap.true_rem.copy()
+    params = datagen.make_plan_params(snap, mem_factor=1.10, max_moves=moves, flags=flags, reserved_seed=n)
+    L = oracle.project(snap.inst, snap.n_tok, n_hat, n, params.H, params.beta_q)["L"]
+    ref = oracle.plan(params, L, snap.req_id, snap.inst, snap.n_tok, n_hat, snap.pinned)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    pp = star.PlanParams.from_host(params)
+    moves_t, nm = star.plan_reschedule_large(pp, d(L), d(snap.req_id), d(snap.inst), d(snap.n_tok),
+                                             d(n_hat.astype(np.int32)), d(snap.pinned))
+    torch.cuda.synchronize()
+    got = star.decode_moves(moves_t, nm)
+    assert got == ref, (n, got, ref)
+    assert len(ref) > 0 or n == 40
+print("global ok")
+'''
+
+
+def test_plan_large_global_terms_subprocess(star):
+    """The cluster-scale plan's per-target terms read from global memory (the form above ~6500
+    instances, where they do not fit shared memory), forced by STAR_PLAN_LARGE_GLOBAL=1 in a fresh
+    process at sizes the oracle finishes: bit-exact vs the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _PLAN_GLOBAL_SCRIPT, root],
+                       env={**os.environ, "STAR_PLAN_LARGE_GLOBAL": "1"}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "global ok" in r.stdout
+
+
 # ============================================================================ prediction cadence (NEXT-1)
 def _nhat_close(got, ref_y, n_tok, tol):
     """Refreshed rows: the GPU's N_hat within the bf16 tolerance of the quantized fp64 oracle."""
