@@ -180,6 +180,25 @@ __device__ __forceinline__ void proj_finalize_lanes(const ProjArgs& a, const uin
   }
 }
 
+// Warp sum of int64 (mod 2^64, i.e. exact two's complement) by redux.sync over four 16-bit chunks
+// (each chunk sum < 2^21 fits 32 bits; the four reductions are independent), and warp max of int64 as
+// (high word signed, then low word unsigned among the lanes holding that high word).
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
+  const uint64_t u = (uint64_t)v;
+  const uint64_t c0 = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)(u & 0xFFFFu));
+  const uint64_t c1 = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)((u >> 16) & 0xFFFFu));
+  const uint64_t c2 = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)((u >> 32) & 0xFFFFu));
+  const uint64_t c3 = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)(u >> 48));
+  return (int64_t)(c0 + (c1 << 16) + (c2 << 32) + (c3 << 48));
+}
+__device__ __forceinline__ int64_t warp_max_i64(int64_t v) {
+  const int32_t hi = (int32_t)(v >> 32);
+  const uint32_t lo = (uint32_t)v;
+  const int32_t mh = __reduce_max_sync(0xFFFFFFFFu, hi);
+  const uint32_t ml = __reduce_max_sync(0xFFFFFFFFu, hi == mh ? lo : 0u);
+  return (int64_t)(((uint64_t)(uint32_t)mh << 32) | ml);
+}
+
 // kLanes: allow the lane-per-instance form (the fused tail, whose projection covers one rank's
 // few instances, instantiates the warp form only and keeps its register budget).
 template <bool kLanes = true>
@@ -226,15 +245,11 @@ __device__ __forceinline__ void proj_finalize(const ProjArgs& a, const uint32_t*
         peak = lt > peak ? lt : peak;
       }
     }
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      L0 += __shfl_xor_sync(0xFFFFFFFFu, L0, off);
-      cnt_all += __shfl_xor_sync(0xFFFFFFFFu, cnt_all, off);
-      grow += __shfl_xor_sync(0xFFFFFFFFu, grow, off);
-      w += __shfl_xor_sync(0xFFFFFFFFu, w, off);
-      const int64_t pk = __shfl_xor_sync(0xFFFFFFFFu, peak, off);
-      peak = pk > peak ? pk : peak;
-    }
+    L0 = warp_sum_i64(L0);   // independent hardware reductions instead of five dependent shuffle rounds
+    cnt_all = warp_sum_i64(cnt_all);
+    grow = warp_sum_i64(grow);
+    w = warp_sum_i64(w);
+    peak = warp_max_i64(peak);
     if (lane == 0) {
       Li[0] = L0;
       if (a.W) a.W[i] = w;
