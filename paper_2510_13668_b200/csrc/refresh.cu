@@ -303,18 +303,22 @@ __global__ void __launch_bounds__(kSel2Threads) refresh_select_gather_age_kernel
     }
   }
   SEL_TS(3);
-  if (tid == 0) {   // every CTA's count is in: this CTA's base is the sum of the lower CTAs' counts
-    spin_wait_geq(a.blk + G, G);
-    int base = 0;
-    for (int j = 0; j < b; ++j) base += __ldcg(a.blk + j);
-    s_base = base;
-    if (b == G - 1) {
-      *a.M_out = base + s_cnt;
-      if (a.n_refreshed) *a.n_refreshed = base + s_cnt;
-    }
-    if (atomicAdd(a.blk + G + 1, 1) == G - 1) {   // the last reader re-arms the counters
-      a.blk[G] = 0;
-      a.blk[G + 1] = 0;
+  if (warp == 0) {   // every CTA's count is in: this CTA's base is the sum of the lower CTAs' counts
+    if (lane == 0) spin_wait_geq(a.blk + G, G);
+    __syncwarp();   // orders the lanes' loads after lane 0's acquire
+    int part = 0;   // lanes load the lower CTAs' counts together (one round trip, not b of them)
+    for (int j = lane; j < b; j += 32) part += __ldcg(a.blk + j);
+    const int base = (int)__reduce_add_sync(0xFFFFFFFFu, (uint32_t)part);
+    if (lane == 0) {
+      s_base = base;
+      if (b == G - 1) {
+        *a.M_out = base + s_cnt;
+        if (a.n_refreshed) *a.n_refreshed = base + s_cnt;
+      }
+      if (atomicAdd(a.blk + G + 1, 1) == G - 1) {   // the last reader re-arms the counters
+        a.blk[G] = 0;
+        a.blk[G + 1] = 0;
+      }
     }
   }
   __syncthreads();
