@@ -363,6 +363,7 @@ __global__ void __launch_bounds__(192, 1)
     float y = head_acc;
     if (splits > 1) {
       y = 0.0f;
+#pragma unroll 8   // splits <= 8: the loads issue together, the sum keeps split order
       for (int s = 0; s < splits; ++s) y += __ldcg(p.head_ws + ((int64_t)tile_id * splits + s) * BM + row_in_tile);
     }
     y += p.b4 ? __ldg(p.b4) : 0.0f;
