@@ -26,9 +26,6 @@ pp = star.PlanParams.from_host(ph, device=dev)
 ws = torch.empty(star.plan_workspace_bytes(n, H, snap.R), dtype=torch.uint8, device=dev)
 moves, nm = star.alloc_moves(mm, dev)
 args = (pp, proj.L, d(snap.req_id), d(snap.inst), d(snap.n_tok), d(snap.true_rem.astype(np.int32)))
-L = proj.L.cpu().numpy()
-W = (L[:, 1:].astype(np.float64) * beta[1:]).sum(1)
-print("overloaded instances (approx, float):", int((n * W > 1.2 * W.sum()).sum()))
 for _ in range(3):
     star.plan_reschedule_large(*args, moves=moves, n_moves=nm, workspace=ws)
 torch.cuda.synchronize()
