@@ -248,6 +248,52 @@ def test_plan_segmented_equals_contiguous(star, oracle_mod, world):
     assert star.decode_moves(moves, nm) == ref
 
 
+@pytest.mark.parametrize("world,r_cap", [(4, 60000), (8, 20000)])
+def test_plan_large_segmented_many_slots(star, oracle_mod, world, r_cap):
+    """The cluster-scale plan over gathered records whose capacity far exceeds their requests:
+    240k / 160k slots (several strided slot chunks per CTA of the scan, the later ones loaded
+    inside the chunk loop), 96 requests per rank at the front of each segment, 4 moves; == the
+    oracle on the concatenated state."""
+    n_loc, r_per = 8 // world, 96
+    snap = datagen.make_snapshot(31, 8, r_per)
+    n_hat = snap.true_rem.astype(np.int32)
+    params = datagen.make_plan_params(snap, max_moves=4)
+    H = params.H
+    order = np.argsort(snap.inst, kind="stable")
+    inst, n_tok, ids, pin, nh = (a[order] for a in (snap.inst, snap.n_tok, snap.req_id, snap.pinned, n_hat))
+    L = oracle_mod.project(inst, n_tok, nh, 8, H, params.beta_q)["L"]
+    ref = oracle_mod.plan(params, L, ids, inst, n_tok, nh, pin)
+    assert len(ref) > 0
+    rec_i64 = n_loc * (H + 1) + 1 + (4 * r_cap + (r_cap + 7) // 8 * 2 + 1) // 2 + 1
+    buf = np.zeros((world, rec_i64), np.int64)
+    offs = {}
+    for k in range(world):
+        sel = (inst >= k * n_loc) & (inst < (k + 1) * n_loc)
+        cnt = int(sel.sum())
+        rec = buf[k].view(np.uint8)
+        o = 0
+        rec[o:o + 8 * n_loc * (H + 1)] = L[k * n_loc:(k + 1) * n_loc].reshape(-1).view(np.uint8); offs["L"] = o
+        o += 8 * n_loc * (H + 1)
+        rec[o:o + 4] = np.array([cnt], np.int32).view(np.uint8); offs["cnt"] = o; o += 8
+        for name, arr in (("id", ids), ("inst", inst), ("ntok", n_tok), ("nhat", nh)):
+            v = np.zeros(r_cap, np.int32)
+            v[:cnt] = arr[sel]
+            rec[o:o + 4 * r_cap] = v.view(np.uint8); offs[name] = o; o += 4 * r_cap
+        v = np.zeros(r_cap, np.uint8)
+        v[:cnt] = pin[sel]
+        rec[o:o + r_cap] = v; offs["pin"] = o
+    d = _dev(buf)
+    base = d.data_ptr()
+    seg = star._lib.PlanSegmentsC(world, n_loc, r_cap, rec_i64 * 8, base + offs["L"], base + offs["cnt"],
+                                  base + offs["id"], base + offs["inst"], base + offs["ntok"], base + offs["nhat"],
+                                  base + offs["pin"])
+    pp = star.PlanParams.from_host(params)
+    ws = torch.empty(star.plan_workspace_bytes(8, H, world * r_cap), dtype=torch.uint8, device="cuda")
+    moves, nm = star.plan_reschedule_segmented_ws(pp, seg, ws)
+    torch.cuda.synchronize()
+    assert star.decode_moves(moves, nm) == ref
+
+
 # ============================================================================ predictor
 def _predict(star, pw, h, biases=False, n_tok=None, max_rows=None):
     W, b = _weights_dev(pw, biases)
