@@ -535,9 +535,11 @@ def test_plan_large_bitexact_tiny(star, oracle_mod, seed):
 
 
 @pytest.mark.parametrize("n,r_per,moves,flags", [(256, 8, 3, 0), (64, 64, 4, 0), (128, 16, 2, 1), (96, 24, 3, 2),
-                                                  (8, 256, 4, 0)])
+                                                  (8, 256, 4, 0),
+                                                  # more instances than scan threads (Phase 1 loops)
+                                                  (300, 4, 2, 0), (600, 2, 2, 1)])
 def test_plan_large_bitexact_cluster_scale(star, oracle_mod, n, r_per, moves, flags):
-    """Cluster-scale shapes (up to 256 instances) vs the from-scratch oracle."""
+    """Cluster-scale shapes (up to 600 instances) vs the from-scratch oracle."""
     snap = datagen.make_snapshot(n + r_per, n, r_per, pinned_frac=0.03)
     n_hat = snap.true_rem.copy()
     params = datagen.make_plan_params(snap, mem_factor=1.10, max_moves=moves, flags=flags, reserved_seed=n)
